@@ -1,0 +1,131 @@
+/*
+ * parmerge_b200.h -- C-ABI of the B200-native parallel in-place merge.
+ *
+ * Drop-in boundary for the reference package `parmerge`, whose native layer is
+ * the numba module `_kernels` (/root/reference/pkg/src/parmerge/_kernels.py,
+ * "every kernel takes the full keys/payload arrays plus integer offsets",
+ * _kernels.py:3-7).  Each entry point below replaces one reference call site;
+ * the replaced interface is cited beside it.  The Python mirror
+ * (paper_2005_12648_b200/) binds these through ctypes exactly as the
+ * reference's L2 wrappers call `_kernels`.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; `keys` / `payload` are DEVICE pointers to
+ *     the base of the caller's arrays (record x at keys + x*key_bytes and
+ *     payload + x*width), positions are absolute int64 record indices;
+ *   - key_bytes is 4 (int32, the reference's KEY_DTYPE, records.py:9) or 8
+ *     (int64, the skewed BASELINE config); payload rows are opaque bytes that
+ *     travel with their key (records.py:15-22); width may be 0;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     stream-ordered and asynchronous -- device-side failures are reported by
+ *     pm_status(), host-side argument errors by the return code;
+ *   - return value: 0 on success, else a PM_ERR_* code; pm_last_error() gives
+ *     the thread's last message;
+ *   - a context owns the persistent device workspace (split table, unit
+ *     bookkeeping, bounded scratch); use one context per stream.
+ */
+#ifndef PARMERGE_B200_H
+#define PARMERGE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PM_OK 0
+#define PM_ERR_ARG 1         /* invalid argument (ValueError/IndexError in the reference wrappers) */
+#define PM_ERR_CUDA 2        /* CUDA runtime failure */
+#define PM_ERR_TIMEOUT 3     /* device wait bound exceeded (protocol fault) */
+#define PM_ERR_NOSPACE 4     /* salvage space exhausted */
+#define PM_ERR_INTERNAL 5
+#define PM_ERR_UNSUPPORTED 6 /* record too wide for the staging buffers */
+
+typedef struct pm_ctx pm_ctx;
+
+/* library version (major*10000 + minor*100 + patch) */
+int pm_version(void);
+/* last error message of the calling thread ("" if none) */
+const char *pm_last_error(void);
+
+int pm_ctx_create(int device, pm_ctx **out);
+int pm_ctx_destroy(pm_ctx *ctx);
+
+/*
+ * Stable in-place merge of the adjacent sorted runs [start, middle) and
+ * [middle, end); ties keep A first, so the result equals the reference's
+ * seq_merge_buffered (seqmerge.py:55-75 -> _kernels.buffered_merge,
+ * _kernels.py:227-313), seq_merge_rotation (_kernels.py:201-223) and
+ * merge_srecpar(threads=1) (srecpar.py:33-60).  Replaces the partition + shift
+ * + leaf-merge pipeline of merge_srecpar / merge_soptmov (srecpar.py:63-84,
+ * soptmov.py:195-240).  `scratch_records` is a lower bound on the bounded
+ * salvage pool (0 = default, O(grid * tile)).
+ */
+int pm_merge(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t width,
+             int64_t start, int64_t middle, int64_t end, int64_t scratch_records, void *stream);
+
+/*
+ * In-place block exchange A|B -> B|A of [lo, lo+len_a) and [lo+len_a,
+ * lo+len_a+len_b).  Replaces _kernels.linear_shift (_kernels.py:92-150) and
+ * _kernels.circular_shift (_kernels.py:154-197) behind shift_region /
+ * linear_shift / circular_shift (shift.py:38-55); both kinds produce the same
+ * array (tests/test_srecpar.py:70-80 of the reference).
+ */
+int pm_shift(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t width,
+             int64_t lo, int64_t len_a, int64_t len_b, void *stream);
+
+/*
+ * Alg. 1 pivot pair of the sorted runs a[0, la) and b[0, lb) (DEVICE
+ * pointers), exactly as find_median (median.py:23-60).  out2 is a DEVICE
+ * int64[2] receiving (p_a, p_b).
+ */
+int pm_find_median(pm_ctx *ctx, const void *a, const void *b, int key_bytes, int64_t la, int64_t lb,
+                   int64_t *out2, void *stream);
+
+/*
+ * Stable merge-path splits of the sorted runs a[0, la) and b[0, lb) (DEVICE
+ * pointers): for each diagonal diags[i] (DEVICE int64[nd]),
+ * out_a[i] (DEVICE) = number of A records among the first diags[i] outputs of
+ * the stable merge (A wins ties).  The GPU pipeline's partition search; the
+ * stable counterpart of plan_intervals' pivots (soptmov.py:93-123).
+ */
+int pm_find_splits(pm_ctx *ctx, const void *a, const void *b, int key_bytes, int64_t la, int64_t lb,
+                   const int64_t *diags, int64_t nd, int64_t *out_a, void *stream);
+
+/*
+ * plan_intervals (soptmov.py:93-123): log2(threads) levels of Alg. 1 over run
+ * pairs.  nodes (DEVICE int64[4*(2*threads-1)]) receives the level-order
+ * RunPairs (a_start, a_end, b_start, b_end), level 0 first.
+ */
+int pm_plan_intervals(pm_ctx *ctx, const void *keys, int key_bytes, int64_t start, int64_t middle,
+                      int64_t end, int32_t threads, int64_t *nodes, void *stream);
+
+/*
+ * Synchronise `stream`, then return (and clear) the sticky device status of the
+ * context's last merges/shifts.  stats (host uint64[4], may be NULL) receives
+ * the last job's counters: salvaged units, salvaged records, merged regions,
+ * identity (skipped) regions.
+ */
+int pm_status(pm_ctx *ctx, void *stream, uint64_t *stats);
+
+/*
+ * End-to-end entry point with HOST buffers (the reference's calling
+ * convention: numpy arrays in host memory).  Copies keys/payload to the
+ * device, merges, copies back, synchronises and returns the status.
+ * Pinned host memory gives full PCIe bandwidth.
+ */
+int pm_merge_host(pm_ctx *ctx, void *keys_host, int key_bytes, void *payload_host, int64_t width,
+                  int64_t start, int64_t middle, int64_t end, void *stream);
+
+/*
+ * Instrumentation (no reference counterpart): when enabled, the context
+ * records CUDA events around the plan and engine kernels of each merge/shift;
+ * pm_kernel_ms() waits for the last one and returns their device durations.
+ */
+int pm_set_timing(pm_ctx *ctx, int on);
+int pm_kernel_ms(pm_ctx *ctx, float *plan_ms, float *engine_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARMERGE_B200_H */

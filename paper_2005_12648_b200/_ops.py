@@ -1,0 +1,128 @@
+"""Device operations: thin typed wrappers over the C-ABI (one call = one C-ABI entry).
+
+All functions take GPU-resident tensors and enqueue work on the current torch
+CUDA stream.  By default every mutating call then synchronises and checks the
+device status word (``pm_status``) so errors surface at the call site, like the
+reference's synchronous numba calls; ``deferred_checks()`` turns that off for
+pipelines that check once at the end (the benchmark).
+"""
+
+from __future__ import annotations
+
+import contextlib
+import ctypes
+
+import torch
+
+from . import _capi
+from .records import KeyedArray, require_cuda
+
+_check_each_call = True
+
+
+@contextlib.contextmanager
+def deferred_checks():
+    """Skip the per-call synchronise+status check inside the block; check on exit."""
+    global _check_each_call
+    old = _check_each_call
+    _check_each_call = False
+    try:
+        yield
+    finally:
+        _check_each_call = old
+        synchronize()
+
+
+def synchronize(device: int | None = None) -> tuple[int, int, int, int]:
+    """Wait for the current stream and raise if any engine call failed; returns last-job stats."""
+    dev = torch.cuda.current_device() if device is None else device
+    return _capi.status(dev, torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _stream(dev: int) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr() if t.numel() else 0)
+
+
+def merge(arr: KeyedArray, start: int, middle: int, end: int, scratch_records: int = 0):
+    """Stable in-place merge of [start, middle) and [middle, end) on the device (pm_merge)."""
+    require_cuda(arr)
+    dev = arr.keys.device.index
+    rc = _capi.lib().pm_merge(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, _ptr(arr.payload),
+                              arr.payload.shape[1], start, middle, end, scratch_records, _stream(dev))
+    _capi.check(rc, "pm_merge")
+    if _check_each_call:
+        return _capi.status(dev, torch.cuda.current_stream(dev).cuda_stream)
+    return None
+
+
+def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
+    """In-place block exchange A|B -> B|A on the device (pm_shift)."""
+    require_cuda(arr)
+    dev = arr.keys.device.index
+    rc = _capi.lib().pm_shift(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, _ptr(arr.payload),
+                              arr.payload.shape[1], lo, len_a, len_b, _stream(dev))
+    _capi.check(rc, "pm_shift")
+    if _check_each_call:
+        return _capi.status(dev, torch.cuda.current_stream(dev).cuda_stream)
+    return None
+
+
+def _run_tensor(x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        t = x
+        if t.dtype not in (torch.int32, torch.int64):
+            raise TypeError(f"keys must be int32 or int64, got {t.dtype}")
+        return t.contiguous()
+    import numpy as np
+
+    a = np.asarray(x)
+    if a.dtype.kind not in "iu" and a.size:
+        raise TypeError("GPU find_median needs integer keys (use key= only with the CPU reference)")
+    a = np.ascontiguousarray(a, dtype=np.int64 if a.dtype.itemsize == 8 else np.int32) if a.size else a.astype(np.int32)
+    return torch.from_numpy(a).cuda()
+
+
+def find_median(a, b) -> tuple[int, int]:
+    """Alg. 1 pivot pair computed on the device (pm_find_median); returns host ints."""
+    ta, tb = _run_tensor(a), _run_tensor(b)
+    if ta.dtype != tb.dtype:
+        wide = torch.int64
+        ta, tb = ta.to(wide), tb.to(wide)
+    dev = ta.device.index
+    out = torch.empty(2, dtype=torch.int64, device=ta.device)
+    rc = _capi.lib().pm_find_median(_capi.context(dev), _ptr(ta), _ptr(tb), ta.element_size(), ta.numel(),
+                                    tb.numel(), _ptr(out), _stream(dev))
+    _capi.check(rc, "pm_find_median")
+    pa, pb = out.tolist()
+    return int(pa), int(pb)
+
+
+def find_splits(a: torch.Tensor, b: torch.Tensor, diags: torch.Tensor) -> torch.Tensor:
+    """Stable merge-path A-counts at the given diagonals (pm_find_splits), on the device."""
+    ta, tb = _run_tensor(a), _run_tensor(b)
+    if ta.dtype != tb.dtype:
+        ta, tb = ta.to(torch.int64), tb.to(torch.int64)
+    d = diags.to(device=ta.device, dtype=torch.int64).contiguous()
+    out = torch.empty_like(d)
+    dev = ta.device.index
+    rc = _capi.lib().pm_find_splits(_capi.context(dev), _ptr(ta), _ptr(tb), ta.element_size(), ta.numel(),
+                                    tb.numel(), _ptr(d), d.numel(), _ptr(out), _stream(dev))
+    _capi.check(rc, "pm_find_splits")
+    return out
+
+
+def plan_nodes(arr: KeyedArray, start: int, middle: int, end: int, threads: int) -> list[tuple[int, int, int, int]]:
+    """Level-order RunPairs of plan_intervals computed on the device (pm_plan_intervals)."""
+    require_cuda(arr)
+    dev = arr.keys.device.index
+    n_nodes = 2 * threads - 1
+    out = torch.empty(4 * n_nodes, dtype=torch.int64, device=arr.keys.device)
+    rc = _capi.lib().pm_plan_intervals(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, start, middle, end,
+                                       threads, _ptr(out), _stream(dev))
+    _capi.check(rc, "pm_plan_intervals")
+    v = out.view(-1, 4).tolist()
+    return [tuple(int(x) for x in r) for r in v]

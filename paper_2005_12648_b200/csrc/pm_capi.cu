@@ -1,0 +1,364 @@
+// pm_capi.cu -- extern "C" boundary (include/parmerge_b200.h) over the sm_100a
+// kernels.  Validation mirrors the reference wrappers' ValueError/IndexError
+// conditions (records.py:100-127, shift.py:156-162); the Python mirror maps
+// PM_ERR_ARG back to those exceptions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/parmerge_b200.h"
+#include "pm_common.cuh"
+#include "pm_engine.cuh"
+#include "pm_launch.h"
+
+using namespace pm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(PM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define PM_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// control block layout (device, bytes)
+struct Ctl {
+  unsigned long long free_top;
+  unsigned long long scr_top;
+  unsigned long long stats[4];
+  int32_t scr_count;
+  int32_t ticket;
+  int32_t err;
+  int32_t noop;
+};
+
+constexpr int kEngineThreads = 256;
+
+}  // namespace
+
+struct pm_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::mutex mu;
+  void* ws = nullptr;  // split_a | state | loc | reads | next_free | next_scr
+  size_t ws_bytes = 0;
+  Ctl* ctl = nullptr;
+  void* scr = nullptr;  // scratch keys + payload
+  size_t scr_bytes = 0;
+  void* stage = nullptr;  // device staging for pm_merge_host
+  size_t stage_bytes = 0;
+  bool timing = false;  // record events around the plan and engine kernels
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  bool ev_recorded = false;
+};
+
+static int ensure(void** p, size_t* have, size_t need) {
+  if (*have >= need) return PM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  size_t sz = std::max(need, (size_t)1 << 20);
+  cudaError_t e = cudaMalloc(p, sz);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+  *have = sz;
+  return PM_OK;
+}
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Tile geometry for a record of ks+w bytes: region M (power of two) so that the
+// staged keys+payload+index map stay ~<=72 KB per CTA (3 CTAs per SM).
+static bool pick_tiles(int ks, int64_t w, int64_t* M, int64_t* T, int32_t* mu) {
+  const int64_t budget = 72 * 1024;
+  int64_t m = 8192;
+  while (m > 16 && m * (ks + w + 5) > budget) m >>= 1;
+  if (m * (ks + w + 5) > budget + 64 * 1024) return false;  // wider than ~130 KB for 16 records
+  *M = m;
+  *T = std::max<int64_t>(16, m / 4);
+  *mu = (int32_t)(m / *T);
+  return true;
+}
+
+static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
+                      int mode, int64_t scratch_records, cudaStream_t st) {
+  if (e - s <= 0 || m == s || m == e) return PM_OK;
+  int64_t M, T;
+  int32_t mu;
+  if (!pick_tiles(ks, w, &M, &T, &mu)) return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
+  EngineParams P{};
+  P.keys = static_cast<char*>(keys);
+  P.pay = static_cast<uint8_t*>(payload);
+  P.w = w;
+  P.ks = ks;
+  P.mode = mode;
+  P.s = s;
+  P.m = m;
+  P.e = e;
+  P.T = T;
+  P.mu = mu;
+  P.nthreads = kEngineThreads;
+  P.M = M;
+  P.k0 = s / T;
+  P.K = (e - 1) / T - P.k0 + 1;
+  P.R0 = s / M;
+  P.Q = (e - 1) / M - P.R0 + 1;
+  P.qc = std::min<int64_t>(std::max<int64_t>(m / M - P.R0, 0), P.Q - 1);
+  if (P.K >= INT32_MAX / 2) return fail(PM_ERR_UNSUPPORTED, "job too large for 32-bit unit indices");
+  // shared memory carve-up (all offsets 16-byte aligned)
+  P.smem_keys = (size_t)align_up(M * ks + 48, 128);
+  P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
+  const size_t smem_src = (size_t)align_up((M + 16 + (M + 16) / 32 + 4) * 4, 128);
+  const size_t smem = P.smem_keys + P.smem_pay + smem_src;
+  // persistent grid: every resident CTA slot on every SM
+  int bps = 0;
+  cudaError_t ce = ks == 4 ? engine_occupancy<int32_t>(kEngineThreads, smem, &bps)
+                           : engine_occupancy<int64_t>(kEngineThreads, smem, &bps);
+  if (ce != cudaSuccess) return cuda_fail(ce, "engine occupancy");
+  if (bps < 1) return fail(PM_ERR_UNSUPPORTED, "engine does not fit on an SM");
+  int grid = (int)std::min<int64_t>((int64_t)bps * ctx->num_sms, P.Q);
+  // bounded salvage pool: O(grid * tile) records, phase matched to the caller's arrays
+  P.reserve = (int64_t)grid * (mu + 4) + 16;
+  int64_t S = std::max<int64_t>(2 * P.reserve, scratch_records / T + P.reserve);
+  S = std::min<int64_t>(S, P.K + P.reserve);
+  P.S = S;
+  // workspace
+  const size_t off_state = (size_t)align_up((P.Q + 1) * 8, 256);
+  const size_t off_loc = off_state + (size_t)align_up(P.K * 4, 256);
+  const size_t off_reads = off_loc + (size_t)align_up(P.K * 4, 256);
+  const size_t off_nf = off_reads + (size_t)align_up(P.K * 4, 256);
+  const size_t off_ns = off_nf + (size_t)align_up(P.K * 4, 256);
+  const size_t ws_need = off_ns + (size_t)align_up(S * 4, 256);
+  int rc = ensure(&ctx->ws, &ctx->ws_bytes, ws_need);
+  if (rc) return rc;
+  const size_t scr_k = (size_t)align_up(S * T * ks + 32, 256);
+  const size_t scr_need = scr_k + (size_t)(w ? S * T * w + 32 : 0);
+  rc = ensure(&ctx->scr, &ctx->scr_bytes, scr_need);
+  if (rc) return rc;
+  char* ws = static_cast<char*>(ctx->ws);
+  P.split_a = reinterpret_cast<int64_t*>(ws);
+  P.state = reinterpret_cast<int32_t*>(ws + off_state);
+  P.loc = reinterpret_cast<int32_t*>(ws + off_loc);
+  P.reads = reinterpret_cast<int32_t*>(ws + off_reads);
+  P.next_free = reinterpret_cast<int32_t*>(ws + off_nf);
+  P.next_scr = reinterpret_cast<int32_t*>(ws + off_ns);
+  P.free_top = &ctx->ctl->free_top;
+  P.scr_top = &ctx->ctl->scr_top;
+  P.stats = ctx->ctl->stats;
+  P.scr_count = &ctx->ctl->scr_count;
+  P.ticket = &ctx->ctl->ticket;
+  P.err = &ctx->ctl->err;
+  P.noop = &ctx->ctl->noop;
+  char* scr = static_cast<char*>(ctx->scr);
+  P.scr_keys = scr + ((uintptr_t)keys & 15);
+  P.scr_pay = reinterpret_cast<uint8_t*>(scr + scr_k + (w ? ((uintptr_t)payload & 15) : 0));
+  // plan (splits + reset) then engine
+  int64_t plan_work = std::max<int64_t>((P.Q + 1) * 32, P.K);
+  int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((plan_work + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
+  if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
+  ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
+  if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[1], st));
+  ce = ks == 4 ? launch_engine<int32_t>(P, grid, kEngineThreads, smem, st)
+               : launch_engine<int64_t>(P, grid, kEngineThreads, smem, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_engine launch");
+  if (ctx->timing) {
+    PM_CUDA(cudaEventRecord(ctx->ev[2], st));
+    ctx->ev_recorded = true;
+  }
+  return PM_OK;
+}
+
+static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* payload, int64_t w) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  if (ks != 4 && ks != 8) return fail(PM_ERR_ARG, "key_bytes must be 4 or 8");
+  if (!keys) return fail(PM_ERR_ARG, "null keys");
+  if (((uintptr_t)keys) % ks) return fail(PM_ERR_ARG, "keys pointer not aligned to key size");
+  if (w < 0) return fail(PM_ERR_ARG, "negative payload width");
+  if (w > 0 && !payload) return fail(PM_ERR_ARG, "null payload with nonzero width");
+  return PM_OK;
+}
+
+extern "C" {
+
+int pm_version(void) { return 100; }
+
+const char* pm_last_error(void) { return g_last_error.c_str(); }
+
+int pm_ctx_create(int device, pm_ctx** out) {
+  if (!out) return fail(PM_ERR_ARG, "null out");
+  PM_CUDA(cudaSetDevice(device));
+  pm_ctx* c = new pm_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaGetDeviceProperties");
+  }
+  c->num_sms = prop.multiProcessorCount;
+  e = cudaMalloc(reinterpret_cast<void**>(&c->ctl), sizeof(Ctl));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(ctl)");
+  }
+  cudaMemset(c->ctl, 0, sizeof(Ctl));
+  *out = c;
+  return PM_OK;
+}
+
+int pm_ctx_destroy(pm_ctx* ctx) {
+  if (!ctx) return PM_OK;
+  cudaSetDevice(ctx->device);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->scr) cudaFree(ctx->scr);
+  if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->ctl) cudaFree(ctx->ctl);
+  delete ctx;
+  return PM_OK;
+}
+
+int pm_set_timing(pm_ctx* ctx, int on) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (on && !ctx->ev[0])
+    for (auto& e : ctx->ev) PM_CUDA(cudaEventCreate(&e));
+  ctx->timing = on != 0;
+  ctx->ev_recorded = false;
+  return PM_OK;
+}
+
+int pm_kernel_ms(pm_ctx* ctx, float* plan_ms, float* engine_ms) {
+  if (!ctx || !plan_ms || !engine_ms) return fail(PM_ERR_ARG, "null argument");
+  if (!ctx->ev_recorded) return fail(PM_ERR_ARG, "no timed launch recorded (pm_set_timing first)");
+  PM_CUDA(cudaEventSynchronize(ctx->ev[2]));
+  PM_CUDA(cudaEventElapsedTime(plan_ms, ctx->ev[0], ctx->ev[1]));
+  PM_CUDA(cudaEventElapsedTime(engine_ms, ctx->ev[1], ctx->ev[2]));
+  return PM_OK;
+}
+
+int pm_merge(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t start, int64_t middle,
+             int64_t end, int64_t scratch_records, void* stream) {
+  int rc = check_common(ctx, keys, key_bytes, payload, width);
+  if (rc) return rc;
+  if (!(0 <= start && start <= middle && middle <= end))  // records.py:100-102
+    return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return run_engine(ctx, keys, key_bytes, payload, width, start, middle, end, MODE_MERGE, scratch_records,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t lo, int64_t len_a,
+             int64_t len_b, void* stream) {
+  int rc = check_common(ctx, keys, key_bytes, payload, width);
+  if (rc) return rc;
+  if (lo < 0 || len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "lengths must be non-negative");  // shift.py:157
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return run_engine(ctx, keys, key_bytes, payload, width, lo, lo + len_a, lo + len_a + len_b, MODE_ROTATE, 0,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int pm_find_median(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int64_t la, int64_t lb, int64_t* out2,
+                   void* stream) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  if (key_bytes != 4 && key_bytes != 8) return fail(PM_ERR_ARG, "key_bytes must be 4 or 8");
+  if (la < 0 || lb < 0 || !out2 || (la && !a) || (lb && !b)) return fail(PM_ERR_ARG, "bad find_median arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = key_bytes == 4 ? launch_find_median<int32_t>(a, b, la, lb, out2, st)
+                                 : launch_find_median<int64_t>(a, b, la, lb, out2, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_find_median launch");
+  return PM_OK;
+}
+
+int pm_find_splits(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int64_t la, int64_t lb,
+                   const int64_t* diags, int64_t nd, int64_t* out_a, void* stream) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  if (key_bytes != 4 && key_bytes != 8) return fail(PM_ERR_ARG, "key_bytes must be 4 or 8");
+  if (la < 0 || lb < 0 || nd < 0 || (nd && (!diags || !out_a)) || (la && !a) || (lb && !b))
+    return fail(PM_ERR_ARG, "bad find_splits arguments");
+  if (nd == 0) return PM_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int grid = (int)std::min<int64_t>((nd * 32 + 255) / 256, (int64_t)ctx->num_sms * 8);
+  cudaError_t e = key_bytes == 4 ? launch_find_splits<int32_t>(a, b, la, lb, diags, nd, out_a, grid, st)
+                                 : launch_find_splits<int64_t>(a, b, la, lb, diags, nd, out_a, grid, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_find_splits launch");
+  return PM_OK;
+}
+
+int pm_plan_intervals(pm_ctx* ctx, const void* keys, int key_bytes, int64_t start, int64_t middle, int64_t end,
+                      int32_t threads, int64_t* nodes, void* stream) {
+  int rc = check_common(ctx, keys, key_bytes, nullptr, 0);
+  if (rc) return rc;
+  if (threads < 1 || (threads & (threads - 1)))  // soptmov.py:87-90
+    return fail(PM_ERR_ARG, "worker count must be a power of two >= 1");
+  if (!(0 <= start && start <= middle && middle <= end) || !nodes) return fail(PM_ERR_ARG, "bad plan arguments");
+  int32_t levels = 0;
+  while ((1 << (levels + 1)) <= threads) ++levels;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = key_bytes == 4 ? launch_plan_intervals<int32_t>(keys, start, middle, end, levels, nodes, st)
+                                 : launch_plan_intervals<int64_t>(keys, start, middle, end, levels, nodes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_plan_intervals launch");
+  return PM_OK;
+}
+
+int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  PM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  Ctl h;
+  PM_CUDA(cudaMemcpy(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (stats)
+    for (int i = 0; i < 4; ++i) stats[i] = h.stats[i];
+  if (h.err != 0) {
+    int32_t zero = 0;
+    cudaMemcpy(&ctx->ctl->err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+    const char* what = h.err == PM_ERR_TIMEOUT   ? "device wait exceeded its bound"
+                       : h.err == PM_ERR_NOSPACE ? "salvage space exhausted"
+                                                 : "device invariant violated";
+    return fail(h.err, std::string("merge engine: ") + what);
+  }
+  return PM_OK;
+}
+
+int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_host, int64_t width, int64_t start,
+                  int64_t middle, int64_t end, void* stream) {
+  if (!ctx || !keys_host || (key_bytes != 4 && key_bytes != 8) || width < 0 || (width && !payload_host))
+    return fail(PM_ERR_ARG, "bad pm_merge_host arguments");
+  if (!(0 <= start && start <= middle && middle <= end)) return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = end - start;
+  const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)(n * width);
+  int rc;
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    rc = ensure(&ctx->stage, &ctx->stage_bytes, kb + pb + 256);
+  }
+  if (rc) return rc;
+  char* dk = static_cast<char*>(ctx->stage);
+  char* dp = dk + kb;
+  char* hk = static_cast<char*>(keys_host) + start * key_bytes;
+  char* hp = width ? static_cast<char*>(payload_host) + start * width : nullptr;
+  PM_CUDA(cudaMemcpyAsync(dk, hk, n * key_bytes, cudaMemcpyHostToDevice, st));
+  if (width) PM_CUDA(cudaMemcpyAsync(dp, hp, pb, cudaMemcpyHostToDevice, st));
+  rc = pm_merge(ctx, dk, key_bytes, width ? dp : nullptr, width, 0, middle - start, n, 0, stream);
+  if (rc) return rc;
+  PM_CUDA(cudaMemcpyAsync(hk, dk, n * key_bytes, cudaMemcpyDeviceToHost, st));
+  if (width) PM_CUDA(cudaMemcpyAsync(hp, dp, pb, cudaMemcpyDeviceToHost, st));
+  return pm_status(ctx, stream, nullptr);
+}
+
+}  // extern "C"

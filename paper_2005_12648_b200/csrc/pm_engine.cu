@@ -1,0 +1,558 @@
+// pm_engine.cu -- plan + in-place merge/rotation engine kernels (sm_100a).
+//
+// k_plan   : stable merge-path splits at every region diagonal (one warp per
+//            split, 33-ary search with warp ballots) + workspace reset.
+// k_engine : persistent kernel; each CTA repeatedly takes a ticket, gathers the
+//            region's A/B ranges into shared memory with TMA bulk copies,
+//            salvages still-needed units out of the region's slots, merges in
+//            shared memory and streams the region back in place.
+//
+// Reference behaviour being reproduced (bit-exact): the stable merge of
+// seq_merge_buffered (seqmerge.py:55-75 / _kernels.py:227-313, A wins ties)
+// and the block exchange of linear_shift / circular_shift (_kernels.py:92-197).
+#include <cuda_runtime.h>
+
+#include "pm_common.cuh"
+#include "pm_engine.cuh"
+#include "pm_search.cuh"
+
+namespace pm {
+
+// ============================================================================
+// geometry helpers (all indices int64; "local" = relative to the job)
+// ============================================================================
+struct Geo {
+  const EngineParams& P;
+  __device__ explicit Geo(const EngineParams& p) : P(p) {}
+  __device__ int64_t LA() const { return P.m - P.s; }
+  __device__ int64_t LB() const { return P.e - P.m; }
+  __device__ int64_t N() const { return P.e - P.s; }
+  // slot j (local) -> absolute element range (clipped to the job)
+  __device__ int64_t slot_lo(int64_t j) const { return max(P.s, (P.k0 + j) * P.T); }
+  __device__ int64_t slot_hi(int64_t j) const { return min(P.e, (P.k0 + j + 1) * P.T); }
+  __device__ int64_t slot_base(int64_t j) const { return (P.k0 + j) * P.T; }  // unclipped
+  __device__ bool slot_full(int64_t j) const { return slot_hi(j) - slot_lo(j) == P.T; }
+  __device__ int64_t region_of_slot(int64_t j) const { return (P.k0 + j) / P.mu - P.R0; }
+  __device__ int64_t region_first_slot(int64_t q) const { return max((int64_t)0, (P.R0 + q) * P.mu - P.k0); }
+  __device__ int64_t region_end_slot(int64_t q) const { return min(P.K, (P.R0 + q + 1) * P.mu - P.k0); }
+  // local output diagonal at the start of region q (q in [0, Q])
+  __device__ int64_t diag(int64_t q) const {
+    if (q <= 0) return 0;
+    if (q >= P.Q) return N();
+    return (P.R0 + q) * P.M - P.s;
+  }
+  // ---- two-front ticket order around the centre region qc ----
+  __device__ int64_t nleft() const { return P.qc; }
+  __device__ int64_t nright() const { return P.Q - 1 - P.qc; }
+  __device__ int64_t region_of_ticket(int64_t t) const {
+    if (t == 0) return P.qc;
+    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr);
+    if (t <= 2 * m2) return (t & 1) ? P.qc - (t + 1) / 2 : P.qc + t / 2;
+    return nl > nr ? P.qc - (t - nr) : P.qc + (t - nl);
+  }
+  __device__ int64_t order(int64_t q) const {
+    if (q == P.qc) return 0;
+    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr);
+    if (q < P.qc) {
+      int64_t i = P.qc - q;
+      return i <= m2 ? 2 * i - 1 : i + nr;
+    }
+    int64_t i = q - P.qc;
+    return i <= m2 ? 2 * i : i + nl;
+  }
+  // regions with order <= t form the window [qc - nl(t), qc + nr(t)]
+  __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const {
+    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr), a, b;
+    if (t <= 2 * m2) {
+      a = (t + 1) / 2;
+      b = t / 2;
+    } else if (nl > nr) {
+      a = t - nr;
+      b = nr;
+    } else {
+      a = nl;
+      b = t - nl;
+    }
+    lo = P.qc - min(a, nl);
+    hi = P.qc + min(b, nr);
+  }
+  // records of unit j consumed by the regions of the ticket window <= t
+  __device__ int64_t consumed_by_window(int64_t j, int64_t t) const {
+    int64_t wl, wr;
+    window(t, wl, wr);
+    int64_t a_lo = P.split_a[wl], a_hi = P.split_a[wr + 1];
+    int64_t b_lo = diag(wl) - a_lo, b_hi = diag(wr + 1) - a_hi;
+    int64_t x0 = slot_lo(j), x1 = slot_hi(j), c = 0;
+    // A part of the unit, A-local indices
+    int64_t ua0 = x0 - P.s, ua1 = min(x1, P.m) - P.s;
+    if (ua1 > ua0) c += max((int64_t)0, min(ua1, a_hi) - max(ua0, a_lo));
+    int64_t ub0 = max(x0, P.m) - P.m, ub1 = x1 - P.m;
+    if (ub1 > ub0) c += max((int64_t)0, min(ub1, b_hi) - max(ub0, b_lo));
+    return c;
+  }
+};
+
+// ============================================================================
+// lock-free stacks of free slots / scratch units (Treiber stack, ABA tag)
+// ============================================================================
+__device__ __forceinline__ void stack_push(unsigned long long* top, int32_t* next, int32_t idx) {
+  unsigned long long old = *(volatile unsigned long long*)top, nw;
+  do {
+    next[idx] = (int32_t)(uint32_t)(old & 0xFFFFFFFFull);
+    __threadfence();
+    nw = (((old >> 32) + 1ull) << 32) | (uint32_t)idx;
+    unsigned long long seen = atomicCAS(top, old, nw);
+    if (seen == old) break;
+    old = seen;
+  } while (true);
+}
+__device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* next) {
+  unsigned long long old = *(volatile unsigned long long*)top;
+  while (true) {
+    uint32_t idx = (uint32_t)(old & 0xFFFFFFFFull);
+    if (idx == kEmpty32) return -1;
+    int32_t nxt = *(volatile int32_t*)&next[idx];
+    unsigned long long nw = (((old >> 32) + 1ull) << 32) | (uint32_t)nxt;
+    unsigned long long seen = atomicCAS(top, old, nw);
+    if (seen == old) {
+      __threadfence();
+      return (int32_t)idx;
+    }
+    old = seen;
+  }
+}
+
+// ============================================================================
+// k_plan: merge-path splits + workspace reset
+// ============================================================================
+template <typename KT>
+__global__ void k_plan(EngineParams P) {
+  Geo g(P);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const KT* keys = reinterpret_cast<const KT*>(P.keys);
+  const int64_t la = g.LA(), lb = g.LB();
+  for (int64_t q = warp; q <= P.Q; q += nwarps) {
+    int64_t d = g.diag(q), a;
+    if (P.mode == MODE_MERGE) {
+      a = merge_path_warp<KT>(keys + P.s, la, keys + P.m, lb, d, lane);
+    } else {  // rotation: outputs are B then A
+      a = d - lb;
+      a = a < 0 ? 0 : (a > la ? la : a);
+    }
+    if (lane == 0) P.split_a[q] = a;
+  }
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j < P.K; j += nthr) {
+    P.state[j] = (int32_t)j;
+    P.loc[j] = (int32_t)j;
+    P.reads[j] = 0;
+  }
+  for (int64_t i = tid; i < P.S; i += nthr) P.next_scr[i] = (i + 1 < P.S) ? (int32_t)(i + 1) : (int32_t)kEmpty32;
+  if (tid == 0) {
+    *P.free_top = (unsigned long long)kEmpty32;
+    *P.scr_top = P.S > 0 ? 0ull : (unsigned long long)kEmpty32;
+    *P.scr_count = (int32_t)P.S;
+    *P.ticket = 0;
+    bool nothing = (la == 0 || lb == 0);
+    if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
+    *P.noop = nothing ? 1 : 0;
+    for (int i = 0; i < 4; ++i) P.stats[i] = 0;
+  }
+}
+
+// ============================================================================
+// k_engine
+// ============================================================================
+struct SmemCtl {
+  uint64_t bar;
+  int64_t tk;
+  int32_t occ[16];
+  int32_t occ_dest[16];
+};
+
+// byte copy global -> shared with identical 16-byte phase; bulk for the body
+__device__ __forceinline__ uint32_t copy_g2s_phased(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar) {
+  if (nbytes <= 0) return 0;
+  int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+  if (head > nbytes) head = nbytes;
+  for (int64_t b = 0; b < head; ++b) dst[b] = src[b];
+  int64_t body = ((nbytes - head) >> 4) << 4;
+  uint32_t tx = 0;
+  if (body > 0) {
+    mbar_expect_tx(bar, (uint32_t)body);
+    bulk_g2s(dst + head, src + head, (uint32_t)body, bar);
+    tx = (uint32_t)body;
+  }
+  for (int64_t b = head + body; b < nbytes; ++b) dst[b] = src[b];
+  return tx;
+}
+
+// warp copy global -> global, identical 16-byte phase on both sides
+__device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, int64_t nbytes, int lane) {
+  if (nbytes <= 0) return;
+  int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+  if (head > nbytes) head = nbytes;
+  if (lane < head) dst[lane] = src[lane];
+  int64_t nvec = (nbytes - head) >> 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  int64_t i = lane;
+  for (; i + 96 < nvec; i += 128) {
+    uint4 v0 = s4[i], v1 = s4[i + 32], v2 = s4[i + 64], v3 = s4[i + 96];
+    d4[i] = v0;
+    d4[i + 32] = v1;
+    d4[i + 64] = v2;
+    d4[i + 96] = v3;
+  }
+  for (; i < nvec; i += 32) d4[i] = s4[i];
+  int64_t tail0 = head + (nvec << 4);
+  if (tail0 + lane < nbytes) dst[tail0 + lane] = src[tail0 + lane];
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256) k_engine(EngineParams P) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  __shared__ SmemCtl ctl;
+  Geo g(P);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int NT = blockDim.x;
+  const int64_t ks = sizeof(KT);
+  const int64_t w = P.w;
+  if (*(volatile int32_t*)P.noop) return;
+
+  uint8_t* kin = dyn;                         // staged keys (A then B, phase-shifted)
+  uint8_t* pin = dyn + P.smem_keys;           // staged payload
+  int32_t* src = reinterpret_cast<int32_t*>(dyn + P.smem_keys + P.smem_pay);  // padded output->input map
+  if (tid == 0) mbar_init(&ctl.bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  const int64_t la = g.LA();
+
+  while (true) {
+    if (tid == 0) {
+      int32_t t = atomicAdd(P.ticket, 1);
+      ctl.tk = (*(volatile int32_t*)P.err) ? P.Q : t;
+    }
+    __syncthreads();
+    const int64_t t = ctl.tk;
+    if (t >= P.Q) break;
+    const int64_t q = g.region_of_ticket(t);
+    const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
+    const int nslot = (int)(j1 - j0);
+    if (tid < nslot) ctl.occ[tid] = atomicExch(&P.state[j0 + tid], ST_CLOSED);
+    const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+    const int64_t a0 = P.split_a[q], a1 = P.split_a[q + 1];
+    const int64_t b0 = d0 - a0, b1 = d1 - a1;
+    const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
+    const bool identity =
+        P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+    __syncthreads();
+    if (identity) {
+      if (tid == 0) atomicAdd(&P.stats[3], 1ull);
+      continue;  // inputs already sit on their outputs; units consumed by q only
+    }
+    // ---------------- phase 1: gather A[a0,a1) and B[b0,b1) ----------------
+    // smem layout: A keys at kin+offA (phase of A[a0]), B keys at kin+offB
+    const int64_t xa = P.s + a0, xb = P.m + b0;  // absolute first elements
+    const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+    const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+    int64_t poffA = 0, poffB = 0;
+    if (w) {
+      poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+      poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+    }
+    {
+      const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
+      const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
+      const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
+      for (int p = tid; p < np; p += NT) {
+        const bool isA = p < npa;
+        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+        // wait until the unit sits in a region that will not move it before we read
+        int32_t l;
+        for (uint32_t it = 0;; ++it) {
+          l = ld_acquire(&P.loc[j]);
+          if (l < 0 || g.order(g.region_of_slot(l)) >= t) break;
+          if (ld_relaxed(P.err)) break;
+          if (it > kSpinLimit) {
+            raise_error(P.err, PM_ERR_TIMEOUT);
+            break;
+          }
+          backoff(it);
+        }
+        // source address of element x of unit j at its current location
+        const int64_t home = g.slot_base(j);
+        const char* ksrc;
+        const uint8_t* psrc;
+        if (l >= 0) {
+          const int64_t base = g.slot_base(l);
+          ksrc = P.keys + (base + (x0 - home)) * ks;
+          psrc = P.pay + (base + (x0 - home)) * w;
+        } else {
+          const int64_t si = -(int64_t)l - 1;
+          ksrc = P.scr_keys + (si * P.T + (x0 - home)) * ks;
+          psrc = P.scr_pay + (si * P.T + (x0 - home)) * w;
+        }
+        uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
+        copy_g2s_phased(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+        if (w) {
+          uint8_t* pdst = pin + (isA ? poffA + (x0 - xa) * w : poffB + (x0 - xb) * w);
+          copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
+        }
+      }
+      __syncthreads();  // every expect_tx registered before the single arrive
+      if (tid == 0) mbar_arrive(&ctl.bar);
+      for (uint32_t it = 0; !mbar_try_wait(&ctl.bar, phase); ++it) {
+      }
+      phase ^= 1;
+      __syncthreads();
+      // publish the reads; the last consumer of a unit frees its location
+      for (int p = tid; p < np; p += NT) {
+        const bool isA = p < npa;
+        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+        __threadfence();
+        const int32_t n = (int32_t)(x1 - x0);
+        const int32_t old = atomicAdd(&P.reads[j], n);
+        if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
+          const int32_t l = ld_acquire(&P.loc[j]);
+          if (l < 0) {
+            stack_push(P.scr_top, P.next_scr, -l - 1);
+            atomicAdd(P.scr_count, 1);
+          } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
+            stack_push(P.free_top, P.next_free, l);
+          }
+        }
+      }
+    }
+    // ---------------- phase 2: salvage still-needed occupants ---------------
+    if (wid < nslot) {
+      const int32_t u = ctl.occ[wid];
+      int32_t dest = 0;
+      int alive = 0;
+      if (u >= 0) {
+        if (lane == 0) {
+          const int32_t slot = (int32_t)(j0 + wid);
+          for (uint32_t it = 0; ld_acquire(&P.loc[u]) != slot; ++it) {  // salvaged-in unit may still be landing
+            if (ld_relaxed(P.err)) break;
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              break;
+            }
+            backoff(it);
+          }
+          const int32_t thr = (int32_t)g.consumed_by_window(u, t);
+          int32_t r;
+          for (uint32_t it = 0; (r = ld_acquire(&P.reads[u])) < thr; ++it) {
+            if (ld_relaxed(P.err)) break;
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              break;
+            }
+            backoff(it);
+          }
+          const int32_t usz = (int32_t)(g.slot_hi(u) - g.slot_lo(u));
+          alive = r < usz && !ld_relaxed(P.err);
+          if (alive) {
+            // destination: scratch while it is plentiful, then free slots, then the reserve
+            dest = INT32_MIN;
+            for (uint32_t it = 0;; ++it) {
+              if (ld_relaxed(P.scr_count) > P.reserve) {
+                int32_t si = stack_pop(P.scr_top, P.next_scr);
+                if (si >= 0) {
+                  atomicSub(P.scr_count, 1);
+                  dest = -si - 1;
+                  break;
+                }
+              }
+              int32_t f = stack_pop(P.free_top, P.next_free);
+              if (f >= 0) {
+                if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) {
+                  dest = f;
+                  break;
+                }
+                continue;  // slot got closed by its region; drop it
+              }
+              int32_t si = stack_pop(P.scr_top, P.next_scr);
+              if (si >= 0) {
+                atomicSub(P.scr_count, 1);
+                dest = -si - 1;
+                break;
+              }
+              if (ld_relaxed(P.err)) break;
+              if (it > kSpinLimit) {
+                raise_error(P.err, PM_ERR_NOSPACE);
+                break;
+              }
+              backoff(it);
+            }
+            if (dest == INT32_MIN) alive = 0;
+          }
+        }
+        alive = __shfl_sync(0xffffffffu, alive, 0);
+        dest = __shfl_sync(0xffffffffu, dest, 0);
+        if (alive) {
+          const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), home = g.slot_base(u);
+          const int64_t sbase = g.slot_base(j0 + wid);
+          char* kd;
+          uint8_t* pd;
+          if (dest >= 0) {
+            kd = P.keys + (g.slot_base(dest) + (x0 - home)) * ks;
+            pd = P.pay + (g.slot_base(dest) + (x0 - home)) * w;
+          } else {
+            const int64_t si = -(int64_t)dest - 1;
+            kd = P.scr_keys + (si * P.T + (x0 - home)) * ks;
+            pd = P.scr_pay + (si * P.T + (x0 - home)) * w;
+          }
+          copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
+                        reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - home)) * ks), (x1 - x0) * ks,
+                        lane);
+          if (w) copy_g2g_warp(pd, P.pay + (sbase + (x0 - home)) * w, (x1 - x0) * w, lane);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            st_release(&P.loc[u], dest);
+            atomicAdd(&P.stats[0], 1ull);
+            atomicAdd(&P.stats[1], (unsigned long long)(x1 - x0));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (ld_relaxed(P.err)) break;
+    // ---------------- phase 3: merge in shared memory -----------------------
+    const KT* As = reinterpret_cast<const KT*>(kin + offA);
+    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+    const int64_t E = (nout + NT - 1) / NT;
+    // output o is staged at padded index P(o + ph) so strided writes avoid bank conflicts
+    const int64_t V = 16 / ks;                                   // keys per 16-byte vector
+    const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
+    {
+      int64_t o = min((int64_t)tid * E, nout), oe = min(o + E, nout);
+      if (P.mode == MODE_MERGE) {
+        // merge-path split of this thread's diagonal (A wins ties)
+        int64_t lo = o > beta ? o - beta : 0, hi = o < alpha ? o : alpha;
+        while (lo < hi) {
+          int64_t mid = (lo + hi) >> 1;
+          if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+          else hi = mid;
+        }
+        int64_t i = lo, jb = o - lo;
+        KT va = i < alpha ? As[i] : KT(0), vb = jb < beta ? Bs[jb] : KT(0);
+        for (; o < oe; ++o) {
+          const bool takeA = jb >= beta || (i < alpha && va <= vb);
+          const int64_t op = o + ph;
+          src[op + (op >> 5)] = takeA ? (int32_t)i : (int32_t)(alpha + jb);
+          if (takeA) {
+            ++i;
+            if (i < alpha) va = As[i];
+          } else {
+            ++jb;
+            if (jb < beta) vb = Bs[jb];
+          }
+        }
+      } else {  // rotation: B piece then A piece
+        for (; o < oe; ++o) {
+          const int64_t op = o + ph;
+          src[op + (op >> 5)] = o < beta ? (int32_t)(alpha + o) : (int32_t)(o - beta);
+        }
+      }
+    }
+    __syncthreads();
+    // ---------------- phase 4: stream the region back in place --------------
+    {
+      KT* kout = reinterpret_cast<KT*>(P.keys) + (P.s + d0) - ph;  // 16B aligned when keys base is
+      const int64_t ngroups = (ph + nout + V - 1) / V;
+      const bool kal = (((uintptr_t)kout) & 15) == 0;
+      for (int64_t gi = tid; gi < ngroups; gi += NT) {
+        const int64_t op0 = gi * V;
+        KT v[4];
+        bool full = kal;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k < V) {
+            const int64_t op = op0 + k, o = op - ph;
+            if (o >= 0 && o < nout) {
+              const int32_t si = src[op + (op >> 5)];
+              v[k] = si < alpha ? As[si] : Bs[si - alpha];
+            } else {
+              full = false;
+            }
+          }
+        }
+        if (full) {
+          if constexpr (sizeof(KT) == 4) {
+            *reinterpret_cast<int4*>(kout + op0) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+          } else {
+            *reinterpret_cast<longlong2*>(kout + op0) = make_longlong2((long long)v[0], (long long)v[1]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k < V) {
+              const int64_t op = op0 + k, o = op - ph;
+              if (o >= 0 && o < nout) kout[op] = v[k];
+            }
+          }
+        }
+      }
+      if (w) {
+        uint8_t* pout = P.pay + (P.s + d0) * w;
+        const uint8_t* PA = pin + poffA;
+        const uint8_t* PB = pin + poffB;
+        if ((w & 3) == 0 && (((uintptr_t)pout | poffA | poffB) & 3) == 0) {
+          const int64_t wq = w >> 2;
+          for (int64_t o = tid; o < nout; o += NT) {
+            const int64_t op = o + ph;
+            const int32_t si = src[op + (op >> 5)];
+            const uint32_t* rs = reinterpret_cast<const uint32_t*>(si < alpha ? PA + si * w : PB + (si - alpha) * w);
+            uint32_t* rd = reinterpret_cast<uint32_t*>(pout + o * w);
+            for (int64_t c = 0; c < wq; ++c) rd[c] = rs[c];
+          }
+        } else {
+          for (int64_t o = tid; o < nout; o += NT) {
+            const int64_t op = o + ph;
+            const int32_t si = src[op + (op >> 5)];
+            const uint8_t* rs = si < alpha ? PA + si * w : PB + (si - alpha) * w;
+            uint8_t* rd = pout + o * w;
+            for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+          }
+        }
+      }
+    }
+    if (tid == 0) atomicAdd(&P.stats[2], 1ull);
+    __syncthreads();
+  }
+}
+
+// ---- host launchers (called from pm_capi.cu) --------------------------------
+template <typename KT>
+cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
+  k_plan<KT><<<grid, 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
+template <typename KT>
+cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+  k_engine<KT><<<grid, block, smem, st>>>(P);
+  return cudaGetLastError();
+}
+template <typename KT>
+cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_engine<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_engine<KT>, block, smem);
+}
+template cudaError_t launch_plan<int32_t>(const EngineParams&, int, cudaStream_t);
+template cudaError_t launch_plan<int64_t>(const EngineParams&, int, cudaStream_t);
+template cudaError_t launch_engine<int32_t>(const EngineParams&, int, int, size_t, cudaStream_t);
+template cudaError_t launch_engine<int64_t>(const EngineParams&, int, int, size_t, cudaStream_t);
+template cudaError_t engine_occupancy<int32_t>(int, size_t, int*);
+template cudaError_t engine_occupancy<int64_t>(int, size_t, int*);
+
+}  // namespace pm

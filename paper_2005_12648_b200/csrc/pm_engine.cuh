@@ -1,0 +1,63 @@
+// pm_engine.cuh -- the in-place merge/rotation engine (shared declarations).
+//
+// One persistent kernel realises, on the caller's buffer and with bounded
+// scratch, either
+//   MODE_MERGE : the stable (A-first) merge of runs A=[s,m) and B=[m,e)
+//                -- the result of the reference's seq_merge_buffered /
+//                merge_srecpar at t=1 (seqmerge.py:55-75, srecpar.py:33-84),
+//   MODE_ROTATE: the block exchange A|B -> B|A of linear/circular shifting
+//                (shift.py:38-55, _kernels.py:92-197).
+// The output is cut into regions of M = mu*T records ("pairs"); region q's
+// inputs are the A and B ranges the stable merge path assigns to it.  The
+// array is also cut into slots of T records ("units").  Regions are processed
+// in ticket order (two fronts growing out of the A/B boundary).  A region
+// gathers its inputs from wherever their units currently live, merges them in
+// shared memory, and writes its slots.  A unit still needed by a later region
+// is first "salvaged" into a free slot (a slot whose unit is fully consumed)
+// or into the bounded scratch pool.  DESIGN.md section 3 has the protocol and
+// its progress/space argument.
+#pragma once
+#include <cstdint>
+
+namespace pm {
+
+enum : int32_t { MODE_MERGE = 0, MODE_ROTATE = 1 };
+enum : int32_t { ST_FREE = -1, ST_CLOSED = -2 };
+constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
+
+struct EngineParams {
+  char* keys;          // element x lives at keys + x*ks
+  uint8_t* pay;        // row x lives at pay + x*w (unused when w == 0)
+  int64_t w;           // payload bytes per record
+  int32_t ks;          // key bytes (4 or 8)
+  int32_t mode;
+  int64_t s, m, e;     // job, absolute element indices
+  int64_t T;           // unit (slot) size, records
+  int32_t mu;          // slots per region
+  int32_t nthreads;    // CTA size used by the launch
+  int64_t M;           // region size = mu*T
+  int64_t k0, K;       // first absolute slot, number of slots
+  int64_t R0, Q;       // first absolute region, number of regions
+  int64_t qc;          // centre region (local) for the two-front order
+  int64_t* split_a;    // [Q+1] A-count at each region diagonal
+  int32_t* state;      // [K] slot state: occupant unit, ST_FREE or ST_CLOSED
+  int32_t* loc;        // [K] unit location: slot index or -(scratch index + 1)
+  int32_t* reads;      // [K] records of the unit already gathered by consumers
+  int32_t* next_free;  // [K] free-slot stack links
+  int32_t* next_scr;   // [S] scratch stack links
+  unsigned long long* free_top;  // tagged stack tops (tag<<32 | index)
+  unsigned long long* scr_top;
+  int32_t* scr_count;  // free scratch units (heuristic only)
+  int64_t S;           // scratch units
+  int64_t reserve;     // keep this many scratch units for the no-free-slot case
+  char* scr_keys;      // phase-matched scratch bases
+  uint8_t* scr_pay;
+  int32_t* ticket;
+  int32_t* err;
+  int32_t* noop;       // set by the plan kernel when the job needs no work
+  unsigned long long* stats;  // [4]: salvaged units, salvaged records, regions, identity regions
+  size_t smem_keys;    // bytes reserved for staged keys
+  size_t smem_pay;     // bytes reserved for staged payload
+};
+
+}  // namespace pm

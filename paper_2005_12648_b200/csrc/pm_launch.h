@@ -1,0 +1,21 @@
+// pm_launch.h -- host launchers exported by pm_engine.cu / pm_plan.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pm_engine.cuh"
+
+namespace pm {
+template <typename KT> cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st);
+template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st);
+template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);
+template <typename KT>
+cudaError_t launch_find_median(const void* a, const void* b, int64_t la, int64_t lb, int64_t* out, cudaStream_t st);
+template <typename KT>
+cudaError_t launch_find_splits(const void* a, const void* b, int64_t la, int64_t lb, const int64_t* diags, int64_t nd,
+                               int64_t* out_a, int grid, cudaStream_t st);
+template <typename KT>
+cudaError_t launch_plan_intervals(const void* keys, int64_t s, int64_t m, int64_t e, int32_t levels, int64_t* nodes,
+                                  cudaStream_t st);
+}  // namespace pm

@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's own outputs.
+
+Bit-exact for every case: keys AND payload bytes (stable order of equal keys).
+Golden fixtures come from the reference itself (tests/golden/make_golden.py);
+random cases are checked against the pinned CPU oracle (oracle/), which
+restates the reference's stable merge (_kernels.py:227-313).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+from gen import config_input, random_instance
+from oracle import oracle as orc
+
+pm = pytest.importorskip("paper_2005_12648_b200")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def to_gpu(keys, payload):
+    return pm.KeyedArray(torch.from_numpy(np.ascontiguousarray(keys)).cuda(),
+                         torch.from_numpy(np.ascontiguousarray(payload)).cuda())
+
+
+def assert_same(arr, keys, payload, what=""):
+    k, p = arr.numpy()
+    assert np.array_equal(k, keys), f"keys differ {what}: first bad index {np.flatnonzero(k != keys)[:5]}"
+    assert np.array_equal(p, payload), f"payload differs {what}"
+
+
+@pytest.mark.parametrize("name", ["merge_i32.npz", "merge_i64.npz"])
+@pytest.mark.parametrize("method", ["buffered", "rotation", "srecpar", "soptmov"])
+def test_golden_merges(name, method):
+    for c in golden_io.merge_cases(name):
+        s, m, e = (int(x) for x in c["job"])
+        arr = to_gpu(c["keys"], c["payload"])
+        job = pm.MergeJob(s, m, e)
+        if method == "buffered":
+            pm.seq_merge_buffered(arr, job)
+        elif method == "rotation":
+            pm.seq_merge_rotation(arr, job)
+        elif method == "srecpar":
+            pm.merge_srecpar(arr, job, 8)
+        else:
+            pm.merge_soptmov(arr, job, 4)
+        assert_same(arr, c["out_keys"], c["out_payload"], f"{name} {method} job={s,m,e}")
+
+
+def test_golden_reference_parallel_keys():
+    # the reference's own t>1 strategies: identical keys (their payload order is unstable)
+    for c in golden_io.merge_cases("merge_i32.npz"):
+        s, m, e = (int(x) for x in c["job"])
+        arr = to_gpu(c["keys"], c["payload"])
+        pm.merge_srecpar(arr, pm.MergeJob(s, m, e), 8, size_limit=2)
+        assert np.array_equal(arr.keys.cpu().numpy(), c["srecpar_keys"])
+        assert np.array_equal(arr.keys.cpu().numpy(), c["soptmov_keys"])
+
+
+def test_golden_find_median():
+    cases = list(golden_io.median_cases())
+    for a, b, piv in cases[::3]:
+        assert tuple(pm.find_median(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())) == piv
+
+
+def test_golden_shifts():
+    for c in golden_io.shift_cases():
+        la, lb = (int(x) for x in c["len"])
+        for fn in (pm.linear_shift, pm.circular_shift):
+            arr = to_gpu(c["keys"], c["payload"])
+            fn(arr, la, lb)
+            assert_same(arr, c["out_keys"], c["out_payload"], f"shift {la},{lb}")
+
+
+def test_golden_plans_and_traces():
+    for c in list(golden_io.plan_cases())[::2]:
+        s, m, e, t = (int(x) for x in c["job"])
+        arr = to_gpu(c["keys"], c["payload"])
+        job = pm.MergeJob(s, m, e)
+        plan = pm.plan_intervals(arr, job, t)
+        assert np.array_equal(np.array(plan.leaf_sources, np.int64).reshape(-1, 2), c["sources"])
+        fin = np.array([(j.start, j.middle, j.end) for j in plan.final_positions], np.int64).reshape(-1, 3)
+        assert np.array_equal(fin, c["finals"])
+        trace = pm.division_trace(arr, job, t, size_limit=2)
+        got = np.array([(r.level, r.split_index, r.pivots[0], r.pivots[1], r.shift_start, r.shift_len_a,
+                         r.shift_len_b) for r in trace.records], np.int64).reshape(-1, 7)
+        assert np.array_equal(got, c["trace_pivots"])
+        assert sha(*trace.divided.numpy()) == str(c["divided_sha"])
+        # reorder_multi realises the same layout
+        work = arr.copy()
+        if t > 1 and len(work) and int(c["keys"].max()) < 2**30:
+            pm.reorder_multi(work, plan, pm.derive_marker(work, s, e))
+            gathered_k = np.concatenate([c["keys"][a:a + n] for a, n in plan.leaf_sources])
+            gathered_p = np.concatenate([c["payload"][a:a + n] for a, n in plan.leaf_sources])
+            assert_same(work, gathered_k, gathered_p, "reorder_multi")
+
+
+@pytest.mark.parametrize("width", [0, 4, 8, 12, 3])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_random_vs_oracle(width, dtype):
+    rng = np.random.default_rng(1000 + width + (7 if dtype == np.int64 else 0))
+    sizes = [0, 1, 2, 17, 255, 4096, 8191, 8192, 8193, 40000, 150000, 1 << 20]
+    for size in sizes:
+        for domain in (3, 1000, 2**31 - 1):
+            split = float(rng.choice([0.0, 0.05, 0.25, 0.5, 0.75, 0.97, 1.0, rng.random()]))
+            keys, payload, middle = random_instance(rng, size, split, domain, width)
+            keys = keys.astype(dtype)
+            if dtype == np.int64 and domain > 1000:
+                keys = keys * np.int64(2**31) + rng.integers(0, 2**31, size)
+                keys[:middle].sort()
+                keys[middle:].sort()
+            lo = int(rng.integers(0, 40))
+            hi = int(rng.integers(0, 40))
+            kk = np.concatenate([np.full(lo, -5, dtype), keys, np.full(hi, -7, dtype)])
+            pp = np.concatenate([np.full((lo, width), 1, np.uint8), payload, np.full((hi, width), 2, np.uint8)])
+            want_k, want_p = kk.copy(), pp.copy()
+            orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
+            arr = to_gpu(kk, pp)
+            pm.merge_srecpar(arr, pm.MergeJob(lo, lo + middle, lo + size), 8)
+            assert_same(arr, want_k, want_p, f"size={size} dom={domain} split={split} w={width}")
+
+
+def test_shift_random_sizes():
+    rng = np.random.default_rng(77)
+    for la, lb in [(1, 1 << 20), (1 << 20, 1), (100000, 33333), (8192, 8192), (5, 7), (123457, 654321)]:
+        for width in (0, 4, 9):
+            keys = rng.integers(-1000, 1000, la + lb).astype(np.int32)
+            payload = rng.integers(0, 256, (la + lb, width), dtype=np.uint8)
+            want_k, want_p = orc.rotate_oracle(keys, payload, la)
+            arr = to_gpu(keys, payload)
+            pm.linear_shift(arr, la, lb)
+            assert_same(arr, want_k, want_p, f"shift {la},{lb},w={width}")
+
+
+def test_config1_matches_reference_checksum():
+    g = golden_io.big()
+    keys, payload, middle = config_input(1, seed=0)
+    assert sha(keys) == g["cfg1_in"]
+    arr = to_gpu(keys, payload)
+    pm.merge_srecpar(arr, pm.MergeJob(0, middle, len(keys)), 8)
+    assert sha(arr.keys.cpu().numpy()) == g["cfg1_out"]
+
+
+def test_config4_reduced_matches_reference_checksum():
+    g = golden_io.big()
+    keys, payload, middle = config_input(4, seed=0, log_len=18)
+    arr = to_gpu(keys, payload)
+    pm.merge_srecpar(arr, pm.MergeJob(0, middle, len(keys)), 8)
+    assert sha(*arr.numpy()) == g["cfg4s_out"]
+
+
+def test_config3_reduced_matches_reference_checksum():
+    g = golden_io.big()
+    keys, payload, middle = config_input(3, seed=0, log_len=20, log_len_b=12)
+    arr = to_gpu(keys, payload)
+    pm.merge_srecpar(arr, pm.MergeJob(0, middle, len(keys)), 8)
+    assert sha(arr.keys.cpu().numpy()) == g["cfg3s_out"]
+
+
+def _device_stable_check(arr, keys_in_sorted_ref=None):
+    k = arr.keys
+    assert bool(torch.all(k[1:] >= k[:-1]).item())
+
+
+@pytest.mark.parametrize("cfg,log_len", [(2, 24), (4, 24), (3, 26)])
+def test_full_size_properties(cfg, log_len):
+    """Size-independent properties at large sizes: sorted, multiset kept, stable payload."""
+    from paper_2005_12648_b200.workloads import config_input_device
+
+    kw = {"log_len_b": 16} if cfg == 3 else {}
+    keys, payload, middle = config_input_device(cfg, seed=3, log_len=log_len, **kw)
+    ref_sorted = torch.sort(keys.to(torch.int64), stable=True)
+    arr = pm.KeyedArray(keys.clone(), payload.clone())
+    pm.merge_srecpar(arr, pm.MergeJob(0, middle, len(keys)), 8)
+    assert torch.equal(arr.keys.to(torch.int64), ref_sorted.values)
+    if cfg == 4:  # payload = original index: stable merge == stable argsort
+        idx = arr.payload.contiguous().view(torch.int32).view(-1).to(torch.int64)
+        assert torch.equal(idx, ref_sorted.indices)
+
+
+def test_error_behaviour():
+    arr = pm.KeyedArray(torch.tensor([2, 1], dtype=torch.int32).cuda())
+    with pytest.raises(ValueError):
+        pm.merge_srecpar(arr, pm.MergeJob(0, 1, 2), 3)
+    with pytest.raises(IndexError):
+        pm.seq_merge_rotation(arr, pm.MergeJob(0, 1, 5))
+    with pytest.raises(ValueError):
+        pm.linear_shift(arr, 1, 2)
+    with pytest.raises(pm.MarkerOverflow):
+        big = pm.KeyedArray(np.array([pm.KEY_MIN, 0, pm.KEY_MAX, pm.KEY_MIN + 1, 5], np.int32))
+        pm.merge_soptmov(big, pm.MergeJob(0, 3, 5), 2, strict_marker=True)
+
+
+def test_fast_path_untouched():
+    arr = pm.KeyedArray(np.array([1, 2, 3, 3, 4, 9], np.int32), np.arange(24, dtype=np.uint8).reshape(6, 4))
+    before = arr.copy()
+    pm.merge_soptmov(arr, pm.MergeJob(0, 4, 6), 4)
+    assert arr.equals(before)
