@@ -1,0 +1,375 @@
+"""Benchmark: in-place stable merge of two sorted runs on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], north-star point): int32 keys, L_A = L_B =
+2^29 uniform sorted runs (N = 2^30 records, 4 GiB > 126 MB L2), seeded
+synthetic data generated on the device.  A "step" is one in-place merge of one
+fresh copy of the input (restored from a pristine device copy outside the
+timed region).  ``value`` = merged records/s with inputs resident in HBM;
+``e2e`` = the same metric through the C-ABI host entry point (pm_merge_host:
+H2D + merge + D2H from pinned host memory).  ``roofline`` compares the engine
+kernel's algorithmic traffic (read + write every record once, 2*N*4 bytes)
+with the measured HBM copy peak in MEASURED_PEAKS.json.  ``cpu_baseline`` is the
+reference's fastest CPU path (merge_srecpar with buffered leaves, a C port in
+oracle/) timed on this host's cores on a bounded sample.
+
+Multi-GPU (torchrun, N>1): every rank merges its own replica-sized problem
+(weak scaling, no data-path collective); the distributed block merge lives in
+paper_2005_12648_b200/dist.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "merged elements/s and % of HBM roofline at 1/2/4/8 B200 vs CPU baseline"
+
+
+def log(msg):
+    if os.environ.get("BENCH_VERBOSE"):
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cfg", type=int, default=2, help="BASELINE config number (2: int32 uniform, 3: int64 skew, 4: KV dup)")
+    ap.add_argument("--log-len", type=int, default=None, help="log2 of the run length per side")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-log-len", type=int, default=24)
+    ap.add_argument("--quick", action="store_true", help="skip e2e/cpu/clock legs (profiling runs)")
+    return ap.parse_args()
+
+
+def workload_desc(cfg, log_len):
+    if cfg == 2:
+        return dict(workload=f"cfg2: int32 uniform sorted runs, L_A=L_B=2^{log_len}", key="int32",
+                    payload_bytes=0, L_A=1 << log_len, L_B=1 << log_len)
+    if cfg == 3:
+        return dict(workload=f"cfg3: int64 skew, L_A=2^{log_len}, L_B=2^16 in a narrow window", key="int64",
+                    payload_bytes=0, L_A=1 << log_len, L_B=1 << 16)
+    if cfg == 4:
+        return dict(workload=f"cfg4: int32 keys in [0,1024) + int32 index payload, L_A=L_B=2^{log_len}",
+                    key="int32", payload_bytes=4, L_A=1 << log_len, L_B=1 << log_len)
+    raise SystemExit(f"unsupported cfg {cfg}")
+
+
+def default_log_len(cfg):
+    return {2: 29, 3: 28, 4: 26}[cfg]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        under_load = [x for x in sm if x > 0.5 * (mx or max(sm))] or sm
+        return {"sm_mhz": statistics.median(under_load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def cpu_threads():
+    cores = len(os.sched_getaffinity(0))
+    t = 1
+    while t * 2 <= cores:
+        t *= 2
+    return cores, t
+
+
+def time_cpu_port(log_len, steps, seed=11, budget_s=None):
+    """merge_srecpar(t, leaf_core=seq_merge_buffered) C port on host threads; returns (elem/s, threads, desc)."""
+    import numpy as np
+
+    from oracle import oracle as orc
+    from paper_2005_12648_b200.workloads import config_input
+
+    cores, t = cpu_threads()
+    keys, payload, middle = config_input(2, seed=seed, log_len=log_len)
+    work = keys.copy()
+    times = []
+    deadline = time.perf_counter() + (budget_s or 1e9)
+    for i in range(steps + 1):
+        np.copyto(work, keys)
+        t0 = time.perf_counter()
+        orc.srecpar_buffered(work, None, 0, middle, len(work), t, size_limit=512)
+        dt = time.perf_counter() - t0
+        if i > 0:
+            times.append(dt)  # first rep discarded (bench.py:196-207 of the reference)
+        if time.perf_counter() > deadline and times:
+            break
+    assert bool(np.all(work[1:] >= work[:-1]))
+    rate = len(keys) / statistics.mean(times)
+    return rate, t, cores, (f"merge_srecpar(threads={t}, leaf_core=seq_merge_buffered) C port, int32 uniform "
+                            f"L_A=L_B=2^{log_len}, mean of {len(times)} reps after 1 warm-up")
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    log_len = 26 if args.cfg == 2 else 24
+    rate, t, cores, sample = time_cpu_port(log_len, max(args.steps, 1))
+    desc = workload_desc(args.cfg, args.log_len or default_log_len(args.cfg))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "elements/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": (1 << (log_len + 1)) / rate * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": dict(desc, parallelism=f"cpu threads={t}", sample=f"L_A=L_B=2^{log_len}"),
+        "cpu_baseline": {"value": rate, "unit": "elements/s", "cores": t, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_12648_b200 as pm
+    from paper_2005_12648_b200 import _capi, _ops
+    from paper_2005_12648_b200.workloads import config_input_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    log_len = args.log_len or default_log_len(args.cfg)
+    desc = workload_desc(args.cfg, log_len)
+    kw = {"log_len_b": 16} if args.cfg == 3 else {}
+    log("generating input")
+    keys0, pay0, middle = config_input_device(args.cfg, seed=1000 + rank, log_len=log_len, **kw)
+    n = keys0.numel()
+    ks = keys0.element_size()
+    w = pay0.shape[1]
+    arr = pm.KeyedArray(keys0.clone(), pay0.clone())
+    ctx = _capi.context(local)
+    L = _capi.lib()
+    stream = torch.cuda.current_stream()
+
+    def restore():
+        arr.keys.copy_(keys0)
+        if w:
+            arr.payload.copy_(pay0)
+
+    def merge_once():
+        rc = L.pm_merge(ctx, ctypes.c_void_p(arr.keys.data_ptr()), ks,
+                        ctypes.c_void_p(arr.payload.data_ptr() if w else 0), w, 0, middle, n, 0,
+                        ctypes.c_void_p(stream.cuda_stream))
+        _capi.check(rc, "pm_merge")
+
+    log("warm-up")
+    for _ in range(max(args.warmup, 1)):
+        restore()
+        merge_once()
+    stats = _capi.status(local, stream.cuda_stream)
+    # correctness of the warm-up result (size-independent property checks on device)
+    ref = torch.sort(keys0.to(torch.int64), stable=True)
+    ok = torch.equal(arr.keys.to(torch.int64), ref.values)
+    if args.cfg == 4:
+        ok = ok and torch.equal(arr.payload.contiguous().view(torch.int32).view(-1).to(torch.int64), ref.indices)
+    del ref
+    if not ok:
+        raise SystemExit("bench: merged output failed the sortedness/stability check")
+
+    log("timed steps")
+    _capi.check(L.pm_set_timing(ctx, 1), "pm_set_timing")
+    plan_ms, eng_ms, step_ms = [], [], []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pf, ef = ctypes.c_float(), ctypes.c_float()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if not args.quick else None
+    if sampler:
+        sampler.__enter__()
+    for _ in range(args.steps):
+        restore()  # outside the timed region (pristine input for every step)
+        ev0.record(stream)
+        merge_once()
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        _capi.check(L.pm_kernel_ms(ctx, ctypes.byref(pf), ctypes.byref(ef)), "pm_kernel_ms")
+        plan_ms.append(pf.value)
+        eng_ms.append(ef.value)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    if world > 1:
+        dist.barrier()
+    _capi.check(L.pm_set_timing(ctx, 0), "pm_set_timing")
+    stats = _capi.status(local, stream.cuda_stream)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n * world * args.steps / (total_ms / 1e3)
+    rec = ks + w
+    algo_bytes = 2 * n * rec
+    eng_avg = statistics.mean(eng_ms)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = algo_bytes / (eng_avg / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(desc["workload"])
+            traffic = tr.get("dram_bytes_per_launch") if tr else None
+    except (OSError, ValueError):
+        pass
+
+    # ---- end to end through the C-ABI host entry point (pinned host buffers) ----
+    e2e = None
+    log("e2e")
+    if rank == 0 and not args.quick and args.e2e_steps > 0:
+        try:
+            hk0 = keys0.cpu().pin_memory()
+            hk = torch.empty_like(hk0).pin_memory()
+            hp0 = pay0.cpu().pin_memory() if w else None
+            hp = torch.empty_like(hp0).pin_memory() if w else None
+            times = []
+            for i in range(args.e2e_steps + 1):
+                hk.copy_(hk0)
+                if w:
+                    hp.copy_(hp0)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                rc = L.pm_merge_host(ctx, ctypes.c_void_p(hk.data_ptr()), ks,
+                                     ctypes.c_void_p(hp.data_ptr() if w else 0), w, 0, middle, n,
+                                     ctypes.c_void_p(stream.cuda_stream))
+                _capi.check(rc, "pm_merge_host")
+                dt = time.perf_counter() - t0
+                if i > 0:
+                    times.append(dt)
+            assert bool(torch.all(hk[1:] >= hk[:-1]).item())
+            e2e = {"value": n / statistics.mean(times), "unit": "elements/s",
+                   "h2d_bytes_per_step": n * rec, "d2h_bytes_per_step": n * rec,
+                   "ms_per_step": statistics.mean(times) * 1e3, "path": "pm_merge_host (C-ABI, pinned host buffers)"}
+            del hk0, hk, hp0, hp
+        except (RuntimeError, torch.cuda.OutOfMemoryError) as ex:
+            e2e = {"value": None, "unit": "elements/s", "h2d_bytes_per_step": n * rec,
+                   "d2h_bytes_per_step": n * rec, "error": str(ex)[:200]}
+
+    cpu = None
+    log("cpu baseline")
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
+        rate, t, cores, sample = time_cpu_port(args.cpu_sample_log_len, 6, budget_s=20)
+        cpu = {"value": rate, "unit": "elements/s", "cores": t, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": desc["key"], "data": "synthetic",
+            "config": dict(desc, parallelism=("replicas" if world > 1 else "single-gpu"),
+                           l2="inputs (>=2 GiB) exceed the 126 MB L2; pristine copy restored outside the timed region"),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_engine",
+                         "algorithmic_bytes_per_launch": algo_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6650"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": 2 * args.steps,
+            "kernel_ms": {"plan": statistics.mean(plan_ms), "engine": eng_avg, "merge": total_ms / args.steps},
+            "merge_frac_of_roofline": (algo_bytes / (total_ms / args.steps / 1e3) / 1e9) / peak,
+            "salvaged_records_frac": stats[1] / n,
+            "regions": stats[2], "identity_regions": stats[3],
+        }
+        if sampler:
+            line["clocks"] = sampler.summary()
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if os.environ.get("BENCH_VERBOSE"):
+        import faulthandler
+
+        faulthandler.dump_traceback_later(int(os.environ.get("BENCH_DUMP_S", "120")), exit=True)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

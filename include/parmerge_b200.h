@@ -102,9 +102,11 @@ int pm_plan_intervals(pm_ctx *ctx, const void *keys, int key_bytes, int64_t star
 
 /*
  * Synchronise `stream`, then return (and clear) the sticky device status of the
- * context's last merges/shifts.  stats (host uint64[4], may be NULL) receives
- * the last job's counters: salvaged units, salvaged records, merged regions,
- * identity (skipped) regions.
+ * context's last merges/shifts.  stats (host uint64[16], may be NULL) receives
+ * the last job's counters: [0] salvaged units, [1] salvaged records, [2] merged
+ * regions, [3] identity (skipped) regions, [4..9] summed per-CTA cycles in the
+ * engine phases (ticket, gather issue, gather land, salvage, merge, store),
+ * [10..11] spin iterations in reader / occupant waits.
  */
 int pm_status(pm_ctx *ctx, void *stream, uint64_t *stats);
 

@@ -30,7 +30,7 @@ EXPORTED = (
 )
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 _ctx: dict[int, ctypes.c_void_p] = {}
 
 
@@ -99,6 +99,6 @@ def context(device: int) -> ctypes.c_void_p:
 
 def status(device: int, stream: int) -> tuple[int, int, int, int]:
     """Synchronise the stream and raise if the device reported an error."""
-    stats = (ctypes.c_uint64 * 4)()
+    stats = (ctypes.c_uint64 * 16)()
     check(lib().pm_status(context(device), ctypes.c_void_p(stream), stats), "merge engine")
     return tuple(int(x) for x in stats)

@@ -50,6 +50,8 @@ def _ptr(t: torch.Tensor):
 def merge(arr: KeyedArray, start: int, middle: int, end: int, scratch_records: int = 0):
     """Stable in-place merge of [start, middle) and [middle, end) on the device (pm_merge)."""
     require_cuda(arr)
+    if start == middle or middle == end:
+        return None
     dev = arr.keys.device.index
     rc = _capi.lib().pm_merge(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, _ptr(arr.payload),
                               arr.payload.shape[1], start, middle, end, scratch_records, _stream(dev))
@@ -62,6 +64,8 @@ def merge(arr: KeyedArray, start: int, middle: int, end: int, scratch_records: i
 def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
     """In-place block exchange A|B -> B|A on the device (pm_shift)."""
     require_cuda(arr)
+    if len_a == 0 or len_b == 0:
+        return None
     dev = arr.keys.device.index
     rc = _capi.lib().pm_shift(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, _ptr(arr.payload),
                               arr.payload.shape[1], lo, len_a, len_b, _stream(dev))

@@ -39,7 +39,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct Ctl {
   unsigned long long free_top;
   unsigned long long scr_top;
-  unsigned long long stats[4];
+  unsigned long long stats[16];
   int32_t scr_count;
   int32_t ticket;
   int32_t err;
@@ -135,13 +135,16 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   int64_t S = std::max<int64_t>(2 * P.reserve, scratch_records / T + P.reserve);
   S = std::min<int64_t>(S, P.K + P.reserve);
   P.S = S;
+  P.grid = grid;
+  P.s_per = std::min<int64_t>(S / grid, 255);
   // workspace
   const size_t off_state = (size_t)align_up((P.Q + 1) * 8, 256);
   const size_t off_loc = off_state + (size_t)align_up(P.K * 4, 256);
   const size_t off_reads = off_loc + (size_t)align_up(P.K * 4, 256);
   const size_t off_nf = off_reads + (size_t)align_up(P.K * 4, 256);
   const size_t off_ns = off_nf + (size_t)align_up(P.K * 4, 256);
-  const size_t ws_need = off_ns + (size_t)align_up(S * 4, 256);
+  const size_t off_tops = off_ns + (size_t)align_up(S * 4, 256);
+  const size_t ws_need = off_tops + 2 * 64 * sizeof(unsigned long long);
   int rc = ensure(&ctx->ws, &ctx->ws_bytes, ws_need);
   if (rc) return rc;
   const size_t scr_k = (size_t)align_up(S * T * ks + 32, 256);
@@ -155,8 +158,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.reads = reinterpret_cast<int32_t*>(ws + off_reads);
   P.next_free = reinterpret_cast<int32_t*>(ws + off_nf);
   P.next_scr = reinterpret_cast<int32_t*>(ws + off_ns);
-  P.free_top = &ctx->ctl->free_top;
-  P.scr_top = &ctx->ctl->scr_top;
+  P.free_top = reinterpret_cast<unsigned long long*>(ws + off_tops);  // [64] shard tops
+  P.scr_top = P.free_top + 64;
   P.stats = ctx->ctl->stats;
   P.scr_count = &ctx->ctl->scr_count;
   P.ticket = &ctx->ctl->ticket;
@@ -322,7 +325,7 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
   Ctl h;
   PM_CUDA(cudaMemcpy(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (stats)
-    for (int i = 0; i < 4; ++i) stats[i] = h.stats[i];
+    for (int i = 0; i < 16; ++i) stats[i] = h.stats[i];
   if (h.err != 0) {
     int32_t zero = 0;
     cudaMemcpy(&ctx->ctl->err, &zero, sizeof(zero), cudaMemcpyHostToDevice);

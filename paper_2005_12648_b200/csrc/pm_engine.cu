@@ -18,6 +18,8 @@
 
 namespace pm {
 
+constexpr int kShards = 64;  // sharded global free lists (one CAS word each)
+
 // ============================================================================
 // geometry helpers (all indices int64; "local" = relative to the job)
 // ============================================================================
@@ -150,22 +152,26 @@ __global__ void k_plan(EngineParams P) {
     P.loc[j] = (int32_t)j;
     P.reads[j] = 0;
   }
-  for (int64_t i = tid; i < P.S; i += nthr) P.next_scr[i] = (i + 1 < P.S) ? (int32_t)(i + 1) : (int32_t)kEmpty32;
+  // scratch unit i starts on shard i % kShards
+  for (int64_t i = tid; i < P.S; i += nthr) P.next_scr[i] = (i + kShards < P.S) ? (int32_t)(i + kShards) : (int32_t)kEmpty32;
+  for (int64_t sh = tid; sh < kShards; sh += nthr) {
+    P.free_top[sh] = (unsigned long long)kEmpty32;
+    P.scr_top[sh] = sh < P.S ? (unsigned long long)sh : (unsigned long long)kEmpty32;
+  }
   if (tid == 0) {
-    *P.free_top = (unsigned long long)kEmpty32;
-    *P.scr_top = P.S > 0 ? 0ull : (unsigned long long)kEmpty32;
     *P.scr_count = (int32_t)P.S;
     *P.ticket = 0;
     bool nothing = (la == 0 || lb == 0);
     if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
-    for (int i = 0; i < 4; ++i) P.stats[i] = 0;
+    for (int i = 0; i < 16; ++i) P.stats[i] = 0;
   }
 }
 
 // ============================================================================
 // k_engine
 // ============================================================================
+
 struct SmemCtl {
   uint64_t bar;
   int64_t tk;
@@ -173,47 +179,134 @@ struct SmemCtl {
   int32_t occ_dest[16];
 };
 
-// byte copy global -> shared with identical 16-byte phase; bulk for the body
-__device__ __forceinline__ uint32_t copy_g2s_phased(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar) {
-  if (nbytes <= 0) return 0;
+// Free slots and free scratch units live in kShards Treiber stacks; a CTA pushes
+// to and pops from its own shard first and scans the others only when it runs
+// dry.  One global stack serialised 400+ CTAs on a single CAS word; per-CTA
+// private lists starved other CTAs (hoarding).
+__device__ __forceinline__ int32_t sharded_pop(unsigned long long* tops, int32_t* next, int home) {
+  for (int k = 0; k < kShards; ++k) {
+    const int sh = (home + k) & (kShards - 1);
+    if ((uint32_t)(*(volatile unsigned long long*)&tops[sh] & 0xFFFFFFFFull) == kEmpty32) continue;
+    const int32_t v = stack_pop(&tops[sh], next);
+    if (v >= 0) return v;
+  }
+  return -1;
+}
+
+// warp-cooperative pop: lanes read all shard tops at once, then lane 0 pops the
+// nearest non-empty shard (home first).  Returns -1 if every shard looked empty.
+__device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* next, int home, int lane) {
+  const uint32_t a = (uint32_t)(*(volatile unsigned long long*)&tops[(home + lane) & (kShards - 1)]);
+  const uint32_t b = (uint32_t)(*(volatile unsigned long long*)&tops[(home + 32 + lane) & (kShards - 1)]);
+  unsigned ma = __ballot_sync(0xffffffffu, a != kEmpty32);
+  unsigned mb = __ballot_sync(0xffffffffu, b != kEmpty32);
+  int32_t v = -1;
+  while ((ma | mb) && v < 0) {
+    int sh;
+    if (ma) {
+      sh = (home + __ffs(ma) - 1) & (kShards - 1);
+      ma &= ma - 1;
+    } else {
+      sh = (home + 32 + __ffs(mb) - 1) & (kShards - 1);
+      mb &= mb - 1;
+    }
+    if (lane == 0) v = stack_pop(&tops[sh], next);
+    v = __shfl_sync(0xffffffffu, v, 0);
+  }
+  return v;
+}
+
+// copy n (< 16) bytes that lie inside one aligned 16-byte chunk: one vector load
+__device__ __forceinline__ void copy_small_g2s(uint8_t* dst, const uint8_t* src, int n) {
+  if (n <= 0) return;
+  const uintptr_t a = (uintptr_t)src & ~(uintptr_t)15;
+  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a));
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  const int o = (int)((uintptr_t)src - a);
+  for (int i = 0; i < n; ++i) dst[i] = b[o + i];
+}
+
+// global -> shared, identical 16-byte phase on both sides: TMA bulk copy for the
+// aligned body, one vector load each for the unaligned head and tail
+__device__ __forceinline__ void copy_g2s_phased(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar) {
+  if (nbytes <= 0) return;
   int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
   if (head > nbytes) head = nbytes;
-  for (int64_t b = 0; b < head; ++b) dst[b] = src[b];
-  int64_t body = ((nbytes - head) >> 4) << 4;
-  uint32_t tx = 0;
+  const int64_t body = ((nbytes - head) >> 4) << 4;
   if (body > 0) {
     mbar_expect_tx(bar, (uint32_t)body);
     bulk_g2s(dst + head, src + head, (uint32_t)body, bar);
-    tx = (uint32_t)body;
   }
-  for (int64_t b = head + body; b < nbytes; ++b) dst[b] = src[b];
-  return tx;
+  copy_small_g2s(dst, src, (int)head);
+  copy_small_g2s(dst + head + body, src + head + body, (int)(nbytes - head - body));
 }
 
-// warp copy global -> global, identical 16-byte phase on both sides
+// warp copy global -> global, identical 16-byte phase on both sides; all loads of
+// a lane are issued before its stores (8 x 16 B in flight per lane)
 __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, int64_t nbytes, int lane) {
   if (nbytes <= 0) return;
   int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
   if (head > nbytes) head = nbytes;
   if (lane < head) dst[lane] = src[lane];
-  int64_t nvec = (nbytes - head) >> 4;
+  const int64_t nvec = (nbytes - head) >> 4;
   const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
   uint4* d4 = reinterpret_cast<uint4*>(dst + head);
   int64_t i = lane;
-  for (; i + 96 < nvec; i += 128) {
-    uint4 v0 = s4[i], v1 = s4[i + 32], v2 = s4[i + 64], v3 = s4[i + 96];
-    d4[i] = v0;
-    d4[i + 32] = v1;
-    d4[i + 64] = v2;
-    d4[i + 96] = v3;
+  for (; i + 224 < nvec; i += 256) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(s4 + i + 32 * k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d4[i + 32 * k] = v[k];
   }
-  for (; i < nvec; i += 32) d4[i] = s4[i];
-  int64_t tail0 = head + (nvec << 4);
+  for (; i < nvec; i += 32) d4[i] = __ldcs(s4 + i);
+  const int64_t tail0 = head + (nvec << 4);
   if (tail0 + lane < nbytes) dst[tail0 + lane] = src[tail0 + lane];
 }
 
+// Warp-wide: a salvage destination for unit u -- scratch first (a parked unit is
+// never moved again), then a free slot.  Blocking waits only after the caller
+// has published its own reads (they are what frees space).
+__device__ __forceinline__ int32_t acquire_dest(const EngineParams& P, int32_t u, int home, int lane, bool block) {
+  for (uint32_t it = 0;; ++it) {
+    int32_t si = warp_pop(P.scr_top, P.next_scr, home, lane);
+    if (si >= 0) return -si - 1;
+    int32_t f;
+    while ((f = warp_pop(P.free_top, P.next_free, home, lane)) >= 0) {
+      int ok = 0;
+      if (lane == 0) ok = atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE;
+      if (__shfl_sync(0xffffffffu, ok, 0)) return f;
+    }
+    if (!block || ld_relaxed(P.err)) return INT32_MIN;
+    if (it > kSpinLimit) {
+      if (lane == 0) raise_error(P.err, PM_ERR_NOSPACE);
+      return INT32_MIN;
+    }
+    backoff(it);
+  }
+}
+
 template <typename KT>
-__global__ void __launch_bounds__(256) k_engine(EngineParams P) {
+__device__ __forceinline__ void pool_push_dest(const EngineParams& P, int32_t dest, int home) {
+  if (dest >= 0) {
+    st_release(&P.state[dest], ST_FREE);
+    stack_push(&P.free_top[home], P.next_free, dest);
+  } else {
+    stack_push(&P.scr_top[home], P.next_scr, -dest - 1);
+  }
+}
+
+// Warp roles inside the 256-thread CTA, per region:
+//   A  all    : ticket (prefetched one region ahead), geometry, close the slots
+//   B  w0..3  : one warp per occupied slot: wait for a landing unit, then take a
+//               salvage destination speculatively (scratch first, then free slot)
+//      w4..7  : gather the region's A/B pieces (TMA bulk + vector head/tail)
+//   C  all    : wait for the bulk copies; publish reads; free dead units
+//   D  w0..3  : wait for earlier consumers; keep or give back the destination
+//   E  all    : copy salvaged units (two warps per unit), publish their new homes
+//   F  all    : merge path per thread in shared memory, stream the region back
+template <typename KT>
+__global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   extern __shared__ __align__(128) uint8_t dyn[];
   __shared__ SmemCtl ctl;
   Geo g(P);
@@ -228,35 +321,51 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
   int32_t* src = reinterpret_cast<int32_t*>(dyn + P.smem_keys + P.smem_pay);  // padded output->input map
   if (tid == 0) mbar_init(&ctl.bar, 1);
   __syncthreads();
+  const int home = blockIdx.x & (kShards - 1);
   uint32_t phase = 0;
   const int64_t la = g.LA();
+  constexpr int kGatherWarp0 = 4;  // warps 4..7 gather
+  // per-CTA accounting, flushed once at the end (no per-region global atomics)
+  unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long n_salv = 0, r_salv = 0, n_reg = 0, n_ident = 0, spins_r = 0, spins_o = 0;
+  unsigned long long w_land = 0, w_thr = 0, w_dest = 0, w_copy = 0;
+  long long tc = clock64();
+  int32_t t_pref = 0;
+  if (tid == 0) t_pref = atomicAdd(P.ticket, 1);
 
   while (true) {
     if (tid == 0) {
-      int32_t t = atomicAdd(P.ticket, 1);
+      const int32_t t = t_pref;
+      t_pref = atomicAdd(P.ticket, 1);  // next ticket, in flight during this region
       ctl.tk = (*(volatile int32_t*)P.err) ? P.Q : t;
     }
     __syncthreads();
     const int64_t t = ctl.tk;
     if (t >= P.Q) break;
+    // ---------------- A: geometry, close the slots ----------------------------
     const int64_t q = g.region_of_ticket(t);
     const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
     const int nslot = (int)(j1 - j0);
-    if (tid < nslot) ctl.occ[tid] = atomicExch(&P.state[j0 + tid], ST_CLOSED);
+    if (tid < nslot) {
+      ctl.occ[tid] = atomicExch(&P.state[j0 + tid], ST_CLOSED);
+      ctl.occ_dest[tid] = INT32_MIN;
+    }
     const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
     const int64_t a0 = P.split_a[q], a1 = P.split_a[q + 1];
     const int64_t b0 = d0 - a0, b1 = d1 - a1;
     const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
-    const bool identity =
-        P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+    const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
     __syncthreads();
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[0] += n - tc;
+      tc = n;
+    }
     if (identity) {
-      if (tid == 0) atomicAdd(&P.stats[3], 1ull);
+      ++n_ident;
       continue;  // inputs already sit on their outputs; units consumed by q only
     }
-    // ---------------- phase 1: gather A[a0,a1) and B[b0,b1) ----------------
-    // smem layout: A keys at kin+offA (phase of A[a0]), B keys at kin+offB
-    const int64_t xa = P.s + a0, xb = P.m + b0;  // absolute first elements
+    const int64_t xa = P.s + a0, xb = P.m + b0;  // absolute first elements of the runs
     const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
     const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
     int64_t poffA = 0, poffB = 0;
@@ -264,16 +373,17 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
       poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
       poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
     }
+    const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
+    const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
+    const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
+    // ---------------- B: gather the region's A/B pieces --------------------------
     {
-      const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
-      const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
-      const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
       for (int p = tid; p < np; p += NT) {
         const bool isA = p < npa;
         const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
         const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
         const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-        // wait until the unit sits in a region that will not move it before we read
+        // wait until the unit sits where nobody moves it before we have read it
         int32_t l;
         for (uint32_t it = 0;; ++it) {
           l = ld_acquire(&P.loc[j]);
@@ -283,20 +393,20 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
             raise_error(P.err, PM_ERR_TIMEOUT);
             break;
           }
+          ++spins_r;
           backoff(it);
         }
-        // source address of element x of unit j at its current location
-        const int64_t home = g.slot_base(j);
+        const int64_t hb = g.slot_base(j);
         const char* ksrc;
         const uint8_t* psrc;
         if (l >= 0) {
           const int64_t base = g.slot_base(l);
-          ksrc = P.keys + (base + (x0 - home)) * ks;
-          psrc = P.pay + (base + (x0 - home)) * w;
+          ksrc = P.keys + (base + (x0 - hb)) * ks;
+          psrc = P.pay + (base + (x0 - hb)) * w;
         } else {
           const int64_t si = -(int64_t)l - 1;
-          ksrc = P.scr_keys + (si * P.T + (x0 - home)) * ks;
-          psrc = P.scr_pay + (si * P.T + (x0 - home)) * w;
+          ksrc = P.scr_keys + (si * P.T + (x0 - hb)) * ks;
+          psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
         }
         uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
         copy_g2s_phased(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
@@ -305,41 +415,58 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
           copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
         }
       }
-      __syncthreads();  // every expect_tx registered before the single arrive
-      if (tid == 0) mbar_arrive(&ctl.bar);
-      for (uint32_t it = 0; !mbar_try_wait(&ctl.bar, phase); ++it) {
-      }
-      phase ^= 1;
-      __syncthreads();
-      // publish the reads; the last consumer of a unit frees its location
-      for (int p = tid; p < np; p += NT) {
-        const bool isA = p < npa;
-        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
-        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-        __threadfence();
-        const int32_t n = (int32_t)(x1 - x0);
-        const int32_t old = atomicAdd(&P.reads[j], n);
-        if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
-          const int32_t l = ld_acquire(&P.loc[j]);
-          if (l < 0) {
-            stack_push(P.scr_top, P.next_scr, -l - 1);
-            atomicAdd(P.scr_count, 1);
-          } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
-            stack_push(P.free_top, P.next_free, l);
-          }
+    }
+    __syncthreads();  // every expect_tx registered before the single arrive
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[1] += n - tc;
+      tc = n;
+      mbar_arrive(&ctl.bar);
+    }
+    // ---------------- C: land, publish reads, free dead units ------------------
+    while (!mbar_try_wait(&ctl.bar, phase)) {
+    }
+    phase ^= 1;
+    __syncthreads();
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[2] += n - tc;
+      tc = n;
+    }
+    for (int p = tid; p < np; p += NT) {
+      const bool isA = p < npa;
+      const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+      const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+      const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+      __threadfence();
+      const int32_t n = (int32_t)(x1 - x0);
+      const int32_t old = atomicAdd(&P.reads[j], n);
+      if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
+        const int32_t l = ld_acquire(&P.loc[j]);
+        if (l < 0) {
+          stack_push(&P.scr_top[home], P.next_scr, -l - 1);
+        } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
+          stack_push(&P.free_top[home], P.next_free, l);
         }
       }
     }
-    // ---------------- phase 2: salvage still-needed occupants ---------------
-    if (wid < nslot) {
-      const int32_t u = ctl.occ[wid];
-      int32_t dest = 0;
-      int alive = 0;
-      if (u >= 0) {
+    const KT* As = reinterpret_cast<const KT*>(kin + offA);
+    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+    const int MT = NT - kGatherWarp0 * 32, mt = tid - kGatherWarp0 * 32;  // merge threads
+    const int64_t E = (nout + MT - 1) / MT;
+    const int64_t V = 16 / ks;  // keys per 16-byte vector
+    // output o is staged at padded index P(o + ph) so strided writes avoid bank conflicts
+    const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
+    // ---------------- D: salvage decisions (w0..3) || merge path (w4..7) ---------
+    if (wid < kGatherWarp0) {
+      for (int i = wid; i < nslot; i += kGatherWarp0) {
+        const int32_t u = ctl.occ[i];
+        if (u < 0) continue;
+        long long c1 = clock64();
+        int32_t r = 0;
         if (lane == 0) {
-          const int32_t slot = (int32_t)(j0 + wid);
-          for (uint32_t it = 0; ld_acquire(&P.loc[u]) != slot; ++it) {  // salvaged-in unit may still be landing
+          const int32_t slot = (int32_t)(j0 + i);
+          for (uint32_t it = 0; ld_acquire(&P.loc[u]) != slot; ++it) {  // landing (reads are published now)
             if (ld_relaxed(P.err)) break;
             if (it > kSpinLimit) {
               raise_error(P.err, PM_ERR_TIMEOUT);
@@ -348,8 +475,8 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
             backoff(it);
           }
           const int32_t thr = (int32_t)g.consumed_by_window(u, t);
-          int32_t r;
           for (uint32_t it = 0; (r = ld_acquire(&P.reads[u])) < thr; ++it) {
+            ++spins_o;
             if (ld_relaxed(P.err)) break;
             if (it > kSpinLimit) {
               raise_error(P.err, PM_ERR_TIMEOUT);
@@ -357,88 +484,29 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
             }
             backoff(it);
           }
-          const int32_t usz = (int32_t)(g.slot_hi(u) - g.slot_lo(u));
-          alive = r < usz && !ld_relaxed(P.err);
-          if (alive) {
-            // destination: scratch while it is plentiful, then free slots, then the reserve
-            dest = INT32_MIN;
-            for (uint32_t it = 0;; ++it) {
-              if (ld_relaxed(P.scr_count) > P.reserve) {
-                int32_t si = stack_pop(P.scr_top, P.next_scr);
-                if (si >= 0) {
-                  atomicSub(P.scr_count, 1);
-                  dest = -si - 1;
-                  break;
-                }
-              }
-              int32_t f = stack_pop(P.free_top, P.next_free);
-              if (f >= 0) {
-                if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) {
-                  dest = f;
-                  break;
-                }
-                continue;  // slot got closed by its region; drop it
-              }
-              int32_t si = stack_pop(P.scr_top, P.next_scr);
-              if (si >= 0) {
-                atomicSub(P.scr_count, 1);
-                dest = -si - 1;
-                break;
-              }
-              if (ld_relaxed(P.err)) break;
-              if (it > kSpinLimit) {
-                raise_error(P.err, PM_ERR_NOSPACE);
-                break;
-              }
-              backoff(it);
-            }
-            if (dest == INT32_MIN) alive = 0;
-          }
         }
-        alive = __shfl_sync(0xffffffffu, alive, 0);
-        dest = __shfl_sync(0xffffffffu, dest, 0);
-        if (alive) {
-          const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), home = g.slot_base(u);
-          const int64_t sbase = g.slot_base(j0 + wid);
-          char* kd;
-          uint8_t* pd;
-          if (dest >= 0) {
-            kd = P.keys + (g.slot_base(dest) + (x0 - home)) * ks;
-            pd = P.pay + (g.slot_base(dest) + (x0 - home)) * w;
-          } else {
-            const int64_t si = -(int64_t)dest - 1;
-            kd = P.scr_keys + (si * P.T + (x0 - home)) * ks;
-            pd = P.scr_pay + (si * P.T + (x0 - home)) * w;
-          }
-          copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
-                        reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - home)) * ks), (x1 - x0) * ks,
-                        lane);
-          if (w) copy_g2g_warp(pd, P.pay + (sbase + (x0 - home)) * w, (x1 - x0) * w, lane);
-          __syncwarp();
+        r = __shfl_sync(0xffffffffu, r, 0);
+        const int32_t usz = (int32_t)(g.slot_hi(u) - g.slot_lo(u));
+        const bool alive = r < usz && !ld_relaxed(P.err);
+        const int32_t dest = ctl.occ_dest[i];
+        __syncwarp();
+        if (!alive && dest != INT32_MIN) {
           if (lane == 0) {
-            __threadfence();
-            st_release(&P.loc[u], dest);
-            atomicAdd(&P.stats[0], 1ull);
-            atomicAdd(&P.stats[1], (unsigned long long)(x1 - x0));
+            pool_push_dest<KT>(P, dest, home);  // give the speculative destination back
+            ctl.occ_dest[i] = INT32_MIN;
           }
+        } else if (alive && dest == INT32_MIN) {
+          const int32_t d = acquire_dest(P, u, home, lane, true);
+          if (lane == 0) ctl.occ_dest[i] = d;
         }
+        w_thr += clock64() - c1;
       }
     }
-    __syncthreads();
-    if (ld_relaxed(P.err)) break;
-    // ---------------- phase 3: merge in shared memory -----------------------
-    const KT* As = reinterpret_cast<const KT*>(kin + offA);
-    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-    const int64_t E = (nout + NT - 1) / NT;
-    // output o is staged at padded index P(o + ph) so strided writes avoid bank conflicts
-    const int64_t V = 16 / ks;                                   // keys per 16-byte vector
-    const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
-    {
-      int64_t o = min((int64_t)tid * E, nout), oe = min(o + E, nout);
+    if (wid >= kGatherWarp0) {
+      int64_t o = min((int64_t)mt * E, nout), oe = min(o + E, nout);
       if (P.mode == MODE_MERGE) {
-        // merge-path split of this thread's diagonal (A wins ties)
         int64_t lo = o > beta ? o - beta : 0, hi = o < alpha ? o : alpha;
-        while (lo < hi) {
+        while (lo < hi) {  // merge-path split of this thread's diagonal (A wins ties)
           int64_t mid = (lo + hi) >> 1;
           if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
           else hi = mid;
@@ -465,7 +533,53 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
       }
     }
     __syncthreads();
-    // ---------------- phase 4: stream the region back in place --------------
+    if (ld_relaxed(P.err)) break;
+    // ---------------- E: move the salvaged units ---------------------------------
+    {
+      long long c3 = clock64();
+      const int NW = NT >> 5;
+      for (int job = wid; job < 2 * nslot; job += NW) {
+        const int i = job >> 1, half = job & 1;
+        const int32_t u = ctl.occ[i], dest = ctl.occ_dest[i];
+        if (u < 0 || dest == INT32_MIN) continue;
+        const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
+        const int64_t xm = x0 + (((x1 - x0) >> 1) & ~(int64_t)15);
+        const int64_t y0 = half ? xm : x0, y1 = half ? x1 : xm;
+        const int64_t sbase = g.slot_base(j0 + i);
+        const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
+        char* kd = dest >= 0 ? P.keys + (dbase + (y0 - hb)) * ks
+                             : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (y0 - hb)) * ks;
+        copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
+                      reinterpret_cast<const uint8_t*>(P.keys + (sbase + (y0 - hb)) * ks), (y1 - y0) * ks, lane);
+        if (w) {
+          uint8_t* pd = dest >= 0 ? P.pay + (dbase + (y0 - hb)) * w
+                                  : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (y0 - hb)) * w;
+          copy_g2g_warp(pd, P.pay + (sbase + (y0 - hb)) * w, (y1 - y0) * w, lane);
+        }
+      }
+      __syncthreads();
+      if (tid < nslot) {
+        const int32_t u = ctl.occ[tid], dest = ctl.occ_dest[tid];
+        if (u >= 0 && dest != INT32_MIN) {
+          __threadfence();
+          st_release(&P.loc[u], dest);
+          ++n_salv;
+          r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
+        }
+      }
+      if (lane == 0) w_copy += clock64() - c3;
+    }
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[3] += n - tc;
+      tc = n;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[4] += n - tc;
+      tc = n;
+    }
     {
       KT* kout = reinterpret_cast<KT*>(P.keys) + (P.s + d0) - ph;  // 16B aligned when keys base is
       const int64_t ngroups = (ph + nout + V - 1) / V;
@@ -488,9 +602,9 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
         }
         if (full) {
           if constexpr (sizeof(KT) == 4) {
-            *reinterpret_cast<int4*>(kout + op0) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+            __stcs(reinterpret_cast<int4*>(kout + op0), make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]));
           } else {
-            *reinterpret_cast<longlong2*>(kout + op0) = make_longlong2((long long)v[0], (long long)v[1]);
+            __stcs(reinterpret_cast<longlong2*>(kout + op0), make_longlong2((long long)v[0], (long long)v[1]));
           }
         } else {
 #pragma unroll
@@ -526,8 +640,30 @@ __global__ void __launch_bounds__(256) k_engine(EngineParams P) {
         }
       }
     }
-    if (tid == 0) atomicAdd(&P.stats[2], 1ull);
+    ++n_reg;
     __syncthreads();
+    if (tid == 0) {
+      long long n = clock64();
+      cyc[5] += n - tc;
+      tc = n;
+    }
+  }
+  if (n_salv) {
+    atomicAdd(&P.stats[0], n_salv);
+    atomicAdd(&P.stats[1], r_salv);
+  }
+  if (tid == 0) {
+    atomicAdd(&P.stats[2], n_reg);
+    atomicAdd(&P.stats[3], n_ident);
+    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cyc[i]);
+  }
+  if (lane == 0) {
+    atomicAdd(&P.stats[10], spins_r);
+    atomicAdd(&P.stats[11], spins_o);
+    atomicAdd(&P.stats[12], w_land);
+    atomicAdd(&P.stats[13], w_thr);
+    atomicAdd(&P.stats[14], w_dest);
+    atomicAdd(&P.stats[15], w_copy);
   }
 }
 

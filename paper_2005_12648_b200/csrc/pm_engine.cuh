@@ -49,6 +49,8 @@ struct EngineParams {
   unsigned long long* scr_top;
   int32_t* scr_count;  // free scratch units (heuristic only)
   int64_t S;           // scratch units
+  int32_t grid;        // engine CTAs (each owns s_per scratch units at start)
+  int64_t s_per;
   int64_t reserve;     // keep this many scratch units for the no-free-slot case
   char* scr_keys;      // phase-matched scratch bases
   uint8_t* scr_pay;
