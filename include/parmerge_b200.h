@@ -125,6 +125,9 @@ int pm_merge_host(pm_ctx *ctx, void *keys_host, int key_bytes, void *payload_hos
  * pm_kernel_ms() waits for the last one and returns their device durations.
  */
 int pm_set_timing(pm_ctx *ctx, int on);
+/* Host evaluation of the engine's two-front ticket order (same source as the
+ * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
+int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
 int pm_kernel_ms(pm_ctx *ctx, float *plan_ms, float *engine_ms);
 
 #ifdef __cplusplus

@@ -199,6 +199,15 @@ extern "C" {
 
 int pm_version(void) { return 100; }
 
+int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t* out4) {
+  if (Q < 1 || qc < 0 || qc >= Q || t < 0 || t >= Q || !out4) return fail(PM_ERR_ARG, "bad order arguments");
+  TwoFront tf{Q, qc};
+  out4[0] = tf.region_of_ticket(t);
+  out4[1] = tf.order(out4[0]);
+  tf.window(t, out4[2], out4[3]);
+  return PM_OK;
+}
+
 const char* pm_last_error(void) { return g_last_error.c_str(); }
 
 int pm_ctx_create(int device, pm_ctx** out) {

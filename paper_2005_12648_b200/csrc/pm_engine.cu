@@ -43,41 +43,11 @@ struct Geo {
     if (q >= P.Q) return N();
     return (P.R0 + q) * P.M - P.s;
   }
-  // ---- two-front ticket order around the centre region qc ----
-  __device__ int64_t nleft() const { return P.qc; }
-  __device__ int64_t nright() const { return P.Q - 1 - P.qc; }
-  __device__ int64_t region_of_ticket(int64_t t) const {
-    if (t == 0) return P.qc;
-    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr);
-    if (t <= 2 * m2) return (t & 1) ? P.qc - (t + 1) / 2 : P.qc + t / 2;
-    return nl > nr ? P.qc - (t - nr) : P.qc + (t - nl);
-  }
-  __device__ int64_t order(int64_t q) const {
-    if (q == P.qc) return 0;
-    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr);
-    if (q < P.qc) {
-      int64_t i = P.qc - q;
-      return i <= m2 ? 2 * i - 1 : i + nr;
-    }
-    int64_t i = q - P.qc;
-    return i <= m2 ? 2 * i : i + nl;
-  }
-  // regions with order <= t form the window [qc - nl(t), qc + nr(t)]
-  __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const {
-    int64_t nl = nleft(), nr = nright(), m2 = min(nl, nr), a, b;
-    if (t <= 2 * m2) {
-      a = (t + 1) / 2;
-      b = t / 2;
-    } else if (nl > nr) {
-      a = t - nr;
-      b = nr;
-    } else {
-      a = nl;
-      b = t - nl;
-    }
-    lo = P.qc - min(a, nl);
-    hi = P.qc + min(b, nr);
-  }
+  // ---- two-front ticket order (pm_engine.cuh) ----
+  __device__ TwoFront tf() const { return TwoFront{P.Q, P.qc}; }
+  __device__ int64_t region_of_ticket(int64_t t) const { return tf().region_of_ticket(t); }
+  __device__ int64_t order(int64_t q) const { return tf().order(q); }
+  __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const { tf().window(t, lo, hi); }
   // records of unit j consumed by the regions of the ticket window <= t
   __device__ int64_t consumed_by_window(int64_t j, int64_t t) const {
     int64_t wl, wr;

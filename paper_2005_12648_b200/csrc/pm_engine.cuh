@@ -25,6 +25,49 @@ enum : int32_t { MODE_MERGE = 0, MODE_ROTATE = 1 };
 enum : int32_t { ST_FREE = -1, ST_CLOSED = -2 };
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 
+// Two-front ticket order around the centre region qc (regions 0..Q-1): ticket 0
+// is qc, then qc-1, qc+1, qc-2, qc+2, ... until one side runs out, then the
+// rest of the longer side.  __host__ __device__ so tests can check the exact
+// device formulas on the CPU (pm_debug_order).
+struct TwoFront {
+  int64_t Q, qc;
+  __host__ __device__ int64_t nleft() const { return qc; }
+  __host__ __device__ int64_t nright() const { return Q - 1 - qc; }
+  __host__ __device__ static int64_t mn(int64_t a, int64_t b) { return a < b ? a : b; }
+  __host__ __device__ int64_t region_of_ticket(int64_t t) const {
+    if (t == 0) return qc;
+    int64_t nl = nleft(), nr = nright(), m2 = mn(nl, nr);
+    if (t <= 2 * m2) return (t & 1) ? qc - (t + 1) / 2 : qc + t / 2;
+    return nl > nr ? qc - (t - nr) : qc + (t - nl);
+  }
+  __host__ __device__ int64_t order(int64_t q) const {
+    if (q == qc) return 0;
+    int64_t nl = nleft(), nr = nright(), m2 = mn(nl, nr);
+    if (q < qc) {
+      int64_t i = qc - q;
+      return i <= m2 ? 2 * i - 1 : i + nr;
+    }
+    int64_t i = q - qc;
+    return i <= m2 ? 2 * i : i + nl;
+  }
+  // regions with order <= t form the window [lo, hi]
+  __host__ __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const {
+    int64_t nl = nleft(), nr = nright(), m2 = mn(nl, nr), a, b;
+    if (t <= 2 * m2) {
+      a = (t + 1) / 2;
+      b = t / 2;
+    } else if (nl > nr) {
+      a = t - nr;
+      b = nr;
+    } else {
+      a = nl;
+      b = t - nl;
+    }
+    lo = qc - mn(a, nl);
+    hi = qc + mn(b, nr);
+  }
+};
+
 struct EngineParams {
   char* keys;          // element x lives at keys + x*ks
   uint8_t* pay;        // row x lives at pay + x*w (unused when w == 0)
