@@ -1,0 +1,143 @@
+"""Multi-GPU merge of a block-distributed A|B (BASELINE config 5).
+
+Rank r holds the contiguous block X[off_r, off_r + n_r) of the concatenation
+X = A|B (|A| = ``global_len_a``).  After ``merge_distributed`` rank r holds
+the same block of the stable merge of A and B -- the distributed form of the
+reference's parallel merge (srecpar.py:33-84: split, exchange, merge pairs),
+with the GPUs as the partitions:
+
+1. **Global split points** (the median search of the reference, made stable):
+   for every rank boundary diagonal d = off_r, the number of A records among
+   the first d outputs.  All G+1 searches run together as a 33-ary search;
+   each round all-reduces the 32 probe keys per diagonal that the owning ranks
+   contribute (about log_33 N rounds of a few-KB all-reduce).
+2. **Partition exchange**: rank r needs A[a_r, a_{r+1}) and B[b_r, b_{r+1});
+   every rank's A part and B part are already ordered by destination, so two
+   ``all_to_all_single`` calls (NCCL send/recv over NVLink) deliver rank r's
+   A slice followed by its B slice, contiguously.
+3. **Local merge**: the in-place device engine (``pm_merge``) merges the pair.
+
+The exchange uses a receive buffer of n_r records per rank (DESIGN.md notes
+the chunked, O(chunk) variant as next work).  ``local_merge`` is injectable so
+the host logic can be tested with the gloo backend on CPU tensors.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+_PROBES = 32
+
+
+def _owned_values(keys_local: torch.Tensor, off: int, positions: torch.Tensor) -> torch.Tensor:
+    """Values at global X positions owned by this rank, 0 elsewhere (for a SUM all-reduce)."""
+    n = keys_local.numel()
+    mine = (positions >= off) & (positions < off + n)
+    idx = (positions - off).clamp(0, max(n - 1, 0))
+    vals = keys_local[idx].to(torch.int64) if n else torch.zeros_like(positions)
+    return torch.where(mine, vals, torch.zeros_like(vals))
+
+
+def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: int, group=None) -> list[int]:
+    """A-count of the stable merge at every rank boundary diagonal (A wins ties)."""
+    rank = dist.get_rank(group)
+    off = offsets[rank]
+    N = offsets[-1]
+    la, lb = global_len_a, N - global_len_a
+    dev = keys_local.device
+    diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
+    lo = torch.clamp(diags - lb, min=0)
+    hi = torch.clamp(diags, max=la)
+    k = torch.arange(1, _PROBES + 1, dtype=torch.int64, device=dev)
+    while True:
+        span = hi - lo
+        if int(span.max().item()) == 0:
+            break
+        small = span <= _PROBES
+        # probes: evenly spaced when the interval is wide, every index when it is small
+        p_wide = lo[:, None] + (k[None, :] * span[:, None]) // (_PROBES + 1)
+        p_small = lo[:, None] + (k[None, :] - 1)
+        p = torch.where(small[:, None], p_small, p_wide)
+        valid = p < hi[:, None]
+        pa = torch.where(valid, p, lo[:, None])                      # A index
+        pb = torch.clamp(diags[:, None] - 1 - pa, min=0)              # B index
+        gpos = torch.stack([pa, la + pb], dim=-1)                    # global X positions
+        vals = _owned_values(keys_local, off, gpos.reshape(-1)).reshape(gpos.shape)
+        dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
+        f = (vals[..., 0] <= vals[..., 1]) & valid                   # A[p] is among the first d
+        # first probe with f false (or none)
+        nf = (~f) & valid
+        has = nf.any(dim=1)
+        first = torch.where(has, nf.float().argmax(dim=1), torch.full_like(lo, _PROBES))
+        last_true = torch.where(first > 0, p.gather(1, (first - 1).clamp(min=0)[:, None])[:, 0], lo - 1)
+        new_hi = torch.where(has, p.gather(1, first.clamp(max=_PROBES - 1)[:, None])[:, 0], hi)
+        # when no probe failed, everything up to the last valid probe is among the first d
+        last_valid = torch.where(valid, p, lo[:, None] - 1).max(dim=1).values
+        new_lo = torch.where(has, torch.where(first > 0, last_true + 1, lo), last_valid + 1)
+        lo, hi = torch.where(span > 0, new_lo, lo), torch.where(span > 0, new_hi, hi)
+    return [int(x) for x in lo.tolist()]
+
+
+def _default_local_merge(keys: torch.Tensor, payload: torch.Tensor, len_a: int) -> None:
+    from . import _ops
+    from .records import KeyedArray
+
+    arr = KeyedArray.__new__(KeyedArray)
+    arr.keys, arr.payload = keys, payload
+    _ops.merge(arr, 0, len_a, keys.numel())
+
+
+def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | None, global_len_a: int,
+                      group=None, local_merge: Callable | None = None):
+    """Stable merge of the block-distributed A|B; returns this rank's output block.
+
+    ``keys_local`` / ``payload_local`` are this rank's block (device tensors for
+    NCCL).  Returns (keys, payload) of the same length, holding the merged
+    records for this rank's block; the input tensors are overwritten too.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = keys_local.device
+    n = keys_local.numel()
+    if payload_local is None:
+        payload_local = torch.empty((n, 0), dtype=torch.uint8, device=dev)
+    sizes = torch.tensor([n], dtype=torch.int64, device=dev)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    offsets = [0]
+    for t in all_sizes:
+        offsets.append(offsets[-1] + int(t.item()))
+    la = global_len_a
+    a = global_splits(keys_local, offsets, la, group)
+    b = [offsets[i] - a[i] for i in range(world + 1)]
+    off = offsets[rank]
+    # this block's A part [off, min(off+n, la)) and B part [max(off, la), off+n) in X coordinates
+    a_lo, a_hi = off, min(off + n, la)
+    b_lo, b_hi = max(off, la), off + n
+    send_a = [max(0, min(a_hi, a[r + 1]) - max(a_lo, a[r])) for r in range(world)]
+    send_b = [max(0, min(b_hi, la + b[r + 1]) - max(b_lo, la + b[r])) for r in range(world)]
+    # what every rank sends to me
+    sa = torch.tensor(send_a, dtype=torch.int64, device=dev)
+    sb = torch.tensor(send_b, dtype=torch.int64, device=dev)
+    ra = torch.empty_like(sa)
+    rb = torch.empty_like(sb)
+    dist.all_to_all_single(ra, sa, group=group)
+    dist.all_to_all_single(rb, sb, group=group)
+    recv_a, recv_b = ra.tolist(), rb.tolist()
+    na, nb = sum(recv_a), sum(recv_b)
+    assert na == a[rank + 1] - a[rank] and nb == b[rank + 1] - b[rank] and na + nb == n
+    split_at = max(0, min(n, la - off))
+    out_k = torch.empty_like(keys_local)
+    out_p = torch.empty_like(payload_local)
+    dist.all_to_all_single(out_k[:na], keys_local[:split_at].contiguous(), recv_a, send_a, group=group)
+    dist.all_to_all_single(out_k[na:], keys_local[split_at:].contiguous(), recv_b, send_b, group=group)
+    if payload_local.shape[1]:
+        dist.all_to_all_single(out_p[:na], payload_local[:split_at].contiguous(), recv_a, send_a, group=group)
+        dist.all_to_all_single(out_p[na:], payload_local[split_at:].contiguous(), recv_b, send_b, group=group)
+    (local_merge or _default_local_merge)(out_k, out_p, na)
+    keys_local.copy_(out_k)
+    payload_local.copy_(out_p)
+    return keys_local, payload_local
