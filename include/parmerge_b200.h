@@ -128,6 +128,8 @@ int pm_set_timing(pm_ctx *ctx, int on);
 /* Host evaluation of the engine's two-front ticket order (same source as the
  * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
+/* Copy the first n entries of the last job's split table to host memory (debug). */
+int pm_debug_splits(pm_ctx *ctx, int64_t *host_out, int64_t n);
 int pm_kernel_ms(pm_ctx *ctx, float *plan_ms, float *engine_ms);
 
 #ifdef __cplusplus

@@ -44,6 +44,8 @@ struct Ctl {
   int32_t ticket;
   int32_t err;
   int32_t noop;
+  int32_t need_space;
+  int32_t pad_;
 };
 
 constexpr int kEngineThreads = 256;
@@ -110,6 +112,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.e = e;
   P.T = T;
   P.mu = mu;
+  if (mu > 8) return fail(PM_ERR_INTERNAL, "slots per region exceed the occupant warps");
   P.nthreads = kEngineThreads;
   P.M = M;
   P.k0 = s / T;
@@ -136,6 +139,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   S = std::min<int64_t>(S, P.K + P.reserve);
   P.S = S;
   P.grid = grid;
+  P.look = std::max<int64_t>(64, 2 * (int64_t)grid);
   P.s_per = std::min<int64_t>(S / grid, 255);
   // workspace
   const size_t off_state = (size_t)align_up((P.Q + 1) * 8, 256);
@@ -165,11 +169,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.ticket = &ctx->ctl->ticket;
   P.err = &ctx->ctl->err;
   P.noop = &ctx->ctl->noop;
+  P.need_space = &ctx->ctl->need_space;
   char* scr = static_cast<char*>(ctx->scr);
   P.scr_keys = scr + ((uintptr_t)keys & 15);
   P.scr_pay = reinterpret_cast<uint8_t*>(scr + scr_k + (w ? ((uintptr_t)payload & 15) : 0));
   // plan (splits + reset) then engine
-  int64_t plan_work = std::max<int64_t>((P.Q + 1) * 32, P.K);
+  int64_t plan_work = std::max<int64_t>(P.Q + 1, P.K);
   int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((plan_work + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
   ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
@@ -198,6 +203,13 @@ static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* paylo
 extern "C" {
 
 int pm_version(void) { return 100; }
+
+int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
+  if (!ctx || !host_out || n < 0) return fail(PM_ERR_ARG, "bad arguments");
+  PM_CUDA(cudaDeviceSynchronize());
+  PM_CUDA(cudaMemcpy(host_out, ctx->ws, (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return PM_OK;
+}
 
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t* out4) {
   if (Q < 1 || qc < 0 || qc >= Q || t < 0 || t >= Q || !out4) return fail(PM_ERR_ARG, "bad order arguments");

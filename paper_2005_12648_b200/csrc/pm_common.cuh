@@ -85,6 +85,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// named barrier among `count` threads (id 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ---- bounded spinning --------------------------------------------------------
 // Every wait polls the job's error word; after ~kSpinLimit polls it raises
 // PM_ERR_TIMEOUT so a protocol bug surfaces as an error, never as a hung GPU.

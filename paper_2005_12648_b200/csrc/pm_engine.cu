@@ -48,11 +48,25 @@ struct Geo {
   __device__ int64_t region_of_ticket(int64_t t) const { return tf().region_of_ticket(t); }
   __device__ int64_t order(int64_t q) const { return tf().order(q); }
   __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const { tf().window(t, lo, hi); }
+  // split of boundary q; boundaries beyond the plan's first `look` tickets are
+  // written by the engine's lookahead (-1 until then)
+  __device__ int64_t split(int64_t q) const {
+    int64_t v = ld_acquire64(&P.split_a[q]);
+    for (uint32_t it = 0; v < 0; ++it) {
+      if (it > kSpinLimit || ld_relaxed(P.err)) {
+        raise_error(P.err, PM_ERR_TIMEOUT);
+        return 0;
+      }
+      backoff(it);
+      v = ld_acquire64(&P.split_a[q]);
+    }
+    return v;
+  }
   // records of unit j consumed by the regions of the ticket window <= t
   __device__ int64_t consumed_by_window(int64_t j, int64_t t) const {
     int64_t wl, wr;
     window(t, wl, wr);
-    int64_t a_lo = P.split_a[wl], a_hi = P.split_a[wr + 1];
+    int64_t a_lo = split(wl), a_hi = split(wr + 1);
     int64_t b_lo = diag(wl) - a_lo, b_hi = diag(wr + 1) - a_hi;
     int64_t x0 = slot_lo(j), x1 = slot_hi(j), c = 0;
     // A part of the unit, A-local indices
@@ -100,20 +114,25 @@ __device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* n
 template <typename KT>
 __global__ void k_plan(EngineParams P) {
   Geo g(P);
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
-  for (int64_t q = warp; q <= P.Q; q += nwarps) {
-    int64_t d = g.diag(q), a;
-    if (P.mode == MODE_MERGE) {
-      a = merge_path_warp<KT>(keys + P.s, la, keys + P.m, lb, d, lane);
-    } else {  // rotation: outputs are B then A
-      a = d - lb;
-      a = a < 0 ? 0 : (a > la ? la : a);
+  // one thread per region boundary: plain binary search of the stable merge path
+  // (2 independent loads per step, every search in flight at once -- far fewer
+  // DRAM sectors than a 33-ary warp search)
+  {
+    const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthr0 = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = tid0; q <= P.Q; q += nthr0) {
+      const int64_t d = g.diag(q);
+      int64_t a;
+      if (P.mode == MODE_MERGE) {
+        a = merge_path_thread<KT>(keys + P.s, la, keys + P.m, lb, d);
+      } else {  // rotation: outputs are B then A
+        a = d - lb;
+        a = a < 0 ? 0 : (a > la ? la : a);
+      }
+      P.split_a[q] = a;
     }
-    if (lane == 0) P.split_a[q] = a;
   }
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
@@ -134,6 +153,7 @@ __global__ void k_plan(EngineParams P) {
     bool nothing = (la == 0 || lb == 0);
     if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
+    *P.need_space = 0;
     for (int i = 0; i < 16; ++i) P.stats[i] = 0;
   }
 }
@@ -142,73 +162,203 @@ __global__ void k_plan(EngineParams P) {
 // k_engine
 // ============================================================================
 
+constexpr int kCache = 64;   // CTA-local caches of free slots / free scratch units
+constexpr int kMaxMu = 8;    // slots per region handled by the occupant warps
+
 struct SmemCtl {
   uint64_t bar;
   int64_t tk;
-  int32_t occ[16];
-  int32_t occ_dest[16];
+  int64_t nx_a0, nx_a1;  // split_a of the next ticket's region (prefetched)
+  int32_t occ[kMaxMu];
+  int32_t early[kMaxMu];
+  int32_t early_cnt;     // occupant warps that sampled reads[] before publishing
+  int32_t published;     // this region's reads are published
+  int32_t lock;          // protects the caches below
+  int32_t n_fs, n_sc;
+  int32_t abort;
+  int32_t fs[kCache];    // free slots (may go stale: their region can start meanwhile)
+  int32_t sc[kCache];    // free scratch units
 };
 
-// Free slots and free scratch units live in kShards Treiber stacks; a CTA pushes
-// to and pops from its own shard first and scans the others only when it runs
-// dry.  One global stack serialised 400+ CTAs on a single CAS word; per-CTA
-// private lists starved other CTAs (hoarding).
-__device__ __forceinline__ int32_t sharded_pop(unsigned long long* tops, int32_t* next, int home) {
-  for (int k = 0; k < kShards; ++k) {
-    const int sh = (home + k) & (kShards - 1);
-    if ((uint32_t)(*(volatile unsigned long long*)&tops[sh] & 0xFFFFFFFFull) == kEmpty32) continue;
-    const int32_t v = stack_pop(&tops[sh], next);
-    if (v >= 0) return v;
-  }
-  return -1;
-}
-
+// ---- sharded global free lists (one CAS word per shard) --------------------
 // warp-cooperative pop: lanes read all shard tops at once, then lane 0 pops the
-// nearest non-empty shard (home first).  Returns -1 if every shard looked empty.
+// nearest non-empty shard (home first), reusing the scanned top as the CAS
+// expectation.  Returns -1 if every shard looked empty.
 __device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* next, int home, int lane) {
-  const uint32_t a = (uint32_t)(*(volatile unsigned long long*)&tops[(home + lane) & (kShards - 1)]);
-  const uint32_t b = (uint32_t)(*(volatile unsigned long long*)&tops[(home + 32 + lane) & (kShards - 1)]);
-  unsigned ma = __ballot_sync(0xffffffffu, a != kEmpty32);
-  unsigned mb = __ballot_sync(0xffffffffu, b != kEmpty32);
+  const unsigned long long a = *(volatile unsigned long long*)&tops[(home + lane) & (kShards - 1)];
+  const unsigned long long b = *(volatile unsigned long long*)&tops[(home + 32 + lane) & (kShards - 1)];
+  unsigned ma = __ballot_sync(0xffffffffu, (uint32_t)a != kEmpty32);
+  unsigned mb = __ballot_sync(0xffffffffu, (uint32_t)b != kEmpty32);
   int32_t v = -1;
   while ((ma | mb) && v < 0) {
-    int sh;
+    int src_lane, sh;
+    unsigned long long old;
     if (ma) {
-      sh = (home + __ffs(ma) - 1) & (kShards - 1);
+      src_lane = __ffs(ma) - 1;
       ma &= ma - 1;
+      old = __shfl_sync(0xffffffffu, a, src_lane);
+      sh = (home + src_lane) & (kShards - 1);
     } else {
-      sh = (home + 32 + __ffs(mb) - 1) & (kShards - 1);
+      src_lane = __ffs(mb) - 1;
       mb &= mb - 1;
+      old = __shfl_sync(0xffffffffu, b, src_lane);
+      sh = (home + 32 + src_lane) & (kShards - 1);
     }
-    if (lane == 0) v = stack_pop(&tops[sh], next);
+    if (lane == 0) {
+      while ((uint32_t)old != kEmpty32) {
+        const uint32_t idx = (uint32_t)old;
+        const int32_t nxt = *(volatile int32_t*)&next[idx];
+        const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (uint32_t)nxt;
+        const unsigned long long seen = atomicCAS(&tops[sh], old, nw);
+        if (seen == old) {
+          __threadfence();
+          v = (int32_t)idx;
+          break;
+        }
+        old = seen;
+      }
+    }
     v = __shfl_sync(0xffffffffu, v, 0);
   }
   return v;
 }
 
-// copy n (< 16) bytes that lie inside one aligned 16-byte chunk: one vector load
-__device__ __forceinline__ void copy_small_g2s(uint8_t* dst, const uint8_t* src, int n) {
-  if (n <= 0) return;
-  const uintptr_t a = (uintptr_t)src & ~(uintptr_t)15;
-  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a));
+// ---- CTA-local caches (shared memory, short spinlock) -----------------------
+__device__ __forceinline__ void cta_lock(SmemCtl& c) {
+  while (atomicCAS(&c.lock, 0, 1) != 0) {
+  }
+  __threadfence_block();
+}
+__device__ __forceinline__ void cta_unlock(SmemCtl& c) {
+  __threadfence_block();
+  atomicExch(&c.lock, 0);
+}
+// push a freed slot (v >= 0) or scratch unit (v = -(i+1)); overflow goes global
+__device__ __forceinline__ void cache_push(SmemCtl& c, const EngineParams& P, int32_t v, int home) {
+  cta_lock(c);
+  bool done = false;
+  if (v >= 0 && c.n_fs < kCache) {
+    c.fs[c.n_fs++] = v;
+    done = true;
+  } else if (v < 0 && c.n_sc < kCache) {
+    c.sc[c.n_sc++] = -v - 1;
+    done = true;
+  }
+  cta_unlock(c);
+  if (!done) {
+    if (v >= 0) stack_push(&P.free_top[home], P.next_free, v);
+    else stack_push(&P.scr_top[home], P.next_scr, -v - 1);
+  }
+}
+// give every cached unit back to the global lists (another CTA is starving)
+__device__ __forceinline__ void cache_flush(SmemCtl& c, const EngineParams& P, int home) {
+  cta_lock(c);
+  const int nf = c.n_fs, ns = c.n_sc;
+  c.n_fs = 0;
+  c.n_sc = 0;
+  int32_t fs[kCache], sc[kCache];
+  for (int i = 0; i < nf; ++i) fs[i] = c.fs[i];
+  for (int i = 0; i < ns; ++i) sc[i] = c.sc[i];
+  cta_unlock(c);
+  for (int i = 0; i < nf; ++i) stack_push(&P.free_top[home], P.next_free, fs[i]);
+  for (int i = 0; i < ns; ++i) stack_push(&P.scr_top[home], P.next_scr, sc[i]);
+}
+
+// Warp-wide: a salvage destination for unit u.  Scratch first (a parked unit is
+// never moved again), then free slots; CTA cache first, then the global lists.
+// Called only after this region has read its inputs (stage B done), so a
+// blocked caller never holds space other regions wait for.  When it has to
+// block it raises need_space so CTAs flush their caches.
+__device__ __forceinline__ int32_t acquire_dest(SmemCtl& c, const EngineParams& P, int32_t u, int home, int lane,
+                                                bool block) {
+  bool flagged = false;
+  int32_t dest = INT32_MIN;
+  for (uint32_t it = 0;; ++it) {
+    int32_t d = INT32_MIN;
+    if (lane == 0) {
+      cta_lock(c);
+      if (c.n_sc > 0) {
+        d = -c.sc[--c.n_sc] - 1;
+        cta_unlock(c);
+      } else {
+        int32_t f = -1;
+        while (c.n_fs > 0) {
+          f = c.fs[--c.n_fs];
+          if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) break;
+          f = -1;  // its region started meanwhile
+        }
+        cta_unlock(c);
+        if (f >= 0) d = f;
+      }
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (d != INT32_MIN) {
+      dest = d;
+      break;
+    }
+    const int32_t si = warp_pop(P.scr_top, P.next_scr, home, lane);
+    if (si >= 0) {
+      dest = -si - 1;
+      break;
+    }
+    int32_t f;
+    bool got = false;
+    while ((f = warp_pop(P.free_top, P.next_free, home, lane)) >= 0) {
+      int ok = 0;
+      if (lane == 0) ok = atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE;
+      if (__shfl_sync(0xffffffffu, ok, 0)) {
+        got = true;
+        break;
+      }
+    }
+    if (got) {
+      dest = f;
+      break;
+    }
+    if (!block || ld_relaxed(P.err)) break;
+    if (!flagged && it > 32) {
+      if (lane == 0) atomicAdd(P.need_space, 1);
+      flagged = true;
+    }
+    if (it > kSpinLimit) {
+      if (lane == 0) raise_error(P.err, PM_ERR_NOSPACE);
+      break;
+    }
+    backoff(it);
+  }
+  if (flagged && lane == 0) atomicSub(P.need_space, 1);
+  return dest;
+}
+
+// copy n (< 16) bytes that lie inside one aligned 16-byte chunk, from a vector
+// already loaded by the caller
+__device__ __forceinline__ void put_small(uint8_t* dst, const uint4& v, const uint8_t* src, int n) {
   const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
-  const int o = (int)((uintptr_t)src - a);
+  const int o = (int)((uintptr_t)src & 15);
   for (int i = 0; i < n; ++i) dst[i] = b[o + i];
+}
+__device__ __forceinline__ uint4 load_chunk(const uint8_t* src, int n) {
+  if (n <= 0) return make_uint4(0, 0, 0, 0);
+  return __ldcg(reinterpret_cast<const uint4*>((uintptr_t)src & ~(uintptr_t)15));
 }
 
 // global -> shared, identical 16-byte phase on both sides: TMA bulk copy for the
-// aligned body, one vector load each for the unaligned head and tail
+// aligned body, one vector load each for the unaligned head and tail (both
+// issued before either is used)
 __device__ __forceinline__ void copy_g2s_phased(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar) {
   if (nbytes <= 0) return;
   int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
   if (head > nbytes) head = nbytes;
   const int64_t body = ((nbytes - head) >> 4) << 4;
+  const int tail = (int)(nbytes - head - body);
+  const uint4 vh = load_chunk(src, (int)head);
+  const uint4 vt = load_chunk(src + head + body, tail);
   if (body > 0) {
     mbar_expect_tx(bar, (uint32_t)body);
     bulk_g2s(dst + head, src + head, (uint32_t)body, bar);
   }
-  copy_small_g2s(dst, src, (int)head);
-  copy_small_g2s(dst + head + body, src + head + body, (int)(nbytes - head - body));
+  if (head) put_small(dst, vh, src, (int)head);
+  if (tail) put_small(dst + head + body, vt, src + head + body, tail);
 }
 
 // warp copy global -> global, identical 16-byte phase on both sides; all loads of
@@ -234,47 +384,16 @@ __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, 
   if (tail0 + lane < nbytes) dst[tail0 + lane] = src[tail0 + lane];
 }
 
-// Warp-wide: a salvage destination for unit u -- scratch first (a parked unit is
-// never moved again), then a free slot.  Blocking waits only after the caller
-// has published its own reads (they are what frees space).
-__device__ __forceinline__ int32_t acquire_dest(const EngineParams& P, int32_t u, int home, int lane, bool block) {
-  for (uint32_t it = 0;; ++it) {
-    int32_t si = warp_pop(P.scr_top, P.next_scr, home, lane);
-    if (si >= 0) return -si - 1;
-    int32_t f;
-    while ((f = warp_pop(P.free_top, P.next_free, home, lane)) >= 0) {
-      int ok = 0;
-      if (lane == 0) ok = atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE;
-      if (__shfl_sync(0xffffffffu, ok, 0)) return f;
-    }
-    if (!block || ld_relaxed(P.err)) return INT32_MIN;
-    if (it > kSpinLimit) {
-      if (lane == 0) raise_error(P.err, PM_ERR_NOSPACE);
-      return INT32_MIN;
-    }
-    backoff(it);
-  }
-}
-
-template <typename KT>
-__device__ __forceinline__ void pool_push_dest(const EngineParams& P, int32_t dest, int home) {
-  if (dest >= 0) {
-    st_release(&P.state[dest], ST_FREE);
-    stack_push(&P.free_top[home], P.next_free, dest);
-  } else {
-    stack_push(&P.scr_top[home], P.next_scr, -dest - 1);
-  }
-}
-
-// Warp roles inside the 256-thread CTA, per region:
-//   A  all    : ticket (prefetched one region ahead), geometry, close the slots
-//   B  w0..3  : one warp per occupied slot: wait for a landing unit, then take a
-//               salvage destination speculatively (scratch first, then free slot)
-//      w4..7  : gather the region's A/B pieces (TMA bulk + vector head/tail)
-//   C  all    : wait for the bulk copies; publish reads; free dead units
-//   D  w0..3  : wait for earlier consumers; keep or give back the destination
-//   E  all    : copy salvaged units (two warps per unit), publish their new homes
-//   F  all    : merge path per thread in shared memory, stream the region back
+// Per region, warp roles in the 256-thread CTA:
+//   A   thread 0 : hand out the prefetched ticket (+ prefetched split values)
+//   B   w0..3    : lane 0 closes slot i, prefetches the occupant's loc / reads
+//       w4..7    : gather the region's A/B pieces (TMA bulk + vector head/tail)
+//   C/D w0..3    : lanes 1-31 publish this region's reads (last reader frees the
+//                  unit into the CTA cache); lane 0 waits for the occupant to
+//                  land and for earlier consumers, takes a destination; then
+//                  the whole warp moves the unit and publishes its new home
+//       w4..7    : merge path of every output in shared memory
+//   F   all      : stream the region back in place (16-byte vector stores)
 template <typename KT>
 __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   extern __shared__ __align__(128) uint8_t dyn[];
@@ -289,52 +408,50 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   uint8_t* kin = dyn;                         // staged keys (A then B, phase-shifted)
   uint8_t* pin = dyn + P.smem_keys;           // staged payload
   int32_t* src = reinterpret_cast<int32_t*>(dyn + P.smem_keys + P.smem_pay);  // padded output->input map
-  if (tid == 0) mbar_init(&ctl.bar, 1);
-  __syncthreads();
+  constexpr int kOccWarps = 4;                 // warps 0..3 own occupants; 4..7 gather + merge
   const int home = blockIdx.x & (kShards - 1);
-  uint32_t phase = 0;
   const int64_t la = g.LA();
-  constexpr int kGatherWarp0 = 4;  // warps 4..7 gather
-  // per-CTA accounting, flushed once at the end (no per-region global atomics)
+  uint32_t phase = 0;
   unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
   unsigned long long n_salv = 0, r_salv = 0, n_reg = 0, n_ident = 0, spins_r = 0, spins_o = 0;
   unsigned long long w_land = 0, w_thr = 0, w_dest = 0, w_copy = 0;
   long long tc = clock64();
   int32_t t_pref = 0;
-  if (tid == 0) t_pref = atomicAdd(P.ticket, 1);
+  if (tid == 0) {
+    mbar_init(&ctl.bar, 1);
+    ctl.lock = 0;
+    ctl.n_fs = 0;
+    ctl.n_sc = 0;
+    ctl.abort = 0;
+    ctl.early_cnt = 0;
+    ctl.published = 0;
+    t_pref = atomicAdd(P.ticket, 1);
+    if (t_pref < P.Q) {
+      const int64_t q = g.region_of_ticket(t_pref);
+      ctl.nx_a0 = g.split(q);
+      ctl.nx_a1 = g.split(q + 1);
+    }
+  }
+  __syncthreads();
 
   while (true) {
+    // ---------------- A: ticket -------------------------------------------------
     if (tid == 0) {
       const int32_t t = t_pref;
+      ctl.tk = ctl.abort ? P.Q : t;
       t_pref = atomicAdd(P.ticket, 1);  // next ticket, in flight during this region
-      ctl.tk = (*(volatile int32_t*)P.err) ? P.Q : t;
     }
     __syncthreads();
     const int64_t t = ctl.tk;
     if (t >= P.Q) break;
-    // ---------------- A: geometry, close the slots ----------------------------
     const int64_t q = g.region_of_ticket(t);
     const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
     const int nslot = (int)(j1 - j0);
-    if (tid < nslot) {
-      ctl.occ[tid] = atomicExch(&P.state[j0 + tid], ST_CLOSED);
-      ctl.occ_dest[tid] = INT32_MIN;
-    }
     const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-    const int64_t a0 = P.split_a[q], a1 = P.split_a[q + 1];
+    const int64_t a0 = ctl.nx_a0, a1 = ctl.nx_a1;
     const int64_t b0 = d0 - a0, b1 = d1 - a1;
     const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
     const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-    __syncthreads();
-    if (tid == 0) {
-      long long n = clock64();
-      cyc[0] += n - tc;
-      tc = n;
-    }
-    if (identity) {
-      ++n_ident;
-      continue;  // inputs already sit on their outputs; units consumed by q only
-    }
     const int64_t xa = P.s + a0, xb = P.m + b0;  // absolute first elements of the runs
     const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
     const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
@@ -346,9 +463,118 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
     const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
     const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
     const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
-    // ---------------- B: gather the region's A/B pieces --------------------------
-    {
-      for (int p = tid; p < np; p += NT) {
+    // ---------------- B/C/D -------------------------------------------------------
+    // occupant warps (0..3): close slot i, then -- concurrently with the gather --
+    // move its unit if a later region still needs it.  Gather warps (4..7): load
+    // the region's pieces, publish the reads, merge in shared memory.
+    if (wid < kOccWarps) {
+      for (int i = wid; i < nslot; i += kOccWarps) {
+        int32_t u = -1, early_r = 0;
+        int32_t early_l = -1;
+        if (lane == 0) {
+          // sample reads[]/loc[] of the home unit together with the exchange (the
+          // occupant is usually the home unit); both are taken before this region
+          // publishes anything (publishers wait for every occupant warp), so the
+          // count covers other consumers only
+          const int32_t home_u = (int32_t)(j0 + i);
+          int32_t r_h = 0, l_h = -1;
+          if (!identity) {
+            r_h = ld_acquire(&P.reads[home_u]);
+            l_h = ld_acquire(&P.loc[home_u]);
+          }
+          u = atomicExch(&P.state[j0 + i], ST_CLOSED);
+          ctl.occ[i] = u;
+          if (u == home_u) {
+            early_r = r_h;
+            early_l = l_h;
+          } else if (u >= 0 && !identity) {
+            early_r = ld_acquire(&P.reads[u]);
+          }
+          ctl.early[i] = early_r;
+        }
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (lane == 0) atomicAdd(&ctl.early_cnt, 1);
+        if (u < 0 || identity) continue;
+        long long c1 = clock64();
+        int alive = 0;
+        if (lane == 0) {
+          const int32_t slot = (int32_t)(j0 + i);
+          for (uint32_t it = 0; early_l != slot && ld_acquire(&P.loc[u]) != slot; ++it) {  // landing
+            if (ld_relaxed(P.err)) {
+              ctl.abort = 1;
+              break;
+            }
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              ctl.abort = 1;
+              break;
+            }
+            backoff(it);
+          }
+          // every consumer of order < t must have read u (our own read is irrelevant:
+          // its data is already on its way to shared memory)
+          const int64_t thr = g.consumed_by_window(u, t);
+          const int64_t own = thr - (t > 0 ? g.consumed_by_window(u, t - 1) : 0);
+          if (early_r < thr - own) {
+            for (uint32_t it = 0; ld_acquire(&P.reads[u]) < thr; ++it) {  // reloads may include ours
+              ++spins_o;
+              if (ld_relaxed(P.err)) {
+                ctl.abort = 1;
+                break;
+              }
+              if (it > kSpinLimit) {
+                raise_error(P.err, PM_ERR_TIMEOUT);
+                ctl.abort = 1;
+                break;
+              }
+              if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
+              backoff(it);
+            }
+          }
+          alive = thr < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
+        }
+        alive = __shfl_sync(0xffffffffu, alive, 0);
+        long long c2 = clock64();
+        w_thr += c2 - c1;
+        if (!alive) continue;
+        // try without blocking first; block only once this region's reads are published
+        int32_t dest = acquire_dest(ctl, P, u, home, lane, false);
+        if (dest == INT32_MIN) {
+          while (!*(volatile int32_t*)&ctl.published) {
+          }
+          dest = acquire_dest(ctl, P, u, home, lane, true);
+        }
+        long long c3 = clock64();
+        w_dest += c3 - c2;
+        if (dest == INT32_MIN) {
+          if (lane == 0) ctl.abort = 1;
+          continue;
+        }
+        const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
+        const int64_t sbase = g.slot_base(j0 + i);
+        const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
+        char* kd = dest >= 0 ? P.keys + (dbase + (x0 - hb)) * ks
+                             : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * ks;
+        copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
+                      reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks), (x1 - x0) * ks, lane);
+        if (w) {
+          uint8_t* pd = dest >= 0 ? P.pay + (dbase + (x0 - hb)) * w
+                                  : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * w;
+          copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          st_release(&P.loc[u], dest);
+          ++n_salv;
+          r_salv += (unsigned long long)(x1 - x0);
+        }
+        w_copy += clock64() - c3;
+      }
+      if (wid >= nslot && lane == 0) atomicAdd(&ctl.early_cnt, 1);  // idle occupant warps sample nothing
+    } else if (!identity) {
+      const int gt = tid - kOccWarps * 32, GT = NT - kOccWarps * 32;  // gather threads
+      for (int p = gt; p < np; p += GT) {
         const bool isA = p < npa;
         const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
         const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
@@ -358,11 +584,16 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
         for (uint32_t it = 0;; ++it) {
           l = ld_acquire(&P.loc[j]);
           if (l < 0 || g.order(g.region_of_slot(l)) >= t) break;
-          if (ld_relaxed(P.err)) break;
-          if (it > kSpinLimit) {
-            raise_error(P.err, PM_ERR_TIMEOUT);
+          if (ld_relaxed(P.err)) {
+            ctl.abort = 1;
             break;
           }
+          if (it > kSpinLimit) {
+            raise_error(P.err, PM_ERR_TIMEOUT);
+            ctl.abort = 1;
+            break;
+          }
+          if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
           ++spins_r;
           backoff(it);
         }
@@ -385,98 +616,42 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
         }
       }
-    }
-    __syncthreads();  // every expect_tx registered before the single arrive
-    if (tid == 0) {
-      long long n = clock64();
-      cyc[1] += n - tc;
-      tc = n;
-      mbar_arrive(&ctl.bar);
-    }
-    // ---------------- C: land, publish reads, free dead units ------------------
-    while (!mbar_try_wait(&ctl.bar, phase)) {
-    }
-    phase ^= 1;
-    __syncthreads();
-    if (tid == 0) {
-      long long n = clock64();
-      cyc[2] += n - tc;
-      tc = n;
-    }
-    for (int p = tid; p < np; p += NT) {
-      const bool isA = p < npa;
-      const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
-      const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-      const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-      __threadfence();
-      const int32_t n = (int32_t)(x1 - x0);
-      const int32_t old = atomicAdd(&P.reads[j], n);
-      if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
-        const int32_t l = ld_acquire(&P.loc[j]);
-        if (l < 0) {
-          stack_push(&P.scr_top[home], P.next_scr, -l - 1);
-        } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
-          stack_push(&P.free_top[home], P.next_free, l);
+      named_barrier_sync(1, GT);  // all expect_tx registered before the single arrive
+      if (gt == 0) mbar_arrive(&ctl.bar);
+      while (!mbar_try_wait(&ctl.bar, phase)) {
+      }
+      // publish the reads (after every occupant warp sampled its early read count);
+      // the last reader frees the unit into the CTA cache
+      while (*(volatile int32_t*)&ctl.early_cnt < nslot + (nslot < kOccWarps ? kOccWarps - nslot : 0)) {
+      }
+      for (int p = gt; p < np; p += GT) {
+        const bool isA = p < npa;
+        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+        __threadfence();
+        const int32_t n = (int32_t)(x1 - x0);
+        const int32_t old = atomicAdd(&P.reads[j], n);
+        if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
+          const int32_t l = ld_acquire(&P.loc[j]);
+          if (l < 0) {
+            cache_push(ctl, P, l, home);
+          } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
+            cache_push(ctl, P, l, home);
+          }
         }
       }
-    }
-    const KT* As = reinterpret_cast<const KT*>(kin + offA);
-    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-    const int MT = NT - kGatherWarp0 * 32, mt = tid - kGatherWarp0 * 32;  // merge threads
-    const int64_t E = (nout + MT - 1) / MT;
-    const int64_t V = 16 / ks;  // keys per 16-byte vector
-    // output o is staged at padded index P(o + ph) so strided writes avoid bank conflicts
-    const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
-    // ---------------- D: salvage decisions (w0..3) || merge path (w4..7) ---------
-    if (wid < kGatherWarp0) {
-      for (int i = wid; i < nslot; i += kGatherWarp0) {
-        const int32_t u = ctl.occ[i];
-        if (u < 0) continue;
-        long long c1 = clock64();
-        int32_t r = 0;
-        if (lane == 0) {
-          const int32_t slot = (int32_t)(j0 + i);
-          for (uint32_t it = 0; ld_acquire(&P.loc[u]) != slot; ++it) {  // landing (reads are published now)
-            if (ld_relaxed(P.err)) break;
-            if (it > kSpinLimit) {
-              raise_error(P.err, PM_ERR_TIMEOUT);
-              break;
-            }
-            backoff(it);
-          }
-          const int32_t thr = (int32_t)g.consumed_by_window(u, t);
-          for (uint32_t it = 0; (r = ld_acquire(&P.reads[u])) < thr; ++it) {
-            ++spins_o;
-            if (ld_relaxed(P.err)) break;
-            if (it > kSpinLimit) {
-              raise_error(P.err, PM_ERR_TIMEOUT);
-              break;
-            }
-            backoff(it);
-          }
-        }
-        r = __shfl_sync(0xffffffffu, r, 0);
-        const int32_t usz = (int32_t)(g.slot_hi(u) - g.slot_lo(u));
-        const bool alive = r < usz && !ld_relaxed(P.err);
-        const int32_t dest = ctl.occ_dest[i];
-        __syncwarp();
-        if (!alive && dest != INT32_MIN) {
-          if (lane == 0) {
-            pool_push_dest<KT>(P, dest, home);  // give the speculative destination back
-            ctl.occ_dest[i] = INT32_MIN;
-          }
-        } else if (alive && dest == INT32_MIN) {
-          const int32_t d = acquire_dest(P, u, home, lane, true);
-          if (lane == 0) ctl.occ_dest[i] = d;
-        }
-        w_thr += clock64() - c1;
-      }
-    }
-    if (wid >= kGatherWarp0) {
-      int64_t o = min((int64_t)mt * E, nout), oe = min(o + E, nout);
+      named_barrier_sync(1, GT);
+      if (gt == 0) atomicExch(&ctl.published, 1);
+      // merge path of every output (A wins ties) into the padded output->input map
+      const KT* As = reinterpret_cast<const KT*>(kin + offA);
+      const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+      const int64_t E = (nout + GT - 1) / GT;
+      const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
+      int64_t o = min((int64_t)gt * E, nout), oe = min(o + E, nout);
       if (P.mode == MODE_MERGE) {
         int64_t lo = o > beta ? o - beta : 0, hi = o < alpha ? o : alpha;
-        while (lo < hi) {  // merge-path split of this thread's diagonal (A wins ties)
+        while (lo < hi) {
           int64_t mid = (lo + hi) >> 1;
           if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
           else hi = mid;
@@ -501,56 +676,45 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           src[op + (op >> 5)] = o < beta ? (int32_t)(alpha + o) : (int32_t)(o - beta);
         }
       }
+    } else {
+      if (wid == kOccWarps && lane == 0) atomicExch(&ctl.published, 1);
     }
-    __syncthreads();
-    if (ld_relaxed(P.err)) break;
-    // ---------------- E: move the salvaged units ---------------------------------
-    {
-      long long c3 = clock64();
-      const int NW = NT >> 5;
-      for (int job = wid; job < 2 * nslot; job += NW) {
-        const int i = job >> 1, half = job & 1;
-        const int32_t u = ctl.occ[i], dest = ctl.occ_dest[i];
-        if (u < 0 || dest == INT32_MIN) continue;
-        const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
-        const int64_t xm = x0 + (((x1 - x0) >> 1) & ~(int64_t)15);
-        const int64_t y0 = half ? xm : x0, y1 = half ? x1 : xm;
-        const int64_t sbase = g.slot_base(j0 + i);
-        const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
-        char* kd = dest >= 0 ? P.keys + (dbase + (y0 - hb)) * ks
-                             : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (y0 - hb)) * ks;
-        copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
-                      reinterpret_cast<const uint8_t*>(P.keys + (sbase + (y0 - hb)) * ks), (y1 - y0) * ks, lane);
-        if (w) {
-          uint8_t* pd = dest >= 0 ? P.pay + (dbase + (y0 - hb)) * w
-                                  : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (y0 - hb)) * w;
-          copy_g2g_warp(pd, P.pay + (sbase + (y0 - hb)) * w, (y1 - y0) * w, lane);
-        }
-      }
+    if (identity) {
+      ++n_ident;
       __syncthreads();
-      if (tid < nslot) {
-        const int32_t u = ctl.occ[tid], dest = ctl.occ_dest[tid];
-        if (u >= 0 && dest != INT32_MIN) {
-          __threadfence();
-          st_release(&P.loc[u], dest);
-          ++n_salv;
-          r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
+      if (tid == 0) {
+        ctl.early_cnt = 0;
+        ctl.published = 0;
+        if (t_pref < P.Q) {
+          const int64_t qn = g.region_of_ticket(t_pref);
+          ctl.nx_a0 = g.split(qn);
+          ctl.nx_a1 = g.split(qn + 1);
         }
       }
-      if (lane == 0) w_copy += clock64() - c3;
+      continue;
     }
+    phase ^= 1;
+    __syncthreads();
     if (tid == 0) {
       long long n = clock64();
       cyc[3] += n - tc;
       tc = n;
+      ctl.early_cnt = 0;
+      ctl.published = 0;
+      // prefetch the next region's splits while this one streams out
+      if (t_pref < P.Q) {
+        const int64_t qn = g.region_of_ticket(t_pref);
+        ctl.nx_a0 = g.split(qn);
+        ctl.nx_a1 = g.split(qn + 1);
+      }
     }
-    __syncthreads();
-    if (tid == 0) {
-      long long n = clock64();
-      cyc[4] += n - tc;
-      tc = n;
-    }
+    if (ctl.abort) break;
+    // ---------------- F: stream the region back in place ----------------------
     {
+      const KT* As = reinterpret_cast<const KT*>(kin + offA);
+      const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+      const int64_t V = 16 / ks;  // keys per 16-byte vector
+      const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
       KT* kout = reinterpret_cast<KT*>(P.keys) + (P.s + d0) - ph;  // 16B aligned when keys base is
       const int64_t ngroups = (ph + nout + V - 1) / V;
       const bool kal = (((uintptr_t)kout) & 15) == 0;
@@ -616,8 +780,11 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
       long long n = clock64();
       cyc[5] += n - tc;
       tc = n;
+      if (*(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
     }
   }
+  // leave nothing behind in the CTA cache (another job reuses the lists)
+  if (tid == 0) cache_flush(ctl, P, home);
   if (n_salv) {
     atomicAdd(&P.stats[0], n_salv);
     atomicAdd(&P.stats[1], r_salv);

@@ -92,7 +92,8 @@ struct EngineParams {
   unsigned long long* scr_top;
   int32_t* scr_count;  // free scratch units (heuristic only)
   int64_t S;           // scratch units
-  int32_t grid;        // engine CTAs (each owns s_per scratch units at start)
+  int32_t grid;        // engine CTAs
+  int64_t look;        // split lookahead distance in tickets (merge mode)
   int64_t s_per;
   int64_t reserve;     // keep this many scratch units for the no-free-slot case
   char* scr_keys;      // phase-matched scratch bases
@@ -100,6 +101,7 @@ struct EngineParams {
   int32_t* ticket;
   int32_t* err;
   int32_t* noop;       // set by the plan kernel when the job needs no work
+  int32_t* need_space; // > 0 while some CTA is blocked on salvage space: CTAs flush their caches
   unsigned long long* stats;  // [4]: salvaged units, salvaged records, regions, identity regions
   size_t smem_keys;    // bytes reserved for staged keys
   size_t smem_pay;     // bytes reserved for staged payload

@@ -9,11 +9,11 @@
 
 namespace pm {
 
+// largest a in [lo, hi] such that A[i] <= B[d-1-i] for every i < a (A wins ties);
+// the caller guarantees the answer lies in [lo, hi].
 template <typename KT>
-__device__ __forceinline__ int64_t merge_path_warp(const KT* A, int64_t la, const KT* B, int64_t lb, int64_t d,
-                                                   int lane) {
-  // largest a in [lo, hi] with: A[i] <= B[d-1-i] for all i < a  (A wins ties)
-  int64_t lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+__device__ __forceinline__ int64_t merge_path_warp_in(const KT* A, const KT* B, int64_t d, int64_t lo, int64_t hi,
+                                                      int lane) {
   while (hi - lo > 32) {
     int64_t span = hi - lo;
     int64_t p = lo + ((int64_t)(lane + 1) * span) / 33;  // p in [lo, hi)
@@ -33,6 +33,26 @@ __device__ __forceinline__ int64_t merge_path_warp(const KT* A, int64_t la, cons
   bool f = p < hi ? (A[p] <= B[d - 1 - p]) : false;
   unsigned fb = __ballot_sync(0xffffffffu, !f && p < hi);
   return fb == 0 ? hi : lo + (__ffs(fb) - 1);
+}
+
+// stable merge-path split of diagonal d over the full feasible range
+template <typename KT>
+__device__ __forceinline__ int64_t merge_path_warp(const KT* A, int64_t la, const KT* B, int64_t lb, int64_t d,
+                                                   int lane) {
+  const int64_t lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+  return merge_path_warp_in<KT>(A, B, d, lo, hi, lane);
+}
+
+// one thread: stable merge-path split of diagonal d (A wins ties)
+template <typename KT>
+__device__ __forceinline__ int64_t merge_path_thread(const KT* A, int64_t la, const KT* B, int64_t lb, int64_t d) {
+  int64_t lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(A + mid) <= __ldg(B + d - 1 - mid)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
 }
 
 template <typename KT>
