@@ -87,8 +87,8 @@ static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 static bool pick_tiles(int ks, int64_t w, int64_t* M, int64_t* T, int32_t* mu) {
   const int64_t budget = 72 * 1024;
   int64_t m = 8192;
-  while (m > 16 && m * (ks + w + 5) > budget) m >>= 1;
-  if (m * (ks + w + 5) > budget + 64 * 1024) return false;  // wider than ~130 KB for 16 records
+  while (m > 16 && m * 2 * (ks + w) + 256 > budget) m >>= 1;
+  if (m * 2 * (ks + w) + 256 > budget + 64 * 1024) return false;  // records too wide
   *M = m;
   *T = std::max<int64_t>(16, m / 4);
   *mu = (int32_t)(m / *T);
@@ -124,8 +124,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // shared memory carve-up (all offsets 16-byte aligned)
   P.smem_keys = (size_t)align_up(M * ks + 48, 128);
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
-  const size_t smem_src = (size_t)align_up((M + 16 + (M + 16) / 32 + 4) * 4, 128);
-  const size_t smem = P.smem_keys + P.smem_pay + smem_src;
+  // staged inputs (keys, payload) + merged output tile (keys, payload), same sizes
+  const size_t smem = 2 * (P.smem_keys + P.smem_pay);
   // persistent grid: every resident CTA slot on every SM
   int bps = 0;
   cudaError_t ce = ks == 4 ? engine_occupancy<int32_t>(kEngineThreads, smem, &bps)

@@ -48,20 +48,8 @@ struct Geo {
   __device__ int64_t region_of_ticket(int64_t t) const { return tf().region_of_ticket(t); }
   __device__ int64_t order(int64_t q) const { return tf().order(q); }
   __device__ void window(int64_t t, int64_t& lo, int64_t& hi) const { tf().window(t, lo, hi); }
-  // split of boundary q; boundaries beyond the plan's first `look` tickets are
-  // written by the engine's lookahead (-1 until then)
-  __device__ int64_t split(int64_t q) const {
-    int64_t v = ld_acquire64(&P.split_a[q]);
-    for (uint32_t it = 0; v < 0; ++it) {
-      if (it > kSpinLimit || ld_relaxed(P.err)) {
-        raise_error(P.err, PM_ERR_TIMEOUT);
-        return 0;
-      }
-      backoff(it);
-      v = ld_acquire64(&P.split_a[q]);
-    }
-    return v;
-  }
+  // split of boundary q (computed by k_plan before the engine starts; read-only here)
+  __device__ int64_t split(int64_t q) const { return __ldg(&P.split_a[q]); }
   // records of unit j consumed by the regions of the ticket window <= t
   __device__ int64_t consumed_by_window(int64_t j, int64_t t) const {
     int64_t wl, wr;
@@ -167,12 +155,12 @@ constexpr int kMaxMu = 8;    // slots per region handled by the occupant warps
 
 struct SmemCtl {
   uint64_t bar;
-  int64_t tk;
-  int64_t nx_a0, nx_a1;  // split_a of the next ticket's region (prefetched)
-  int32_t occ[kMaxMu];
-  int32_t early[kMaxMu];
-  int32_t early_cnt;     // occupant warps that sampled reads[] before publishing
-  int32_t published;     // this region's reads are published
+  int64_t t_cur, t_nxt;  // data-team region, salvage-team region (tickets; >= Q: none)
+  int32_t def_u[2][kMaxMu];   // occupants whose move was deferred (no space yet), per parity
+  int32_t def_slot[2][kMaxMu];
+  int32_t n_def[2];
+  int32_t published;     // the data team has published t_cur's reads
+  int32_t deferred_done; // the salvage team has moved t_cur's deferred occupants
   int32_t lock;          // protects the caches below
   int32_t n_fs, n_sc;
   int32_t abort;
@@ -384,16 +372,54 @@ __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, 
   if (tail0 + lane < nbytes) dst[tail0 + lane] = src[tail0 + lane];
 }
 
-// Per region, warp roles in the 256-thread CTA:
-//   A   thread 0 : hand out the prefetched ticket (+ prefetched split values)
-//   B   w0..3    : lane 0 closes slot i, prefetches the occupant's loc / reads
-//       w4..7    : gather the region's A/B pieces (TMA bulk + vector head/tail)
-//   C/D w0..3    : lanes 1-31 publish this region's reads (last reader frees the
-//                  unit into the CTA cache); lane 0 waits for the occupant to
-//                  land and for earlier consumers, takes a destination; then
-//                  the whole warp moves the unit and publishes its new home
-//       w4..7    : merge path of every output in shared memory
-//   F   all      : stream the region back in place (16-byte vector stores)
+// Stream n bytes from a shared-memory tile to global memory with the same 16-byte
+// phase: thread `gt` == 0 issues one TMA bulk store for the aligned body; the
+// first threads write the unaligned head / tail bytes.
+__device__ __forceinline__ void stream_out(const uint8_t* src_s, uint8_t* dst_g, int64_t n, int gt, int GT) {
+  if (n <= 0) return;
+  int64_t head = (16 - ((uintptr_t)dst_g & 15)) & 15;
+  if (head > n) head = n;
+  const int64_t body = ((n - head) >> 4) << 4;
+  const int64_t tail0 = head + body;
+  if (gt == 0 && body > 0) {
+    bulk_s2g(dst_g + head, src_s + head, (uint32_t)body);
+    bulk_commit();
+  }
+  for (int64_t b = gt; b < head; b += GT) dst_g[b] = src_s[b];
+  for (int64_t b = tail0 + gt; b < n; b += GT) dst_g[b] = src_s[b];
+}
+
+// Move unit u out of slot `slot` into `dest` (warp-wide) and publish its new home.
+template <typename KT>
+__device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, int32_t u, int64_t slot, int32_t dest,
+                                          int lane) {
+  const int64_t ks = sizeof(KT), w = P.w;
+  const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
+  const int64_t sbase = g.slot_base(slot);
+  const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
+  char* kd = dest >= 0 ? P.keys + (dbase + (x0 - hb)) * ks : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * ks;
+  copy_g2g_warp(reinterpret_cast<uint8_t*>(kd), reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks),
+                (x1 - x0) * ks, lane);
+  if (w) {
+    uint8_t* pd = dest >= 0 ? P.pay + (dbase + (x0 - hb)) * w : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * w;
+    copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
+  }
+  __threadfence();  // every lane's part is visible before the new home is published
+  __syncwarp();
+  if (lane == 0) st_release(&P.loc[u], dest);
+}
+
+// Software-pipelined persistent engine.  Each iteration of a CTA:
+//   salvage team (warps 0..3) works on ticket t_nxt: closes its slots and moves
+//     every occupant that a later region still needs (after all earlier
+//     consumers have read it) to scratch or a free slot -- without blocking on
+//     space (a miss is deferred); first it finishes t_cur's deferred moves,
+//     which may block, because t_cur's reads are published by then;
+//   data team (warps 4..7) works on ticket t_cur: gathers its A/B pieces into
+//     shared memory (TMA bulk + vector head/tail), publishes the reads, merges
+//     in shared memory, waits for t_cur's deferred moves, streams the region back.
+// The salvage chain (exchange, waits, copies, fences) thus overlaps the
+// previous region's data phase instead of holding the shared-memory buffer.
 template <typename KT>
 __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   extern __shared__ __align__(128) uint8_t dyn[];
@@ -407,8 +433,9 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
 
   uint8_t* kin = dyn;                         // staged keys (A then B, phase-shifted)
   uint8_t* pin = dyn + P.smem_keys;           // staged payload
-  int32_t* src = reinterpret_cast<int32_t*>(dyn + P.smem_keys + P.smem_pay);  // padded output->input map
-  constexpr int kOccWarps = 4;                 // warps 0..3 own occupants; 4..7 gather + merge
+  uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;  // merged output tile (keys), phase-aligned
+  uint8_t* pout_s = kout_s + P.smem_keys;            // merged output tile (payload)
+  constexpr int kTeam = 4;                     // warps per team
   const int home = blockIdx.x & (kShards - 1);
   const int64_t la = g.LA();
   uint32_t phase = 0;
@@ -423,101 +450,101 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
     ctl.n_fs = 0;
     ctl.n_sc = 0;
     ctl.abort = 0;
-    ctl.early_cnt = 0;
-    ctl.published = 0;
+    ctl.n_def[0] = ctl.n_def[1] = 0;
+    ctl.t_cur = P.Q;
+    ctl.t_nxt = atomicAdd(P.ticket, 1);
     t_pref = atomicAdd(P.ticket, 1);
-    if (t_pref < P.Q) {
-      const int64_t q = g.region_of_ticket(t_pref);
-      ctl.nx_a0 = g.split(q);
-      ctl.nx_a1 = g.split(q + 1);
-    }
   }
   __syncthreads();
+  int it_par = 0;  // parity of the deferred list written by the salvage team this iteration
 
   while (true) {
-    // ---------------- A: ticket -------------------------------------------------
-    if (tid == 0) {
-      const int32_t t = t_pref;
-      ctl.tk = ctl.abort ? P.Q : t;
-      t_pref = atomicAdd(P.ticket, 1);  // next ticket, in flight during this region
-    }
-    __syncthreads();
-    const int64_t t = ctl.tk;
-    if (t >= P.Q) break;
-    const int64_t q = g.region_of_ticket(t);
-    const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
-    const int nslot = (int)(j1 - j0);
-    const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-    const int64_t a0 = ctl.nx_a0, a1 = ctl.nx_a1;
-    const int64_t b0 = d0 - a0, b1 = d1 - a1;
-    const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
-    const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-    const int64_t xa = P.s + a0, xb = P.m + b0;  // absolute first elements of the runs
-    const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-    const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
-    int64_t poffA = 0, poffB = 0;
-    if (w) {
-      poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
-      poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
-    }
-    const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
-    const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
-    const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
-    // ---------------- B/C/D -------------------------------------------------------
-    // occupant warps (0..3): close slot i, then -- concurrently with the gather --
-    // move its unit if a later region still needs it.  Gather warps (4..7): load
-    // the region's pieces, publish the reads, merge in shared memory.
-    if (wid < kOccWarps) {
-      for (int i = wid; i < nslot; i += kOccWarps) {
-        int32_t u = -1, early_r = 0;
-        int32_t early_l = -1;
-        if (lane == 0) {
-          // sample reads[]/loc[] of the home unit together with the exchange (the
-          // occupant is usually the home unit); both are taken before this region
-          // publishes anything (publishers wait for every occupant warp), so the
-          // count covers other consumers only
-          const int32_t home_u = (int32_t)(j0 + i);
-          int32_t r_h = 0, l_h = -1;
-          if (!identity) {
-            r_h = ld_acquire(&P.reads[home_u]);
-            l_h = ld_acquire(&P.loc[home_u]);
-          }
-          u = atomicExch(&P.state[j0 + i], ST_CLOSED);
-          ctl.occ[i] = u;
-          if (u == home_u) {
-            early_r = r_h;
-            early_l = l_h;
-          } else if (u >= 0 && !identity) {
-            early_r = ld_acquire(&P.reads[u]);
-          }
-          ctl.early[i] = early_r;
+    const int64_t t_cur = ctl.t_cur, t_nxt = ctl.t_nxt;
+    if ((t_cur >= P.Q && t_nxt >= P.Q) || ctl.abort) break;
+    if (wid < kTeam) {
+      // ===================== salvage team ======================================
+      long long ts = clock64();
+      // (1) t_cur's deferred moves: t_cur's reads are published first
+      const int cp = it_par ^ 1;
+      const int nd = ctl.n_def[cp];
+      if (nd) {
+        while (!*(volatile int32_t*)&ctl.published) {
         }
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (lane == 0) atomicAdd(&ctl.early_cnt, 1);
-        if (u < 0 || identity) continue;
-        long long c1 = clock64();
-        int alive = 0;
-        if (lane == 0) {
-          const int32_t slot = (int32_t)(j0 + i);
-          for (uint32_t it = 0; early_l != slot && ld_acquire(&P.loc[u]) != slot; ++it) {  // landing
-            if (ld_relaxed(P.err)) {
-              ctl.abort = 1;
-              break;
-            }
-            if (it > kSpinLimit) {
-              raise_error(P.err, PM_ERR_TIMEOUT);
-              ctl.abort = 1;
-              break;
-            }
-            backoff(it);
+        for (int k = wid; k < nd; k += kTeam) {
+          const int32_t u = ctl.def_u[cp][k];
+          long long c2 = clock64();
+          const int32_t dest = acquire_dest(ctl, P, u, home, lane, true);
+          w_dest += clock64() - c2;
+          if (dest == INT32_MIN) {
+            if (lane == 0) ctl.abort = 1;
+            continue;
           }
-          // every consumer of order < t must have read u (our own read is irrelevant:
-          // its data is already on its way to shared memory)
-          const int64_t thr = g.consumed_by_window(u, t);
-          const int64_t own = thr - (t > 0 ? g.consumed_by_window(u, t - 1) : 0);
-          if (early_r < thr - own) {
-            for (uint32_t it = 0; ld_acquire(&P.reads[u]) < thr; ++it) {  // reloads may include ours
-              ++spins_o;
+          long long c3 = clock64();
+          move_unit<KT>(g, P, u, ctl.def_slot[cp][k], dest, lane);
+          w_copy += clock64() - c3;
+          if (lane == 0) {
+            ++n_salv;
+            r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
+          }
+        }
+      }
+      named_barrier_sync(2, kTeam * 32);
+      if (tid == 0) {
+        atomicExch(&ctl.deferred_done, 1);
+        const long long n_ = clock64();
+        spins_r += n_ - ts;  // (stats[10]: salvage step 1 cycles)
+        ts = n_;
+      }
+      // (2) salvage for t_nxt
+      if (t_nxt < P.Q) {
+        const int64_t q = g.region_of_ticket(t_nxt);
+        const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
+        const int nslot = (int)(j1 - j0);
+        const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+        const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+        const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+        for (int i = wid; i < nslot; i += kTeam) {
+          int32_t u = -1, early_r = 0, early_l = -1;
+          if (lane == 0) {
+            // sample the home unit's state together with the exchange (usually the occupant)
+            const int32_t home_u = (int32_t)(j0 + i);
+            int32_t r_h = 0, l_h = -1;
+            if (!identity) {
+              r_h = ld_acquire(&P.reads[home_u]);
+              l_h = ld_acquire(&P.loc[home_u]);
+            }
+            u = atomicExch(&P.state[j0 + i], ST_CLOSED);
+            if (u == home_u) {
+              early_r = r_h;
+              early_l = l_h;
+            } else if (u >= 0 && !identity) {
+              early_r = ld_acquire(&P.reads[u]);
+            }
+          }
+          u = __shfl_sync(0xffffffffu, u, 0);
+          if (u < 0 || identity) continue;
+          long long c1 = clock64();
+          int alive = 0;
+          if (lane == 0) {
+            const int32_t slot = (int32_t)(j0 + i);
+            for (uint32_t it = 0; early_l != slot && ld_acquire(&P.loc[u]) != slot; ++it) {  // landing
+              if (ld_relaxed(P.err)) {
+                ctl.abort = 1;
+                break;
+              }
+              if (it > kSpinLimit) {
+                raise_error(P.err, PM_ERR_TIMEOUT);
+                ctl.abort = 1;
+                break;
+              }
+              backoff(it);
+            }
+            // every consumer of order < t_nxt must have read u (t_nxt itself has not
+            // published yet, so reads[] counts exactly those)
+            const int64_t before = t_nxt > 0 ? g.consumed_by_window(u, t_nxt - 1) : 0;
+            for (uint32_t it = 0; early_r < before; ++it) {
+              early_r = ld_acquire(&P.reads[u]);
+              if (early_r >= before) break;
               if (ld_relaxed(P.err)) {
                 ctl.abort = 1;
                 break;
@@ -530,273 +557,264 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
               if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
               backoff(it);
             }
+            alive = g.consumed_by_window(u, t_nxt) < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
           }
-          alive = thr < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
-        }
-        alive = __shfl_sync(0xffffffffu, alive, 0);
-        long long c2 = clock64();
-        w_thr += c2 - c1;
-        if (!alive) continue;
-        // try without blocking first; block only once this region's reads are published
-        int32_t dest = acquire_dest(ctl, P, u, home, lane, false);
-        if (dest == INT32_MIN) {
-          while (!*(volatile int32_t*)&ctl.published) {
+          alive = __shfl_sync(0xffffffffu, alive, 0);
+          long long c2 = clock64();
+          w_thr += c2 - c1;
+          if (!alive) continue;
+          const int32_t dest = acquire_dest(ctl, P, u, home, lane, false);  // never block here
+          w_dest += clock64() - c2;
+          if (dest == INT32_MIN) {
+            if (lane == 0) {
+              const int k = atomicAdd(&ctl.n_def[it_par], 1);
+              ctl.def_u[it_par][k] = u;
+              ctl.def_slot[it_par][k] = (int32_t)(j0 + i);
+            }
+            continue;
           }
-          dest = acquire_dest(ctl, P, u, home, lane, true);
-        }
-        long long c3 = clock64();
-        w_dest += c3 - c2;
-        if (dest == INT32_MIN) {
-          if (lane == 0) ctl.abort = 1;
-          continue;
-        }
-        const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
-        const int64_t sbase = g.slot_base(j0 + i);
-        const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
-        char* kd = dest >= 0 ? P.keys + (dbase + (x0 - hb)) * ks
-                             : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * ks;
-        copy_g2g_warp(reinterpret_cast<uint8_t*>(kd),
-                      reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks), (x1 - x0) * ks, lane);
-        if (w) {
-          uint8_t* pd = dest >= 0 ? P.pay + (dbase + (x0 - hb)) * w
-                                  : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * w;
-          copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
-        }
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          st_release(&P.loc[u], dest);
-          ++n_salv;
-          r_salv += (unsigned long long)(x1 - x0);
-        }
-        w_copy += clock64() - c3;
-      }
-      if (wid >= nslot && lane == 0) atomicAdd(&ctl.early_cnt, 1);  // idle occupant warps sample nothing
-    } else if (!identity) {
-      const int gt = tid - kOccWarps * 32, GT = NT - kOccWarps * 32;  // gather threads
-      for (int p = gt; p < np; p += GT) {
-        const bool isA = p < npa;
-        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
-        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-        // wait until the unit sits where nobody moves it before we have read it
-        int32_t l;
-        for (uint32_t it = 0;; ++it) {
-          l = ld_acquire(&P.loc[j]);
-          if (l < 0 || g.order(g.region_of_slot(l)) >= t) break;
-          if (ld_relaxed(P.err)) {
-            ctl.abort = 1;
-            break;
-          }
-          if (it > kSpinLimit) {
-            raise_error(P.err, PM_ERR_TIMEOUT);
-            ctl.abort = 1;
-            break;
-          }
-          if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
-          ++spins_r;
-          backoff(it);
-        }
-        const int64_t hb = g.slot_base(j);
-        const char* ksrc;
-        const uint8_t* psrc;
-        if (l >= 0) {
-          const int64_t base = g.slot_base(l);
-          ksrc = P.keys + (base + (x0 - hb)) * ks;
-          psrc = P.pay + (base + (x0 - hb)) * w;
-        } else {
-          const int64_t si = -(int64_t)l - 1;
-          ksrc = P.scr_keys + (si * P.T + (x0 - hb)) * ks;
-          psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
-        }
-        uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
-        copy_g2s_phased(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
-        if (w) {
-          uint8_t* pdst = pin + (isA ? poffA + (x0 - xa) * w : poffB + (x0 - xb) * w);
-          copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
-        }
-      }
-      named_barrier_sync(1, GT);  // all expect_tx registered before the single arrive
-      if (gt == 0) mbar_arrive(&ctl.bar);
-      while (!mbar_try_wait(&ctl.bar, phase)) {
-      }
-      // publish the reads (after every occupant warp sampled its early read count);
-      // the last reader frees the unit into the CTA cache
-      while (*(volatile int32_t*)&ctl.early_cnt < nslot + (nslot < kOccWarps ? kOccWarps - nslot : 0)) {
-      }
-      for (int p = gt; p < np; p += GT) {
-        const bool isA = p < npa;
-        const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
-        const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-        __threadfence();
-        const int32_t n = (int32_t)(x1 - x0);
-        const int32_t old = atomicAdd(&P.reads[j], n);
-        if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
-          const int32_t l = ld_acquire(&P.loc[j]);
-          if (l < 0) {
-            cache_push(ctl, P, l, home);
-          } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
-            cache_push(ctl, P, l, home);
+          long long c3 = clock64();
+          move_unit<KT>(g, P, u, j0 + i, dest, lane);
+          w_copy += clock64() - c3;
+          if (lane == 0) {
+            ++n_salv;
+            r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
           }
         }
       }
-      named_barrier_sync(1, GT);
-      if (gt == 0) atomicExch(&ctl.published, 1);
-      // merge path of every output (A wins ties) into the padded output->input map
-      const KT* As = reinterpret_cast<const KT*>(kin + offA);
-      const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-      const int64_t E = (nout + GT - 1) / GT;
-      const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
-      int64_t o = min((int64_t)gt * E, nout), oe = min(o + E, nout);
-      if (P.mode == MODE_MERGE) {
-        int64_t lo = o > beta ? o - beta : 0, hi = o < alpha ? o : alpha;
-        while (lo < hi) {
-          int64_t mid = (lo + hi) >> 1;
-          if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
-          else hi = mid;
-        }
-        int64_t i = lo, jb = o - lo;
-        KT va = i < alpha ? As[i] : KT(0), vb = jb < beta ? Bs[jb] : KT(0);
-        for (; o < oe; ++o) {
-          const bool takeA = jb >= beta || (i < alpha && va <= vb);
-          const int64_t op = o + ph;
-          src[op + (op >> 5)] = takeA ? (int32_t)i : (int32_t)(alpha + jb);
-          if (takeA) {
-            ++i;
-            if (i < alpha) va = As[i];
-          } else {
-            ++jb;
-            if (jb < beta) vb = Bs[jb];
-          }
-        }
-      } else {  // rotation: B piece then A piece
-        for (; o < oe; ++o) {
-          const int64_t op = o + ph;
-          src[op + (op >> 5)] = o < beta ? (int32_t)(alpha + o) : (int32_t)(o - beta);
-        }
-      }
+      named_barrier_sync(2, kTeam * 32);
+      if (tid == 0) spins_o += clock64() - ts;  // (stats[11]: salvage step 2 cycles)
     } else {
-      if (wid == kOccWarps && lane == 0) atomicExch(&ctl.published, 1);
-    }
-    if (identity) {
-      ++n_ident;
-      __syncthreads();
-      if (tid == 0) {
-        ctl.early_cnt = 0;
-        ctl.published = 0;
-        if (t_pref < P.Q) {
-          const int64_t qn = g.region_of_ticket(t_pref);
-          ctl.nx_a0 = g.split(qn);
-          ctl.nx_a1 = g.split(qn + 1);
-        }
-      }
-      continue;
-    }
-    phase ^= 1;
-    __syncthreads();
-    if (tid == 0) {
-      long long n = clock64();
-      cyc[3] += n - tc;
-      tc = n;
-      ctl.early_cnt = 0;
-      ctl.published = 0;
-      // prefetch the next region's splits while this one streams out
-      if (t_pref < P.Q) {
-        const int64_t qn = g.region_of_ticket(t_pref);
-        ctl.nx_a0 = g.split(qn);
-        ctl.nx_a1 = g.split(qn + 1);
-      }
-    }
-    if (ctl.abort) break;
-    // ---------------- F: stream the region back in place ----------------------
-    {
-      const KT* As = reinterpret_cast<const KT*>(kin + offA);
-      const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-      const int64_t V = 16 / ks;  // keys per 16-byte vector
-      const int64_t ph = ((uintptr_t)(P.keys + (P.s + d0) * ks) & 15) / ks;
-      KT* kout = reinterpret_cast<KT*>(P.keys) + (P.s + d0) - ph;  // 16B aligned when keys base is
-      const int64_t ngroups = (ph + nout + V - 1) / V;
-      const bool kal = (((uintptr_t)kout) & 15) == 0;
-      for (int64_t gi = tid; gi < ngroups; gi += NT) {
-        const int64_t op0 = gi * V;
-        KT v[4];
-        bool full = kal;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k < V) {
-            const int64_t op = op0 + k, o = op - ph;
-            if (o >= 0 && o < nout) {
-              const int32_t si = src[op + (op >> 5)];
-              v[k] = si < alpha ? As[si] : Bs[si - alpha];
+      // ===================== data team ==========================================
+      const int gt = tid - kTeam * 32, GT = NT - kTeam * 32;
+      long long td = clock64();
+#define PM_TICK(k)                 \
+  if (gt == 0) {                   \
+    const long long n_ = clock64(); \
+    cyc[k] += n_ - td;             \
+    td = n_;                       \
+  }
+      if (t_cur < P.Q) {
+        const int64_t q = g.region_of_ticket(t_cur);
+        const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+        const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+        const int64_t b0 = d0 - a0, b1 = d1 - a1;
+        const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
+        const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+        if (identity) {
+          if (gt == 0) {
+            ++n_ident;
+            atomicExch(&ctl.published, 1);
+          }
+        } else {
+          const int64_t xa = P.s + a0, xb = P.m + b0;
+          const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+          const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+          int64_t poffA = 0, poffB = 0;
+          if (w) {
+            poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+            poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+          }
+          const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
+          const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
+          const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
+          for (int p = gt; p < np; p += GT) {
+            const bool isA = p < npa;
+            const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+            const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+            const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+            // wait until the unit sits where nobody moves it before we have read it
+            int32_t l;
+            for (uint32_t it = 0;; ++it) {
+              l = ld_acquire(&P.loc[j]);
+              if (l < 0 || g.order(g.region_of_slot(l)) >= t_cur) break;
+              if (ld_relaxed(P.err)) {
+                ctl.abort = 1;
+                break;
+              }
+              if (it > kSpinLimit) {
+                raise_error(P.err, PM_ERR_TIMEOUT);
+                ctl.abort = 1;
+                break;
+              }
+              if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
+              backoff(it);
+            }
+            const int64_t hb = g.slot_base(j);
+            const char* ksrc;
+            const uint8_t* psrc;
+            if (l >= 0) {
+              const int64_t base = g.slot_base(l);
+              ksrc = P.keys + (base + (x0 - hb)) * ks;
+              psrc = P.pay + (base + (x0 - hb)) * w;
             } else {
-              full = false;
+              const int64_t si = -(int64_t)l - 1;
+              ksrc = P.scr_keys + (si * P.T + (x0 - hb)) * ks;
+              psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
+            }
+            uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
+            copy_g2s_phased(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+            if (w) {
+              uint8_t* pdst = pin + (isA ? poffA + (x0 - xa) * w : poffB + (x0 - xb) * w);
+              copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
             }
           }
-        }
-        if (full) {
-          if constexpr (sizeof(KT) == 4) {
-            __stcs(reinterpret_cast<int4*>(kout + op0), make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]));
-          } else {
-            __stcs(reinterpret_cast<longlong2*>(kout + op0), make_longlong2((long long)v[0], (long long)v[1]));
+          named_barrier_sync(1, GT);  // every expect_tx registered before the single arrive
+          PM_TICK(0);
+          if (gt == 0) mbar_arrive(&ctl.bar);
+          while (!mbar_try_wait(&ctl.bar, phase)) {
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (k < V) {
-              const int64_t op = op0 + k, o = op - ph;
-              if (o >= 0 && o < nout) kout[op] = v[k];
+          phase ^= 1;
+          PM_TICK(1);
+          // publish the reads; the last reader frees the unit into the CTA cache
+          for (int p = gt; p < np; p += GT) {
+            const bool isA = p < npa;
+            const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+            const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
+            const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+            __threadfence();
+            const int32_t n = (int32_t)(x1 - x0);
+            const int32_t old = atomicAdd(&P.reads[j], n);
+            if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
+              const int32_t l = ld_acquire(&P.loc[j]);
+              if (l < 0) {
+                cache_push(ctl, P, l, home);
+              } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
+                cache_push(ctl, P, l, home);
+              }
             }
           }
-        }
-      }
-      if (w) {
-        uint8_t* pout = P.pay + (P.s + d0) * w;
-        const uint8_t* PA = pin + poffA;
-        const uint8_t* PB = pin + poffB;
-        if ((w & 3) == 0 && (((uintptr_t)pout | poffA | poffB) & 3) == 0) {
-          const int64_t wq = w >> 2;
-          for (int64_t o = tid; o < nout; o += NT) {
-            const int64_t op = o + ph;
-            const int32_t si = src[op + (op >> 5)];
-            const uint32_t* rs = reinterpret_cast<const uint32_t*>(si < alpha ? PA + si * w : PB + (si - alpha) * w);
-            uint32_t* rd = reinterpret_cast<uint32_t*>(pout + o * w);
-            for (int64_t c = 0; c < wq; ++c) rd[c] = rs[c];
+          if (gt == 0) bulk_wait_read_all();  // last tile's TMA store has read the buffer
+          named_barrier_sync(1, GT);
+          if (gt == 0) atomicExch(&ctl.published, 1);
+          PM_TICK(2);
+          // merge path (A wins ties): every thread merges an odd-length run of outputs
+          // (odd stride -> conflict-free smem) straight into the phase-aligned output tile
+          const KT* As = reinterpret_cast<const KT*>(kin + offA);
+          const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+          int64_t E = (nout + GT - 1) / GT;
+          E |= 1;
+          const int64_t phk = ((uintptr_t)(P.keys + (P.s + d0) * ks)) & 15;
+          KT* ko = reinterpret_cast<KT*>(kout_s + phk);
+          const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + d0) * w)) & 15) : 0;
+          uint8_t* po = pout_s + php;
+          const uint8_t* PA = pin + poffA;
+          const uint8_t* PB = pin + poffB;
+          const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
+          {
+            // region-local indices fit in 32 bits (nout <= M)
+            const int32_t al = (int32_t)alpha, bl = (int32_t)beta, no = (int32_t)nout, e32 = (int32_t)E;
+            int32_t o = min(gt * e32, no);
+            const int32_t oe = min(o + e32, no);
+            if (P.mode == MODE_MERGE) {
+              int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
+              while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+                else hi = mid;
+              }
+              int32_t i = lo, jb = o - lo;
+              const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
+              KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
+              if (!w) {
+#pragma unroll 4
+                for (; o < oe; ++o) {
+                  const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+                  ko[o] = takeA ? va : vb;
+                  if (takeA) {
+                    ++i;
+                    va = As[min(i, amax)];
+                  } else {
+                    ++jb;
+                    vb = Bs[min(jb, bmax)];
+                  }
+                }
+              } else {
+                for (; o < oe; ++o) {
+                  const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+                  ko[o] = takeA ? va : vb;
+                  const uint8_t* rs = takeA ? PA + (int64_t)i * w : PB + (int64_t)jb * w;
+                  uint8_t* rd = po + (int64_t)o * w;
+                  if (wq4) {
+                    for (int64_t c = 0; c < w; c += 4)
+                      *reinterpret_cast<uint32_t*>(rd + c) = *reinterpret_cast<const uint32_t*>(rs + c);
+                  } else {
+                    for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+                  }
+                  if (takeA) {
+                    ++i;
+                    va = As[min(i, amax)];
+                  } else {
+                    ++jb;
+                    vb = Bs[min(jb, bmax)];
+                  }
+                }
+              }
+            } else {  // rotation: B piece then A piece
+              for (; o < oe; ++o) {
+                const bool fromB = o < bl;
+                const int32_t si = fromB ? o : o - bl;
+                ko[o] = fromB ? Bs[si] : As[si];
+                if (w) {
+                  const uint8_t* rs = fromB ? PB + (int64_t)si * w : PA + (int64_t)si * w;
+                  uint8_t* rd = po + (int64_t)o * w;
+                  for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+                }
+              }
+            }
           }
-        } else {
-          for (int64_t o = tid; o < nout; o += NT) {
-            const int64_t op = o + ph;
-            const int32_t si = src[op + (op >> 5)];
-            const uint8_t* rs = si < alpha ? PA + si * w : PB + (si - alpha) * w;
-            uint8_t* rd = pout + o * w;
-            for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+          fence_proxy_async_smem();   // our smem writes -> visible to the TMA (async proxy)
+          named_barrier_sync(1, GT);  // the output tile is complete
+          PM_TICK(3);
+          // every slot of t_cur must be cleared: deferred moves finish first
+          while (!*(volatile int32_t*)&ctl.deferred_done) {
           }
+          PM_TICK(4);
+          if (!*(volatile int32_t*)&ctl.abort) {
+            // stream the tile back in place: TMA bulk store for the 16-byte-aligned body,
+            // generic stores for the unaligned head and tail bytes
+            stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + d0) * ks), nout * ks, gt, GT);
+            if (w) stream_out(pout_s + php, P.pay + (P.s + d0) * w, nout * w, gt, GT);
+          }
+          PM_TICK(5);
+          if (gt == 0) ++n_reg;
         }
+      } else if (gt == 0) {
+        atomicExch(&ctl.published, 1);
       }
     }
-    ++n_reg;
     __syncthreads();
     if (tid == 0) {
-      long long n = clock64();
-      cyc[5] += n - tc;
-      tc = n;
+      // rotate the pipeline: t_nxt becomes current, take the prefetched ticket
+      ctl.t_cur = ctl.t_nxt;
+      ctl.t_nxt = t_pref < P.Q ? t_pref : P.Q;
+      if (t_pref < P.Q) t_pref = atomicAdd(P.ticket, 1);
+      ctl.n_def[it_par ^ 1] = 0;  // the list t_cur used is consumed
+      ctl.published = 0;
+      ctl.deferred_done = 0;
       if (*(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
     }
+    it_par ^= 1;
+    __syncthreads();
   }
+  if (tid == kTeam * 32) bulk_wait_all();  // the last output tile has landed
   // leave nothing behind in the CTA cache (another job reuses the lists)
   if (tid == 0) cache_flush(ctl, P, home);
-  if (n_salv) {
+  if (lane == 0 && n_salv) {
     atomicAdd(&P.stats[0], n_salv);
     atomicAdd(&P.stats[1], r_salv);
   }
-  if (tid == 0) {
+  if (tid == kTeam * 32) {
     atomicAdd(&P.stats[2], n_reg);
     atomicAdd(&P.stats[3], n_ident);
-    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cyc[i]);
   }
-  if (lane == 0) {
+  if (tid == kTeam * 32)
+    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cyc[i]);
+  if (tid == 0) {
     atomicAdd(&P.stats[10], spins_r);
     atomicAdd(&P.stats[11], spins_o);
+  }
+  if (lane == 0) {
     atomicAdd(&P.stats[12], w_land);
     atomicAdd(&P.stats[13], w_thr);
     atomicAdd(&P.stats[14], w_dest);

@@ -5,7 +5,7 @@ import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 from paper_2005_12648_b200.workloads import config_input_device
 cfg = int(sys.argv[1]); sizes = [int(x) for x in sys.argv[2].split(',')]
-names = ['ticket', 'g_issue', 'g_land', 'salvage', 'merge', 'store']
+names = ['d_gather', 'd_land', 'd_publish', 'd_merge', 'd_waitdefer', 'd_store']
 for L in sizes:
     kw = {"log_len_b": 16} if cfg == 3 else {}
     k0, p0, m = config_input_device(cfg, seed=1, log_len=L, **kw)
@@ -16,8 +16,9 @@ for L in sizes:
             _ops.merge(arr, 0, m, len(k0))
         dt = time.time() - t0
         st = pm.synchronize()
-    tot = sum(st[4:10])
-    br = ' '.join(f"{n}={st[4+i]/tot*100:.1f}%" for i, n in enumerate(names))
+    nr = max(st[2] + st[3], 1)
+    br = ' '.join(f"{n}={st[4+i]/nr:.0f}" for i, n in enumerate(names)) + f" s_step1={st[10]/nr:.0f} s_step2={st[11]/nr:.0f}"
+    tot = 1
     print(f"L={L} {dt*1e3:.2f}ms salv_units={st[0]} salv_frac={st[1]/len(k0):.3f} regions={st[2]} ident={st[3]} "
-          f"cycles/region={tot/max(st[2]+st[3],1):.0f} {br} spins_r={st[10]} spins_o={st[11]} "
+          f"(cycles per region, CTA-summed) {br} "
           f"salvage-split(warp-cycles): land={st[12]:.3g} thr={st[13]:.3g} dest={st[14]:.3g} copy={st[15]:.3g}", flush=True)
