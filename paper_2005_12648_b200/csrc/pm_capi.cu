@@ -63,6 +63,8 @@ struct pm_ctx {
   size_t scr_bytes = 0;
   void* stage = nullptr;  // device staging for pm_merge_host
   size_t stage_bytes = 0;
+  void* buf = nullptr;    // min-side buffer of the buffered mode
+  size_t buf_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   bool ev_recorded = false;
@@ -173,6 +175,19 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   char* scr = static_cast<char*>(ctx->scr);
   P.scr_keys = scr + ((uintptr_t)keys & 15);
   P.scr_pay = reinterpret_cast<uint8_t*>(scr + scr_k + (w ? ((uintptr_t)payload & 15) : 0));
+  // buffered mode: the caller granted a min(|A|,|B|) buffer (seq_merge_buffered)
+  const int64_t la = m - s, lb = e - m, mn = std::min(la, lb);
+  const bool buffered = mode == MODE_MERGE && scratch_records >= mn;
+  const int32_t buf_a = la <= lb ? 1 : 0;
+  if (buffered) {
+    const size_t bk = (size_t)align_up(mn * ks + 64, 256), bp = (size_t)(w ? mn * w + 64 : 0);
+    rc = ensure(&ctx->buf, &ctx->buf_bytes, bk + bp);
+    if (rc) return rc;
+    const int64_t x0 = buf_a ? s : m;
+    char* b = static_cast<char*>(ctx->buf);
+    P.scr_keys = b + (((uintptr_t)keys + x0 * ks) & 15);
+    P.scr_pay = reinterpret_cast<uint8_t*>(b + bk + (w ? (((uintptr_t)payload + x0 * w) & 15) : 0));
+  }
   // plan (splits + reset) then engine
   int64_t plan_work = std::max<int64_t>(P.Q + 1, P.K);
   int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((plan_work + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
@@ -180,8 +195,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[1], st));
-  ce = ks == 4 ? launch_engine<int32_t>(P, grid, kEngineThreads, smem, st)
-               : launch_engine<int64_t>(P, grid, kEngineThreads, smem, st);
+  if (buffered) {
+    ce = ks == 4 ? launch_buffered<int32_t>(P, buf_a, grid, smem, st) : launch_buffered<int64_t>(P, buf_a, grid, smem, st);
+  } else {
+    ce = ks == 4 ? launch_engine<int32_t>(P, grid, kEngineThreads, smem, st)
+                 : launch_engine<int64_t>(P, grid, kEngineThreads, smem, st);
+  }
   if (ce != cudaSuccess) return cuda_fail(ce, "k_engine launch");
   if (ctx->timing) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
@@ -252,6 +271,7 @@ int pm_ctx_destroy(pm_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->buf) cudaFree(ctx->buf);
   if (ctx->ctl) cudaFree(ctx->ctl);
   delete ctx;
   return PM_OK;

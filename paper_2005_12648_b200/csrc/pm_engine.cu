@@ -12,6 +12,8 @@
 // and the block exchange of linear_shift / circular_shift (_kernels.py:92-197).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "pm_common.cuh"
 #include "pm_engine.cuh"
 #include "pm_search.cuh"
@@ -159,6 +161,9 @@ struct SmemCtl {
   int32_t def_u[2][kMaxMu];   // occupants whose move was deferred (no space yet), per parity
   int32_t def_slot[2][kMaxMu];
   int32_t n_def[2];
+  int64_t t_pref;        // the ticket after t_nxt (its slots are closed early by the salvage team)
+  int64_t pre_t;         // ticket whose occupants pre_* hold
+  int32_t pre_occ[kMaxMu], pre_r[kMaxMu], pre_l[kMaxMu];
   int32_t published;     // the data team has published t_cur's reads
   int32_t deferred_done; // the salvage team has moved t_cur's deferred occupants
   int32_t lock;          // protects the caches below
@@ -349,6 +354,18 @@ __device__ __forceinline__ void copy_g2s_phased(uint8_t* dst, const uint8_t* src
   if (tail) put_small(dst + head + body, vt, src + head + body, tail);
 }
 
+// global -> shared by TMA over the 16-byte-aligned superset of the piece: bytes
+// just outside it are copied too and ignored (they land in the tile's phase/pad
+// bytes; interior piece boundaries are unit boundaries, which are aligned)
+__device__ __forceinline__ void copy_g2s_superset(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar) {
+  if (nbytes <= 0) return;
+  const uintptr_t a = (uintptr_t)src & ~(uintptr_t)15;
+  const uintptr_t b = ((uintptr_t)src + nbytes + 15) & ~(uintptr_t)15;
+  const uint32_t n = (uint32_t)(b - a);
+  mbar_expect_tx(bar, n);
+  bulk_g2s(dst - ((uintptr_t)src - a), reinterpret_cast<const void*>(a), n, bar);
+}
+
 // warp copy global -> global, identical 16-byte phase on both sides; all loads of
 // a lane are issued before its stores (8 x 16 B in flight per lane)
 __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, int64_t nbytes, int lane) {
@@ -372,6 +389,80 @@ __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, 
   if (tail0 + lane < nbytes) dst[tail0 + lane] = src[tail0 + lane];
 }
 
+// Merge (A wins ties) or concatenate (rotation: B then A) the staged runs As[0,alpha),
+// Bs[0,beta) into the output tile ko[0,nout) (+ payload rows), thread gt of GT.
+// Every thread takes an odd-length run of outputs: odd strides keep the shared
+// memory accesses of a warp on distinct banks.
+template <typename KT>
+__device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT* Bs, int64_t alpha, int64_t beta,
+                                           int64_t nout, KT* ko, uint8_t* po, const uint8_t* PA, const uint8_t* PB,
+                                           int64_t w, bool wq4, int gt, int GT) {
+  int64_t E = (nout + GT - 1) / GT;
+  E |= 1;
+  {
+    // region-local indices fit in 32 bits (nout <= M)
+    const int32_t al = (int32_t)alpha, bl = (int32_t)beta, no = (int32_t)nout, e32 = (int32_t)E;
+    int32_t o = min(gt * e32, no);
+    const int32_t oe = min(o + e32, no);
+    if (mode == MODE_MERGE) {
+      int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+      }
+      int32_t i = lo, jb = o - lo;
+      const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
+      KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
+      if (!w) {
+#pragma unroll 4
+        for (; o < oe; ++o) {
+          const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+          ko[o] = takeA ? va : vb;
+          if (takeA) {
+            ++i;
+            va = As[min(i, amax)];
+          } else {
+            ++jb;
+            vb = Bs[min(jb, bmax)];
+          }
+        }
+      } else {
+        for (; o < oe; ++o) {
+          const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+          ko[o] = takeA ? va : vb;
+          const uint8_t* rs = takeA ? PA + (int64_t)i * w : PB + (int64_t)jb * w;
+          uint8_t* rd = po + (int64_t)o * w;
+          if (wq4) {
+            for (int64_t c = 0; c < w; c += 4)
+              *reinterpret_cast<uint32_t*>(rd + c) = *reinterpret_cast<const uint32_t*>(rs + c);
+          } else {
+            for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+          }
+          if (takeA) {
+            ++i;
+            va = As[min(i, amax)];
+          } else {
+            ++jb;
+            vb = Bs[min(jb, bmax)];
+          }
+        }
+      }
+    } else {  // rotation: B piece then A piece
+      for (; o < oe; ++o) {
+        const bool fromB = o < bl;
+        const int32_t si = fromB ? o : o - bl;
+        ko[o] = fromB ? Bs[si] : As[si];
+        if (w) {
+          const uint8_t* rs = fromB ? PB + (int64_t)si * w : PA + (int64_t)si * w;
+          uint8_t* rd = po + (int64_t)o * w;
+          for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
+        }
+      }
+    }
+  }
+}
+
 // Stream n bytes from a shared-memory tile to global memory with the same 16-byte
 // phase: thread `gt` == 0 issues one TMA bulk store for the aligned body; the
 // first threads write the unaligned head / tail bytes.
@@ -387,6 +478,28 @@ __device__ __forceinline__ void stream_out(const uint8_t* src_s, uint8_t* dst_g,
   }
   for (int64_t b = gt; b < head; b += GT) dst_g[b] = src_s[b];
   for (int64_t b = tail0 + gt; b < n; b += GT) dst_g[b] = src_s[b];
+}
+
+// Close slot j (the region has started) and sample its occupant's reads / loc.
+// The home unit's state is read together with the exchange (it is usually the
+// occupant); the sample precedes any read this region publishes.
+__device__ __forceinline__ void close_and_sample(const Geo& g, const EngineParams& P, int64_t j, bool identity,
+                                                 int32_t& u, int32_t& r, int32_t& l) {
+  const int32_t home_u = (int32_t)j;
+  int32_t r_h = 0, l_h = -1;
+  if (!identity) {
+    r_h = ld_acquire(&P.reads[home_u]);
+    l_h = ld_acquire(&P.loc[home_u]);
+  }
+  u = atomicExch(&P.state[j], ST_CLOSED);
+  r = 0;
+  l = -1;
+  if (u == home_u) {
+    r = r_h;
+    l = l_h;
+  } else if (u >= 0 && !identity) {
+    r = ld_acquire(&P.reads[u]);
+  }
 }
 
 // Move unit u out of slot `slot` into `dest` (warp-wide) and publish its new home.
@@ -453,7 +566,9 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
     ctl.n_def[0] = ctl.n_def[1] = 0;
     ctl.t_cur = P.Q;
     ctl.t_nxt = atomicAdd(P.ticket, 1);
-    t_pref = atomicAdd(P.ticket, 1);
+    ctl.t_pref = atomicAdd(P.ticket, 1);
+    ctl.pre_t = -1;
+    t_pref = atomicAdd(P.ticket, 1);  // two ahead of t_nxt, in flight
   }
   __syncthreads();
   int it_par = 0;  // parity of the deferred list written by the salvage team this iteration
@@ -503,22 +618,16 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
         const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
         const int64_t a0 = g.split(q), a1 = g.split(q + 1);
         const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+        const bool pre = ctl.pre_t == t_nxt;  // closed and sampled last iteration
         for (int i = wid; i < nslot; i += kTeam) {
           int32_t u = -1, early_r = 0, early_l = -1;
           if (lane == 0) {
-            // sample the home unit's state together with the exchange (usually the occupant)
-            const int32_t home_u = (int32_t)(j0 + i);
-            int32_t r_h = 0, l_h = -1;
-            if (!identity) {
-              r_h = ld_acquire(&P.reads[home_u]);
-              l_h = ld_acquire(&P.loc[home_u]);
-            }
-            u = atomicExch(&P.state[j0 + i], ST_CLOSED);
-            if (u == home_u) {
-              early_r = r_h;
-              early_l = l_h;
-            } else if (u >= 0 && !identity) {
-              early_r = ld_acquire(&P.reads[u]);
+            if (pre) {
+              u = ctl.pre_occ[i];
+              early_r = ctl.pre_r[i];
+              early_l = ctl.pre_l[i];
+            } else {
+              close_and_sample(g, P, j0 + i, identity, u, early_r, early_l);
             }
           }
           u = __shfl_sync(0xffffffffu, u, 0);
@@ -582,7 +691,31 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           }
         }
       }
-      named_barrier_sync(2, kTeam * 32);
+      named_barrier_sync(2, kTeam * 32);  // everyone is done with pre_*
+      // (3) close the following region's slots now and sample its occupants, so the
+      //     next iteration's step (2) starts without a round trip
+      {
+        const int64_t tp = ctl.t_pref;
+        if (tp < P.Q) {
+          const int64_t q = g.region_of_ticket(tp);
+          const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
+          const int nslot = (int)(j1 - j0);
+          const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+          const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+          const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+          for (int i = wid; i < nslot; i += kTeam) {
+            if (lane == 0) {
+              int32_t u, r, l;
+              close_and_sample(g, P, j0 + i, identity, u, r, l);
+              ctl.pre_occ[i] = u;
+              ctl.pre_r[i] = r;
+              ctl.pre_l[i] = l;
+            }
+          }
+        }
+        named_barrier_sync(2, kTeam * 32);
+        if (tid == 0) ctl.pre_t = tp;
+      }
       if (tid == 0) spins_o += clock64() - ts;  // (stats[11]: salvage step 2 cycles)
     } else {
       // ===================== data team ==========================================
@@ -653,10 +786,10 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
               psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
             }
             uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
-            copy_g2s_phased(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+            copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
             if (w) {
               uint8_t* pdst = pin + (isA ? poffA + (x0 - xa) * w : poffB + (x0 - xb) * w);
-              copy_g2s_phased(pdst, psrc, (x1 - x0) * w, &ctl.bar);
+              copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
             }
           }
           named_barrier_sync(1, GT);  // every expect_tx registered before the single arrive
@@ -666,34 +799,25 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           }
           phase ^= 1;
           PM_TICK(1);
-          // publish the reads; the last reader frees the unit into the CTA cache
-          for (int p = gt; p < np; p += GT) {
-            const bool isA = p < npa;
-            const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
+          // publish the reads (one piece per thread; np <= GT): the atomics stay in
+          // flight during the merge, deaths are handled after it
+          int64_t pj = -1;
+          int32_t pn = 0, pold = 0;
+          if (gt < np) {
+            const bool isA = gt < npa;
+            pj = isA ? ua0 + gt : ub0 + (gt - npa);
             const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-            const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+            pn = (int32_t)(min(run1, g.slot_hi(pj)) - max(run0, g.slot_lo(pj)));
             __threadfence();
-            const int32_t n = (int32_t)(x1 - x0);
-            const int32_t old = atomicAdd(&P.reads[j], n);
-            if (old + n == (int32_t)(g.slot_hi(j) - g.slot_lo(j))) {
-              const int32_t l = ld_acquire(&P.loc[j]);
-              if (l < 0) {
-                cache_push(ctl, P, l, home);
-              } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)j, ST_FREE) == (int32_t)j) {
-                cache_push(ctl, P, l, home);
-              }
-            }
+            pold = atomicAdd(&P.reads[pj], pn);
           }
           if (gt == 0) bulk_wait_read_all();  // last tile's TMA store has read the buffer
           named_barrier_sync(1, GT);
-          if (gt == 0) atomicExch(&ctl.published, 1);
           PM_TICK(2);
           // merge path (A wins ties): every thread merges an odd-length run of outputs
           // (odd stride -> conflict-free smem) straight into the phase-aligned output tile
           const KT* As = reinterpret_cast<const KT*>(kin + offA);
           const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-          int64_t E = (nout + GT - 1) / GT;
-          E |= 1;
           const int64_t phk = ((uintptr_t)(P.keys + (P.s + d0) * ks)) & 15;
           KT* ko = reinterpret_cast<KT*>(kout_s + phk);
           const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + d0) * w)) & 15) : 0;
@@ -701,70 +825,19 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           const uint8_t* PA = pin + poffA;
           const uint8_t* PB = pin + poffB;
           const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
-          {
-            // region-local indices fit in 32 bits (nout <= M)
-            const int32_t al = (int32_t)alpha, bl = (int32_t)beta, no = (int32_t)nout, e32 = (int32_t)E;
-            int32_t o = min(gt * e32, no);
-            const int32_t oe = min(o + e32, no);
-            if (P.mode == MODE_MERGE) {
-              int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
-              while (lo < hi) {
-                const int32_t mid = (lo + hi) >> 1;
-                if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
-                else hi = mid;
-              }
-              int32_t i = lo, jb = o - lo;
-              const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
-              KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
-              if (!w) {
-#pragma unroll 4
-                for (; o < oe; ++o) {
-                  const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
-                  ko[o] = takeA ? va : vb;
-                  if (takeA) {
-                    ++i;
-                    va = As[min(i, amax)];
-                  } else {
-                    ++jb;
-                    vb = Bs[min(jb, bmax)];
-                  }
-                }
-              } else {
-                for (; o < oe; ++o) {
-                  const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
-                  ko[o] = takeA ? va : vb;
-                  const uint8_t* rs = takeA ? PA + (int64_t)i * w : PB + (int64_t)jb * w;
-                  uint8_t* rd = po + (int64_t)o * w;
-                  if (wq4) {
-                    for (int64_t c = 0; c < w; c += 4)
-                      *reinterpret_cast<uint32_t*>(rd + c) = *reinterpret_cast<const uint32_t*>(rs + c);
-                  } else {
-                    for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
-                  }
-                  if (takeA) {
-                    ++i;
-                    va = As[min(i, amax)];
-                  } else {
-                    ++jb;
-                    vb = Bs[min(jb, bmax)];
-                  }
-                }
-              }
-            } else {  // rotation: B piece then A piece
-              for (; o < oe; ++o) {
-                const bool fromB = o < bl;
-                const int32_t si = fromB ? o : o - bl;
-                ko[o] = fromB ? Bs[si] : As[si];
-                if (w) {
-                  const uint8_t* rs = fromB ? PB + (int64_t)si * w : PA + (int64_t)si * w;
-                  uint8_t* rd = po + (int64_t)o * w;
-                  for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
-                }
-              }
+          merge_tile<KT>(P.mode, As, Bs, alpha, beta, nout, ko, po, PA, PB, w, wq4, gt, GT);
+          fence_proxy_async_smem();   // our smem writes -> visible to the TMA (async proxy)
+          if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
+            // last reader: free the unit's location into the CTA cache
+            const int32_t l = ld_acquire(&P.loc[pj]);
+            if (l < 0) {
+              cache_push(ctl, P, l, home);
+            } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)pj, ST_FREE) == (int32_t)pj) {
+              cache_push(ctl, P, l, home);
             }
           }
-          fence_proxy_async_smem();   // our smem writes -> visible to the TMA (async proxy)
-          named_barrier_sync(1, GT);  // the output tile is complete
+          named_barrier_sync(1, GT);  // the output tile is complete, reads are published
+          if (gt == 0) atomicExch(&ctl.published, 1);
           PM_TICK(3);
           // every slot of t_cur must be cleared: deferred moves finish first
           while (!*(volatile int32_t*)&ctl.deferred_done) {
@@ -785,9 +858,10 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
     }
     __syncthreads();
     if (tid == 0) {
-      // rotate the pipeline: t_nxt becomes current, take the prefetched ticket
+      // rotate the pipeline: t_nxt becomes current; tickets are fetched two ahead
       ctl.t_cur = ctl.t_nxt;
-      ctl.t_nxt = t_pref < P.Q ? t_pref : P.Q;
+      ctl.t_nxt = ctl.t_pref < P.Q ? ctl.t_pref : P.Q;
+      ctl.t_pref = t_pref < P.Q ? t_pref : P.Q;
       if (t_pref < P.Q) t_pref = atomicAdd(P.ticket, 1);
       ctl.n_def[it_par ^ 1] = 0;  // the list t_cur used is consumed
       ctl.published = 0;
@@ -822,6 +896,160 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   }
 }
 
+
+// ============================================================================
+// Buffered mode: the reference's min-side-buffered core (seq_merge_buffered,
+// seqmerge.py:55-75 / _kernels.py:227-313) as a streaming GPU pipeline.  The
+// shorter run is copied to the caller-sized buffer; regions are then merged in
+// the direction that only ever overwrites already-consumed records of the
+// other run (ascending when A is buffered, descending when B is), each region
+// waiting only for the few earlier regions that read the records it overwrites.
+// 1.5 passes over the data for equal runs, no unit bookkeeping.
+// ============================================================================
+template <typename KT>
+__global__ void __launch_bounds__(256) k_copy_run(EngineParams P, int64_t x0, int64_t x1) {
+  const int64_t ks = sizeof(KT);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int part = 0; part < (P.w ? 2 : 1); ++part) {
+    const int64_t rb = part ? P.w : ks;
+    const uint8_t* src = part ? P.pay + x0 * rb : reinterpret_cast<const uint8_t*>(P.keys) + x0 * rb;
+    uint8_t* dst = part ? P.scr_pay : reinterpret_cast<uint8_t*>(P.scr_keys);  // same 16-byte phase as src
+    const int64_t n = (x1 - x0) * rb;
+    int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+    if (head > n) head = n;
+    const int64_t nv = (n - head) >> 4;
+    for (int64_t b = tid; b < head; b += nthr) dst[b] = src[b];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (int64_t i = tid; i < nv; i += nthr) d4[i] = __ldcs(s4 + i);
+    for (int64_t b = head + (nv << 4) + tid; b < n; b += nthr) dst[b] = src[b];
+  }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  __shared__ uint64_t bar;
+  __shared__ int64_t s_t;
+  Geo g(P);
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int64_t ks = sizeof(KT), w = P.w;
+  if (*(volatile int32_t*)P.noop) return;
+  uint8_t* kin = dyn;
+  uint8_t* pin = dyn + P.smem_keys;
+  uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;
+  uint8_t* pout_s = kout_s + P.smem_keys;
+  int32_t* flags = P.reads;  // flags[r] = 1 once region r has read its inputs
+  const int64_t la = g.LA();
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  unsigned long long n_reg = 0;
+  while (true) {
+    if (tid == 0) s_t = (*(volatile int32_t*)P.err) ? P.Q : atomicAdd(P.ticket, 1);
+    __syncthreads();
+    const int64_t t = s_t;
+    if (t >= P.Q) break;
+    const int64_t r = buf_a ? t : P.Q - 1 - t;
+    const int64_t d0 = g.diag(r), d1 = g.diag(r + 1);
+    const int64_t a0 = g.split(r), a1 = g.split(r + 1);
+    const int64_t b0 = d0 - a0, b1 = d1 - a1;
+    const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
+    const bool identity = (a0 == d0 && a1 == d1) || (a0 == la && a1 == la);
+    if (identity) {  // records already on their outputs and read by r only
+      if (tid == 0) st_release(&flags[r], 1);
+      __syncthreads();
+      continue;
+    }
+    const int64_t xa = P.s + a0, xb = P.m + b0;
+    const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+    const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+    int64_t poffA = 0, poffB = 0;
+    if (w) {
+      poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+      poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+    }
+    if (tid == 0) {
+      // the buffered run is read from the phase-matched scratch copy
+      const char* ka = buf_a ? P.scr_keys + a0 * ks : P.keys + xa * ks;
+      const char* kb = buf_a ? P.keys + xb * ks : P.scr_keys + b0 * ks;
+      copy_g2s_superset(kin + offA, reinterpret_cast<const uint8_t*>(ka), alpha * ks, &bar);
+      copy_g2s_superset(kin + offB, reinterpret_cast<const uint8_t*>(kb), beta * ks, &bar);
+      if (w) {
+        const uint8_t* pa = buf_a ? P.scr_pay + a0 * w : P.pay + xa * w;
+        const uint8_t* pb = buf_a ? P.pay + xb * w : P.scr_pay + b0 * w;
+        copy_g2s_superset(pin + poffA, pa, alpha * w, &bar);
+        copy_g2s_superset(pin + poffB, pb, beta * w, &bar);
+      }
+      bulk_wait_read_all();  // the previous tile's TMA store has read kout
+      mbar_arrive(&bar);
+    }
+    while (!mbar_try_wait(&bar, phase)) {
+    }
+    phase ^= 1;
+    if (tid == 0) {
+      __threadfence();
+      st_release(&flags[r], 1);
+    }
+    const KT* As = reinterpret_cast<const KT*>(kin + offA);
+    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
+    const int64_t phk = ((uintptr_t)(P.keys + (P.s + d0) * ks)) & 15;
+    const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + d0) * w)) & 15) : 0;
+    const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
+    merge_tile<KT>(MODE_MERGE, As, Bs, alpha, beta, nout, reinterpret_cast<KT*>(kout_s + phk), pout_s + php,
+                   pin + poffA, pin + poffB, w, wq4, tid, NT);
+    fence_proxy_async_smem();
+    // the records this region overwrites in the unbuffered run must have been read
+    if (tid < 32) {
+      // consumers of a run range [x, y) are the regions c with [run_c, run_{c+1}) intersecting
+      // it: from the last c with run_c <= x to the last c with run_c <= y - 1
+      int64_t c_lo = 0, c_hi = -1;
+      auto last_le = [&](int64_t v, int64_t lo, int64_t hi, bool on_b) {  // largest c in [lo,hi] with run_c <= v
+        while (lo < hi) {
+          const int64_t mid = (lo + hi + 1) >> 1;
+          const int64_t rc = on_b ? g.diag(mid) - g.split(mid) : g.split(mid);
+          if (rc <= v) lo = mid;
+          else hi = mid - 1;
+        }
+        return lo;
+      };
+      if (buf_a) {  // writes into B's area [m, e): B indices [jlo, jhi); consumers are regions <= r
+        const int64_t jlo = max(P.s + d0, P.m) - P.m, jhi = P.s + d1 - P.m;
+        if (jhi > jlo) {
+          c_lo = last_le(jlo, 0, r, true);
+          c_hi = last_le(jhi - 1, c_lo, r, true);
+        }
+      } else {  // writes into A's area [s, m): A indices [ilo, ihi); consumers are regions >= r
+        const int64_t ilo = d0, ihi = min(d1, la);
+        if (ihi > ilo) {
+          c_lo = last_le(ilo, r, P.Q - 1, false);
+          c_hi = last_le(ihi - 1, c_lo, P.Q - 1, false);
+        }
+      }
+      for (int64_t c = c_lo + (tid & 31); c <= c_hi; c += 32) {
+        if (c == r) continue;
+        for (uint32_t it = 0; ld_acquire(&flags[c]) == 0; ++it) {
+          if (ld_relaxed(P.err)) break;
+          if (it > kSpinLimit) {
+            raise_error(P.err, PM_ERR_TIMEOUT);
+            break;
+          }
+          backoff(it);
+        }
+      }
+    }
+    __syncthreads();
+    stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + d0) * ks), nout * ks, tid, NT);
+    if (w) stream_out(pout_s + php, P.pay + (P.s + d0) * w, nout * w, tid, NT);
+    ++n_reg;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    bulk_wait_all();
+    atomicAdd(&P.stats[2], n_reg);
+  }
+}
+
 // ---- host launchers (called from pm_capi.cu) --------------------------------
 template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
@@ -839,6 +1067,21 @@ cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm) {
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_engine<KT>, block, smem);
 }
+template <typename KT>
+cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st) {
+  const int64_t x0 = buf_a ? P.s : P.m, x1 = buf_a ? P.m : P.e;
+  const int cgrid = (int)std::min<int64_t>(std::max<int64_t>(((x1 - x0) * (int64_t)sizeof(KT) / 16 + 255) / 256, 1),
+                                           (int64_t)grid * 4);
+  k_copy_run<KT><<<cgrid, 256, 0, st>>>(P, x0, x1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_buffered<KT><<<grid, 256, smem, st>>>(P, buf_a);
+  return cudaGetLastError();
+}
+template cudaError_t launch_buffered<int32_t>(const EngineParams&, int32_t, int, size_t, cudaStream_t);
+template cudaError_t launch_buffered<int64_t>(const EngineParams&, int32_t, int, size_t, cudaStream_t);
 template cudaError_t launch_plan<int32_t>(const EngineParams&, int, cudaStream_t);
 template cudaError_t launch_plan<int64_t>(const EngineParams&, int, cudaStream_t);
 template cudaError_t launch_engine<int32_t>(const EngineParams&, int, int, size_t, cudaStream_t);

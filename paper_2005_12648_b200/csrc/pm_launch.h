@@ -11,6 +11,8 @@ template <typename KT> cudaError_t launch_plan(const EngineParams& P, int grid, 
 template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);
 template <typename KT>
+cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st);
+template <typename KT>
 cudaError_t launch_find_median(const void* a, const void* b, int64_t la, int64_t lb, int64_t* out, cudaStream_t st);
 template <typename KT>
 cudaError_t launch_find_splits(const void* a, const void* b, int64_t la, int64_t lb, const int64_t* diags, int64_t nd,

@@ -5,6 +5,7 @@ import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 from paper_2005_12648_b200.workloads import config_input_device
 cfg = int(sys.argv[1]); sizes = [int(x) for x in sys.argv[2].split(',')]
+scr_div = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 names = ['d_gather', 'd_land', 'd_publish', 'd_merge', 'd_waitdefer', 'd_store']
 for L in sizes:
     kw = {"log_len_b": 16} if cfg == 3 else {}
@@ -13,7 +14,7 @@ for L in sizes:
         arr = pm.KeyedArray(k0.clone(), p0.clone())
         torch.cuda.synchronize(); t0 = time.time()
         with pm.deferred_checks():
-            _ops.merge(arr, 0, m, len(k0))
+            _ops.merge(arr, 0, m, len(k0), scratch_records=(len(k0) // scr_div if scr_div else 0))
         dt = time.time() - t0
         st = pm.synchronize()
     nr = max(st[2] + st[3], 1)

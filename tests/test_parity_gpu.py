@@ -207,3 +207,21 @@ def test_fast_path_untouched():
     before = arr.copy()
     pm.merge_soptmov(arr, pm.MergeJob(0, 4, 6), 4)
     assert arr.equals(before)
+
+
+@pytest.mark.parametrize("width", [0, 4, 5])
+def test_buffered_mode_vs_oracle(width):
+    """seq_merge_buffered's min-side buffer -> the streaming buffered kernel (both directions)."""
+    rng = np.random.default_rng(4242 + width)
+    for size in (3, 100, 8193, 50000, 300000, 1 << 20):
+        for split in (0.1, 0.5, 0.9):
+            for domain in (7, 2**31 - 1):
+                keys, payload, middle = random_instance(rng, size, split, domain, width)
+                lo = int(rng.integers(0, 9))
+                kk = np.concatenate([np.full(lo, -4, np.int32), keys, np.full(5, -6, np.int32)])
+                pp = np.concatenate([np.zeros((lo, width), np.uint8), payload, np.ones((5, width), np.uint8)])
+                want_k, want_p = kk.copy(), pp.copy()
+                orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
+                arr = to_gpu(kk, pp)
+                pm.seq_merge_buffered(arr, pm.MergeJob(lo, lo + middle, lo + size))
+                assert_same(arr, want_k, want_p, f"buffered size={size} split={split} w={width}")
