@@ -103,6 +103,14 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   int64_t M, T;
   int32_t mu;
   if (!pick_tiles(ks, w, &M, &T, &mu)) return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
+  // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
+  // half-size regions, two staging + two output tiles (same shared-memory budget)
+  const bool buffered = mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m);
+  if (buffered && M >= 32) {
+    M /= 2;
+    T = std::max<int64_t>(16, M / 4);
+    mu = (int32_t)(M / T);
+  }
   EngineParams P{};
   P.keys = static_cast<char*>(keys);
   P.pay = static_cast<uint8_t*>(payload);
@@ -126,8 +134,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // shared memory carve-up (all offsets 16-byte aligned)
   P.smem_keys = (size_t)align_up(M * ks + 48, 128);
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
-  // staged inputs (keys, payload) + merged output tile (keys, payload), same sizes
-  const size_t smem = 2 * (P.smem_keys + P.smem_pay);
+  // staged inputs (keys, payload) + merged output tile (keys, payload), same sizes;
+  // the buffered pipeline double-buffers both
+  const size_t smem = (buffered ? 4 : 2) * (P.smem_keys + P.smem_pay);
   // persistent grid: every resident CTA slot on every SM
   int bps = 0;
   cudaError_t ce = ks == 4 ? engine_occupancy<int32_t>(kEngineThreads, smem, &bps)
@@ -177,7 +186,6 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.scr_pay = reinterpret_cast<uint8_t*>(scr + scr_k + (w ? ((uintptr_t)payload & 15) : 0));
   // buffered mode: the caller granted a min(|A|,|B|) buffer (seq_merge_buffered)
   const int64_t la = m - s, lb = e - m, mn = std::min(la, lb);
-  const bool buffered = mode == MODE_MERGE && scratch_records >= mn;
   const int32_t buf_a = la <= lb ? 1 : 0;
   if (buffered) {
     const size_t bk = (size_t)align_up(mn * ks + 64, 256), bp = (size_t)(w ? mn * w + 64 : 0);

@@ -397,14 +397,37 @@ template <typename KT>
 __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT* Bs, int64_t alpha, int64_t beta,
                                            int64_t nout, KT* ko, uint8_t* po, const uint8_t* PA, const uint8_t* PB,
                                            int64_t w, bool wq4, int gt, int GT) {
-  int64_t E = (nout + GT - 1) / GT;
+  int32_t E = ((int32_t)nout + GT - 1) / GT;  // 32-bit: nout <= M
   E |= 1;
   {
     // region-local indices fit in 32 bits (nout <= M)
     const int32_t al = (int32_t)alpha, bl = (int32_t)beta, no = (int32_t)nout, e32 = (int32_t)E;
     int32_t o = min(gt * e32, no);
     const int32_t oe = min(o + e32, no);
-    if (mode == MODE_MERGE) {
+    if (mode == MODE_MERGE && !w) {
+      // keys only.  Shared-memory bandwidth bounds this loop (lanes sit at random
+      // offsets, ~3.5-way bank conflicts per load), so each step loads exactly one
+      // candidate -- the replacement for the side just taken -- via an address select
+      int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+      }
+      const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
+      int32_t i = lo, jb = o - lo;
+      KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
+#pragma unroll 4
+      for (; o < oe; ++o) {
+        const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+        ko[o] = takeA ? va : vb;
+        i += takeA;
+        jb += !takeA;
+        const KT v = *(takeA ? As + min(i, amax) : Bs + min(jb, bmax));
+        va = takeA ? v : va;
+        vb = takeA ? vb : v;
+      }
+    } else if (mode == MODE_MERGE) {
       int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
       while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
@@ -415,17 +438,16 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
       const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
       KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
       if (!w) {
+        // branch-free: both candidates are reloaded every step (two independent LDS per
+        // element instead of the warp diverging on every element)
 #pragma unroll 4
         for (; o < oe; ++o) {
           const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
           ko[o] = takeA ? va : vb;
-          if (takeA) {
-            ++i;
-            va = As[min(i, amax)];
-          } else {
-            ++jb;
-            vb = Bs[min(jb, bmax)];
-          }
+          i += takeA;
+          jb += !takeA;
+          va = As[min(i, amax)];
+          vb = Bs[min(jb, bmax)];
         }
       } else {
         for (; o < oe; ++o) {
@@ -906,6 +928,42 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
 // waiting only for the few earlier regions that read the records it overwrites.
 // 1.5 passes over the data for equal runs, no unit bookkeeping.
 // ============================================================================
+// For every region r of the buffered pipeline: the regions that read the
+// unbuffered-run records r overwrites (c_lo..c_hi, stored in state[] / loc[],
+// which the buffered mode does not otherwise use).  One thread per region.
+__global__ void __launch_bounds__(256) k_consumers(EngineParams P, int32_t buf_a) {
+  Geo g(P);
+  const int64_t la = g.LA();
+  auto last_le = [&](int64_t v, int64_t lo, int64_t hi, bool on_b) {  // largest c in [lo,hi], run_c <= v
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      const int64_t rc = on_b ? g.diag(mid) - g.split(mid) : g.split(mid);
+      if (rc <= v) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < P.Q; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d0 = g.diag(r), d1 = g.diag(r + 1);
+    int64_t c_lo = 0, c_hi = -1;
+    if (buf_a) {  // r writes into B's area [m, e): B indices [jlo, jhi); consumers are <= r
+      const int64_t jlo = max(P.s + d0, P.m) - P.m, jhi = P.s + d1 - P.m;
+      if (jhi > jlo) {
+        c_lo = last_le(jlo, 0, r, true);
+        c_hi = last_le(jhi - 1, c_lo, r, true);
+      }
+    } else {  // r writes into A's area [s, m): A indices [ilo, ihi); consumers are >= r
+      const int64_t ilo = d0, ihi = min(d1, la);
+      if (ihi > ilo) {
+        c_lo = last_le(ilo, r, P.Q - 1, false);
+        c_hi = last_le(ihi - 1, c_lo, P.Q - 1, false);
+      }
+    }
+    P.state[r] = (int32_t)c_lo;
+    P.loc[r] = (int32_t)c_hi;
+  }
+}
+
 template <typename KT>
 __global__ void __launch_bounds__(256) k_copy_run(EngineParams P, int64_t x0, int64_t x1) {
   const int64_t ks = sizeof(KT);
@@ -926,128 +984,196 @@ __global__ void __launch_bounds__(256) k_copy_run(EngineParams P, int64_t x0, in
   }
 }
 
+// Per-region geometry of the buffered pipeline (staged tile layout in smem).
+struct BufRegion {
+  int64_t r, d0, d1, a0, a1, b0, b1, alpha, beta, nout;
+  int64_t offA, offB, poffA, poffB;
+  bool identity;
+};
+
+template <typename KT>
+__device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams& P, int64_t t, int32_t buf_a) {
+  BufRegion R;
+  const int64_t ks = sizeof(KT), w = P.w, la = g.LA();
+  R.r = buf_a ? t : P.Q - 1 - t;
+  R.d0 = g.diag(R.r);
+  R.d1 = g.diag(R.r + 1);
+  R.a0 = g.split(R.r);
+  R.a1 = g.split(R.r + 1);
+  R.b0 = R.d0 - R.a0;
+  R.b1 = R.d1 - R.a1;
+  R.alpha = R.a1 - R.a0;
+  R.beta = R.b1 - R.b0;
+  R.nout = R.d1 - R.d0;
+  R.identity = (R.a0 == R.d0 && R.a1 == R.d1) || (R.a0 == la && R.a1 == la);
+  const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
+  R.offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+  R.offB = ((R.offA + R.alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+  R.poffA = R.poffB = 0;
+  if (w) {
+    R.poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+    R.poffB = ((R.poffA + R.alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+  }
+  return R;
+}
+
+// thread 0: TMA-load region R's runs into staging buffer (kin, pin); the
+// buffered run comes from the phase-matched scratch copy
+template <typename KT>
+__device__ __forceinline__ void buf_issue(const EngineParams& P, const BufRegion& R, int32_t buf_a, uint8_t* kin,
+                                          uint8_t* pin, uint64_t* bar) {
+  const int64_t ks = sizeof(KT), w = P.w;
+  const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
+  const char* ka = buf_a ? P.scr_keys + R.a0 * ks : P.keys + xa * ks;
+  const char* kb = buf_a ? P.keys + xb * ks : P.scr_keys + R.b0 * ks;
+  copy_g2s_superset(kin + R.offA, reinterpret_cast<const uint8_t*>(ka), R.alpha * ks, bar);
+  copy_g2s_superset(kin + R.offB, reinterpret_cast<const uint8_t*>(kb), R.beta * ks, bar);
+  if (w) {
+    const uint8_t* pa = buf_a ? P.scr_pay + R.a0 * w : P.pay + xa * w;
+    const uint8_t* pb = buf_a ? P.pay + xb * w : P.scr_pay + R.b0 * w;
+    copy_g2s_superset(pin + R.poffA, pa, R.alpha * w, bar);
+    copy_g2s_superset(pin + R.poffB, pb, R.beta * w, bar);
+  }
+  mbar_arrive(bar);
+}
+
+// Persistent, software-pipelined: while the CTA merges region t out of staging
+// buffer b, the next region's TMA loads are already landing in buffer b^1; the
+// merged tile leaves through a TMA bulk store from one of two output buffers.
+// The last warp is the control warp (tickets, TMA issue, read flags, consumer
+// checks, bulk stores); the other warps only merge, so no round trip sits on
+// the merge's critical path.
 template <typename KT>
 __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a) {
   extern __shared__ __align__(128) uint8_t dyn[];
-  __shared__ uint64_t bar;
-  __shared__ int64_t s_t;
+  __shared__ uint64_t bar[2];
+  __shared__ int64_t s_t[2];
+  __shared__ int32_t s_early[2];  // the region's read flag was already raised
   Geo g(P);
-  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  const int NW = NT >> 5;
+  const bool ctrl = (tid >> 5) == NW - 1;
+  const bool leader = ctrl && lane == 0;  // issues every TMA op of the CTA
+  const int MT = NT - 32;                 // merge threads
   const int64_t ks = sizeof(KT), w = P.w;
   if (*(volatile int32_t*)P.noop) return;
-  uint8_t* kin = dyn;
-  uint8_t* pin = dyn + P.smem_keys;
-  uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;
-  uint8_t* pout_s = kout_s + P.smem_keys;
+  int32_t t_pref = 0;
+  const size_t tile = P.smem_keys + P.smem_pay;
+  // tiles are addressed as dyn + offset so the compiler keeps them in the shared
+  // space (a local pointer array would turn every access into a generic LD/ST)
+#define STAGE(b) (dyn + (size_t)(b) * tile)
+#define OUTB(b) (dyn + (size_t)(2 + (b)) * tile)
   int32_t* flags = P.reads;  // flags[r] = 1 once region r has read its inputs
-  const int64_t la = g.LA();
-  if (tid == 0) mbar_init(&bar, 1);
-  __syncthreads();
-  uint32_t phase = 0;
-  unsigned long long n_reg = 0;
-  while (true) {
-    if (tid == 0) s_t = (*(volatile int32_t*)P.err) ? P.Q : atomicAdd(P.ticket, 1);
-    __syncthreads();
-    const int64_t t = s_t;
-    if (t >= P.Q) break;
-    const int64_t r = buf_a ? t : P.Q - 1 - t;
-    const int64_t d0 = g.diag(r), d1 = g.diag(r + 1);
-    const int64_t a0 = g.split(r), a1 = g.split(r + 1);
-    const int64_t b0 = d0 - a0, b1 = d1 - a1;
-    const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
-    const bool identity = (a0 == d0 && a1 == d1) || (a0 == la && a1 == la);
-    if (identity) {  // records already on their outputs and read by r only
-      if (tid == 0) st_release(&flags[r], 1);
-      __syncthreads();
-      continue;
+  if (leader) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    s_early[0] = s_early[1] = 0;
+    const int64_t t0 = (*(volatile int32_t*)P.err) ? P.Q : atomicAdd(P.ticket, 1);
+    s_t[0] = t0;
+    t_pref = atomicAdd(P.ticket, 1);  // the ticket after the next one, in flight
+    if (t0 < P.Q) {
+      const BufRegion R = buf_region<KT>(g, P, t0, buf_a);
+      if (!R.identity) buf_issue<KT>(P, R, buf_a, STAGE(0), STAGE(0) + P.smem_keys, &bar[0]);
     }
-    const int64_t xa = P.s + a0, xb = P.m + b0;
-    const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-    const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
-    int64_t poffA = 0, poffB = 0;
-    if (w) {
-      poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
-      poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
-    }
-    if (tid == 0) {
-      // the buffered run is read from the phase-matched scratch copy
-      const char* ka = buf_a ? P.scr_keys + a0 * ks : P.keys + xa * ks;
-      const char* kb = buf_a ? P.keys + xb * ks : P.scr_keys + b0 * ks;
-      copy_g2s_superset(kin + offA, reinterpret_cast<const uint8_t*>(ka), alpha * ks, &bar);
-      copy_g2s_superset(kin + offB, reinterpret_cast<const uint8_t*>(kb), beta * ks, &bar);
-      if (w) {
-        const uint8_t* pa = buf_a ? P.scr_pay + a0 * w : P.pay + xa * w;
-        const uint8_t* pb = buf_a ? P.pay + xb * w : P.scr_pay + b0 * w;
-        copy_g2s_superset(pin + poffA, pa, alpha * w, &bar);
-        copy_g2s_superset(pin + poffB, pb, beta * w, &bar);
-      }
-      bulk_wait_read_all();  // the previous tile's TMA store has read kout
-      mbar_arrive(&bar);
-    }
-    while (!mbar_try_wait(&bar, phase)) {
-    }
-    phase ^= 1;
-    if (tid == 0) {
-      __threadfence();
-      st_release(&flags[r], 1);
-    }
-    const KT* As = reinterpret_cast<const KT*>(kin + offA);
-    const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-    const int64_t phk = ((uintptr_t)(P.keys + (P.s + d0) * ks)) & 15;
-    const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + d0) * w)) & 15) : 0;
-    const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
-    merge_tile<KT>(MODE_MERGE, As, Bs, alpha, beta, nout, reinterpret_cast<KT*>(kout_s + phk), pout_s + php,
-                   pin + poffA, pin + poffB, w, wq4, tid, NT);
-    fence_proxy_async_smem();
-    // the records this region overwrites in the unbuffered run must have been read
-    if (tid < 32) {
-      // consumers of a run range [x, y) are the regions c with [run_c, run_{c+1}) intersecting
-      // it: from the last c with run_c <= x to the last c with run_c <= y - 1
-      int64_t c_lo = 0, c_hi = -1;
-      auto last_le = [&](int64_t v, int64_t lo, int64_t hi, bool on_b) {  // largest c in [lo,hi] with run_c <= v
-        while (lo < hi) {
-          const int64_t mid = (lo + hi + 1) >> 1;
-          const int64_t rc = on_b ? g.diag(mid) - g.split(mid) : g.split(mid);
-          if (rc <= v) lo = mid;
-          else hi = mid - 1;
-        }
-        return lo;
-      };
-      if (buf_a) {  // writes into B's area [m, e): B indices [jlo, jhi); consumers are regions <= r
-        const int64_t jlo = max(P.s + d0, P.m) - P.m, jhi = P.s + d1 - P.m;
-        if (jhi > jlo) {
-          c_lo = last_le(jlo, 0, r, true);
-          c_hi = last_le(jhi - 1, c_lo, r, true);
-        }
-      } else {  // writes into A's area [s, m): A indices [ilo, ihi); consumers are regions >= r
-        const int64_t ilo = d0, ihi = min(d1, la);
-        if (ihi > ilo) {
-          c_lo = last_le(ilo, r, P.Q - 1, false);
-          c_hi = last_le(ihi - 1, c_lo, P.Q - 1, false);
-        }
-      }
-      for (int64_t c = c_lo + (tid & 31); c <= c_hi; c += 32) {
-        if (c == r) continue;
-        for (uint32_t it = 0; ld_acquire(&flags[c]) == 0; ++it) {
-          if (ld_relaxed(P.err)) break;
-          if (it > kSpinLimit) {
-            raise_error(P.err, PM_ERR_TIMEOUT);
-            break;
-          }
-          backoff(it);
-        }
-      }
-    }
-    __syncthreads();
-    stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + d0) * ks), nout * ks, tid, NT);
-    if (w) stream_out(pout_s + php, P.pay + (P.s + d0) * w, nout * w, tid, NT);
-    ++n_reg;
-    __syncthreads();
   }
-  if (tid == 0) {
+  __syncthreads();
+  uint32_t ph[2] = {0, 0};
+  int cur = 0;
+  unsigned long long n_reg = 0;
+  unsigned long long cy[6] = {0, 0, 0, 0, 0, 0};
+  long long tb = clock64();
+#define PB_TICK(k)                  \
+  if (tid == 0) {                   \
+    const long long n_ = clock64(); \
+    cy[k] += n_ - tb;               \
+    tb = n_;                        \
+  }
+  while (true) {
+    const int64_t t = s_t[cur];
+    if (t >= P.Q) break;
+    const BufRegion R = buf_region<KT>(g, P, t, buf_a);
+    if (leader) {
+      // keep the next region in flight (its ticket was fetched one iteration ago)
+      const int64_t tn = (*(volatile int32_t*)P.err) ? P.Q : (t_pref < P.Q ? t_pref : P.Q);
+      if (t_pref < P.Q) t_pref = atomicAdd(P.ticket, 1);
+      s_t[cur ^ 1] = tn;
+      if (tn < P.Q) {
+        const BufRegion Rn = buf_region<KT>(g, P, tn, buf_a);
+        if (!Rn.identity) buf_issue<KT>(P, Rn, buf_a, STAGE(cur ^ 1), STAGE(cur ^ 1) + P.smem_keys, &bar[cur ^ 1]);
+      }
+    }
+    PB_TICK(0);
+    if (R.identity) {  // records already on their outputs and read by r only
+      if (leader) st_release(&flags[R.r], 1);
+    } else {
+      while (!mbar_try_wait(&bar[cur], ph[cur])) {
+      }
+      ph[cur] ^= 1;
+      PB_TICK(1);
+      const int64_t phk = ((uintptr_t)(P.keys + (P.s + R.d0) * ks)) & 15;
+      const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + R.d0) * w)) & 15) : 0;
+      uint8_t* kout_s = OUTB(cur);
+      uint8_t* pout_s = OUTB(cur) + P.smem_keys;
+      if (ctrl) {
+        if (leader && !s_early[cur]) {
+          __threadfence();
+          st_release(&flags[R.r], 1);
+        }
+        // the records this region overwrites in the unbuffered run must have been read
+        // by their consumers (regions c_lo..c_hi, precomputed by k_consumers)
+        const int64_t c_lo = __ldg(&P.state[R.r]), c_hi = __ldg(&P.loc[R.r]);
+        for (int64_t c = c_lo + lane; c <= c_hi; c += 32) {
+          if (c == R.r) continue;
+          for (uint32_t it = 0; ld_acquire(&flags[c]) == 0; ++it) {
+            if (ld_relaxed(P.err)) break;
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              break;
+            }
+            backoff(it);
+          }
+        }
+        // the prefetched region's loads often land meanwhile: announce its reads early
+        if (leader) {
+          s_early[cur ^ 1] = 0;
+          const int64_t tn = s_t[cur ^ 1];
+          if (tn < P.Q && mbar_try_wait(&bar[cur ^ 1], ph[cur ^ 1])) {
+            __threadfence();
+            st_release(&flags[buf_region<KT>(g, P, tn, buf_a).r], 1);
+            s_early[cur ^ 1] = 1;
+          }
+        }
+      } else {
+        uint8_t* kin = STAGE(cur);
+        uint8_t* pin = STAGE(cur) + P.smem_keys;
+        const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
+        merge_tile<KT>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
+                       reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                       reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA, pin + R.poffB, w, wq4,
+                       tid, MT);
+        PB_TICK(2);
+        fence_proxy_async_smem();
+      }
+      PB_TICK(5);
+      __syncthreads();  // tile complete, consumers done
+      PB_TICK(3);
+      // the leader (gt == 0) issues the bulk stores; everyone writes unaligned edges
+      const int gt = (tid + 32) % NT;
+      stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), R.nout * ks, gt, NT);
+      if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, R.nout * w, gt, NT);
+      ++n_reg;
+    }
+    cur ^= 1;
+    if (leader) bulk_wait_read<1>();  // the store that used outb[cur] (next) has read it
+    __syncthreads();
+    PB_TICK(4);
+  }
+  if (leader) {
     bulk_wait_all();
     atomicAdd(&P.stats[2], n_reg);
   }
+  if (tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cy[i]);
 }
 
 // ---- host launchers (called from pm_capi.cu) --------------------------------
@@ -1073,6 +1199,7 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
   const int cgrid = (int)std::min<int64_t>(std::max<int64_t>(((x1 - x0) * (int64_t)sizeof(KT) / 16 + 255) / 256, 1),
                                            (int64_t)grid * 4);
   k_copy_run<KT><<<cgrid, 256, 0, st>>>(P, x0, x1);
+  k_consumers<<<(int)std::min<int64_t>((P.Q + 255) / 256, 4096), 256, 0, st>>>(P, buf_a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
