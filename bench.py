@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-sample-log-len", type=int, default=24)
     ap.add_argument("--quick", action="store_true", help="skip e2e/cpu/clock legs (profiling runs)")
     ap.add_argument("--no-buffered", action="store_true", help="skip the buffered-mode leg")
+    ap.add_argument("--dist", action="store_true", help="distributed block merge even at one rank")
     return ap.parse_args()
 
 
@@ -187,6 +188,118 @@ def run_reference(args):
         "e2e": {"value": rate, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- distributed (N GPUs)
+def block_input(rank, world, n, seed):
+    """Rank `rank`'s block of the global X = A|B (config-5 recipe).
+
+    |A| = |B| = world*n/2.  Each run is filled bucket by bucket: the records of
+    run block k hold uniform int32 values from the k-th slice of [0, 2^31),
+    sorted locally -- globally sorted runs without a global sort.
+    """
+    import torch
+
+    N = world * n
+    la = N // 2
+    lo, hi = rank * n, (rank + 1) * n
+    parts = []
+    g = torch.Generator(device="cuda")
+    for run0, run1 in ((0, la), (la, N)):
+        a, b = max(lo, run0), min(hi, run1)
+        if b <= a:
+            continue
+        runlen = run1 - run0
+        nb = max(1, runlen // n)                      # buckets of the run
+        span = (1 << 31) // nb
+        x = a
+        while x < b:
+            k = min((x - run0) // n, nb - 1)          # bucket of x
+            bend = run0 + (k + 1) * n if k < nb - 1 else run1
+            e = min(b, bend)
+            g.manual_seed(seed * 1000003 + (run0 == 0) * 7919 + k)
+            vals = torch.randint(k * span, (k + 1) * span, (e - x,), generator=g, device="cuda", dtype=torch.int64)
+            parts.append(vals.sort().values.to(torch.int32))
+            x = e
+    return torch.cat(parts), la
+
+
+def run_dist(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_12648_b200.dist import merge_distributed
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    log_len = args.log_len or 29
+    n = 1 << (log_len + 1)                            # records per GPU (weak scaling)
+    keys0, la = block_input(rank, world, n, 5)
+    work = keys0.clone()
+    pay = torch.empty((n, 0), dtype=torch.uint8, device="cuda")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(max(args.warmup, 1)):
+        work.copy_(keys0)
+        merge_distributed(work, pay, la)
+    # correctness: each block sorted and blocks in order across ranks
+    ends = torch.stack([work[0].to(torch.int64), work[-1].to(torch.int64)])
+    allends = [torch.zeros_like(ends) for _ in range(world)]
+    dist.all_gather(allends, ends)
+    ok = bool(torch.all(work[1:] >= work[:-1]).item()) and all(
+        int(allends[i][1]) <= int(allends[i + 1][0]) for i in range(world - 1))
+    if not ok:
+        raise SystemExit("bench: distributed merge output is not sorted")
+    times = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if not args.quick else None
+    if sampler:
+        sampler.__enter__()
+    for _ in range(args.steps):
+        work.copy_(keys0)
+        dist.barrier()
+        ev0.record()
+        merge_distributed(work, pay, la)
+        ev1.record()
+        ev1.synchronize()
+        times.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    t = torch.tensor([sum(times)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    N = world * n
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    value = N * args.steps / (total_ms / 1e3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"cfg5: int32 uniform sorted runs, block-distributed A|B, {n} records per GPU "
+                                   f"(N = {N})", "key": "int32", "payload_bytes": 0, "L_A": la, "L_B": N - la,
+                       "parallelism": f"dist{world}: global stable splits + NCCL all-to-all + local engine",
+                       "l2": "per-GPU blocks exceed the 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9 / peak,
+                         "traffic": None, "kernel": "whole distributed step per GPU"},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": None,
+        }
+        if sampler:
+            line["clocks"] = sampler.summary()
+        print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 
@@ -400,6 +513,8 @@ def main():
         faulthandler.dump_traceback_later(int(os.environ.get("BENCH_DUMP_S", "120")), exit=True)
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
+        return run_dist(args)
     return run_ours(args)
 
 
