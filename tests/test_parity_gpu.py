@@ -225,3 +225,21 @@ def test_buffered_mode_vs_oracle(width):
                 arr = to_gpu(kk, pp)
                 pm.seq_merge_buffered(arr, pm.MergeJob(lo, lo + middle, lo + size))
                 assert_same(arr, want_k, want_p, f"buffered size={size} split={split} w={width}")
+
+
+@pytest.mark.parametrize("width", [0, 4])
+def test_scratch_sizes_vs_oracle(width):
+    """pm_merge's scratch_records argument (pool size) never changes the result."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(9090 + width)
+    for size in (50000, 1 << 20, 3 << 20):
+        for split in (0.3, 0.5):
+            keys, payload, middle = random_instance(rng, size, split, 2**31 - 1, width)
+            want_k, want_p = keys.copy(), payload.copy()
+            orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+            mn = min(middle, size - middle)
+            for scratch in (0, 1000, size // 64, size // 8, size // 4, mn - 1, mn, size):
+                arr = to_gpu(keys, payload)
+                _ops.merge(arr, 0, middle, size, scratch_records=scratch)
+                assert_same(arr, want_k, want_p, f"size={size} split={split} scratch={scratch}")
