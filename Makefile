@@ -27,4 +27,10 @@ clean:
 	rm -f $(OBJ) $(LIB)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean ptxas
+.PHONY: all oracle clean ptxas variant
+
+# tuning variant: make variant VNAME=t2 VFLAGS="-DPM_ENGINE_TEAM=2 -DPM_ENGINE_MINB=6 -DPM_TILE_BUDGET=36864"
+variant:
+	mkdir -p /tmp/pmv_$(VNAME)
+	for f in $(SRC); do $(NVCC) $(NVFLAGS) $(VFLAGS) -c $$f -o /tmp/pmv_$(VNAME)/$$(basename $$f .cu).o & done; wait
+	$(NVCC) $(ARCH) -shared -o $(PKG)/libparmerge_b200_$(VNAME).so /tmp/pmv_$(VNAME)/*.o -lcudart

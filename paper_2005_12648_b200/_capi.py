@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libparmerge_b200.so")
+# PM_LIB selects an alternative in-tree build (tuning experiments); default the main one
+LIB_PATH = os.path.join(_HERE, os.environ.get("PM_LIB", "libparmerge_b200.so"))
 
 PM_OK = 0
 PM_ERR_ARG = 1

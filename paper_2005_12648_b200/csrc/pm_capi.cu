@@ -48,7 +48,6 @@ struct Ctl {
   int32_t pad_;
 };
 
-constexpr int kEngineThreads = 256;
 
 }  // namespace
 
@@ -86,8 +85,7 @@ static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 
 // Tile geometry for a record of ks+w bytes: region M (power of two) so that the
 // staged keys+payload+index map stay ~<=72 KB per CTA (3 CTAs per SM).
-static bool pick_tiles(int ks, int64_t w, int64_t* M, int64_t* T, int32_t* mu) {
-  const int64_t budget = 72 * 1024;
+static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T, int32_t* mu) {
   int64_t m = 8192;
   while (m > 16 && m * 2 * (ks + w) + 256 > budget) m >>= 1;
   if (m * 2 * (ks + w) + 256 > budget + 64 * 1024) return false;  // records too wide
@@ -102,10 +100,11 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   if (e - s <= 0 || m == s || m == e) return PM_OK;
   int64_t M, T;
   int32_t mu;
-  if (!pick_tiles(ks, w, &M, &T, &mu)) return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
   // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
-  // half-size regions, two staging + two output tiles (same shared-memory budget)
+  // half-size regions, two staging + two output tiles (72 KB of shared memory)
   const bool buffered = mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m);
+  if (!pick_tiles(ks, w, buffered ? 72 * 1024 : kTileBudget, &M, &T, &mu))
+    return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
   if (buffered && M >= 32) {
     M /= 2;
     T = std::max<int64_t>(16, M / 4);
@@ -139,8 +138,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   const size_t smem = (buffered ? 4 : 2) * (P.smem_keys + P.smem_pay);
   // persistent grid: every resident CTA slot on every SM
   int bps = 0;
-  cudaError_t ce = ks == 4 ? engine_occupancy<int32_t>(kEngineThreads, smem, &bps)
-                           : engine_occupancy<int64_t>(kEngineThreads, smem, &bps);
+  cudaError_t ce;
+  if (buffered)
+    ce = ks == 4 ? buffered_occupancy<int32_t>(smem, &bps) : buffered_occupancy<int64_t>(smem, &bps);
+  else
+    ce = ks == 4 ? engine_occupancy<int32_t>(kEngineThreads, smem, &bps)
+                 : engine_occupancy<int64_t>(kEngineThreads, smem, &bps);
   if (ce != cudaSuccess) return cuda_fail(ce, "engine occupancy");
   if (bps < 1) return fail(PM_ERR_UNSUPPORTED, "engine does not fit on an SM");
   int grid = (int)std::min<int64_t>((int64_t)bps * ctx->num_sms, P.Q);

@@ -56,7 +56,10 @@ struct Geo {
   __device__ int64_t consumed_by_window(int64_t j, int64_t t) const {
     int64_t wl, wr;
     window(t, wl, wr);
-    int64_t a_lo = split(wl), a_hi = split(wr + 1);
+    return consumed_in(j, wl, wr, split(wl), split(wr + 1));
+  }
+  // same, with the window [wl, wr] and its boundary splits already at hand
+  __device__ int64_t consumed_in(int64_t j, int64_t wl, int64_t wr, int64_t a_lo, int64_t a_hi) const {
     int64_t b_lo = diag(wl) - a_lo, b_hi = diag(wr + 1) - a_hi;
     int64_t x0 = slot_lo(j), x1 = slot_hi(j), c = 0;
     // A part of the unit, A-local indices
@@ -155,15 +158,40 @@ __global__ void k_plan(EngineParams P) {
 constexpr int kCache = 64;   // CTA-local caches of free slots / free scratch units
 constexpr int kMaxMu = 8;    // slots per region handled by the occupant warps
 
+// Splits a ticket's salvage and data phases need, loaded once (one round trip of
+// independent loads) an iteration ahead: region q = region_of_ticket(t) has
+// splits a0 = split(q), a1 = split(q+1); the windows of tickets t-1 and t have
+// boundary splits (plo, phi) and (clo, chi).
+struct TInfo {
+  int64_t t, a0, a1, plo, phi, clo, chi;
+};
+__device__ __forceinline__ void load_tinfo(const Geo& g, int64_t t, TInfo& o) {
+  const int64_t q = g.region_of_ticket(t);
+  int64_t pl = 0, pr = -1, cl, cr;
+  if (t > 0) g.window(t - 1, pl, pr);
+  g.window(t, cl, cr);
+  const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+  const int64_t plo = t > 0 ? g.split(pl) : 0, phi = t > 0 ? g.split(pr + 1) : 0;
+  const int64_t clo = g.split(cl), chi = g.split(cr + 1);
+  o.a0 = a0;
+  o.a1 = a1;
+  o.plo = plo;
+  o.phi = phi;
+  o.clo = clo;
+  o.chi = chi;
+  o.t = t;
+}
+
 struct SmemCtl {
   uint64_t bar;
+  TInfo ti[4];           // ring: step (3) of iteration k fills ti[k&3] for t_pref
   int64_t t_cur, t_nxt;  // data-team region, salvage-team region (tickets; >= Q: none)
   int32_t def_u[2][kMaxMu];   // occupants whose move was deferred (no space yet), per parity
   int32_t def_slot[2][kMaxMu];
   int32_t n_def[2];
   int64_t t_pref;        // the ticket after t_nxt (its slots are closed early by the salvage team)
-  int64_t pre_t;         // ticket whose occupants pre_* hold
-  int32_t pre_occ[kMaxMu], pre_r[kMaxMu], pre_l[kMaxMu];
+  int64_t pre_t[2];      // ticket whose occupants pre_*[p] hold (double buffered by iteration parity)
+  int32_t pre_occ[2][kMaxMu], pre_r[2][kMaxMu], pre_l[2][kMaxMu];
   int32_t published;     // the data team has published t_cur's reads
   int32_t deferred_done; // the salvage team has moved t_cur's deferred occupants
   int32_t lock;          // protects the caches below
@@ -524,10 +552,33 @@ __device__ __forceinline__ void close_and_sample(const Geo& g, const EngineParam
   }
 }
 
+// Cycle counters of the engine phases (pm_status stats[4..15]); compiled in only
+// with -DPM_STATS=1 (tuning builds) -- the counters cost registers.
+#ifndef PM_STATS
+#define PM_STATS 0
+#endif
+enum : int { PS_GATHER = 4, PS_LAND = 5, PS_PUBLISH = 6, PS_MERGE = 7, PS_WAITDEF = 8, PS_STORE = 9,
+             PS_STEP1 = 10, PS_STEP2 = 11, PS_SLAND = 12, PS_THR = 13, PS_DEST = 14, PS_COPY = 15 };
+struct Prof {
+#if PM_STATS
+  unsigned long long v[16] = {};
+  __device__ __forceinline__ long long now() const { return clock64(); }
+  __device__ __forceinline__ void add(int k, long long d) { v[k] += (unsigned long long)d; }
+  __device__ __forceinline__ void flush(unsigned long long* stats) const {
+    for (int k = 4; k < 16; ++k)
+      if (v[k]) atomicAdd(&stats[k], v[k]);
+  }
+#else
+  __device__ __forceinline__ long long now() const { return 0; }
+  __device__ __forceinline__ void add(int, long long) {}
+  __device__ __forceinline__ void flush(unsigned long long*) const {}
+#endif
+};
+
 // Move unit u out of slot `slot` into `dest` (warp-wide) and publish its new home.
 template <typename KT>
 __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, int32_t u, int64_t slot, int32_t dest,
-                                          int lane) {
+                                          int lane, Prof& prof, bool publish = true) {
   const int64_t ks = sizeof(KT), w = P.w;
   const int64_t x0 = g.slot_lo(u), x1 = g.slot_hi(u), hb = g.slot_base(u);
   const int64_t sbase = g.slot_base(slot);
@@ -539,8 +590,11 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
     uint8_t* pd = dest >= 0 ? P.pay + (dbase + (x0 - hb)) * w : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * w;
     copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
   }
+  if (!publish) return;  // the caller fences and publishes later (publish_pending)
+  const long long cf = prof.now();
   __threadfence();  // every lane's part is visible before the new home is published
   __syncwarp();
+  prof.add(PS_COPY, prof.now() - cf);
   if (lane == 0) st_release(&P.loc[u], dest);
 }
 
@@ -556,7 +610,7 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
 // The salvage chain (exchange, waits, copies, fences) thus overlaps the
 // previous region's data phase instead of holding the shared-memory buffer.
 template <typename KT>
-__global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
+__global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(EngineParams P) {
   extern __shared__ __align__(128) uint8_t dyn[];
   __shared__ SmemCtl ctl;
   Geo g(P);
@@ -570,14 +624,12 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
   uint8_t* pin = dyn + P.smem_keys;           // staged payload
   uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;  // merged output tile (keys), phase-aligned
   uint8_t* pout_s = kout_s + P.smem_keys;            // merged output tile (payload)
-  constexpr int kTeam = 4;                     // warps per team
+  constexpr int kTeam = kEngineTeam;           // warps per team
   const int home = blockIdx.x & (kShards - 1);
   const int64_t la = g.LA();
   uint32_t phase = 0;
-  unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long n_salv = 0, r_salv = 0, n_reg = 0, n_ident = 0, spins_r = 0, spins_o = 0;
-  unsigned long long w_land = 0, w_thr = 0, w_dest = 0, w_copy = 0;
-  long long tc = clock64();
+  Prof prof;
+  uint32_t n_salv = 0, r_salv = 0, n_reg = 0, n_ident = 0;
   int32_t t_pref = 0;
   if (tid == 0) {
     mbar_init(&ctl.bar, 1);
@@ -589,18 +641,20 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
     ctl.t_cur = P.Q;
     ctl.t_nxt = atomicAdd(P.ticket, 1);
     ctl.t_pref = atomicAdd(P.ticket, 1);
-    ctl.pre_t = -1;
+    ctl.pre_t[0] = ctl.pre_t[1] = -1;
+    for (int k = 0; k < 4; ++k) ctl.ti[k].t = -1;
     t_pref = atomicAdd(P.ticket, 1);  // two ahead of t_nxt, in flight
   }
   __syncthreads();
   int it_par = 0;  // parity of the deferred list written by the salvage team this iteration
+  int iter = 0;    // iteration count (TInfo ring index)
 
   while (true) {
     const int64_t t_cur = ctl.t_cur, t_nxt = ctl.t_nxt;
     if ((t_cur >= P.Q && t_nxt >= P.Q) || ctl.abort) break;
     if (wid < kTeam) {
       // ===================== salvage team ======================================
-      long long ts = clock64();
+      long long ts = prof.now();
       // (1) t_cur's deferred moves: t_cur's reads are published first
       const int cp = it_par ^ 1;
       const int nd = ctl.n_def[cp];
@@ -609,52 +663,70 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
         }
         for (int k = wid; k < nd; k += kTeam) {
           const int32_t u = ctl.def_u[cp][k];
-          long long c2 = clock64();
+          const long long c2 = prof.now();
           const int32_t dest = acquire_dest(ctl, P, u, home, lane, true);
-          w_dest += clock64() - c2;
+          prof.add(PS_DEST, prof.now() - c2);
           if (dest == INT32_MIN) {
             if (lane == 0) ctl.abort = 1;
             continue;
           }
-          long long c3 = clock64();
-          move_unit<KT>(g, P, u, ctl.def_slot[cp][k], dest, lane);
-          w_copy += clock64() - c3;
+          const long long c3 = prof.now();
+          move_unit<KT>(g, P, u, ctl.def_slot[cp][k], dest, lane, prof);
+          prof.add(PS_COPY, prof.now() - c3);
           if (lane == 0) {
             ++n_salv;
-            r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
+            r_salv += (uint32_t)(g.slot_hi(u) - g.slot_lo(u));
           }
         }
       }
+      if (tid == 0 && t_nxt < P.Q && ctl.ti[(iter - 1) & 3].t != t_nxt) load_tinfo(g, t_nxt, ctl.ti[(iter - 1) & 3]);
       named_barrier_sync(2, kTeam * 32);
       if (tid == 0) {
         atomicExch(&ctl.deferred_done, 1);
-        const long long n_ = clock64();
-        spins_r += n_ - ts;  // (stats[10]: salvage step 1 cycles)
+        const long long n_ = prof.now();
+        prof.add(PS_STEP1, n_ - ts);
         ts = n_;
       }
       // (2) salvage for t_nxt
+      int32_t pend_u[(kMaxMu + kTeam - 1) / kTeam], pend_d[(kMaxMu + kTeam - 1) / kTeam], n_pend = 0;
+#define PM_FLUSH_PENDING()                                                                  \
+  if (n_pend) {                                                                             \
+    const long long cf = prof.now();                                                        \
+    __threadfence(); /* the copies are visible before their new homes are published */     \
+    __syncwarp();                                                                           \
+    prof.add(PS_COPY, prof.now() - cf);                                                    \
+    if (lane == 0)                                                                          \
+      for (int k = 0; k < n_pend; ++k) st_release(&P.loc[pend_u[k]], pend_d[k]);           \
+    n_pend = 0;                                                                             \
+  }  // moved units whose new home is unpublished
       if (t_nxt < P.Q) {
         const int64_t q = g.region_of_ticket(t_nxt);
         const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
         const int nslot = (int)(j1 - j0);
         const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-        const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+        const TInfo& ti = ctl.ti[(iter - 1) & 3];  // == t_nxt (filled by step (3) or step (1))
+        const int64_t a0 = ti.a0, a1 = ti.a1;
         const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-        const bool pre = ctl.pre_t == t_nxt;  // closed and sampled last iteration
+        int64_t pwl = 0, pwr = -1, cwl, cwr;
+        if (t_nxt > 0) g.window(t_nxt - 1, pwl, pwr);
+        g.window(t_nxt, cwl, cwr);
+        const int rp = it_par ^ 1;             // the buffer last iteration's step (3) filled
+        const bool pre = ctl.pre_t[rp] == t_nxt;  // closed and sampled last iteration
         for (int i = wid; i < nslot; i += kTeam) {
           int32_t u = -1, early_r = 0, early_l = -1;
           if (lane == 0) {
             if (pre) {
-              u = ctl.pre_occ[i];
-              early_r = ctl.pre_r[i];
-              early_l = ctl.pre_l[i];
+              u = ctl.pre_occ[rp][i];
+              early_r = ctl.pre_r[rp][i];
+              early_l = ctl.pre_l[rp][i];
             } else {
               close_and_sample(g, P, j0 + i, identity, u, early_r, early_l);
             }
           }
           u = __shfl_sync(0xffffffffu, u, 0);
           if (u < 0 || identity) continue;
-          long long c1 = clock64();
+          PM_FLUSH_PENDING();  // never wait with an unpublished move
+          const long long c1 = prof.now();
           int alive = 0;
           if (lane == 0) {
             const int32_t slot = (int32_t)(j0 + i);
@@ -670,9 +742,10 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
               }
               backoff(it);
             }
+            prof.add(PS_SLAND, prof.now() - c1);
             // every consumer of order < t_nxt must have read u (t_nxt itself has not
             // published yet, so reads[] counts exactly those)
-            const int64_t before = t_nxt > 0 ? g.consumed_by_window(u, t_nxt - 1) : 0;
+            const int64_t before = t_nxt > 0 ? g.consumed_in(u, pwl, pwr, ti.plo, ti.phi) : 0;
             for (uint32_t it = 0; early_r < before; ++it) {
               early_r = ld_acquire(&P.reads[u]);
               if (early_r >= before) break;
@@ -688,14 +761,14 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
               if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
               backoff(it);
             }
-            alive = g.consumed_by_window(u, t_nxt) < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
+            alive = g.consumed_in(u, cwl, cwr, ti.clo, ti.chi) < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
           }
           alive = __shfl_sync(0xffffffffu, alive, 0);
-          long long c2 = clock64();
-          w_thr += c2 - c1;
+          const long long c2 = prof.now();
+          prof.add(PS_THR, c2 - c1);
           if (!alive) continue;
           const int32_t dest = acquire_dest(ctl, P, u, home, lane, false);  // never block here
-          w_dest += clock64() - c2;
+          prof.add(PS_DEST, prof.now() - c2);
           if (dest == INT32_MIN) {
             if (lane == 0) {
               const int k = atomicAdd(&ctl.n_def[it_par], 1);
@@ -704,18 +777,24 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
             }
             continue;
           }
-          long long c3 = clock64();
-          move_unit<KT>(g, P, u, j0 + i, dest, lane);
-          w_copy += clock64() - c3;
+          const long long c3 = prof.now();
+          // the new home is published after step (3): the copy's stores drain
+          // meanwhile (readers of u all have order > t_nxt; t_nxt itself may still
+          // read the old slot, which it alone overwrites later)
+          move_unit<KT>(g, P, u, j0 + i, dest, lane, prof, false);
+          pend_u[n_pend] = u;
+          pend_d[n_pend] = dest;
+          ++n_pend;
+          prof.add(PS_COPY, prof.now() - c3);
           if (lane == 0) {
             ++n_salv;
-            r_salv += (unsigned long long)(g.slot_hi(u) - g.slot_lo(u));
+            r_salv += (uint32_t)(g.slot_hi(u) - g.slot_lo(u));
           }
         }
       }
-      named_barrier_sync(2, kTeam * 32);  // everyone is done with pre_*
       // (3) close the following region's slots now and sample its occupants, so the
-      //     next iteration's step (2) starts without a round trip
+      //     next iteration's step (2) starts without a round trip (no waits here:
+      //     this warp's moves are still unpublished)
       {
         const int64_t tp = ctl.t_pref;
         if (tp < P.Q) {
@@ -729,30 +808,40 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
             if (lane == 0) {
               int32_t u, r, l;
               close_and_sample(g, P, j0 + i, identity, u, r, l);
-              ctl.pre_occ[i] = u;
-              ctl.pre_r[i] = r;
-              ctl.pre_l[i] = l;
+              if (u >= 0 && !identity && l == (int32_t)(j0 + i) && r < g.slot_hi(u) - g.slot_lo(u)) {
+                // the occupant will probably be salvaged next iteration: warm L2
+                const int64_t x0 = g.slot_lo(u), n = g.slot_hi(u) - x0, src = g.slot_base(j0 + i) + (x0 - g.slot_base(u));
+                prefetch_l2(P.keys + src * (int64_t)sizeof(KT), n * (int64_t)sizeof(KT));
+                if (w) prefetch_l2(P.pay + src * w, n * w);
+              }
+              ctl.pre_occ[it_par][i] = u;
+              ctl.pre_r[it_par][i] = r;
+              ctl.pre_l[it_par][i] = l;
             }
           }
         }
+        if (tid == 0 && tp < P.Q) load_tinfo(g, tp, ctl.ti[iter & 3]);
+        PM_FLUSH_PENDING();
         named_barrier_sync(2, kTeam * 32);
-        if (tid == 0) ctl.pre_t = tp;
+        if (tid == 0) ctl.pre_t[it_par] = tp;
       }
-      if (tid == 0) spins_o += clock64() - ts;  // (stats[11]: salvage step 2 cycles)
+      if (tid == 0) prof.add(PS_STEP2, prof.now() - ts);
     } else {
       // ===================== data team ==========================================
       const int gt = tid - kTeam * 32, GT = NT - kTeam * 32;
-      long long td = clock64();
-#define PM_TICK(k)                 \
-  if (gt == 0) {                   \
-    const long long n_ = clock64(); \
-    cyc[k] += n_ - td;             \
-    td = n_;                       \
+      long long td = prof.now();
+#define PM_TICK(k)                   \
+  if (gt == 0) {                     \
+    const long long n_ = prof.now(); \
+    prof.add(PS_GATHER + (k), n_ - td); \
+    td = n_;                         \
   }
       if (t_cur < P.Q) {
         const int64_t q = g.region_of_ticket(t_cur);
         const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-        const int64_t a0 = g.split(q), a1 = g.split(q + 1);
+        const TInfo& tc = ctl.ti[(iter - 2) & 3];
+        const bool have = tc.t == t_cur;
+        const int64_t a0 = have ? tc.a0 : g.split(q), a1 = have ? tc.a1 : g.split(q + 1);
         const int64_t b0 = d0 - a0, b1 = d1 - a1;
         const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
         const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
@@ -849,6 +938,7 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
           merge_tile<KT>(P.mode, As, Bs, alpha, beta, nout, ko, po, PA, PB, w, wq4, gt, GT);
           fence_proxy_async_smem();   // our smem writes -> visible to the TMA (async proxy)
+          PM_TICK(3);
           if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
             // last reader: free the unit's location into the CTA cache
             const int32_t l = ld_acquire(&P.loc[pj]);
@@ -860,7 +950,7 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
           }
           named_barrier_sync(1, GT);  // the output tile is complete, reads are published
           if (gt == 0) atomicExch(&ctl.published, 1);
-          PM_TICK(3);
+          PM_TICK(4);
           // every slot of t_cur must be cleared: deferred moves finish first
           while (!*(volatile int32_t*)&ctl.deferred_done) {
           }
@@ -891,31 +981,21 @@ __global__ void __launch_bounds__(256, 3) k_engine(EngineParams P) {
       if (*(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
     }
     it_par ^= 1;
+    ++iter;
     __syncthreads();
   }
   if (tid == kTeam * 32) bulk_wait_all();  // the last output tile has landed
   // leave nothing behind in the CTA cache (another job reuses the lists)
   if (tid == 0) cache_flush(ctl, P, home);
   if (lane == 0 && n_salv) {
-    atomicAdd(&P.stats[0], n_salv);
-    atomicAdd(&P.stats[1], r_salv);
+    atomicAdd(&P.stats[0], (unsigned long long)n_salv);
+    atomicAdd(&P.stats[1], (unsigned long long)r_salv);
   }
   if (tid == kTeam * 32) {
-    atomicAdd(&P.stats[2], n_reg);
-    atomicAdd(&P.stats[3], n_ident);
+    atomicAdd(&P.stats[2], (unsigned long long)n_reg);
+    atomicAdd(&P.stats[3], (unsigned long long)n_ident);
   }
-  if (tid == kTeam * 32)
-    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cyc[i]);
-  if (tid == 0) {
-    atomicAdd(&P.stats[10], spins_r);
-    atomicAdd(&P.stats[11], spins_o);
-  }
-  if (lane == 0) {
-    atomicAdd(&P.stats[12], w_land);
-    atomicAdd(&P.stats[13], w_thr);
-    atomicAdd(&P.stats[14], w_dest);
-    atomicAdd(&P.stats[15], w_copy);
-  }
+  if (lane == 0) prof.flush(P.stats);
 }
 
 
@@ -1080,13 +1160,13 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
   uint32_t ph[2] = {0, 0};
   int cur = 0;
   unsigned long long n_reg = 0;
-  unsigned long long cy[6] = {0, 0, 0, 0, 0, 0};
-  long long tb = clock64();
-#define PB_TICK(k)                  \
-  if (tid == 0) {                   \
-    const long long n_ = clock64(); \
-    cy[k] += n_ - tb;               \
-    tb = n_;                        \
+  Prof prof;
+  long long tb = prof.now();
+#define PB_TICK(k)                       \
+  if (tid == 0) {                        \
+    const long long n_ = prof.now();     \
+    prof.add(PS_GATHER + (k), n_ - tb);  \
+    tb = n_;                             \
   }
   while (true) {
     const int64_t t = s_t[cur];
@@ -1172,8 +1252,7 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
     bulk_wait_all();
     atomicAdd(&P.stats[2], n_reg);
   }
-  if (tid == 0)
-    for (int i = 0; i < 6; ++i) atomicAdd(&P.stats[4 + i], cy[i]);
+  if (tid == 0) prof.flush(P.stats);
 }
 
 // ---- host launchers (called from pm_capi.cu) --------------------------------
@@ -1194,6 +1273,12 @@ cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_engine<KT>, block, smem);
 }
 template <typename KT>
+cudaError_t buffered_occupancy(size_t smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_buffered<KT>, kBufferedThreads, smem);
+}
+template <typename KT>
 cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st) {
   const int64_t x0 = buf_a ? P.s : P.m, x1 = buf_a ? P.m : P.e;
   const int cgrid = (int)std::min<int64_t>(std::max<int64_t>(((x1 - x0) * (int64_t)sizeof(KT) / 16 + 255) / 256, 1),
@@ -1204,7 +1289,7 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_buffered<KT><<<grid, 256, smem, st>>>(P, buf_a);
+  k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, buf_a);
   return cudaGetLastError();
 }
 template cudaError_t launch_buffered<int32_t>(const EngineParams&, int32_t, int, size_t, cudaStream_t);
@@ -1214,6 +1299,8 @@ template cudaError_t launch_plan<int64_t>(const EngineParams&, int, cudaStream_t
 template cudaError_t launch_engine<int32_t>(const EngineParams&, int, int, size_t, cudaStream_t);
 template cudaError_t launch_engine<int64_t>(const EngineParams&, int, int, size_t, cudaStream_t);
 template cudaError_t engine_occupancy<int32_t>(int, size_t, int*);
+template cudaError_t buffered_occupancy<int32_t>(size_t, int*);
+template cudaError_t buffered_occupancy<int64_t>(size_t, int*);
 template cudaError_t engine_occupancy<int64_t>(int, size_t, int*);
 
 }  // namespace pm

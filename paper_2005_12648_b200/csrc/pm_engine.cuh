@@ -25,6 +25,23 @@ enum : int32_t { MODE_MERGE = 0, MODE_ROTATE = 1 };
 enum : int32_t { ST_FREE = -1, ST_CLOSED = -2 };
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 
+// k_engine shape: two teams of kEngineTeam warps, kEngineMinBlocks resident CTAs
+// per SM, staging tiles sized to kTileBudget bytes of shared memory per CTA.
+#ifndef PM_ENGINE_TEAM
+#define PM_ENGINE_TEAM 4
+#endif
+#ifndef PM_ENGINE_MINB
+#define PM_ENGINE_MINB 3
+#endif
+#ifndef PM_TILE_BUDGET
+#define PM_TILE_BUDGET (72 * 1024)
+#endif
+constexpr int kEngineTeam = PM_ENGINE_TEAM;
+constexpr int kEngineThreads = 64 * PM_ENGINE_TEAM;
+constexpr int kEngineMinBlocks = PM_ENGINE_MINB;
+constexpr int64_t kTileBudget = PM_TILE_BUDGET;
+constexpr int kBufferedThreads = 256;
+
 // Two-front ticket order around the centre region qc (regions 0..Q-1): ticket 0
 // is qc, then qc-1, qc+1, qc-2, qc+2, ... until one side runs out, then the
 // rest of the longer side.  __host__ __device__ so tests can check the exact
