@@ -130,6 +130,10 @@ int pm_set_timing(pm_ctx *ctx, int on);
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
 /* Copy the first n entries of the last job's split table to host memory (debug). */
 int pm_debug_splits(pm_ctx *ctx, int64_t *host_out, int64_t n);
+
+/* Debug: the 64 device counters of the last job ([0,16) as pm_status; [16,64)
+ * per-ticket-range histograms filled only by -DPM_STATS=1 tuning builds). */
+int pm_debug_stats(pm_ctx *ctx, uint64_t *host_out64);
 int pm_kernel_ms(pm_ctx *ctx, float *plan_ms, float *engine_ms);
 
 #ifdef __cplusplus

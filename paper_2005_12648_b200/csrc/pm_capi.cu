@@ -36,16 +36,21 @@ int cuda_fail(cudaError_t e, const char* what) {
   } while (0)
 
 // control block layout (device, bytes)
+// Words polled or hammered by every CTA live on their own 256-byte lines (distinct
+// L2 slices): a spin loop on `err` must not queue up the ticket atomics.
+struct alignas(256) Line32 {
+  int32_t v;
+  int32_t pad_[63];
+};
 struct Ctl {
   unsigned long long free_top;
   unsigned long long scr_top;
-  unsigned long long stats[16];
-  int32_t scr_count;
-  int32_t ticket;
-  int32_t err;
-  int32_t noop;
-  int32_t need_space;
-  int32_t pad_;
+  unsigned long long stats[64];  // [0,16): pm_status; [16,64): tuning histograms (PM_STATS builds)
+  Line32 scr_count_;
+  Line32 ticket_;
+  Line32 err_;
+  Line32 noop_;
+  Line32 need_space_;
 };
 
 
@@ -121,7 +126,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.e = e;
   P.T = T;
   P.mu = mu;
-  if (mu > 8) return fail(PM_ERR_INTERNAL, "slots per region exceed the occupant warps");
+  if (mu > 8) return fail(PM_ERR_INTERNAL, "too many slots per region");
   P.nthreads = kEngineThreads;
   P.M = M;
   P.k0 = s / T;
@@ -148,7 +153,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   if (bps < 1) return fail(PM_ERR_UNSUPPORTED, "engine does not fit on an SM");
   int grid = (int)std::min<int64_t>((int64_t)bps * ctx->num_sms, P.Q);
   // bounded salvage pool: O(grid * tile) records, phase matched to the caller's arrays
-  P.reserve = (int64_t)grid * (mu + 4) + 16;
+  // every CTA may hold kRing tickets' moved-but-unread units at once
+  P.reserve = (int64_t)grid * (kRing * mu + 4) + 16;
   int64_t S = std::max<int64_t>(2 * P.reserve, scratch_records / T + P.reserve);
   S = std::min<int64_t>(S, P.K + P.reserve);
   P.S = S;
@@ -162,7 +168,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   const size_t off_nf = off_reads + (size_t)align_up(P.K * 4, 256);
   const size_t off_ns = off_nf + (size_t)align_up(P.K * 4, 256);
   const size_t off_tops = off_ns + (size_t)align_up(S * 4, 256);
-  const size_t ws_need = off_tops + 2 * 64 * sizeof(unsigned long long);
+  const size_t ws_need = off_tops + 2 * kShards * kTopStride * sizeof(unsigned long long);
   int rc = ensure(&ctx->ws, &ctx->ws_bytes, ws_need);
   if (rc) return rc;
   const size_t scr_k = (size_t)align_up(S * T * ks + 32, 256);
@@ -177,13 +183,13 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.next_free = reinterpret_cast<int32_t*>(ws + off_nf);
   P.next_scr = reinterpret_cast<int32_t*>(ws + off_ns);
   P.free_top = reinterpret_cast<unsigned long long*>(ws + off_tops);  // [64] shard tops
-  P.scr_top = P.free_top + 64;
+  P.scr_top = P.free_top + kShards * kTopStride;
   P.stats = ctx->ctl->stats;
-  P.scr_count = &ctx->ctl->scr_count;
-  P.ticket = &ctx->ctl->ticket;
-  P.err = &ctx->ctl->err;
-  P.noop = &ctx->ctl->noop;
-  P.need_space = &ctx->ctl->need_space;
+  P.scr_count = &ctx->ctl->scr_count_.v;
+  P.ticket = &ctx->ctl->ticket_.v;
+  P.err = &ctx->ctl->err_.v;
+  P.noop = &ctx->ctl->noop_.v;
+  P.need_space = &ctx->ctl->need_space_.v;
   char* scr = static_cast<char*>(ctx->scr);
   P.scr_keys = scr + ((uintptr_t)keys & 15);
   P.scr_pay = reinterpret_cast<uint8_t*>(scr + scr_k + (w ? ((uintptr_t)payload & 15) : 0));
@@ -233,6 +239,15 @@ static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* paylo
 extern "C" {
 
 int pm_version(void) { return 100; }
+
+int pm_debug_stats(pm_ctx* ctx, uint64_t* host_out64) {
+  if (!ctx || !host_out64) return fail(PM_ERR_ARG, "bad arguments");
+  PM_CUDA(cudaDeviceSynchronize());
+  Ctl h;
+  PM_CUDA(cudaMemcpy(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 64; ++i) host_out64[i] = h.stats[i];
+  return PM_OK;
+}
 
 int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   if (!ctx || !host_out || n < 0) return fail(PM_ERR_ARG, "bad arguments");
@@ -378,13 +393,13 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
   PM_CUDA(cudaMemcpy(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (stats)
     for (int i = 0; i < 16; ++i) stats[i] = h.stats[i];
-  if (h.err != 0) {
+  if (h.err_.v != 0) {
     int32_t zero = 0;
-    cudaMemcpy(&ctx->ctl->err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
-    const char* what = h.err == PM_ERR_TIMEOUT   ? "device wait exceeded its bound"
-                       : h.err == PM_ERR_NOSPACE ? "salvage space exhausted"
+    cudaMemcpy(&ctx->ctl->err_.v, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+    const char* what = h.err_.v == PM_ERR_TIMEOUT   ? "device wait exceeded its bound"
+                       : h.err_.v == PM_ERR_NOSPACE ? "salvage space exhausted"
                                                  : "device invariant violated";
-    return fail(h.err, std::string("merge engine: ") + what);
+    return fail(h.err_.v, std::string("merge engine: ") + what);
   }
   return PM_OK;
 }

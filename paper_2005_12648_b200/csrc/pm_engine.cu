@@ -20,7 +20,11 @@
 
 namespace pm {
 
-constexpr int kShards = 64;  // sharded global free lists (one CAS word each)
+// -DPM_STATS=1 (tuning builds): cycle counters and path counters in pm_debug_stats
+#ifndef PM_STATS
+#define PM_STATS 0
+#endif
+
 
 // ============================================================================
 // geometry helpers (all indices int64; "local" = relative to the job)
@@ -137,8 +141,8 @@ __global__ void k_plan(EngineParams P) {
   // scratch unit i starts on shard i % kShards
   for (int64_t i = tid; i < P.S; i += nthr) P.next_scr[i] = (i + kShards < P.S) ? (int32_t)(i + kShards) : (int32_t)kEmpty32;
   for (int64_t sh = tid; sh < kShards; sh += nthr) {
-    P.free_top[sh] = (unsigned long long)kEmpty32;
-    P.scr_top[sh] = sh < P.S ? (unsigned long long)sh : (unsigned long long)kEmpty32;
+    P.free_top[sh * kTopStride] = (unsigned long long)kEmpty32;
+    P.scr_top[sh * kTopStride] = sh < P.S ? (unsigned long long)sh : (unsigned long long)kEmpty32;
   }
   if (tid == 0) {
     *P.scr_count = (int32_t)P.S;
@@ -147,7 +151,7 @@ __global__ void k_plan(EngineParams P) {
     if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
     *P.need_space = 0;
-    for (int i = 0; i < 16; ++i) P.stats[i] = 0;
+    for (int i = 0; i < 64; ++i) P.stats[i] = 0;
   }
 }
 
@@ -156,7 +160,6 @@ __global__ void k_plan(EngineParams P) {
 // ============================================================================
 
 constexpr int kCache = 64;   // CTA-local caches of free slots / free scratch units
-constexpr int kMaxMu = 8;    // slots per region handled by the occupant warps
 
 // Splits a ticket's salvage and data phases need, loaded once (one round trip of
 // independent loads) an iteration ahead: region q = region_of_ticket(t) has
@@ -182,32 +185,14 @@ __device__ __forceinline__ void load_tinfo(const Geo& g, int64_t t, TInfo& o) {
   o.t = t;
 }
 
-struct SmemCtl {
-  uint64_t bar;
-  TInfo ti[4];           // ring: step (3) of iteration k fills ti[k&3] for t_pref
-  int64_t t_cur, t_nxt;  // data-team region, salvage-team region (tickets; >= Q: none)
-  int32_t def_u[2][kMaxMu];   // occupants whose move was deferred (no space yet), per parity
-  int32_t def_slot[2][kMaxMu];
-  int32_t n_def[2];
-  int64_t t_pref;        // the ticket after t_nxt (its slots are closed early by the salvage team)
-  int64_t pre_t[2];      // ticket whose occupants pre_*[p] hold (double buffered by iteration parity)
-  int32_t pre_occ[2][kMaxMu], pre_r[2][kMaxMu], pre_l[2][kMaxMu];
-  int32_t published;     // the data team has published t_cur's reads
-  int32_t deferred_done; // the salvage team has moved t_cur's deferred occupants
-  int32_t lock;          // protects the caches below
-  int32_t n_fs, n_sc;
-  int32_t abort;
-  int32_t fs[kCache];    // free slots (may go stale: their region can start meanwhile)
-  int32_t sc[kCache];    // free scratch units
-};
 
 // ---- sharded global free lists (one CAS word per shard) --------------------
 // warp-cooperative pop: lanes read all shard tops at once, then lane 0 pops the
 // nearest non-empty shard (home first), reusing the scanned top as the CAS
 // expectation.  Returns -1 if every shard looked empty.
 __device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* next, int home, int lane) {
-  const unsigned long long a = *(volatile unsigned long long*)&tops[(home + lane) & (kShards - 1)];
-  const unsigned long long b = *(volatile unsigned long long*)&tops[(home + 32 + lane) & (kShards - 1)];
+  const unsigned long long a = *(volatile unsigned long long*)&tops[((home + lane) & (kShards - 1)) * kTopStride];
+  const unsigned long long b = *(volatile unsigned long long*)&tops[((home + 32 + lane) & (kShards - 1)) * kTopStride];
   unsigned ma = __ballot_sync(0xffffffffu, (uint32_t)a != kEmpty32);
   unsigned mb = __ballot_sync(0xffffffffu, (uint32_t)b != kEmpty32);
   int32_t v = -1;
@@ -230,7 +215,7 @@ __device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* n
         const uint32_t idx = (uint32_t)old;
         const int32_t nxt = *(volatile int32_t*)&next[idx];
         const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (uint32_t)nxt;
-        const unsigned long long seen = atomicCAS(&tops[sh], old, nw);
+        const unsigned long long seen = atomicCAS(&tops[sh * kTopStride], old, nw);
         if (seen == old) {
           __threadfence();
           v = (int32_t)idx;
@@ -245,17 +230,20 @@ __device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* n
 }
 
 // ---- CTA-local caches (shared memory, short spinlock) -----------------------
-__device__ __forceinline__ void cta_lock(SmemCtl& c) {
+template <class Ctl>
+__device__ __forceinline__ void cta_lock(Ctl& c) {
   while (atomicCAS(&c.lock, 0, 1) != 0) {
   }
   __threadfence_block();
 }
-__device__ __forceinline__ void cta_unlock(SmemCtl& c) {
+template <class Ctl>
+__device__ __forceinline__ void cta_unlock(Ctl& c) {
   __threadfence_block();
   atomicExch(&c.lock, 0);
 }
 // push a freed slot (v >= 0) or scratch unit (v = -(i+1)); overflow goes global
-__device__ __forceinline__ void cache_push(SmemCtl& c, const EngineParams& P, int32_t v, int home) {
+template <class Ctl>
+__device__ __forceinline__ void cache_push(Ctl& c, const EngineParams& P, int32_t v, int home) {
   cta_lock(c);
   bool done = false;
   if (v >= 0 && c.n_fs < kCache) {
@@ -267,12 +255,13 @@ __device__ __forceinline__ void cache_push(SmemCtl& c, const EngineParams& P, in
   }
   cta_unlock(c);
   if (!done) {
-    if (v >= 0) stack_push(&P.free_top[home], P.next_free, v);
-    else stack_push(&P.scr_top[home], P.next_scr, -v - 1);
+    if (v >= 0) stack_push(&P.free_top[home * kTopStride], P.next_free, v);
+    else stack_push(&P.scr_top[home * kTopStride], P.next_scr, -v - 1);
   }
 }
 // give every cached unit back to the global lists (another CTA is starving)
-__device__ __forceinline__ void cache_flush(SmemCtl& c, const EngineParams& P, int home) {
+template <class Ctl>
+__device__ __forceinline__ void cache_flush(Ctl& c, const EngineParams& P, int home) {
   cta_lock(c);
   const int nf = c.n_fs, ns = c.n_sc;
   c.n_fs = 0;
@@ -281,8 +270,8 @@ __device__ __forceinline__ void cache_flush(SmemCtl& c, const EngineParams& P, i
   for (int i = 0; i < nf; ++i) fs[i] = c.fs[i];
   for (int i = 0; i < ns; ++i) sc[i] = c.sc[i];
   cta_unlock(c);
-  for (int i = 0; i < nf; ++i) stack_push(&P.free_top[home], P.next_free, fs[i]);
-  for (int i = 0; i < ns; ++i) stack_push(&P.scr_top[home], P.next_scr, sc[i]);
+  for (int i = 0; i < nf; ++i) stack_push(&P.free_top[home * kTopStride], P.next_free, fs[i]);
+  for (int i = 0; i < ns; ++i) stack_push(&P.scr_top[home * kTopStride], P.next_scr, sc[i]);
 }
 
 // Warp-wide: a salvage destination for unit u.  Scratch first (a parked unit is
@@ -290,36 +279,53 @@ __device__ __forceinline__ void cache_flush(SmemCtl& c, const EngineParams& P, i
 // Called only after this region has read its inputs (stage B done), so a
 // blocked caller never holds space other regions wait for.  When it has to
 // block it raises need_space so CTAs flush their caches.
-__device__ __forceinline__ int32_t acquire_dest(SmemCtl& c, const EngineParams& P, int32_t u, int home, int lane,
+template <class Ctl>
+__device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, int32_t u, int home, int lane,
                                                 bool block) {
   bool flagged = false;
   int32_t dest = INT32_MIN;
   for (uint32_t it = 0;; ++it) {
+    // scratch first (cache, then the global lists): a unit parked in scratch is
+    // final, one parked in a free slot moves again when that slot's region starts
     int32_t d = INT32_MIN;
     if (lane == 0) {
       cta_lock(c);
-      if (c.n_sc > 0) {
-        d = -c.sc[--c.n_sc] - 1;
-        cta_unlock(c);
-      } else {
-        int32_t f = -1;
-        while (c.n_fs > 0) {
-          f = c.fs[--c.n_fs];
-          if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) break;
-          f = -1;  // its region started meanwhile
-        }
-        cta_unlock(c);
-        if (f >= 0) d = f;
-      }
+      if (c.n_sc > 0) d = -c.sc[--c.n_sc] - 1;
+      cta_unlock(c);
     }
     d = __shfl_sync(0xffffffffu, d, 0);
     if (d != INT32_MIN) {
       dest = d;
+#if PM_STATS
+      if (lane == 0) atomicAdd(&P.stats[16], 1ull);
+#endif
       break;
     }
     const int32_t si = warp_pop(P.scr_top, P.next_scr, home, lane);
     if (si >= 0) {
       dest = -si - 1;
+#if PM_STATS
+      if (lane == 0) atomicAdd(&P.stats[18], 1ull);
+#endif
+      break;
+    }
+    if (lane == 0) {
+      cta_lock(c);
+      int32_t f = -1;
+      while (c.n_fs > 0) {
+        f = c.fs[--c.n_fs];
+        if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) break;
+        f = -1;  // its region started meanwhile
+      }
+      cta_unlock(c);
+      if (f >= 0) d = f;
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (d != INT32_MIN) {
+      dest = d;
+#if PM_STATS
+      if (lane == 0) atomicAdd(&P.stats[17], 1ull);
+#endif
       break;
     }
     int32_t f;
@@ -334,9 +340,12 @@ __device__ __forceinline__ int32_t acquire_dest(SmemCtl& c, const EngineParams& 
     }
     if (got) {
       dest = f;
+#if PM_STATS
+      if (lane == 0) atomicAdd(&P.stats[19], 1ull);
+#endif
       break;
     }
-    if (!block || ld_relaxed(P.err)) break;
+    if (!block || ((it & 15) == 15 && ld_relaxed(P.err))) break;
     if (!flagged && it > 32) {
       if (lane == 0) atomicAdd(P.need_space, 1);
       flagged = true;
@@ -554,9 +563,6 @@ __device__ __forceinline__ void close_and_sample(const Geo& g, const EngineParam
 
 // Cycle counters of the engine phases (pm_status stats[4..15]); compiled in only
 // with -DPM_STATS=1 (tuning builds) -- the counters cost registers.
-#ifndef PM_STATS
-#define PM_STATS 0
-#endif
 enum : int { PS_GATHER = 4, PS_LAND = 5, PS_PUBLISH = 6, PS_MERGE = 7, PS_WAITDEF = 8, PS_STORE = 9,
              PS_STEP1 = 10, PS_STEP2 = 11, PS_SLAND = 12, PS_THR = 13, PS_DEST = 14, PS_COPY = 15 };
 struct Prof {
@@ -568,10 +574,15 @@ struct Prof {
     for (int k = 4; k < 16; ++k)
       if (v[k]) atomicAdd(&stats[k], v[k]);
   }
+  // per-ticket-range histogram: stats[base + 16*t/Q] += d
+  __device__ __forceinline__ void hist(unsigned long long* stats, int base, int64_t t, int64_t Q, long long d) const {
+    atomicAdd(&stats[base + (int)(t * 16 / Q)], (unsigned long long)d);
+  }
 #else
   __device__ __forceinline__ long long now() const { return 0; }
   __device__ __forceinline__ void add(int, long long) {}
   __device__ __forceinline__ void flush(unsigned long long*) const {}
+  __device__ __forceinline__ void hist(unsigned long long*, int, int64_t, int64_t, long long) const {}
 #endif
 };
 
@@ -591,28 +602,119 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
     copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
   }
   if (!publish) return;  // the caller fences and publishes later (publish_pending)
-  const long long cf = prof.now();
   __threadfence();  // every lane's part is visible before the new home is published
   __syncwarp();
-  prof.add(PS_COPY, prof.now() - cf);
   if (lane == 0) st_release(&P.loc[u], dest);
 }
 
-// Software-pipelined persistent engine.  Each iteration of a CTA:
-//   salvage team (warps 0..3) works on ticket t_nxt: closes its slots and moves
-//     every occupant that a later region still needs (after all earlier
-//     consumers have read it) to scratch or a free slot -- without blocking on
-//     space (a miss is deferred); first it finishes t_cur's deferred moves,
-//     which may block, because t_cur's reads are published by then;
-//   data team (warps 4..7) works on ticket t_cur: gathers its A/B pieces into
-//     shared memory (TMA bulk + vector head/tail), publishes the reads, merges
-//     in shared memory, waits for t_cur's deferred moves, streams the region back.
-// The salvage chain (exchange, waits, copies, fences) thus overlaps the
-// previous region's data phase instead of holding the shared-memory buffer.
+// Decoupled persistent engine.  A CTA holds a ring of up to kRing tickets:
+//   salvage workers (warps 0..kTeam-1) each take the next (ticket, slot) item in
+//     ticket order and run its chain on their own: close the slot and sample its
+//     occupant, wait for the occupant to land and for every earlier consumer to
+//     read it, then move it (scratch first, else a free slot) if a later region
+//     still needs it.  No space -> wait for the ticket's reads to be published,
+//     then block for space (the region's own reads free space first).
+//   data team (warps kTeam..2*kTeam-1) takes the ring's tickets in order: gathers
+//     the A/B pieces into shared memory (TMA bulk), publishes the reads, merges in
+//     shared memory, waits until every slot item of the ticket is done, and
+//     streams the output tile back in place (TMA bulk store).
+// The teams meet only on shared-memory counters, so a worker's long chain
+// (waits on other CTAs, round trips of the copy) overlaps the other workers'
+// chains and the data team's work on earlier tickets.
+
+constexpr int kMaxMu = 8;  // slots per region (pm_capi.cu enforces mu <= kMaxMu)
+struct RingEntry {
+  TInfo ti;             // ti.t = ticket (>= Q: the end)
+  int32_t nslot;        // slot items of the ticket
+  int32_t items_done;   // finished slot items
+  int32_t published;    // the data team has published the ticket's reads
+  int32_t pad_;
+  int32_t occ[kMaxMu];  // occupant sampled by each slot item (-1: none)
+};
+struct EngCtl {
+  uint64_t bar;
+  RingEntry ring[kRing];
+  int32_t filled;       // entries filled so far (monotone)
+  int32_t d_done;       // entries the data team has finished (monotone)
+  int32_t cur_e, cur_i; // next salvage item: entry, slot
+  int32_t claim_lock;
+  int32_t next_t;       // prefetched ticket
+  int32_t lock;         // protects the caches below (cache_push / acquire_dest)
+  int32_t n_fs, n_sc;
+  int32_t abort;
+  int32_t fs[kCache];
+  int32_t sc[kCache];
+};
+
+// The data team's view of one region: its input pieces and staging offsets.
+struct DataRegion {
+  int64_t t, d0, nout, alpha, beta, xa, xb, offA, offB, poffA, poffB, ua0, ub0;
+  int32_t npa, np;
+  bool identity;
+  __device__ __forceinline__ void init(const Geo& g, const EngineParams& P, const TInfo& ti, int64_t la) {
+    t = ti.t;
+    if (t >= P.Q) return;
+    const int64_t ks = P.ks, w = P.w;
+    const int64_t q = g.region_of_ticket(t);
+    d0 = g.diag(q);
+    const int64_t d1 = g.diag(q + 1);
+    const int64_t a0 = ti.a0, a1 = ti.a1, b0 = d0 - a0, b1 = d1 - a1;
+    alpha = a1 - a0;
+    beta = b1 - b0;
+    nout = d1 - d0;
+    identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+    xa = P.s + a0;
+    xb = P.m + b0;
+    offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+    offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+    poffA = poffB = 0;
+    if (w) {
+      poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+      poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+    }
+    ua0 = alpha ? (xa / P.T - P.k0) : 0;
+    const int64_t ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
+    ub0 = beta ? (xb / P.T - P.k0) : 0;
+    const int64_t ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
+    npa = (int32_t)(ua1 - ua0);
+    np = npa + (int32_t)(ub1 - ub0);
+  }
+};
+
+// Fill ring entry e with the prefetched ticket (caller holds the claim lock and
+// has checked that the entry is free: e - d_done < kRing).
+__device__ __forceinline__ void open_entry(EngCtl& c, const Geo& g, const EngineParams& P, int32_t e) {
+  volatile EngCtl& vc = c;
+  RingEntry& re = c.ring[e % kRing];
+  const int64_t t = vc.next_t;
+  if (t < P.Q) {
+    load_tinfo(g, t, re.ti);
+    const int64_t q = g.region_of_ticket(t);
+    re.nslot = (int32_t)(g.region_end_slot(q) - g.region_first_slot(q));
+    vc.next_t = atomicAdd(P.ticket, 1);
+  } else {
+    re.ti.t = P.Q;
+    re.nslot = 0;
+  }
+  re.items_done = 0;
+  re.published = 0;
+  __threadfence_block();
+  vc.filled = e + 1;
+}
+__device__ __forceinline__ void claim_lock(EngCtl& c) {
+  while (atomicCAS(&c.claim_lock, 0, 1) != 0) {
+  }
+  __threadfence_block();
+}
+__device__ __forceinline__ void claim_unlock(EngCtl& c) {
+  __threadfence_block();
+  atomicExch(&c.claim_lock, 0);
+}
+
 template <typename KT>
 __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(EngineParams P) {
   extern __shared__ __align__(128) uint8_t dyn[];
-  __shared__ SmemCtl ctl;
+  __shared__ EngCtl ctl;
   Geo g(P);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int NT = blockDim.x;
@@ -620,371 +722,371 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
   const int64_t w = P.w;
   if (*(volatile int32_t*)P.noop) return;
 
-  uint8_t* kin = dyn;                         // staged keys (A then B, phase-shifted)
-  uint8_t* pin = dyn + P.smem_keys;           // staged payload
-  uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;  // merged output tile (keys), phase-aligned
-  uint8_t* pout_s = kout_s + P.smem_keys;            // merged output tile (payload)
-  constexpr int kTeam = kEngineTeam;           // warps per team
+  uint8_t* kin = dyn;                                 // staged keys (A then B, phase-shifted)
+  uint8_t* pin = dyn + P.smem_keys;                   // staged payload
+  uint8_t* kout_s = dyn + P.smem_keys + P.smem_pay;   // merged output tile (keys), phase-aligned
+  uint8_t* pout_s = kout_s + P.smem_keys;             // merged output tile (payload)
+  constexpr int kTeam = kEngineTeam;                  // warps per team
   const int home = blockIdx.x & (kShards - 1);
   const int64_t la = g.LA();
-  uint32_t phase = 0;
   Prof prof;
   uint32_t n_salv = 0, r_salv = 0, n_reg = 0, n_ident = 0;
-  int32_t t_pref = 0;
   if (tid == 0) {
     mbar_init(&ctl.bar, 1);
     ctl.lock = 0;
+    ctl.claim_lock = 0;
     ctl.n_fs = 0;
     ctl.n_sc = 0;
     ctl.abort = 0;
-    ctl.n_def[0] = ctl.n_def[1] = 0;
-    ctl.t_cur = P.Q;
-    ctl.t_nxt = atomicAdd(P.ticket, 1);
-    ctl.t_pref = atomicAdd(P.ticket, 1);
-    ctl.pre_t[0] = ctl.pre_t[1] = -1;
-    for (int k = 0; k < 4; ++k) ctl.ti[k].t = -1;
-    t_pref = atomicAdd(P.ticket, 1);  // two ahead of t_nxt, in flight
+    ctl.filled = 0;
+    ctl.d_done = 0;
+    ctl.cur_e = 0;
+    ctl.cur_i = 0;
+    ctl.next_t = atomicAdd(P.ticket, 1);
   }
   __syncthreads();
-  int it_par = 0;  // parity of the deferred list written by the salvage team this iteration
-  int iter = 0;    // iteration count (TInfo ring index)
+  volatile EngCtl& vc = ctl;
 
-  while (true) {
-    const int64_t t_cur = ctl.t_cur, t_nxt = ctl.t_nxt;
-    if ((t_cur >= P.Q && t_nxt >= P.Q) || ctl.abort) break;
-    if (wid < kTeam) {
-      // ===================== salvage team ======================================
-      long long ts = prof.now();
-      // (1) t_cur's deferred moves: t_cur's reads are published first
-      const int cp = it_par ^ 1;
-      const int nd = ctl.n_def[cp];
-      if (nd) {
-        while (!*(volatile int32_t*)&ctl.published) {
+  if (wid < kTeam) {
+    // ===================== salvage workers ====================================
+    long long cw = prof.now();
+    for (uint32_t spin = 0;;) {
+      // ---- claim the next item (lane 0, under the claim lock) ----
+      int32_t e = -1, i = 0;
+      int status = 0;  // 0 = got an item, 1 = retry (ring full), 2 = finished
+      if (lane == 0) {
+        claim_lock(ctl);
+        e = vc.cur_e;
+        if (vc.abort) {
+          status = 2;
+        } else if (e == vc.filled) {
+          if (e - vc.d_done >= kRing) status = 1;  // ring full: the data team is behind
+          else open_entry(ctl, g, P, e);
         }
-        for (int k = wid; k < nd; k += kTeam) {
-          const int32_t u = ctl.def_u[cp][k];
-          const long long c2 = prof.now();
-          const int32_t dest = acquire_dest(ctl, P, u, home, lane, true);
+        if (status == 0) {
+          const RingEntry& re = ctl.ring[e % kRing];
+          if (re.ti.t >= P.Q) {
+            status = 2;
+          } else {
+            i = vc.cur_i;
+            if (i + 1 >= re.nslot) {
+              vc.cur_e = e + 1;
+              vc.cur_i = 0;
+            } else {
+              vc.cur_i = i + 1;
+            }
+          }
+        }
+        claim_unlock(ctl);
+      }
+      status = __shfl_sync(0xffffffffu, status, 0);
+      if (status == 2) break;
+      if (status == 1) {
+        if (lane == 0 && (++spin & 63) == 0 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
+        __nanosleep(64);
+        continue;
+      }
+      e = __shfl_sync(0xffffffffu, e, 0);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      const long long c0 = prof.now();
+      prof.add(PS_STEP1, c0 - cw);  // claiming, incl. waiting for ring space
+      // ---- run the item: slot j0 + i of ticket t ----
+      RingEntry& re = ctl.ring[e % kRing];
+      const int64_t t = re.ti.t;
+      const int64_t q = g.region_of_ticket(t);
+      const int64_t j0 = g.region_first_slot(q);
+      const int32_t slot = (int32_t)(j0 + i);
+      const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+      const int64_t a0 = re.ti.a0, a1 = re.ti.a1;
+      const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+      int32_t u = -1, early_r = 0, early_l = -1;
+      if (lane == 0) {
+        close_and_sample(g, P, slot, identity, u, early_r, early_l);
+        re.occ[i] = identity ? -1 : u;
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= 0 && !identity) {
+        int alive = 0;
+        if (lane == 0) {
+          for (uint32_t it = 0; early_l != slot && ld_acquire(&P.loc[u]) != slot; ++it) {  // landing
+            if ((it & 255) == 255 && ld_relaxed(P.err)) {
+              ctl.abort = 1;
+              break;
+            }
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              ctl.abort = 1;
+              break;
+            }
+            backoff(it);
+          }
+          prof.add(PS_SLAND, prof.now() - c0);
+          // move u now if a region after t still needs it: earlier consumers that
+          // have not read it yet read either copy -- t's store waits for them
+          int64_t cwl, cwr;
+          g.window(t, cwl, cwr);
+          alive = g.consumed_in(u, cwl, cwr, re.ti.clo, re.ti.chi) < g.slot_hi(u) - g.slot_lo(u) && !vc.abort;
+        }
+        alive = __shfl_sync(0xffffffffu, alive, 0);
+        const long long c2 = prof.now();
+        prof.add(PS_THR, c2 - c0);
+        if (alive) {
+          int32_t dest = acquire_dest(ctl, P, u, home, lane, false);
+          if (dest == INT32_MIN) {
+            // no space: the region's own reads free space first, then block
+            const long long cb = prof.now();
+            if (lane == 0)
+              while (!vc.ring[e % kRing].published && !vc.abort) __nanosleep(128);
+            __syncwarp();
+            if (!vc.abort) dest = acquire_dest(ctl, P, u, home, lane, true);
+            if (lane == 0) {
+              prof.hist(P.stats, 20, 0, 1, 1);
+              prof.hist(P.stats, 21, 0, 1, prof.now() - cb);
+            }
+          }
           prof.add(PS_DEST, prof.now() - c2);
           if (dest == INT32_MIN) {
             if (lane == 0) ctl.abort = 1;
-            continue;
-          }
-          const long long c3 = prof.now();
-          move_unit<KT>(g, P, u, ctl.def_slot[cp][k], dest, lane, prof);
-          prof.add(PS_COPY, prof.now() - c3);
-          if (lane == 0) {
-            ++n_salv;
-            r_salv += (uint32_t)(g.slot_hi(u) - g.slot_lo(u));
-          }
-        }
-      }
-      if (tid == 0 && t_nxt < P.Q && ctl.ti[(iter - 1) & 3].t != t_nxt) load_tinfo(g, t_nxt, ctl.ti[(iter - 1) & 3]);
-      named_barrier_sync(2, kTeam * 32);
-      if (tid == 0) {
-        atomicExch(&ctl.deferred_done, 1);
-        const long long n_ = prof.now();
-        prof.add(PS_STEP1, n_ - ts);
-        ts = n_;
-      }
-      // (2) salvage for t_nxt
-      int32_t pend_u[(kMaxMu + kTeam - 1) / kTeam], pend_d[(kMaxMu + kTeam - 1) / kTeam], n_pend = 0;
-#define PM_FLUSH_PENDING()                                                                  \
-  if (n_pend) {                                                                             \
-    const long long cf = prof.now();                                                        \
-    __threadfence(); /* the copies are visible before their new homes are published */     \
-    __syncwarp();                                                                           \
-    prof.add(PS_COPY, prof.now() - cf);                                                    \
-    if (lane == 0)                                                                          \
-      for (int k = 0; k < n_pend; ++k) st_release(&P.loc[pend_u[k]], pend_d[k]);           \
-    n_pend = 0;                                                                             \
-  }  // moved units whose new home is unpublished
-      if (t_nxt < P.Q) {
-        const int64_t q = g.region_of_ticket(t_nxt);
-        const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
-        const int nslot = (int)(j1 - j0);
-        const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-        const TInfo& ti = ctl.ti[(iter - 1) & 3];  // == t_nxt (filled by step (3) or step (1))
-        const int64_t a0 = ti.a0, a1 = ti.a1;
-        const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-        int64_t pwl = 0, pwr = -1, cwl, cwr;
-        if (t_nxt > 0) g.window(t_nxt - 1, pwl, pwr);
-        g.window(t_nxt, cwl, cwr);
-        const int rp = it_par ^ 1;             // the buffer last iteration's step (3) filled
-        const bool pre = ctl.pre_t[rp] == t_nxt;  // closed and sampled last iteration
-        for (int i = wid; i < nslot; i += kTeam) {
-          int32_t u = -1, early_r = 0, early_l = -1;
-          if (lane == 0) {
-            if (pre) {
-              u = ctl.pre_occ[rp][i];
-              early_r = ctl.pre_r[rp][i];
-              early_l = ctl.pre_l[rp][i];
-            } else {
-              close_and_sample(g, P, j0 + i, identity, u, early_r, early_l);
-            }
-          }
-          u = __shfl_sync(0xffffffffu, u, 0);
-          if (u < 0 || identity) continue;
-          PM_FLUSH_PENDING();  // never wait with an unpublished move
-          const long long c1 = prof.now();
-          int alive = 0;
-          if (lane == 0) {
-            const int32_t slot = (int32_t)(j0 + i);
-            for (uint32_t it = 0; early_l != slot && ld_acquire(&P.loc[u]) != slot; ++it) {  // landing
-              if (ld_relaxed(P.err)) {
-                ctl.abort = 1;
-                break;
-              }
-              if (it > kSpinLimit) {
-                raise_error(P.err, PM_ERR_TIMEOUT);
-                ctl.abort = 1;
-                break;
-              }
-              backoff(it);
-            }
-            prof.add(PS_SLAND, prof.now() - c1);
-            // every consumer of order < t_nxt must have read u (t_nxt itself has not
-            // published yet, so reads[] counts exactly those)
-            const int64_t before = t_nxt > 0 ? g.consumed_in(u, pwl, pwr, ti.plo, ti.phi) : 0;
-            for (uint32_t it = 0; early_r < before; ++it) {
-              early_r = ld_acquire(&P.reads[u]);
-              if (early_r >= before) break;
-              if (ld_relaxed(P.err)) {
-                ctl.abort = 1;
-                break;
-              }
-              if (it > kSpinLimit) {
-                raise_error(P.err, PM_ERR_TIMEOUT);
-                ctl.abort = 1;
-                break;
-              }
-              if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
-              backoff(it);
-            }
-            alive = g.consumed_in(u, cwl, cwr, ti.clo, ti.chi) < g.slot_hi(u) - g.slot_lo(u) && !ctl.abort;
-          }
-          alive = __shfl_sync(0xffffffffu, alive, 0);
-          const long long c2 = prof.now();
-          prof.add(PS_THR, c2 - c1);
-          if (!alive) continue;
-          const int32_t dest = acquire_dest(ctl, P, u, home, lane, false);  // never block here
-          prof.add(PS_DEST, prof.now() - c2);
-          if (dest == INT32_MIN) {
+          } else {
+            const long long c3 = prof.now();
+            move_unit<KT>(g, P, u, slot, dest, lane, prof);
+            prof.add(PS_COPY, prof.now() - c3);
             if (lane == 0) {
-              const int k = atomicAdd(&ctl.n_def[it_par], 1);
-              ctl.def_u[it_par][k] = u;
-              ctl.def_slot[it_par][k] = (int32_t)(j0 + i);
-            }
-            continue;
-          }
-          const long long c3 = prof.now();
-          // the new home is published after step (3): the copy's stores drain
-          // meanwhile (readers of u all have order > t_nxt; t_nxt itself may still
-          // read the old slot, which it alone overwrites later)
-          move_unit<KT>(g, P, u, j0 + i, dest, lane, prof, false);
-          pend_u[n_pend] = u;
-          pend_d[n_pend] = dest;
-          ++n_pend;
-          prof.add(PS_COPY, prof.now() - c3);
-          if (lane == 0) {
-            ++n_salv;
-            r_salv += (uint32_t)(g.slot_hi(u) - g.slot_lo(u));
-          }
-        }
-      }
-      // (3) close the following region's slots now and sample its occupants, so the
-      //     next iteration's step (2) starts without a round trip (no waits here:
-      //     this warp's moves are still unpublished)
-      {
-        const int64_t tp = ctl.t_pref;
-        if (tp < P.Q) {
-          const int64_t q = g.region_of_ticket(tp);
-          const int64_t j0 = g.region_first_slot(q), j1 = g.region_end_slot(q);
-          const int nslot = (int)(j1 - j0);
-          const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-          const int64_t a0 = g.split(q), a1 = g.split(q + 1);
-          const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-          for (int i = wid; i < nslot; i += kTeam) {
-            if (lane == 0) {
-              int32_t u, r, l;
-              close_and_sample(g, P, j0 + i, identity, u, r, l);
-              if (u >= 0 && !identity && l == (int32_t)(j0 + i) && r < g.slot_hi(u) - g.slot_lo(u)) {
-                // the occupant will probably be salvaged next iteration: warm L2
-                const int64_t x0 = g.slot_lo(u), n = g.slot_hi(u) - x0, src = g.slot_base(j0 + i) + (x0 - g.slot_base(u));
-                prefetch_l2(P.keys + src * (int64_t)sizeof(KT), n * (int64_t)sizeof(KT));
-                if (w) prefetch_l2(P.pay + src * w, n * w);
-              }
-              ctl.pre_occ[it_par][i] = u;
-              ctl.pre_r[it_par][i] = r;
-              ctl.pre_l[it_par][i] = l;
+              ++n_salv;
+              r_salv += (uint32_t)(g.slot_hi(u) - g.slot_lo(u));
             }
           }
         }
-        if (tid == 0 && tp < P.Q) load_tinfo(g, tp, ctl.ti[iter & 3]);
-        PM_FLUSH_PENDING();
-        named_barrier_sync(2, kTeam * 32);
-        if (tid == 0) ctl.pre_t[it_par] = tp;
       }
-      if (tid == 0) prof.add(PS_STEP2, prof.now() - ts);
-    } else {
-      // ===================== data team ==========================================
-      const int gt = tid - kTeam * 32, GT = NT - kTeam * 32;
-      long long td = prof.now();
-#define PM_TICK(k)                   \
-  if (gt == 0) {                     \
-    const long long n_ = prof.now(); \
+      __syncwarp();
+      if (lane == 0) atomicAdd(&re.items_done, 1);
+      cw = prof.now();
+      prof.add(PS_STEP2, cw - c0);
+    }
+  } else {
+    // ===================== data team ==========================================
+    // Per entry: land the gathered pieces, publish the reads, merge into the output
+    // tile, issue the NEXT entry's gather into the freed input tile, then wait for
+    // the slot items and earlier consumers and stream the tile back.
+    const int gt = tid - kTeam * 32, GT = NT - kTeam * 32;
+    uint32_t phase = 0;
+    long long td = prof.now();
+#define PM_TICK(k)                      \
+  if (gt == 0) {                        \
+    const long long n_ = prof.now();    \
     prof.add(PS_GATHER + (k), n_ - td); \
-    td = n_;                         \
+    td = n_;                            \
   }
-      if (t_cur < P.Q) {
-        const int64_t q = g.region_of_ticket(t_cur);
-        const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-        const TInfo& tc = ctl.ti[(iter - 2) & 3];
-        const bool have = tc.t == t_cur;
-        const int64_t a0 = have ? tc.a0 : g.split(q), a1 = have ? tc.a1 : g.split(q + 1);
-        const int64_t b0 = d0 - a0, b1 = d1 - a1;
-        const int64_t alpha = a1 - a0, beta = b1 - b0, nout = d1 - d0;
-        const bool identity = P.mode == MODE_MERGE && ((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
-        if (identity) {
-          if (gt == 0) {
-            ++n_ident;
-            atomicExch(&ctl.published, 1);
-          }
-        } else {
-          const int64_t xa = P.s + a0, xb = P.m + b0;
-          const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-          const int64_t offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
-          int64_t poffA = 0, poffB = 0;
-          if (w) {
-            poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
-            poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
-          }
-          const int64_t ua0 = alpha ? (xa / P.T - P.k0) : 0, ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
-          const int64_t ub0 = beta ? (xb / P.T - P.k0) : 0, ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
-          const int npa = (int)(ua1 - ua0), np = npa + (int)(ub1 - ub0);
-          for (int p = gt; p < np; p += GT) {
-            const bool isA = p < npa;
-            const int64_t j = isA ? ua0 + p : ub0 + (p - npa);
-            const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-            const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-            // wait until the unit sits where nobody moves it before we have read it
-            int32_t l;
-            for (uint32_t it = 0;; ++it) {
-              l = ld_acquire(&P.loc[j]);
-              if (l < 0 || g.order(g.region_of_slot(l)) >= t_cur) break;
-              if (ld_relaxed(P.err)) {
-                ctl.abort = 1;
-                break;
-              }
-              if (it > kSpinLimit) {
-                raise_error(P.err, PM_ERR_TIMEOUT);
-                ctl.abort = 1;
-                break;
-              }
-              if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
-              backoff(it);
-            }
-            const int64_t hb = g.slot_base(j);
-            const char* ksrc;
-            const uint8_t* psrc;
-            if (l >= 0) {
-              const int64_t base = g.slot_base(l);
-              ksrc = P.keys + (base + (x0 - hb)) * ks;
-              psrc = P.pay + (base + (x0 - hb)) * w;
-            } else {
-              const int64_t si = -(int64_t)l - 1;
-              ksrc = P.scr_keys + (si * P.T + (x0 - hb)) * ks;
-              psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
-            }
-            uint8_t* kdst = kin + (isA ? offA + (x0 - xa) * ks : offB + (x0 - xb) * ks);
-            copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
-            if (w) {
-              uint8_t* pdst = pin + (isA ? poffA + (x0 - xa) * w : poffB + (x0 - xb) * w);
-              copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
-            }
-          }
-          named_barrier_sync(1, GT);  // every expect_tx registered before the single arrive
-          PM_TICK(0);
-          if (gt == 0) mbar_arrive(&ctl.bar);
-          while (!mbar_try_wait(&ctl.bar, phase)) {
-          }
-          phase ^= 1;
-          PM_TICK(1);
-          // publish the reads (one piece per thread; np <= GT): the atomics stay in
-          // flight during the merge, deaths are handled after it
-          int64_t pj = -1;
-          int32_t pn = 0, pold = 0;
-          if (gt < np) {
-            const bool isA = gt < npa;
-            pj = isA ? ua0 + gt : ub0 + (gt - npa);
-            const int64_t run0 = isA ? xa : xb, run1 = isA ? xa + alpha : xb + beta;
-            pn = (int32_t)(min(run1, g.slot_hi(pj)) - max(run0, g.slot_lo(pj)));
-            __threadfence();
-            pold = atomicAdd(&P.reads[pj], pn);
-          }
-          if (gt == 0) bulk_wait_read_all();  // last tile's TMA store has read the buffer
-          named_barrier_sync(1, GT);
-          PM_TICK(2);
-          // merge path (A wins ties): every thread merges an odd-length run of outputs
-          // (odd stride -> conflict-free smem) straight into the phase-aligned output tile
-          const KT* As = reinterpret_cast<const KT*>(kin + offA);
-          const KT* Bs = reinterpret_cast<const KT*>(kin + offB);
-          const int64_t phk = ((uintptr_t)(P.keys + (P.s + d0) * ks)) & 15;
-          KT* ko = reinterpret_cast<KT*>(kout_s + phk);
-          const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + d0) * w)) & 15) : 0;
-          uint8_t* po = pout_s + php;
-          const uint8_t* PA = pin + poffA;
-          const uint8_t* PB = pin + poffB;
-          const bool wq4 = w && (w & 3) == 0 && ((php | poffA | poffB) & 3) == 0;
-          merge_tile<KT>(P.mode, As, Bs, alpha, beta, nout, ko, po, PA, PB, w, wq4, gt, GT);
-          fence_proxy_async_smem();   // our smem writes -> visible to the TMA (async proxy)
-          PM_TICK(3);
-          if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
-            // last reader: free the unit's location into the CTA cache
-            const int32_t l = ld_acquire(&P.loc[pj]);
-            if (l < 0) {
-              cache_push(ctl, P, l, home);
-            } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)pj, ST_FREE) == (int32_t)pj) {
-              cache_push(ctl, P, l, home);
-            }
-          }
-          named_barrier_sync(1, GT);  // the output tile is complete, reads are published
-          if (gt == 0) atomicExch(&ctl.published, 1);
-          PM_TICK(4);
-          // every slot of t_cur must be cleared: deferred moves finish first
-          while (!*(volatile int32_t*)&ctl.deferred_done) {
-          }
-          PM_TICK(4);
-          if (!*(volatile int32_t*)&ctl.abort) {
-            // stream the tile back in place: TMA bulk store for the 16-byte-aligned body,
-            // generic stores for the unaligned head and tail bytes
-            stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + d0) * ks), nout * ks, gt, GT);
-            if (w) stream_out(pout_s + php, P.pay + (P.s + d0) * w, nout * w, gt, GT);
-          }
-          PM_TICK(5);
-          if (gt == 0) ++n_reg;
-        }
-      } else if (gt == 0) {
-        atomicExch(&ctl.published, 1);
+    // open entry e (if the workers have not) and describe its region
+    auto open_and_describe = [&](int32_t e, DataRegion& R) {
+      if (gt == 0 && vc.filled <= e && !vc.abort) {
+        claim_lock(ctl);
+        if (vc.filled <= e) open_entry(ctl, g, P, e);
+        claim_unlock(ctl);
       }
+      named_barrier_sync(1, GT);
+      R.init(g, P, ctl.ring[e % kRing].ti, la);
+    };
+    // open entries up to e ahead of need (thread gt == 0, while the team waits anyway)
+    auto open_ahead = [&](int32_t e) {
+      if (gt == 0 && vc.filled <= e && !vc.abort) {
+        claim_lock(ctl);
+        while (vc.filled <= e && vc.filled - vc.d_done < kRing) {
+          const int32_t f = vc.filled;
+          if (f > 0 && ctl.ring[(f - 1) % kRing].ti.t >= P.Q) break;  // the end is open already
+          open_entry(ctl, g, P, f);
+        }
+        claim_unlock(ctl);
+      }
+    };
+    // wait until every piece sits where nobody moves it before it is read, then
+    // issue its TMA bulk load (thread per piece) and arm the barrier
+    auto gather_issue = [&](const DataRegion& R) {
+      for (int p = gt; p < R.np; p += GT) {
+        const bool isA = p < R.npa;
+        const int64_t j = isA ? R.ua0 + p : R.ub0 + (p - R.npa);
+        const int64_t run0 = isA ? R.xa : R.xb, run1 = isA ? R.xa + R.alpha : R.xb + R.beta;
+        const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
+        int32_t l;
+        for (uint32_t it = 0;; ++it) {
+          l = ld_acquire(&P.loc[j]);
+          if (l < 0 || g.order(g.region_of_slot(l)) >= R.t) break;
+          if ((it & 255) == 255 && ld_relaxed(P.err)) {
+            ctl.abort = 1;
+            break;
+          }
+          if (it > kSpinLimit) {
+            raise_error(P.err, PM_ERR_TIMEOUT);
+            ctl.abort = 1;
+            break;
+          }
+          if ((it & 63) == 63 && *(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
+          backoff(it);
+        }
+        const int64_t hb = g.slot_base(j);
+        const char* ksrc;
+        const uint8_t* psrc;
+        if (l >= 0) {
+          const int64_t base = g.slot_base(l);
+          ksrc = P.keys + (base + (x0 - hb)) * ks;
+          psrc = P.pay + (base + (x0 - hb)) * w;
+        } else {
+          const int64_t si = -(int64_t)l - 1;
+          ksrc = P.scr_keys + (si * P.T + (x0 - hb)) * ks;
+          psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
+        }
+        uint8_t* kdst = kin + (isA ? R.offA + (x0 - R.xa) * ks : R.offB + (x0 - R.xb) * ks);
+        copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+        if (w) {
+          uint8_t* pdst = pin + (isA ? R.poffA + (x0 - R.xa) * w : R.poffB + (x0 - R.xb) * w);
+          copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
+        }
+      }
+      named_barrier_sync(1, GT);  // every expect_tx registered before the single arrive
+      if (gt == 0) mbar_arrive(&ctl.bar);
+    };
+
+    DataRegion R;
+    int32_t e = 0;
+    open_and_describe(0, R);
+    bool pending = false;  // a gather is in flight on ctl.bar
+    if (R.t < P.Q && !R.identity && !vc.abort) {
+      gather_issue(R);
+      pending = true;
     }
-    __syncthreads();
-    if (tid == 0) {
-      // rotate the pipeline: t_nxt becomes current; tickets are fetched two ahead
-      ctl.t_cur = ctl.t_nxt;
-      ctl.t_nxt = ctl.t_pref < P.Q ? ctl.t_pref : P.Q;
-      ctl.t_pref = t_pref < P.Q ? t_pref : P.Q;
-      if (t_pref < P.Q) t_pref = atomicAdd(P.ticket, 1);
-      ctl.n_def[it_par ^ 1] = 0;  // the list t_cur used is consumed
-      ctl.published = 0;
-      ctl.deferred_done = 0;
-      if (*(volatile int32_t*)P.need_space) cache_flush(ctl, P, home);
+    while (true) {
+      RingEntry& re = ctl.ring[e % kRing];
+      if (R.t >= P.Q || vc.abort) break;
+      td = prof.now();
+      DataRegion Rn;
+      if (R.identity) {
+        if (gt == 0) {
+          ++n_ident;
+          atomicExch(&re.published, 1);
+          // the slot items still close the region's slots; wait for them so the
+          // ring entry is not reused under a worker
+          while (vc.ring[e % kRing].items_done < re.nslot && !vc.abort) {
+          }
+          __threadfence_block();
+          vc.d_done = e + 1;
+        }
+        open_and_describe(e + 1, Rn);
+        if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
+          gather_issue(Rn);
+          pending = true;
+        }
+        R = Rn;
+        ++e;
+        continue;
+      }
+      // ---- land entry e ----
+      while (!mbar_try_wait(&ctl.bar, phase)) {
+      }
+      phase ^= 1;
+      pending = false;
+      PM_TICK(1);
+      // publish the reads (one piece per thread; np <= GT): the atomics stay in
+      // flight during the merge, deaths are handled after it
+      int64_t pj = -1;
+      int32_t pn = 0, pold = 0;
+      if (gt < R.np) {
+        const bool isA = gt < R.npa;
+        pj = isA ? R.ua0 + gt : R.ub0 + (gt - R.npa);
+        const int64_t run0 = isA ? R.xa : R.xb, run1 = isA ? R.xa + R.alpha : R.xb + R.beta;
+        pn = (int32_t)(min(run1, g.slot_hi(pj)) - max(run0, g.slot_lo(pj)));
+        __threadfence();
+        pold = atomicAdd(&P.reads[pj], pn);
+      }
+      if (gt == 0) bulk_wait_read_all();  // the previous tile's TMA store has read the output tile
+      named_barrier_sync(1, GT);
+      if (gt == 0) atomicExch(&re.published, 1);
+      PM_TICK(2);
+      // merge path (A wins ties): every thread merges an odd-length run of outputs
+      // (odd stride -> conflict-free smem) straight into the phase-aligned output tile
+      const KT* As = reinterpret_cast<const KT*>(kin + R.offA);
+      const KT* Bs = reinterpret_cast<const KT*>(kin + R.offB);
+      const int64_t phk = ((uintptr_t)(P.keys + (P.s + R.d0) * ks)) & 15;
+      KT* ko = reinterpret_cast<KT*>(kout_s + phk);
+      const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + R.d0) * w)) & 15) : 0;
+      uint8_t* po = pout_s + php;
+      const uint8_t* PA = pin + R.poffA;
+      const uint8_t* PB = pin + R.poffB;
+      const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
+      merge_tile<KT>(P.mode, As, Bs, R.alpha, R.beta, R.nout, ko, po, PA, PB, w, wq4, gt, GT);
+      fence_proxy_async_smem();  // our smem writes -> visible to the TMA (async proxy)
+      PM_TICK(3);
+      // ---- the input tile is free: start the next entry's gather now ----
+      open_and_describe(e + 1, Rn);  // (its barrier also ends every thread's merge)
+      PM_TICK(1);
+      if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
+        gather_issue(Rn);
+        pending = true;
+      }
+      PM_TICK(0);
+      if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
+        // last reader: free the unit's location into the CTA cache
+        const int32_t l = ld_acquire(&P.loc[pj]);
+        if (l < 0) {
+          cache_push(ctl, P, l, home);
+        } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)pj, ST_FREE) == (int32_t)pj) {
+          cache_push(ctl, P, l, home);
+        }
+      }
+      open_ahead(e + 2);
+      // ---- every slot of the region must be cleared before the tile lands there:
+      //      all slot items are done, and every consumer of order <= t has read
+      //      each occupant (t's own reads are published by now) ----
+      if (gt == 0)
+        while (vc.ring[e % kRing].items_done < re.nslot && !vc.abort) {
+        }
+      named_barrier_sync(1, GT);
+      if (gt < re.nslot) {
+        const int32_t u = re.occ[gt];
+        if (u >= 0) {
+          int64_t cwl, cwr;
+          g.window(R.t, cwl, cwr);
+          const int64_t before = g.consumed_in(u, cwl, cwr, re.ti.clo, re.ti.chi);
+          for (uint32_t it = 0; ld_acquire(&P.reads[u]) < before; ++it) {
+            if ((it & 255) == 255 && ld_relaxed(P.err)) {
+              ctl.abort = 1;
+              break;
+            }
+            if (it > kSpinLimit) {
+              raise_error(P.err, PM_ERR_TIMEOUT);
+              ctl.abort = 1;
+              break;
+            }
+            backoff(it);
+          }
+        }
+      }
+      named_barrier_sync(1, GT);
+      PM_TICK(4);
+      if (!vc.abort) {
+        // stream the tile back in place: TMA bulk store for the 16-byte-aligned body,
+        // generic stores for the unaligned head and tail bytes
+        stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), R.nout * ks, gt, GT);
+        if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, R.nout * w, gt, GT);
+      }
+      if (gt == 0) {
+        ++n_reg;
+        __threadfence_block();
+        vc.d_done = e + 1;  // the ring entry may be reused
+      }
+      PM_TICK(5);
+      R = Rn;
+      ++e;
     }
-    it_par ^= 1;
-    ++iter;
-    __syncthreads();
+    if (gt == 0) {
+      // an aborted job may leave a gather in flight: let it land before the CTA exits
+      if (pending)
+        for (uint32_t it = 0; !mbar_try_wait(&ctl.bar, phase) && it < (1u << 20); ++it) {
+        }
+      bulk_wait_all();  // the last output tile has landed
+    }
+#undef PM_TICK
   }
-  if (tid == kTeam * 32) bulk_wait_all();  // the last output tile has landed
+  __syncthreads();
   // leave nothing behind in the CTA cache (another job reuses the lists)
   if (tid == 0) cache_flush(ctl, P, home);
   if (lane == 0 && n_salv) {
@@ -1205,7 +1307,7 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
         for (int64_t c = c_lo + lane; c <= c_hi; c += 32) {
           if (c == R.r) continue;
           for (uint32_t it = 0; ld_acquire(&flags[c]) == 0; ++it) {
-            if (ld_relaxed(P.err)) break;
+            if ((it & 255) == 255 && ld_relaxed(P.err)) break;
             if (it > kSpinLimit) {
               raise_error(P.err, PM_ERR_TIMEOUT);
               break;

@@ -41,6 +41,15 @@ constexpr int kEngineThreads = 64 * PM_ENGINE_TEAM;
 constexpr int kEngineMinBlocks = PM_ENGINE_MINB;
 constexpr int64_t kTileBudget = PM_TILE_BUDGET;
 constexpr int kBufferedThreads = 256;
+// free-list shards: each tagged top word on its own 256-byte line (its own L2
+// slice), so CAS traffic on one shard does not queue behind another's
+constexpr int kShards = 64;
+constexpr int kTopStride = 32;  // unsigned long long words between shard tops
+// tickets a k_engine CTA holds at once (its salvage workers run ahead of its data team)
+#ifndef PM_RING
+#define PM_RING 2
+#endif
+constexpr int kRing = PM_RING;
 
 // Two-front ticket order around the centre region qc (regions 0..Q-1): ticket 0
 // is qc, then qc-1, qc+1, qc-2, qc+2, ... until one side runs out, then the

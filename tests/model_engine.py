@@ -1,17 +1,20 @@
 """Executable model of the k_engine protocol (pm_engine.cu), for CPU tests.
 
-Each in-flight region is a Python generator that yields at every point where
-the device code spins (reader wait, landing wait, threshold wait, space wait)
-and at the points where device threads of other CTAs may interleave.  A
-scheduler runs W regions at a time and steps a random runnable one, so the
-tests explore many interleavings of exactly the rules the kernel implements:
+Each in-flight ticket is a set of Python generators -- one salvage item per
+slot of its region and one data phase -- that yield at every point where the
+device code spins (reader wait, landing wait, space wait, item wait, consumer
+wait) and where threads of other CTAs may interleave.  A scheduler keeps W
+tickets in flight and steps a random runnable generator, so the tests explore
+many interleavings of exactly the rules the kernel implements:
 
   * two-front ticket order (TwoFront in pm_engine.cuh),
-  * gather: wait until the unit's location is a region of order >= t (or scratch),
-  * publish reads; the last consumer frees the unit's slot / scratch unit,
-  * occupants: wait for landing, wait for reads by consumers of order <= t,
-    then (if still alive) take scratch first, else a free slot, copy, publish,
-  * merge (stable, A wins ties) and write the region's slots.
+  * salvage item: close the slot, wait for its occupant to land, and if a region
+    of higher order still needs it, move it (scratch first, else a free slot;
+    no space -> wait for the ticket's reads to be published, then block),
+  * data: gather (wait until each unit sits in a region of order >= t or in
+    scratch), publish reads (the last consumer frees the unit's location), merge
+    (stable, A wins ties), wait for every slot item and for every consumer of
+    order <= t to have read each occupant, then write the region's slots.
 
 The data really moves (numpy), so the final array is checked bit for bit.
 """
@@ -155,106 +158,132 @@ class EngineModel:
             self.state[l] = FREE
             self.free_slots.append(l)
 
-    # ---- one region, as a generator of wait points ----
-    def region(self, t):
+    # ---- one ticket: slot items + the data phase, as generators of wait points ----
+    def ticket(self, t):
+        """Return the generators of ticket t (k_engine in pm_engine.cu): one salvage
+        item per slot of its region, and the data phase."""
         q = self.tf.region_of_ticket(t)
         j0 = max(0, (self.R0 + q) * self.mu - self.k0)
         j1 = min(self.K, (self.R0 + q + 1) * self.mu - self.k0)
-        occ = []
-        for j in range(j0, j1):
-            occ.append(self.state[j])
-            self.state[j] = CLOSED
         d0, d1 = self.diag(q), self.diag(q + 1)
         a0, a1 = self.split[q], self.split[q + 1]
-        b0, b1 = d0 - a0, d1 - a1
         la = self.m - self.s
-        if self.mode == "merge" and ((a0 == d0 and a1 == d1) or (a0 == la and a1 == la)):
-            return
-        yield
-        xa, xb = self.s + a0, self.m + b0
-        pieces = []
-        for run0, run1 in ((xa, self.s + a1), (xb, self.m + b1)):
-            if run1 > run0:
-                for j in range(run0 // self.T - self.k0, (run1 - 1) // self.T - self.k0 + 1):
-                    pieces.append((j, max(run0, self.slot_lo(j)), min(run1, self.slot_hi(j)), run0 == xa))
-        got = {}
-        for j, x0, x1, isA in pieces:  # gather
-            while True:
-                l = self.loc[j]
-                if l < 0 or self.tf.order(self.region_of_slot(l)) >= t:
-                    break
-                yield "wait"
-            got[(j, isA)] = self.read_unit(j, x0, x1)
-            yield
-        for j, x0, x1, isA in pieces:  # publish reads
-            self.reads[j] += x1 - x0
-            if self.reads[j] == self.slot_hi(j) - self.slot_lo(j):
-                self.free_location(j)
-        yield
-        for i, u in enumerate(occ):  # occupants
-            if u < 0:
-                continue
+        identity = self.mode == "merge" and ((a0 == d0 and a1 == d1) or (a0 == la and a1 == la))
+        st = {"items_done": 0, "published": False, "occ": [-1] * (j1 - j0)}
+
+        def item(i):
             slot = j0 + i
-            while self.loc[u] != slot:
-                yield "wait"
-            thr = self.consumed_by_window(u, t)
-            while self.reads[u] < thr:
-                yield "wait"
-            if self.reads[u] >= self.slot_hi(u) - self.slot_lo(u):
-                continue
-            spins = 0
-            while True:
-                if self.free_scr:
-                    dest = -self.free_scr.pop() - 1
-                    break
-                f = None
-                while self.free_slots:
-                    f = self.free_slots.pop()
-                    if self.state[f] == FREE:
-                        self.state[f] = u
-                        break
-                    f = None
-                if f is not None:
-                    dest = f
-                    break
-                spins += 1
-                if spins > 10000:
-                    raise NoSpace(f"ticket {t} found no salvage space")
-                yield "wait"
-            x0, x1, hb = self.slot_lo(u), self.slot_hi(u), self.slot_base(u)
-            sb = self.slot_base(slot) + (x0 - hb)
-            k, p = self.keys[sb:sb + x1 - x0].copy(), self.pay[sb:sb + x1 - x0].copy()
+            u = self.state[slot]  # close the slot (atomicExch) and sample its occupant
+            self.state[slot] = CLOSED
             yield
-            if dest >= 0:
-                db = self.slot_base(dest) + (x0 - hb)
-                self.keys[db:db + x1 - x0], self.pay[db:db + x1 - x0] = k, p
+            if u >= 0 and not identity:
+                st["occ"][i] = u
+                while self.loc[u] != slot:  # landing: the mover has published
+                    yield "wait"
+                if self.consumed_by_window(u, t) < self.slot_hi(u) - self.slot_lo(u):
+                    # a later region still needs u: move it now (no wait for earlier
+                    # consumers -- they read either copy; the data phase waits for them)
+                    dest = self.take_space(u, block=False)
+                    if dest is None:
+                        while not st["published"]:  # the region's own reads free space first
+                            yield "wait"
+                        spins = 0
+                        while (dest := self.take_space(u, block=True)) is None:
+                            spins += 1
+                            if spins > 10000:
+                                raise NoSpace(f"ticket {t} found no salvage space")
+                            yield "wait"
+                    x0, x1, hb = self.slot_lo(u), self.slot_hi(u), self.slot_base(u)
+                    sb = self.slot_base(slot) + (x0 - hb)
+                    k, p = self.keys[sb:sb + x1 - x0].copy(), self.pay[sb:sb + x1 - x0].copy()
+                    yield
+                    if dest >= 0:
+                        db = self.slot_base(dest) + (x0 - hb)
+                        self.keys[db:db + x1 - x0], self.pay[db:db + x1 - x0] = k, p
+                    else:
+                        self.scr_k[-dest - 1, x0 - hb:x1 - hb], self.scr_p[-dest - 1, x0 - hb:x1 - hb] = k, p
+                    yield
+                    self.loc[u] = dest  # publish (after the copy is visible)
+                    self.salvaged += 1
+            st["items_done"] += 1
+
+        def data():
+            if identity:
+                st["published"] = True
+                while st["items_done"] < j1 - j0:
+                    yield "wait"
+                return
+            yield
+            xa, xb = self.s + a0, self.m + (d0 - a0)
+            b1 = d1 - a1
+            pieces = []
+            for run0, run1 in ((xa, self.s + a1), (xb, self.m + b1)):
+                if run1 > run0:
+                    for j in range(run0 // self.T - self.k0, (run1 - 1) // self.T - self.k0 + 1):
+                        pieces.append((j, max(run0, self.slot_lo(j)), min(run1, self.slot_hi(j)), run0 == xa))
+            got = {}
+            for j, x0, x1, isA in pieces:  # gather
+                while True:
+                    l = self.loc[j]
+                    if l < 0 or self.tf.order(self.region_of_slot(l)) >= t:
+                        break
+                    yield "wait"
+                got[(j, isA)] = self.read_unit(j, x0, x1)
+                yield
+            last = []
+            for j, x0, x1, isA in pieces:  # publish reads
+                self.reads[j] += x1 - x0
+                if self.reads[j] == self.slot_hi(j) - self.slot_lo(j):
+                    last.append(j)
+            st["published"] = True
+            yield
+            ka = np.concatenate([got[(j, True)][0] for j, _, _, isA in pieces if isA] or [self.keys[:0]])
+            pa = np.concatenate([got[(j, True)][1] for j, _, _, isA in pieces if isA] or [self.pay[:0]])
+            kb = np.concatenate([got[(j, False)][0] for j, _, _, isA in pieces if not isA] or [self.keys[:0]])
+            pb = np.concatenate([got[(j, False)][1] for j, _, _, isA in pieces if not isA] or [self.pay[:0]])
+            if self.mode == "merge":
+                tag = np.concatenate([np.zeros(len(ka), np.int8), np.ones(len(kb), np.int8)])
+                order = np.lexsort((tag, np.concatenate([ka, kb])))  # stable: key, then A before B
             else:
-                self.scr_k[-dest - 1, x0 - hb:x1 - hb], self.scr_p[-dest - 1, x0 - hb:x1 - hb] = k, p
-            self.loc[u] = dest
-            self.salvaged += 1
-        yield
-        ka = np.concatenate([got[(j, True)][0] for j, _, _, isA in pieces if isA] or [self.keys[:0]])
-        pa = np.concatenate([got[(j, True)][1] for j, _, _, isA in pieces if isA] or [self.pay[:0]])
-        kb = np.concatenate([got[(j, False)][0] for j, _, _, isA in pieces if not isA] or [self.keys[:0]])
-        pb = np.concatenate([got[(j, False)][1] for j, _, _, isA in pieces if not isA] or [self.pay[:0]])
-        if self.mode == "merge":
-            tag = np.concatenate([np.zeros(len(ka), np.int8), np.ones(len(kb), np.int8)])
-            order = np.lexsort((tag, np.concatenate([ka, kb])))  # stable: key, then A before B
-        else:
-            order = np.concatenate([np.arange(len(ka), len(ka) + len(kb)), np.arange(len(ka))])
-        kk = np.concatenate([ka, kb])[order]
-        pp = np.concatenate([pa, pb])[order]
-        o0 = self.s + d0
-        self.keys[o0:o0 + len(kk)] = kk
-        self.pay[o0:o0 + len(kk)] = pp
+                order = np.concatenate([np.arange(len(ka), len(ka) + len(kb)), np.arange(len(ka))])
+            kk = np.concatenate([ka, kb])[order]
+            pp = np.concatenate([pa, pb])[order]
+            yield
+            for j in last:  # last reader frees the unit's location
+                self.free_location(j)
+            yield
+            while st["items_done"] < j1 - j0:  # every slot item is done
+                yield "wait"
+            for u in st["occ"]:  # every consumer of order <= t has read each occupant
+                if u >= 0:
+                    while self.reads[u] < self.consumed_by_window(u, t):
+                        yield "wait"
+            o0 = self.s + d0
+            self.keys[o0:o0 + len(kk)] = kk
+            self.pay[o0:o0 + len(kk)] = pp
+
+        return [item(i) for i in range(j1 - j0)] + [data()]
+
+    def take_space(self, u, block):
+        """Scratch first, then a free slot (acquire_dest); None if there is none."""
+        if self.free_scr:
+            return -self.free_scr.pop() - 1
+        while self.free_slots:
+            f = self.free_slots.pop()
+            if self.state[f] == FREE:
+                self.state[f] = u
+                return f
+        return None
 
     def run(self, inflight, rng: random.Random):
-        """Run all tickets with `inflight` concurrent regions under a random scheduler."""
-        nxt, active = 0, []
+        """Run all tickets with at most `inflight` unfinished tickets under a random scheduler."""
+        nxt, active, tickets = 0, [], []
         waits = 0
         while nxt < self.Q or active:
-            while len(active) < inflight and nxt < self.Q:
-                active.append(self.region(nxt))
+            while len(tickets) < inflight and nxt < self.Q:
+                gens = self.ticket(nxt)
+                tickets.append(gens[-1])  # a ticket is finished when its data phase is
+                active.extend(gens)
                 nxt += 1
             gen = rng.choice(active)
             try:
@@ -265,4 +294,6 @@ class EngineModel:
                         raise RuntimeError("model livelock")
             except StopIteration:
                 active.remove(gen)
+                if gen in tickets:
+                    tickets.remove(gen)
         return self
