@@ -65,6 +65,19 @@ int pm_merge(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t widt
              int64_t start, int64_t middle, int64_t end, int64_t scratch_records, void *stream);
 
 /*
+ * Out-of-place stable merge: src holds the sorted runs A = src[0, len_a) and
+ * B = src[len_a, len_a+len_b); the merged records (A wins ties, as pm_merge)
+ * go to dst[0, len_a+len_b).  src and dst must not overlap.  The partition
+ * exchange of the reference's parallel merge lands a GPU's two runs in a
+ * receive buffer (srecpar.py:63-84 across ranks, paper_2005_12648_b200/dist.py);
+ * this merges them straight into the rank's block, one read and one write per
+ * record.
+ */
+int pm_merge_copy(pm_ctx *ctx, const void *src_keys, const void *src_payload, void *dst_keys,
+                  void *dst_payload, int key_bytes, int64_t width, int64_t len_a, int64_t len_b,
+                  void *stream);
+
+/*
  * In-place block exchange A|B -> B|A of [lo, lo+len_a) and [lo+len_a,
  * lo+len_a+len_b).  Replaces _kernels.linear_shift (_kernels.py:92-150) and
  * _kernels.circular_shift (_kernels.py:154-197) behind shift_region /

@@ -61,6 +61,32 @@ def merge(arr: KeyedArray, start: int, middle: int, end: int, scratch_records: i
     return None
 
 
+def merge_copy(src_keys: torch.Tensor, src_payload: torch.Tensor, dst_keys: torch.Tensor, dst_payload: torch.Tensor,
+               len_a: int):
+    """Out-of-place stable merge (pm_merge_copy): src = A|B with |A| = len_a -> dst.
+
+    Device tensors: keys int32/int64 [n], payload uint8 [n, w] (w may be 0).
+    """
+    for t in (src_keys, src_payload, dst_keys, dst_payload):
+        if not t.is_cuda:
+            raise _capi.MergeEngineError("merge_copy needs CUDA tensors (no CPU fallback)")
+    n = src_keys.numel()
+    if dst_keys.numel() != n or src_keys.dtype != dst_keys.dtype or src_payload.shape != dst_payload.shape:
+        raise ValueError("source and destination must have the same shape and dtype")
+    if not 0 <= len_a <= n:
+        raise ValueError("need 0 <= len_a <= len(src)")
+    if n == 0:
+        return None
+    dev = src_keys.device.index
+    w = src_payload.shape[1] if src_payload.dim() == 2 else 0
+    rc = _capi.lib().pm_merge_copy(_capi.context(dev), _ptr(src_keys), _ptr(src_payload), _ptr(dst_keys),
+                                   _ptr(dst_payload), src_keys.element_size(), w, len_a, n - len_a, _stream(dev))
+    _capi.check(rc, "pm_merge_copy")
+    if _check_each_call:
+        return _capi.status(dev, torch.cuda.current_stream(dev).cuda_stream)
+    return None
+
+
 def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
     """In-place block exchange A|B -> B|A on the device (pm_shift)."""
     require_cuda(arr)

@@ -100,14 +100,18 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
   return true;
 }
 
+// out_keys / out_payload non-null: copy mode -- merge keys[s,m) and keys[m,e) into
+// out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                      int mode, int64_t scratch_records, cudaStream_t st) {
-  if (e - s <= 0 || m == s || m == e) return PM_OK;
+                      int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
+                      void* out_payload = nullptr) {
+  const bool copy = out_keys != nullptr;
+  if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
   int32_t mu;
   // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
   // half-size regions, two staging + two output tiles (72 KB of shared memory)
-  const bool buffered = mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m);
+  const bool buffered = copy || (mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
   if (!pick_tiles(ks, w, buffered ? 72 * 1024 : kTileBudget, &M, &T, &mu))
     return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
   if (buffered && M >= 32) {
@@ -118,6 +122,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   EngineParams P{};
   P.keys = static_cast<char*>(keys);
   P.pay = static_cast<uint8_t*>(payload);
+  P.out_keys = static_cast<char*>(out_keys);
+  P.out_pay = static_cast<uint8_t*>(out_payload);
   P.w = w;
   P.ks = ks;
   P.mode = mode;
@@ -196,7 +202,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // buffered mode: the caller granted a min(|A|,|B|) buffer (seq_merge_buffered)
   const int64_t la = m - s, lb = e - m, mn = std::min(la, lb);
   const int32_t buf_a = la <= lb ? 1 : 0;
-  if (buffered) {
+  if (buffered && !copy) {
     const size_t bk = (size_t)align_up(mn * ks + 64, 256), bp = (size_t)(w ? mn * w + 64 : 0);
     rc = ensure(&ctx->buf, &ctx->buf_bytes, bk + bp);
     if (rc) return rc;
@@ -212,7 +218,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[1], st));
-  if (buffered) {
+  if (copy) {
+    ce = ks == 4 ? launch_merge_copy<int32_t>(P, grid, smem, st) : launch_merge_copy<int64_t>(P, grid, smem, st);
+  } else if (buffered) {
     ce = ks == 4 ? launch_buffered<int32_t>(P, buf_a, grid, smem, st) : launch_buffered<int64_t>(P, buf_a, grid, smem, st);
   } else {
     ce = ks == 4 ? launch_engine<int32_t>(P, grid, kEngineThreads, smem, st)
@@ -320,6 +328,26 @@ int pm_kernel_ms(pm_ctx* ctx, float* plan_ms, float* engine_ms) {
   PM_CUDA(cudaEventElapsedTime(plan_ms, ctx->ev[0], ctx->ev[1]));
   PM_CUDA(cudaEventElapsedTime(engine_ms, ctx->ev[1], ctx->ev[2]));
   return PM_OK;
+}
+
+int pm_merge_copy(pm_ctx* ctx, const void* src_keys, const void* src_payload, void* dst_keys, void* dst_payload,
+                  int key_bytes, int64_t width, int64_t len_a, int64_t len_b, void* stream) {
+  int rc = check_common(ctx, src_keys, key_bytes, src_payload, width);
+  if (rc) return rc;
+  rc = check_common(ctx, dst_keys, key_bytes, dst_payload, width);
+  if (rc) return rc;
+  if (len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "negative run length");
+  const int64_t n = len_a + len_b;
+  auto overlap = [n](const void* a, const void* b, int64_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + (uintptr_t)(n * bytes) && y < x + (uintptr_t)(n * bytes);
+  };
+  if (n && (overlap(src_keys, dst_keys, key_bytes) || (width && overlap(src_payload, dst_payload, width))))
+    return fail(PM_ERR_ARG, "source and destination overlap (use pm_merge for in-place)");
+  if (n == 0) return PM_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return run_engine(ctx, const_cast<void*>(src_keys), key_bytes, const_cast<void*>(src_payload), width, 0, len_a, n,
+                    MODE_MERGE, 0, static_cast<cudaStream_t>(stream), dst_keys, width ? dst_payload : nullptr);
 }
 
 int pm_merge(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t start, int64_t middle,

@@ -149,6 +149,7 @@ __global__ void k_plan(EngineParams P) {
     *P.ticket = 0;
     bool nothing = (la == 0 || lb == 0);
     if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
+    if (P.out_keys) nothing = false;  // out of place: every record still moves
     *P.noop = nothing ? 1 : 0;
     *P.need_space = 0;
     for (int i = 0; i < 64; ++i) P.stats[i] = 0;
@@ -1187,7 +1188,7 @@ __device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams
   R.alpha = R.a1 - R.a0;
   R.beta = R.b1 - R.b0;
   R.nout = R.d1 - R.d0;
-  R.identity = (R.a0 == R.d0 && R.a1 == R.d1) || (R.a0 == la && R.a1 == la);
+  R.identity = !P.out_keys && ((R.a0 == R.d0 && R.a1 == R.d1) || (R.a0 == la && R.a1 == la));
   const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
   R.offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
   R.offB = ((R.offA + R.alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
@@ -1206,13 +1207,15 @@ __device__ __forceinline__ void buf_issue(const EngineParams& P, const BufRegion
                                           uint8_t* pin, uint64_t* bar) {
   const int64_t ks = sizeof(KT), w = P.w;
   const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
-  const char* ka = buf_a ? P.scr_keys + R.a0 * ks : P.keys + xa * ks;
-  const char* kb = buf_a ? P.keys + xb * ks : P.scr_keys + R.b0 * ks;
+  // (copy mode: both runs come from the source array)
+  const bool oop = P.out_keys != nullptr;
+  const char* ka = buf_a && !oop ? P.scr_keys + R.a0 * ks : P.keys + xa * ks;
+  const char* kb = buf_a || oop ? P.keys + xb * ks : P.scr_keys + R.b0 * ks;
   copy_g2s_superset(kin + R.offA, reinterpret_cast<const uint8_t*>(ka), R.alpha * ks, bar);
   copy_g2s_superset(kin + R.offB, reinterpret_cast<const uint8_t*>(kb), R.beta * ks, bar);
   if (w) {
-    const uint8_t* pa = buf_a ? P.scr_pay + R.a0 * w : P.pay + xa * w;
-    const uint8_t* pb = buf_a ? P.pay + xb * w : P.scr_pay + R.b0 * w;
+    const uint8_t* pa = buf_a && !oop ? P.scr_pay + R.a0 * w : P.pay + xa * w;
+    const uint8_t* pb = buf_a || oop ? P.pay + xb * w : P.scr_pay + R.b0 * w;
     copy_g2s_superset(pin + R.poffA, pa, R.alpha * w, bar);
     copy_g2s_superset(pin + R.poffB, pb, R.beta * w, bar);
   }
@@ -1246,6 +1249,9 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
 #define STAGE(b) (dyn + (size_t)(b) * tile)
 #define OUTB(b) (dyn + (size_t)(2 + (b)) * tile)
   int32_t* flags = P.reads;  // flags[r] = 1 once region r has read its inputs
+  const bool oop = P.out_keys != nullptr;  // copy mode: no overlap, no flags
+  char* const okeys = oop ? P.out_keys : P.keys;
+  uint8_t* const opay = oop ? P.out_pay : P.pay;
   if (leader) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -1292,11 +1298,13 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
       }
       ph[cur] ^= 1;
       PB_TICK(1);
-      const int64_t phk = ((uintptr_t)(P.keys + (P.s + R.d0) * ks)) & 15;
-      const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + R.d0) * w)) & 15) : 0;
+      const int64_t phk = ((uintptr_t)(okeys + (P.s + R.d0) * ks)) & 15;
+      const int64_t php = w ? (((uintptr_t)(opay + (P.s + R.d0) * w)) & 15) : 0;
       uint8_t* kout_s = OUTB(cur);
       uint8_t* pout_s = OUTB(cur) + P.smem_keys;
-      if (ctrl) {
+      if (ctrl && oop) {
+        // copy mode: nothing to announce or wait for
+      } else if (ctrl) {
         if (leader && !s_early[cur]) {
           __threadfence();
           st_release(&flags[R.r], 1);
@@ -1341,8 +1349,8 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
       PB_TICK(3);
       // the leader (gt == 0) issues the bulk stores; everyone writes unaligned edges
       const int gt = (tid + 32) % NT;
-      stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), R.nout * ks, gt, NT);
-      if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, R.nout * w, gt, NT);
+      stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(okeys + (P.s + R.d0) * ks), R.nout * ks, gt, NT);
+      if (w) stream_out(pout_s + php, opay + (P.s + R.d0) * w, R.nout * w, gt, NT);
       ++n_reg;
     }
     cur ^= 1;
@@ -1394,6 +1402,15 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
   k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, buf_a);
   return cudaGetLastError();
 }
+template <typename KT>
+cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, 1);
+  return cudaGetLastError();
+}
+template cudaError_t launch_merge_copy<int32_t>(const EngineParams&, int, size_t, cudaStream_t);
+template cudaError_t launch_merge_copy<int64_t>(const EngineParams&, int, size_t, cudaStream_t);
 template cudaError_t launch_buffered<int32_t>(const EngineParams&, int32_t, int, size_t, cudaStream_t);
 template cudaError_t launch_buffered<int64_t>(const EngineParams&, int32_t, int, size_t, cudaStream_t);
 template cudaError_t launch_plan<int32_t>(const EngineParams&, int, cudaStream_t);

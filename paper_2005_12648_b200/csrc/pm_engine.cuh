@@ -131,6 +131,8 @@ struct EngineParams {
   unsigned long long* stats;  // [4]: salvaged units, salvaged records, regions, identity regions
   size_t smem_keys;    // bytes reserved for staged keys
   size_t smem_pay;     // bytes reserved for staged payload
+  char* out_keys;      // out-of-place merge (k_buffered copy mode): destination, else null
+  uint8_t* out_pay;
 };
 
 }  // namespace pm

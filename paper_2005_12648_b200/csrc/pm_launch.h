@@ -11,6 +11,7 @@ template <typename KT> cudaError_t launch_plan(const EngineParams& P, int grid, 
 template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);
 template <typename KT> cudaError_t buffered_occupancy(size_t smem, int* blocks_per_sm);
+template <typename KT> cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cudaStream_t st);
 template <typename KT>
 cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st);
 template <typename KT>

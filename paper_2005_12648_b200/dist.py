@@ -15,7 +15,8 @@ with the GPUs as the partitions:
    every rank's A part and B part are already ordered by destination, so two
    ``all_to_all_single`` calls (NCCL send/recv over NVLink) deliver rank r's
    A slice followed by its B slice, contiguously.
-3. **Local merge**: the in-place device engine (``pm_merge``) merges the pair.
+3. **Local merge**: the received pair is merged out of place straight into the
+   rank's block (``pm_merge_copy``: one read and one write per record).
 
 The exchange uses a receive buffer of n_r records per rank (DESIGN.md notes
 the chunked, O(chunk) variant as next work).  ``local_merge`` is injectable so
@@ -81,13 +82,12 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
     return [int(x) for x in lo.tolist()]
 
 
-def _default_local_merge(keys: torch.Tensor, payload: torch.Tensor, len_a: int) -> None:
+def _default_local_merge(src_k: torch.Tensor, src_p: torch.Tensor, len_a: int, dst_k: torch.Tensor,
+                         dst_p: torch.Tensor) -> None:
+    """The received A|B pair merged straight into the rank's block (pm_merge_copy)."""
     from . import _ops
-    from .records import KeyedArray
 
-    arr = KeyedArray.__new__(KeyedArray)
-    arr.keys, arr.payload = keys, payload
-    _ops.merge(arr, 0, len_a, keys.numel())
+    _ops.merge_copy(src_k, src_p, dst_k, dst_p, len_a)
 
 
 def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | None, global_len_a: int,
@@ -137,7 +137,10 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
     if payload_local.shape[1]:
         dist.all_to_all_single(out_p[:na], payload_local[:split_at].contiguous(), recv_a, send_a, group=group)
         dist.all_to_all_single(out_p[na:], payload_local[split_at:].contiguous(), recv_b, send_b, group=group)
-    (local_merge or _default_local_merge)(out_k, out_p, na)
-    keys_local.copy_(out_k)
-    payload_local.copy_(out_p)
+    if local_merge is None:
+        _default_local_merge(out_k, out_p, na, keys_local, payload_local)
+    else:  # (host-logic tests: any in-place merge of the received pair)
+        local_merge(out_k, out_p, na)
+        keys_local.copy_(out_k)
+        payload_local.copy_(out_p)
     return keys_local, payload_local

@@ -243,3 +243,70 @@ def test_scratch_sizes_vs_oracle(width):
                 arr = to_gpu(keys, payload)
                 _ops.merge(arr, 0, middle, size, scratch_records=scratch)
                 assert_same(arr, want_k, want_p, f"size={size} split={split} scratch={scratch}")
+
+
+@pytest.mark.parametrize("width", [0, 4, 8, 3])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_merge_copy_vs_oracle(width, dtype):
+    """pm_merge_copy: out-of-place stable merge == the reference's stable merge."""
+    import torch
+
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(5150 + width)
+    for size in (1, 2, 100, 8191, 70000, 1 << 20):
+        for split in (0.0, 0.3, 0.5, 1.0):
+            for domain in (5, 2**31 - 1):
+                keys, payload, middle = random_instance(rng, size, split, domain, width)
+                keys = keys.astype(dtype)
+                want_k, want_p = keys.copy(), payload.copy()
+                orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+                sk = torch.from_numpy(keys).cuda()
+                sp = torch.from_numpy(payload).cuda()
+                dk = torch.full_like(sk, -1)
+                dp = torch.zeros_like(sp)
+                _ops.merge_copy(sk, sp, dk, dp, middle)
+                pm.synchronize()
+                assert np.array_equal(dk.cpu().numpy(), want_k), f"keys size={size} split={split}"
+                assert np.array_equal(dp.cpu().numpy(), want_p), f"payload size={size} split={split}"
+                assert np.array_equal(sk.cpu().numpy(), keys)  # the source is untouched
+
+
+def test_merge_copy_errors():
+    import torch
+
+    from paper_2005_12648_b200 import _ops
+
+    k = torch.arange(10, dtype=torch.int32, device="cuda")
+    p = torch.zeros((10, 0), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        _ops.merge_copy(k, p, k, p, 5)  # overlap
+    with pytest.raises(ValueError):
+        _ops.merge_copy(k, p, torch.empty(9, dtype=torch.int32, device="cuda"), p[:9], 5)
+    with pytest.raises(ValueError):
+        _ops.merge_copy(k, p, torch.empty_like(k), p.clone(), 11)
+
+
+def test_distributed_merge_single_rank_nccl():
+    """merge_distributed over a 1-rank NCCL group: splits, exchange and the copy merge."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_12648_b200.dist import merge_distributed
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29631")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(77)
+        keys, payload, middle = random_instance(rng, 300000, 0.4, 1000, 4)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, len(keys))
+        k = torch.from_numpy(keys).cuda()
+        p = torch.from_numpy(payload).cuda()
+        rk, rp = merge_distributed(k, p, middle)
+        assert np.array_equal(rk.cpu().numpy(), want_k) and np.array_equal(rp.cpu().numpy(), want_p)
+    finally:
+        dist.destroy_process_group()
