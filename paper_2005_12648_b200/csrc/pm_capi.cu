@@ -112,13 +112,10 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
   // half-size regions, two staging + two output tiles (72 KB of shared memory)
   const bool buffered = copy || (mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
-  if (!pick_tiles(ks, w, buffered ? 72 * 1024 : kTileBudget, &M, &T, &mu))
+  // (the engine stages one input and one output tile; the buffered pipeline
+  //  kBufStages inputs and two outputs)
+  if (!pick_tiles(ks, w, buffered ? kBufBudget * 2 / (kBufStages + 2) : kTileBudget, &M, &T, &mu))
     return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
-  if (buffered && M >= 32) {
-    M /= 2;
-    T = std::max<int64_t>(16, M / 4);
-    mu = (int32_t)(M / T);
-  }
   EngineParams P{};
   P.keys = static_cast<char*>(keys);
   P.pay = static_cast<uint8_t*>(payload);
@@ -146,7 +143,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
   // staged inputs (keys, payload) + merged output tile (keys, payload), same sizes;
   // the buffered pipeline double-buffers both
-  const size_t smem = (buffered ? 4 : 2) * (P.smem_keys + P.smem_pay);
+  const size_t smem = (buffered ? kBufStages + 2 : 2) * (P.smem_keys + P.smem_pay);
   // persistent grid: every resident CTA slot on every SM
   int bps = 0;
   cudaError_t ce;

@@ -1174,15 +1174,18 @@ struct BufRegion {
   bool identity;
 };
 
+// region of ticket t; its boundary splits a0/a1 are passed in when already at hand
+// (a0 < 0: load them)
 template <typename KT>
-__device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams& P, int64_t t, int32_t buf_a) {
+__device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams& P, int64_t t, int32_t buf_a,
+                                                int64_t a0 = -1, int64_t a1 = -1) {
   BufRegion R;
   const int64_t ks = sizeof(KT), w = P.w, la = g.LA();
   R.r = buf_a ? t : P.Q - 1 - t;
   R.d0 = g.diag(R.r);
   R.d1 = g.diag(R.r + 1);
-  R.a0 = g.split(R.r);
-  R.a1 = g.split(R.r + 1);
+  R.a0 = a0 >= 0 ? a0 : g.split(R.r);
+  R.a1 = a0 >= 0 ? a1 : g.split(R.r + 1);
   R.b0 = R.d0 - R.a0;
   R.b1 = R.d1 - R.a1;
   R.alpha = R.a1 - R.a0;
@@ -1222,18 +1225,20 @@ __device__ __forceinline__ void buf_issue(const EngineParams& P, const BufRegion
   mbar_arrive(bar);
 }
 
-// Persistent, software-pipelined: while the CTA merges region t out of staging
-// buffer b, the next region's TMA loads are already landing in buffer b^1; the
-// merged tile leaves through a TMA bulk store from one of two output buffers.
-// The last warp is the control warp (tickets, TMA issue, read flags, consumer
-// checks, bulk stores); the other warps only merge, so no round trip sits on
-// the merge's critical path.
+// Persistent, software-pipelined: while the CTA merges one region out of its
+// staging buffer, the TMA loads of the next kBufStages-1 regions are already in
+// flight in the other staging buffers; the merged tile leaves through a TMA bulk
+// store from one of two output buffers.  The last warp is the control warp
+// (tickets, TMA issue, read flags, consumer checks, bulk stores); the other warps
+// only merge, so no round trip sits on the merge's critical path.
 template <typename KT>
-__global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a) {
+__global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, int32_t buf_a) {
+  constexpr int NS = kBufStages;
   extern __shared__ __align__(128) uint8_t dyn[];
-  __shared__ uint64_t bar[2];
-  __shared__ int64_t s_t[2];
-  __shared__ int32_t s_early[2];  // the region's read flag was already raised
+  __shared__ uint64_t bar[NS];
+  __shared__ int64_t s_t[NS];
+  __shared__ int64_t s_a[NS][2];   // the region's splits (loaded once, by the leader)
+  __shared__ int32_t s_early[NS];  // the region's read flag was already raised
   Geo g(P);
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
   const int NW = NT >> 5;
@@ -1247,26 +1252,34 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
   // tiles are addressed as dyn + offset so the compiler keeps them in the shared
   // space (a local pointer array would turn every access into a generic LD/ST)
 #define STAGE(b) (dyn + (size_t)(b) * tile)
-#define OUTB(b) (dyn + (size_t)(2 + (b)) * tile)
+#define OUTB(b) (dyn + (size_t)(NS + (b)) * tile)
   int32_t* flags = P.reads;  // flags[r] = 1 once region r has read its inputs
   const bool oop = P.out_keys != nullptr;  // copy mode: no overlap, no flags
   char* const okeys = oop ? P.out_keys : P.keys;
   uint8_t* const opay = oop ? P.out_pay : P.pay;
   if (leader) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    s_early[0] = s_early[1] = 0;
-    const int64_t t0 = (*(volatile int32_t*)P.err) ? P.Q : atomicAdd(P.ticket, 1);
-    s_t[0] = t0;
-    t_pref = atomicAdd(P.ticket, 1);  // the ticket after the next one, in flight
-    if (t0 < P.Q) {
-      const BufRegion R = buf_region<KT>(g, P, t0, buf_a);
-      if (!R.identity) buf_issue<KT>(P, R, buf_a, STAGE(0), STAGE(0) + P.smem_keys, &bar[0]);
+    // fill the pipeline: tickets of the first NS-1 iterations, their loads in flight
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&bar[k], 1);
+      s_early[k] = 0;
+      s_t[k] = P.Q;
     }
+    for (int k = 0; k < NS - 1; ++k) {
+      const int64_t t0 = (*(volatile int32_t*)P.err) ? P.Q : atomicAdd(P.ticket, 1);
+      s_t[k] = t0 < P.Q ? t0 : P.Q;
+      if (t0 < P.Q) {
+        const BufRegion R = buf_region<KT>(g, P, t0, buf_a);
+        s_a[k][0] = R.a0;
+        s_a[k][1] = R.a1;
+        if (!R.identity) buf_issue<KT>(P, R, buf_a, STAGE(k), STAGE(k) + P.smem_keys, &bar[k]);
+      } else {
+        break;
+      }
+    }
+    t_pref = atomicAdd(P.ticket, 1);  // the ticket after those, in flight
   }
   __syncthreads();
-  uint32_t ph[2] = {0, 0};
-  int cur = 0;
+  uint32_t phmask = 0;  // bit k: parity of stage k's barrier
   unsigned long long n_reg = 0;
   Prof prof;
   long long tb = prof.now();
@@ -1276,32 +1289,38 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
     prof.add(PS_GATHER + (k), n_ - tb);  \
     tb = n_;                             \
   }
-  while (true) {
+  for (int it = 0;; ++it) {
+    const int cur = it % NS, ob = it & 1;
     const int64_t t = s_t[cur];
     if (t >= P.Q) break;
-    const BufRegion R = buf_region<KT>(g, P, t, buf_a);
+    const BufRegion R = buf_region<KT>(g, P, t, buf_a, s_a[cur][0], s_a[cur][1]);
+    __syncthreads();  // everyone has the region before the leader reuses a stage slot
     if (leader) {
-      // keep the next region in flight (its ticket was fetched one iteration ago)
+      // keep NS-1 regions in flight: the stage of the previous iteration is free
+      const int nx = (it + NS - 1) % NS;
       const int64_t tn = (*(volatile int32_t*)P.err) ? P.Q : (t_pref < P.Q ? t_pref : P.Q);
       if (t_pref < P.Q) t_pref = atomicAdd(P.ticket, 1);
-      s_t[cur ^ 1] = tn;
+      s_t[nx] = tn;
+      s_early[nx] = 0;
       if (tn < P.Q) {
         const BufRegion Rn = buf_region<KT>(g, P, tn, buf_a);
-        if (!Rn.identity) buf_issue<KT>(P, Rn, buf_a, STAGE(cur ^ 1), STAGE(cur ^ 1) + P.smem_keys, &bar[cur ^ 1]);
+        s_a[nx][0] = Rn.a0;
+        s_a[nx][1] = Rn.a1;
+        if (!Rn.identity) buf_issue<KT>(P, Rn, buf_a, STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
       }
     }
     PB_TICK(0);
     if (R.identity) {  // records already on their outputs and read by r only
       if (leader) st_release(&flags[R.r], 1);
     } else {
-      while (!mbar_try_wait(&bar[cur], ph[cur])) {
+      while (!mbar_try_wait(&bar[cur], (phmask >> cur) & 1)) {
       }
-      ph[cur] ^= 1;
+      phmask ^= 1u << cur;
       PB_TICK(1);
       const int64_t phk = ((uintptr_t)(okeys + (P.s + R.d0) * ks)) & 15;
       const int64_t php = w ? (((uintptr_t)(opay + (P.s + R.d0) * w)) & 15) : 0;
-      uint8_t* kout_s = OUTB(cur);
-      uint8_t* pout_s = OUTB(cur) + P.smem_keys;
+      uint8_t* kout_s = OUTB(ob);
+      uint8_t* pout_s = OUTB(ob) + P.smem_keys;
       if (ctrl && oop) {
         // copy mode: nothing to announce or wait for
       } else if (ctrl) {
@@ -1314,23 +1333,28 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
         const int64_t c_lo = __ldg(&P.state[R.r]), c_hi = __ldg(&P.loc[R.r]);
         for (int64_t c = c_lo + lane; c <= c_hi; c += 32) {
           if (c == R.r) continue;
-          for (uint32_t it = 0; ld_acquire(&flags[c]) == 0; ++it) {
-            if ((it & 255) == 255 && ld_relaxed(P.err)) break;
-            if (it > kSpinLimit) {
+          for (uint32_t it2 = 0; ld_acquire(&flags[c]) == 0; ++it2) {
+            if ((it2 & 255) == 255 && ld_relaxed(P.err)) break;
+            if (it2 > kSpinLimit) {
               raise_error(P.err, PM_ERR_TIMEOUT);
               break;
             }
-            backoff(it);
+            backoff(it2);
           }
         }
-        // the prefetched region's loads often land meanwhile: announce its reads early
+        // regions in flight whose loads have landed: announce their reads early
         if (leader) {
-          s_early[cur ^ 1] = 0;
-          const int64_t tn = s_t[cur ^ 1];
-          if (tn < P.Q && mbar_try_wait(&bar[cur ^ 1], ph[cur ^ 1])) {
-            __threadfence();
-            st_release(&flags[buf_region<KT>(g, P, tn, buf_a).r], 1);
-            s_early[cur ^ 1] = 1;
+          for (int k = 1; k < NS; ++k) {
+            const int sk = (it + k) % NS;
+            const int64_t tk = s_t[sk];
+            if (tk < P.Q && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
+              const BufRegion Rk = buf_region<KT>(g, P, tk, buf_a, s_a[sk][0], s_a[sk][1]);
+              if (!Rk.identity) {
+                __threadfence();
+                st_release(&flags[Rk.r], 1);
+                s_early[sk] = 1;
+              }
+            }
           }
         }
       } else {
@@ -1353,8 +1377,7 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
       if (w) stream_out(pout_s + php, opay + (P.s + R.d0) * w, R.nout * w, gt, NT);
       ++n_reg;
     }
-    cur ^= 1;
-    if (leader) bulk_wait_read<1>();  // the store that used outb[cur] (next) has read it
+    if (leader) bulk_wait_read<1>();  // the store that used the other output buffer has read it
     __syncthreads();
     PB_TICK(4);
   }
@@ -1363,6 +1386,8 @@ __global__ void __launch_bounds__(256) k_buffered(EngineParams P, int32_t buf_a)
     atomicAdd(&P.stats[2], n_reg);
   }
   if (tid == 0) prof.flush(P.stats);
+#undef STAGE
+#undef OUTB
 }
 
 // ---- host launchers (called from pm_capi.cu) --------------------------------

@@ -40,7 +40,20 @@ constexpr int kEngineTeam = PM_ENGINE_TEAM;
 constexpr int kEngineThreads = 64 * PM_ENGINE_TEAM;
 constexpr int kEngineMinBlocks = PM_ENGINE_MINB;
 constexpr int64_t kTileBudget = PM_TILE_BUDGET;
-constexpr int kBufferedThreads = 256;
+#ifndef PM_BUF_THREADS
+#define PM_BUF_THREADS 256
+#endif
+constexpr int kBufferedThreads = PM_BUF_THREADS;
+// k_buffered (buffered / copy modes): staging ring depth and the shared-memory
+// budget its (stages + 2 output) tiles are sized to
+#ifndef PM_BUF_STAGES
+#define PM_BUF_STAGES 2
+#endif
+#ifndef PM_BUF_BUDGET
+#define PM_BUF_BUDGET (72 * 1024)
+#endif
+constexpr int kBufStages = PM_BUF_STAGES;
+constexpr int64_t kBufBudget = PM_BUF_BUDGET;
 // free-list shards: each tagged top word on its own 256-byte line (its own L2
 // slice), so CAS traffic on one shard does not queue behind another's
 constexpr int kShards = 64;
