@@ -289,7 +289,7 @@ def run_dist(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"cfg5: int32 uniform sorted runs, block-distributed A|B, {n} records per GPU "
                                    f"(N = {N})", "key": "int32", "payload_bytes": 0, "L_A": la, "L_B": N - la,
-                       "parallelism": f"dist{world}: global stable splits + NCCL all-to-all + local engine",
+                       "parallelism": f"dist{world}: global stable splits + NCCL all-to-all + local copy merge (pm_merge_copy)",
                        "l2": "per-GPU blocks exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9 / peak,
