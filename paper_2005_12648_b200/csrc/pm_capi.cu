@@ -139,7 +139,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.qc = std::min<int64_t>(std::max<int64_t>(m / M - P.R0, 0), P.Q - 1);
   if (P.K >= INT32_MAX / 2) return fail(PM_ERR_UNSUPPORTED, "job too large for 32-bit unit indices");
   // shared memory carve-up (all offsets 16-byte aligned)
-  P.smem_keys = (size_t)align_up(M * ks + 48, 128);
+  P.smem_keys = (size_t)align_up((M + 2 * kSent) * ks + 64, 128);  // + sentinel gaps (write_sentinels)
+  {
+    const int64_t merge_threads = buffered ? kBufferedThreads - 32 : kEngineThreads - 32 * kEngineTeam;
+    if ((((M + merge_threads - 1) / merge_threads) | 1) + 1 > kSent)
+      return fail(PM_ERR_INTERNAL, "tile merge span exceeds the sentinel gap");
+  }
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
   // staged inputs (keys, payload) + merged output tile (keys, payload), same sizes;
   // the buffered pipeline double-buffers both

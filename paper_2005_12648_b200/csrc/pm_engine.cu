@@ -431,6 +431,16 @@ __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, 
 // Bs[0,beta) into the output tile ko[0,nout) (+ payload rows), thread gt of GT.
 // Every thread takes an odd-length run of outputs: odd strides keep the shared
 // memory accesses of a warp on distinct banks.
+// +max sentinels after both staged runs (keys-only merges; threads gt of GT).
+template <typename KT>
+__device__ __forceinline__ void write_sentinels(uint8_t* kin, int64_t offA, int64_t alpha, int64_t offB, int64_t beta,
+                                                int gt, int GT) {
+  KT* a = reinterpret_cast<KT*>(kin + offA) + alpha;
+  KT* b = reinterpret_cast<KT*>(kin + offB) + beta;
+  const KT mx = sizeof(KT) == 4 ? (KT)INT32_MAX : (KT)INT64_MAX;
+  for (int k = gt; k < 2 * kSent; k += GT) (k < kSent ? a[k] : b[k - kSent]) = mx;
+}
+
 template <typename KT>
 __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT* Bs, int64_t alpha, int64_t beta,
                                            int64_t nout, KT* ko, uint8_t* po, const uint8_t* PA, const uint8_t* PB,
@@ -446,22 +456,24 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
       // keys only.  Shared-memory bandwidth bounds this loop (lanes sit at random
       // offsets, ~3.5-way bank conflicts per load), so each step loads exactly one
       // candidate -- the replacement for the side just taken -- via an address select
+      // Both runs are followed by kSent +max sentinels (write_sentinels): an
+      // exhausted run offers +max, which loses to every real key except +max
+      // itself -- and then either choice emits the same value.  No bound checks.
       int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
       while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
         if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
         else hi = mid;
       }
-      const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
       int32_t i = lo, jb = o - lo;
-      KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
+      KT va = As[i], vb = Bs[jb];
 #pragma unroll 4
       for (; o < oe; ++o) {
-        const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
+        const bool takeA = va <= vb;
         ko[o] = takeA ? va : vb;
         i += takeA;
         jb += !takeA;
-        const KT v = *(takeA ? As + min(i, amax) : Bs + min(jb, bmax));
+        const KT v = *(takeA ? As + i : Bs + jb);
         va = takeA ? v : va;
         vb = takeA ? vb : v;
       }
@@ -667,7 +679,7 @@ struct DataRegion {
     xa = P.s + a0;
     xb = P.m + b0;
     offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-    offB = ((offA + alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+    offB = ((offA + (alpha + kSent) * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
     poffA = poffB = 0;
     if (w) {
       poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
@@ -998,6 +1010,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         __threadfence();
         pold = atomicAdd(&P.reads[pj], pn);
       }
+      if (P.mode == MODE_MERGE && !w) write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, gt, GT);
       if (gt == 0) bulk_wait_read_all();  // the previous tile's TMA store has read the output tile
       named_barrier_sync(1, GT);
       if (gt == 0) atomicExch(&re.published, 1);
@@ -1194,7 +1207,7 @@ __device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams
   R.identity = !P.out_keys && ((R.a0 == R.d0 && R.a1 == R.d1) || (R.a0 == la && R.a1 == la));
   const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
   R.offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-  R.offB = ((R.offA + R.alpha * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+  R.offB = ((R.offA + (R.alpha + kSent) * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
   R.poffA = R.poffB = 0;
   if (w) {
     R.poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
@@ -1294,8 +1307,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
     const int64_t t = s_t[cur];
     if (t >= P.Q) break;
     const BufRegion R = buf_region<KT>(g, P, t, buf_a, s_a[cur][0], s_a[cur][1]);
-    __syncthreads();  // everyone has the region before the leader reuses a stage slot
-    if (leader) {
+    if (leader) {  // (writes only the previous iteration's stage slot: no race with R above)
       // keep NS-1 regions in flight: the stage of the previous iteration is free
       const int nx = (it + NS - 1) % NS;
       const int64_t tn = (*(volatile int32_t*)P.err) ? P.Q : (t_pref < P.Q ? t_pref : P.Q);
@@ -1360,6 +1372,10 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
       } else {
         uint8_t* kin = STAGE(cur);
         uint8_t* pin = STAGE(cur) + P.smem_keys;
+        if (!w) {
+          write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, tid, MT);
+          named_barrier_sync(1, MT);
+        }
         const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
         merge_tile<KT>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
                        reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,

@@ -37,6 +37,10 @@ constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 #define PM_TILE_BUDGET (72 * 1024)
 #endif
 constexpr int kEngineTeam = PM_ENGINE_TEAM;
+// staged runs are followed by kSent slots of +max sentinels (keys-only merges
+// then need no bound checks in their dependent chain); kSent > the longest
+// per-thread output span of any tile merge (checked on the host)
+constexpr int kSent = 80;
 constexpr int kEngineThreads = 64 * PM_ENGINE_TEAM;
 constexpr int kEngineMinBlocks = PM_ENGINE_MINB;
 constexpr int64_t kTileBudget = PM_TILE_BUDGET;
