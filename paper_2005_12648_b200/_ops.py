@@ -87,6 +87,26 @@ def merge_copy(src_keys: torch.Tensor, src_payload: torch.Tensor, dst_keys: torc
     return None
 
 
+def merge_host(keys, payload, start: int, middle: int, end: int, device: int = 0):
+    """In-place stable merge of host (numpy) arrays through pm_merge_host.
+
+    keys: int32/int64 [n] C-contiguous; payload: uint8 [n, w] C-contiguous.  The
+    transfer, the device merge and the write-back are pipelined per output chunk
+    (pinned host memory overlaps both PCIe directions; pageable memory works too).
+    """
+    import numpy as np
+
+    if keys.dtype not in (np.int32, np.int64) or not keys.flags.c_contiguous:
+        raise ValueError("keys must be a C-contiguous int32/int64 array")
+    if payload.ndim != 2 or payload.dtype != np.uint8 or not payload.flags.c_contiguous or len(payload) != len(keys):
+        raise ValueError("payload must be a C-contiguous uint8 array of shape (len(keys), w)")
+    w = payload.shape[1]
+    rc = _capi.lib().pm_merge_host(_capi.context(device), ctypes.c_void_p(keys.ctypes.data), keys.itemsize,
+                                   ctypes.c_void_p(payload.ctypes.data if w else 0), w, start, middle, end,
+                                   ctypes.c_void_p(0))
+    _capi.check(rc, "pm_merge_host")
+
+
 def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
     """In-place block exchange A|B -> B|A on the device (pm_shift)."""
     require_cuda(arr)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/parmerge_b200.h"
@@ -65,8 +66,10 @@ struct pm_ctx {
   Ctl* ctl = nullptr;
   void* scr = nullptr;  // scratch keys + payload
   size_t scr_bytes = 0;
-  void* stage = nullptr;  // device staging for pm_merge_host
+  void* stage = nullptr;  // device staging for pm_merge_host (input copy + output)
   size_t stage_bytes = 0;
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // pm_merge_host: H2D, merge, D2H
+  cudaEvent_t hev[33] = {};                          // [0]: joins; then per-chunk events (ring)
   void* buf = nullptr;    // min-side buffer of the buffered mode
   size_t buf_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
@@ -102,9 +105,10 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
 
 // out_keys / out_payload non-null: copy mode -- merge keys[s,m) and keys[m,e) into
 // out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
+// keys_b / pay_b (copy mode only): the B run lives there instead of at keys + m.
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
-                      void* out_payload = nullptr) {
+                      void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr) {
   const bool copy = out_keys != nullptr;
   if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
@@ -121,6 +125,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.pay = static_cast<uint8_t*>(payload);
   P.out_keys = static_cast<char*>(out_keys);
   P.out_pay = static_cast<uint8_t*>(out_payload);
+  P.keys_b = static_cast<const char*>(keys_b);
+  P.pay_b = static_cast<const uint8_t*>(pay_b);
   P.w = w;
   P.ks = ks;
   P.mode = mode;
@@ -246,6 +252,19 @@ static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* paylo
   return PM_OK;
 }
 
+// Stable merge path on host arrays: number of A records among the first d outputs
+// (A wins ties).  Reads ~2*log2(n) records of the (pinned) host arrays.
+template <typename KT>
+static int64_t host_split(const KT* A, int64_t la, const KT* B, int64_t lb, int64_t d) {
+  int64_t lo = std::max<int64_t>(0, d - lb), hi = std::min(d, la);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 extern "C" {
 
 int pm_version(void) { return 100; }
@@ -308,6 +327,10 @@ int pm_ctx_destroy(pm_ctx* ctx) {
   if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->buf) cudaFree(ctx->buf);
+  for (auto& x : ctx->hs)
+    if (x) cudaStreamDestroy(x);
+  for (auto& x : ctx->hev)
+    if (x) cudaEventDestroy(x);
   if (ctx->ctl) cudaFree(ctx->ctl);
   delete ctx;
   return PM_OK;
@@ -434,30 +457,100 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
   return PM_OK;
 }
 
+// Host-buffer merge, pipelined over output chunks on three streams: H2D of the
+// input prefixes chunk k needs, the out-of-place device merge of chunk k
+// (copy mode), and D2H of chunk k back into the caller's (in-place) array.
+// Chunk k's output [d_k, d_{k+1}) is written back only once every input record
+// that lived there is on the device, so the in-place host semantics hold while
+// the two PCIe directions overlap.
 int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_host, int64_t width, int64_t start,
                   int64_t middle, int64_t end, void* stream) {
   if (!ctx || !keys_host || (key_bytes != 4 && key_bytes != 8) || width < 0 || (width && !payload_host))
     return fail(PM_ERR_ARG, "bad pm_merge_host arguments");
   if (!(0 <= start && start <= middle && middle <= end)) return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t n = end - start;
-  const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)(n * width);
+  const int64_t n = end - start, la = middle - start, lb = end - middle;
+  if (la == 0 || lb == 0) return PM_OK;
+  char* hk = static_cast<char*>(keys_host) + start * key_bytes;
+  char* hp = width ? static_cast<char*>(payload_host) + start * width : nullptr;
+  // already in order (srecpar.py:56-57): nothing moves
+  {
+    bool sorted;
+    if (key_bytes == 4) sorted = reinterpret_cast<int32_t*>(hk)[la - 1] <= reinterpret_cast<int32_t*>(hk)[la];
+    else sorted = reinterpret_cast<int64_t*>(hk)[la - 1] <= reinterpret_cast<int64_t*>(hk)[la];
+    if (sorted) return PM_OK;
+  }
+  const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)align_up(n * width, 256);
   int rc;
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    rc = ensure(&ctx->stage, &ctx->stage_bytes, kb + pb + 256);
+    rc = ensure(&ctx->stage, &ctx->stage_bytes, 2 * (kb + pb) + 256);
+    if (!rc && !ctx->hs[0]) {
+      for (auto& x : ctx->hs) PM_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+      for (auto& x : ctx->hev) PM_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
   }
   if (rc) return rc;
-  char* dk = static_cast<char*>(ctx->stage);
-  char* dp = dk + kb;
-  char* hk = static_cast<char*>(keys_host) + start * key_bytes;
-  char* hp = width ? static_cast<char*>(payload_host) + start * width : nullptr;
-  PM_CUDA(cudaMemcpyAsync(dk, hk, n * key_bytes, cudaMemcpyHostToDevice, st));
-  if (width) PM_CUDA(cudaMemcpyAsync(dp, hp, pb, cudaMemcpyHostToDevice, st));
-  rc = pm_merge(ctx, dk, key_bytes, width ? dp : nullptr, width, 0, middle - start, n, 0, stream);
-  if (rc) return rc;
-  PM_CUDA(cudaMemcpyAsync(hk, dk, n * key_bytes, cudaMemcpyDeviceToHost, st));
-  if (width) PM_CUDA(cudaMemcpyAsync(hp, dp, pb, cudaMemcpyDeviceToHost, st));
+  char* dxk = static_cast<char*>(ctx->stage);  // input copy X
+  char* dxp = dxk + kb;
+  char* dok = dxp + pb;                        // merged output O
+  char* dop = dok + kb;
+  cudaStream_t sH = ctx->hs[0], sC = ctx->hs[1], sD = ctx->hs[2];
+  // order after the caller's stream
+  PM_CUDA(cudaEventRecord(ctx->hev[0], st));
+  PM_CUDA(cudaStreamWaitEvent(sH, ctx->hev[0], 0));
+  const int64_t chunk = std::max<int64_t>((int64_t)1 << 21, (n + 95) / 96);
+  const int nch = (int)((n + chunk - 1) / chunk);
+  auto split = [&](int64_t d) -> int64_t {
+    if (key_bytes == 4)
+      return host_split(reinterpret_cast<const int32_t*>(hk), la, reinterpret_cast<const int32_t*>(hk) + la, lb, d);
+    return host_split(reinterpret_cast<const int64_t*>(hk), la, reinterpret_cast<const int64_t*>(hk) + la, lb, d);
+  };
+  // the splits are read from the host arrays before any chunk is written back
+  std::vector<int64_t> dk(nch + 1), ak(nch + 1);
+  for (int k = 0; k <= nch; ++k) {
+    dk[k] = std::min<int64_t>((int64_t)k * chunk, n);
+    ak[k] = split(dk[k]);
+  }
+  auto h2d = [&](int64_t x0, int64_t x1) -> int {
+    if (x1 <= x0) return PM_OK;
+    PM_CUDA(cudaMemcpyAsync(dxk + x0 * key_bytes, hk + x0 * key_bytes, (x1 - x0) * key_bytes,
+                            cudaMemcpyHostToDevice, sH));
+    if (width)
+      PM_CUDA(cudaMemcpyAsync(dxp + x0 * width, hp + x0 * width, (x1 - x0) * width, cudaMemcpyHostToDevice, sH));
+    return PM_OK;
+  };
+  int64_t cA = 0, cB = 0;  // on the device: X[0, cA) and X[la, la + cB)
+  constexpr int kEv = (int)(sizeof(((pm_ctx*)nullptr)->hev) / sizeof(cudaEvent_t)) - 1;
+  for (int k = 0; k < nch; ++k) {
+    // the inputs of chunk k and every record living in its output range
+    const int64_t d1 = dk[k + 1], a1 = ak[k + 1], b1 = d1 - a1;
+    const int64_t tA = std::min(d1, la), tB = std::max(b1, d1 > la ? d1 - la : 0);
+    if (tA > cA) rc = h2d(cA, tA);
+    if (!rc && tB > cB) rc = h2d(la + cB, la + tB);
+    if (rc) return rc;
+    cA = std::max(cA, tA);
+    cB = std::max(cB, tB);
+    cudaEvent_t eh = ctx->hev[1 + (2 * k) % kEv], ec = ctx->hev[1 + (2 * k + 1) % kEv];
+    PM_CUDA(cudaEventRecord(eh, sH));
+    PM_CUDA(cudaStreamWaitEvent(sC, eh, 0));
+    const int64_t d0 = dk[k], a0 = ak[k], b0 = d0 - a0;
+    {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      rc = run_engine(ctx, dxk + a0 * key_bytes, key_bytes, width ? dxp + a0 * width : nullptr, width, 0, a1 - a0,
+                      d1 - d0, MODE_MERGE, 0, sC, dok + d0 * key_bytes, width ? dop + d0 * width : nullptr,
+                      dxk + (la + b0) * key_bytes, width ? dxp + (la + b0) * width : nullptr);
+    }
+    if (rc) return rc;
+    PM_CUDA(cudaEventRecord(ec, sC));
+    PM_CUDA(cudaStreamWaitEvent(sD, ec, 0));
+    PM_CUDA(cudaMemcpyAsync(hk + d0 * key_bytes, dok + d0 * key_bytes, (d1 - d0) * key_bytes,
+                            cudaMemcpyDeviceToHost, sD));
+    if (width)
+      PM_CUDA(cudaMemcpyAsync(hp + d0 * width, dop + d0 * width, (d1 - d0) * width, cudaMemcpyDeviceToHost, sD));
+  }
+  PM_CUDA(cudaEventRecord(ctx->hev[0], sD));
+  PM_CUDA(cudaStreamWaitEvent(st, ctx->hev[0], 0));
   return pm_status(ctx, stream, nullptr);
 }
 

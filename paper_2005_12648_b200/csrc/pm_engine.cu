@@ -123,7 +123,7 @@ __global__ void k_plan(EngineParams P) {
       const int64_t d = g.diag(q);
       int64_t a;
       if (P.mode == MODE_MERGE) {
-        a = merge_path_thread<KT>(keys + P.s, la, keys + P.m, lb, d);
+        a = merge_path_thread<KT>(keys + P.s, la, P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m, lb, d);
       } else {  // rotation: outputs are B then A
         a = d - lb;
         a = a < 0 ? 0 : (a > la ? la : a);
@@ -148,8 +148,8 @@ __global__ void k_plan(EngineParams P) {
     *P.scr_count = (int32_t)P.S;
     *P.ticket = 0;
     bool nothing = (la == 0 || lb == 0);
-    if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     if (P.out_keys) nothing = false;  // out of place: every record still moves
+    else if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
     *P.need_space = 0;
     for (int i = 0; i < 64; ++i) P.stats[i] = 0;
@@ -1206,12 +1206,14 @@ __device__ __forceinline__ BufRegion buf_region(const Geo& g, const EngineParams
   R.nout = R.d1 - R.d0;
   R.identity = !P.out_keys && ((R.a0 == R.d0 && R.a1 == R.d1) || (R.a0 == la && R.a1 == la));
   const int64_t xa = P.s + R.a0, xb = P.m + R.b0;
+  const char* kbsrc = P.keys_b ? P.keys_b + R.b0 * ks : P.keys + xb * ks;
   R.offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
-  R.offB = ((R.offA + (R.alpha + kSent) * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+  R.offB = ((R.offA + (R.alpha + kSent) * ks + 15) & ~(int64_t)15) + (((uintptr_t)kbsrc) & 15);
   R.poffA = R.poffB = 0;
   if (w) {
+    const uint8_t* pbsrc = P.pay_b ? P.pay_b + R.b0 * w : P.pay + xb * w;
     R.poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
-    R.poffB = ((R.poffA + R.alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+    R.poffB = ((R.poffA + R.alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)pbsrc) & 15);
   }
   return R;
 }
@@ -1226,12 +1228,12 @@ __device__ __forceinline__ void buf_issue(const EngineParams& P, const BufRegion
   // (copy mode: both runs come from the source array)
   const bool oop = P.out_keys != nullptr;
   const char* ka = buf_a && !oop ? P.scr_keys + R.a0 * ks : P.keys + xa * ks;
-  const char* kb = buf_a || oop ? P.keys + xb * ks : P.scr_keys + R.b0 * ks;
+  const char* kb = P.keys_b ? P.keys_b + R.b0 * ks : buf_a || oop ? P.keys + xb * ks : P.scr_keys + R.b0 * ks;
   copy_g2s_superset(kin + R.offA, reinterpret_cast<const uint8_t*>(ka), R.alpha * ks, bar);
   copy_g2s_superset(kin + R.offB, reinterpret_cast<const uint8_t*>(kb), R.beta * ks, bar);
   if (w) {
     const uint8_t* pa = buf_a && !oop ? P.scr_pay + R.a0 * w : P.pay + xa * w;
-    const uint8_t* pb = buf_a || oop ? P.pay + xb * w : P.scr_pay + R.b0 * w;
+    const uint8_t* pb = P.pay_b ? P.pay_b + R.b0 * w : buf_a || oop ? P.pay + xb * w : P.scr_pay + R.b0 * w;
     copy_g2s_superset(pin + R.poffA, pa, R.alpha * w, bar);
     copy_g2s_superset(pin + R.poffB, pb, R.beta * w, bar);
   }

@@ -25,10 +25,14 @@ enum : int32_t { MODE_MERGE = 0, MODE_ROTATE = 1 };
 enum : int32_t { ST_FREE = -1, ST_CLOSED = -2 };
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 
-// k_engine shape: two teams of kEngineTeam warps, kEngineMinBlocks resident CTAs
-// per SM, staging tiles sized to kTileBudget bytes of shared memory per CTA.
+// k_engine shape: kEngineTeam salvage-worker warps + kDataWarps data-team warps,
+// kEngineMinBlocks resident CTAs per SM, staging tiles sized to kTileBudget bytes
+// of shared memory per CTA.
 #ifndef PM_ENGINE_TEAM
 #define PM_ENGINE_TEAM 4
+#endif
+#ifndef PM_DATA_WARPS
+#define PM_DATA_WARPS PM_ENGINE_TEAM
 #endif
 #ifndef PM_ENGINE_MINB
 #define PM_ENGINE_MINB 3
@@ -41,7 +45,8 @@ constexpr int kEngineTeam = PM_ENGINE_TEAM;
 // then need no bound checks in their dependent chain); kSent > the longest
 // per-thread output span of any tile merge (checked on the host)
 constexpr int kSent = 80;
-constexpr int kEngineThreads = 64 * PM_ENGINE_TEAM;
+constexpr int kDataWarps = PM_DATA_WARPS;
+constexpr int kEngineThreads = 32 * (PM_ENGINE_TEAM + PM_DATA_WARPS);
 constexpr int kEngineMinBlocks = PM_ENGINE_MINB;
 constexpr int64_t kTileBudget = PM_TILE_BUDGET;
 #ifndef PM_BUF_THREADS
@@ -150,6 +155,8 @@ struct EngineParams {
   size_t smem_pay;     // bytes reserved for staged payload
   char* out_keys;      // out-of-place merge (k_buffered copy mode): destination, else null
   uint8_t* out_pay;
+  const char* keys_b;  // copy mode: B run base (record j at keys_b + j*ks), else null (B = keys + m)
+  const uint8_t* pay_b;
 };
 
 }  // namespace pm

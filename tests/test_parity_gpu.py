@@ -310,3 +310,23 @@ def test_distributed_merge_single_rank_nccl():
         assert np.array_equal(rk.cpu().numpy(), want_k) and np.array_equal(rp.cpu().numpy(), want_p)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("width", [0, 4, 5])
+def test_merge_host_vs_oracle(width):
+    """pm_merge_host: chunk-pipelined H2D / device merge / in-place D2H == the stable merge."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(2024 + width)
+    for size, split, domain, dtype in ((1000, 0.5, 100, np.int32), (10_000_000, 0.5, 2**31 - 1, np.int32),
+                                       (9_000_001, 0.13, 50, np.int32), (6_000_000, 0.8, 2**31 - 1, np.int64)):
+        keys, payload, middle = random_instance(rng, size, split, domain, width)
+        keys = keys.astype(dtype)
+        lo, hi = 7, 5
+        kk = np.concatenate([np.full(lo, -3, dtype), keys, np.full(hi, -9, dtype)])
+        pp = np.concatenate([np.full((lo, width), 1, np.uint8), payload, np.full((hi, width), 2, np.uint8)])
+        want_k, want_p = kk.copy(), pp.copy()
+        orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
+        _ops.merge_host(kk, pp, lo, lo + middle, lo + size)
+        assert np.array_equal(kk, want_k), f"keys size={size}"
+        assert np.array_equal(pp, want_p), f"payload size={size}"
