@@ -391,9 +391,14 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
   int rc = check_common(ctx, keys, key_bytes, payload, width);
   if (rc) return rc;
   if (lo < 0 || len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "lengths must be non-negative");  // shift.py:157
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  return run_engine(ctx, keys, key_bytes, payload, width, lo, lo + len_a, lo + len_a + len_b, MODE_ROTATE, 0,
-                    static_cast<cudaStream_t>(stream));
+  if (len_a == 0 || len_b == 0) return PM_OK;
+  // three reversals (pm_rotate.cu): two streaming passes, no workspace
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaError_t e = key_bytes == 4
+                            ? launch_rotate<int32_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st)
+                            : launch_rotate<int64_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_reverse launch");
+  return PM_OK;
 }
 
 int pm_find_median(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int64_t la, int64_t lb, int64_t* out2,
