@@ -65,6 +65,50 @@ __device__ __forceinline__ void merge_chunks(const KT* As, const KT* Bs, int al,
     }
   }
 }
+template <typename KT, int C>
+__device__ __forceinline__ void merge_chunks_shfl(const KT* As, const KT* Bs, int al, int bl, int no, KT* ko, int gt, int GT) {
+  const int lane = gt & 31, wid = gt >> 5, NW = GT >> 5;
+  const int nch = (no + C - 1) / C;
+  for (int c0 = wid * 31; c0 < nch; c0 += NW * 31) {
+    const int c = c0 + lane;  // lane 31 only supplies the end split of lane 30
+    const int o = min(c * C, no);
+    const int i0 = mp_search(As, Bs, al, bl, o);
+    const int i1 = __shfl_down_sync(0xffffffffu, i0, 1);
+    if (lane == 31 || c >= nch) continue;
+    const int oe = min(o + C, no);
+    const int na = i1 - i0, nb = (oe - o) - na, j0 = o - i0;
+    KT v[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int kb = C - 1 - k;
+      const bool isA = k < na, isB = kb < nb;
+      const KT* p = isA ? As + i0 + k : Bs + j0 + kb;
+      v[k] = (isA | isB) ? *p : kmax<KT>();
+    }
+#pragma unroll
+    for (int d = C / 2; d >= 1; d >>= 1) {
+#pragma unroll
+      for (int k = 0; k < C; ++k)
+        if ((k & d) == 0) cas(v[k], v[k + d]);
+    }
+    if (oe - o == C && (((uintptr_t)(ko + o)) & 15) == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(ko + o);
+#pragma unroll
+      for (int s = 0; s < C / 4; ++s) {
+        const int pc = (s + (lane >> 1)) & (C / 4 - 1);
+        uint4 val = make_uint4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int q = 1; q < C / 4; ++q)
+          if (pc == q) val = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        dst[pc] = val;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < C; ++k)
+        if (o + k < oe) ko[o + k] = v[k];
+    }
+  }
+}
 template <typename KT>
 __device__ __forceinline__ void merge_serial(const KT* As, const KT* Bs, int al, int bl, int no, KT* ko, int gt, int GT) {
   int E = (no + GT - 1) / GT;
@@ -100,7 +144,9 @@ __global__ void k(int variant, int reps, int GTw, int M, int al, unsigned long l
     asm volatile("bar.sync 1, %0;" ::"r"(GT));
     long long c0 = clock64();
     if (variant == 0) merge_serial<int>(in, in + al, al, bl, M, out, threadIdx.x, GT);
-    else merge_chunks<int>(in, in + al, al, bl, M, out, threadIdx.x, GT);
+    else if (variant == 1) merge_chunks<int>(in, in + al, al, bl, M, out, threadIdx.x, GT);
+    else if (variant == 2) merge_chunks_shfl<int, 16>(in, in + al, al, bl, M, out, threadIdx.x, GT);
+    else merge_chunks_shfl<int, 8>(in, in + al, al, bl, M, out, threadIdx.x, GT);
     asm volatile("bar.sync 1, %0;" ::"r"(GT));
     tot += clock64() - c0;
   }
@@ -118,14 +164,14 @@ int main() {
   unsigned long long* cyc; cudaMalloc(&cyc, 8);
   int* bad; cudaMalloc(&bad, 4);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
-  int cfgs[][4] = {{0, 7, 4096, 2048}, {1, 7, 4096, 2048}, {0, 4, 8192, 4096}, {1, 4, 8192, 4096}, {1, 7, 4096, 1000}, {1, 7, 4090, 3000}};
+  int cfgs[][4] = {{0, 7, 4096, 2048}, {2, 7, 4096, 2048}, {3, 7, 4096, 2048}, {0, 4, 8192, 4096}, {2, 4, 8192, 4096}, {3, 4, 8192, 4096}, {2, 7, 4096, 1000}, {2, 7, 4090, 3000}, {3, 7, 4090, 3000}};
   for (auto& c : cfgs) {
     cudaMemset(cyc, 0, 8); cudaMemset(bad, 0, 4);
     k<<<444, 32 * c[1], 70000>>>(c[0], 64, c[1], c[2], c[3], cyc, bad);
     cudaDeviceSynchronize();
     unsigned long long h; int hb;
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&hb, bad, 4, cudaMemcpyDeviceToHost);
-    printf("%s warps=%d M=%d al=%d: %.0f cycles per tile (unsorted %d)\n", c[0] ? "network" : "serial ", c[1], c[2], c[3],
+    printf("variant %d warps=%d M=%d al=%d: %.0f cycles per tile (unsorted %d)\n", c[0], c[1], c[2], c[3],
            (double)h / 444 / 64, hb % 1000);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
