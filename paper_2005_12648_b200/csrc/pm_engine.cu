@@ -275,16 +275,23 @@ __device__ __forceinline__ void cache_flush(Ctl& c, const EngineParams& P, int h
   for (int i = 0; i < ns; ++i) stack_push(&P.scr_top[home * kTopStride], P.next_scr, sc[i]);
 }
 
-// Warp-wide: a salvage destination for unit u.  Scratch first (a parked unit is
-// never moved again), then free slots; CTA cache first, then the global lists.
-// Called only after this region has read its inputs (stage B done), so a
-// blocked caller never holds space other regions wait for.  When it has to
-// block it raises need_space so CTAs flush their caches.
+// Warp-wide: a salvage destination for unit u, moved by ticket t.  Scratch first
+// (a parked unit is never moved again), then free slots; CTA cache first, then
+// the global lists.  A free slot qualifies only if its region's order exceeds t:
+// units only ever move to higher order (or scratch), so while u sits in region
+// r's slot, reads[u] counts exactly its consumers of order <= r -- the count
+// the region's store waits on.  (A free slot of a lower-order region belongs to a
+// ticket already in flight that is about to close it: it is dropped.)
+// Blocking callers have published their own region's reads first, so a blocked
+// caller never holds space other regions wait for; after a while they raise
+// need_space so CTAs flush their caches.
 template <class Ctl>
-__device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, int32_t u, int home, int lane,
-                                                bool block) {
+__device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, int32_t u, int64_t t, int home,
+                                                int lane, bool block) {
   bool flagged = false;
   int32_t dest = INT32_MIN;
+  const Geo g(P);
+  auto usable = [&](int32_t f) { return g.order(g.region_of_slot(f)) > t && atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE; };
   for (uint32_t it = 0;; ++it) {
     // scratch first (cache, then the global lists): a unit parked in scratch is
     // final, one parked in a free slot moves again when that slot's region starts
@@ -315,8 +322,8 @@ __device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, i
       int32_t f = -1;
       while (c.n_fs > 0) {
         f = c.fs[--c.n_fs];
-        if (atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE) break;
-        f = -1;  // its region started meanwhile
+        if (usable(f)) break;
+        f = -1;  // its region started meanwhile (or precedes t)
       }
       cta_unlock(c);
       if (f >= 0) d = f;
@@ -333,7 +340,7 @@ __device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, i
     bool got = false;
     while ((f = warp_pop(P.free_top, P.next_free, home, lane)) >= 0) {
       int ok = 0;
-      if (lane == 0) ok = atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE;
+      if (lane == 0) ok = usable(f);
       if (__shfl_sync(0xffffffffu, ok, 0)) {
         got = true;
         break;
@@ -642,7 +649,8 @@ struct RingEntry {
   int32_t items_done;   // finished slot items
   int32_t published;    // the data team has published the ticket's reads
   int32_t pad_;
-  int32_t occ[kMaxMu];  // occupant sampled by each slot item (-1: none)
+  int32_t occ[kMaxMu];    // occupant sampled by each slot item (-1: none)
+  int32_t occ_r[kMaxMu];  // its reads[] as sampled by the item
 };
 struct EngCtl {
   uint64_t bar;
@@ -816,6 +824,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       if (lane == 0) {
         close_and_sample(g, P, slot, identity, u, early_r, early_l);
         re.occ[i] = identity ? -1 : u;
+        re.occ_r[i] = early_r;
       }
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= 0 && !identity) {
@@ -844,14 +853,14 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         const long long c2 = prof.now();
         prof.add(PS_THR, c2 - c0);
         if (alive) {
-          int32_t dest = acquire_dest(ctl, P, u, home, lane, false);
+          int32_t dest = acquire_dest(ctl, P, u, t, home, lane, false);
           if (dest == INT32_MIN) {
             // no space: the region's own reads free space first, then block
             const long long cb = prof.now();
             if (lane == 0)
               while (!vc.ring[e % kRing].published && !vc.abort) __nanosleep(128);
             __syncwarp();
-            if (!vc.abort) dest = acquire_dest(ctl, P, u, home, lane, true);
+            if (!vc.abort) dest = acquire_dest(ctl, P, u, t, home, lane, true);
             if (lane == 0) {
               prof.hist(P.stats, 20, 0, 1, 1);
               prof.hist(P.stats, 21, 0, 1, prof.now() - cb);
@@ -1060,7 +1069,9 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           int64_t cwl, cwr;
           g.window(R.t, cwl, cwr);
           const int64_t before = g.consumed_in(u, cwl, cwr, re.ti.clo, re.ti.chi);
-          for (uint32_t it = 0; ld_acquire(&P.reads[u]) < before; ++it) {
+          // (reads[] only counts consumers of order <= t while u sits in t's slot, so
+          // the item's sample settles it without a round trip when it suffices)
+          for (uint32_t it = 0; re.occ_r[gt] < before && ld_acquire(&P.reads[u]) < before; ++it) {
             if ((it & 255) == 255 && ld_relaxed(P.err)) {
               ctl.abort = 1;
               break;

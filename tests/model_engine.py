@@ -142,8 +142,9 @@ class EngineModel:
         return c
 
     # ---- unit data access ----
-    def read_unit(self, j, x0, x1):
-        l, hb = self.loc[j], self.slot_base(j)
+    def read_unit(self, j, x0, x1, l=None):
+        l = self.loc[j] if l is None else l
+        hb = self.slot_base(j)
         if l >= 0:
             b = self.slot_base(l) + (x0 - hb)
             return self.keys[b:b + x1 - x0].copy(), self.pay[b:b + x1 - x0].copy()
@@ -183,12 +184,12 @@ class EngineModel:
                 if self.consumed_by_window(u, t) < self.slot_hi(u) - self.slot_lo(u):
                     # a later region still needs u: move it now (no wait for earlier
                     # consumers -- they read either copy; the data phase waits for them)
-                    dest = self.take_space(u, block=False)
+                    dest = self.take_space(u, t, block=False)
                     if dest is None:
                         while not st["published"]:  # the region's own reads free space first
                             yield "wait"
                         spins = 0
-                        while (dest := self.take_space(u, block=True)) is None:
+                        while (dest := self.take_space(u, t, block=True)) is None:
                             spins += 1
                             if spins > 10000:
                                 raise NoSpace(f"ticket {t} found no salvage space")
@@ -228,7 +229,8 @@ class EngineModel:
                     if l < 0 or self.tf.order(self.region_of_slot(l)) >= t:
                         break
                     yield "wait"
-                got[(j, isA)] = self.read_unit(j, x0, x1)
+                yield  # the bulk copy reads the location seen above, later (TMA is asynchronous)
+                got[(j, isA)] = self.read_unit(j, x0, x1, l)
                 yield
             last = []
             for j, x0, x1, isA in pieces:  # publish reads
@@ -264,13 +266,15 @@ class EngineModel:
 
         return [item(i) for i in range(j1 - j0)] + [data()]
 
-    def take_space(self, u, block):
-        """Scratch first, then a free slot (acquire_dest); None if there is none."""
+    def take_space(self, u, t, block):
+        """Scratch first, then a free slot of a region of order > t (acquire_dest:
+        units only move to higher order, so reads[u] counts exactly the consumers
+        of order <= r while u sits in region r); None if there is none."""
         if self.free_scr:
             return -self.free_scr.pop() - 1
         while self.free_slots:
             f = self.free_slots.pop()
-            if self.state[f] == FREE:
+            if self.state[f] == FREE and self.tf.order(self.region_of_slot(f)) > t:
                 self.state[f] = u
                 return f
         return None
