@@ -134,6 +134,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.m = m;
   P.e = e;
   P.T = T;
+  P.lT = 63 - __builtin_clzll((unsigned long long)T);
+  P.lmu = 31 - __builtin_clz((unsigned)mu);
+  if ((1ll << P.lT) != T || (1 << P.lmu) != mu) return fail(PM_ERR_INTERNAL, "unit geometry must be powers of two");
   P.mu = mu;
   if (mu > 8) return fail(PM_ERR_INTERNAL, "too many slots per region");
   P.nthreads = kEngineThreads;

@@ -40,7 +40,7 @@ struct Geo {
   __device__ int64_t slot_hi(int64_t j) const { return min(P.e, (P.k0 + j + 1) * P.T); }
   __device__ int64_t slot_base(int64_t j) const { return (P.k0 + j) * P.T; }  // unclipped
   __device__ bool slot_full(int64_t j) const { return slot_hi(j) - slot_lo(j) == P.T; }
-  __device__ int64_t region_of_slot(int64_t j) const { return (P.k0 + j) / P.mu - P.R0; }
+  __device__ int64_t region_of_slot(int64_t j) const { return ((P.k0 + j) >> P.lmu) - P.R0; }
   __device__ int64_t region_first_slot(int64_t q) const { return max((int64_t)0, (P.R0 + q) * P.mu - P.k0); }
   __device__ int64_t region_end_slot(int64_t q) const { return min(P.K, (P.R0 + q + 1) * P.mu - P.k0); }
   // local output diagonal at the start of region q (q in [0, Q])
@@ -693,10 +693,10 @@ struct DataRegion {
       poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
       poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
     }
-    ua0 = alpha ? (xa / P.T - P.k0) : 0;
-    const int64_t ua1 = alpha ? ((xa + alpha - 1) / P.T - P.k0 + 1) : 0;
-    ub0 = beta ? (xb / P.T - P.k0) : 0;
-    const int64_t ub1 = beta ? ((xb + beta - 1) / P.T - P.k0 + 1) : 0;
+    ua0 = alpha ? ((xa >> P.lT) - P.k0) : 0;
+    const int64_t ua1 = alpha ? (((xa + alpha - 1) >> P.lT) - P.k0 + 1) : 0;
+    ub0 = beta ? ((xb >> P.lT) - P.k0) : 0;
+    const int64_t ub1 = beta ? (((xb + beta - 1) >> P.lT) - P.k0 + 1) : 0;
     npa = (int32_t)(ua1 - ua0);
     np = npa + (int32_t)(ub1 - ub0);
   }

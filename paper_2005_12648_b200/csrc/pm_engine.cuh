@@ -125,6 +125,7 @@ struct EngineParams {
   int64_t s, m, e;     // job, absolute element indices
   int64_t T;           // unit (slot) size, records
   int32_t mu;          // slots per region
+  int32_t lT, lmu;     // log2 T, log2 mu (both powers of two)
   int32_t nthreads;    // CTA size used by the launch
   int64_t M;           // region size = mu*T
   int64_t k0, K;       // first absolute slot, number of slots
