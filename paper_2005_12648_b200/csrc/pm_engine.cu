@@ -422,12 +422,16 @@ __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, 
   const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
   uint4* d4 = reinterpret_cast<uint4*>(dst + head);
   int64_t i = lane;
-  for (; i + 224 < nvec; i += 256) {
-    uint4 v[8];
+#ifndef PM_COPY_UNROLL
+#define PM_COPY_UNROLL 8
+#endif
+  constexpr int CU = PM_COPY_UNROLL;
+  for (; i + 32 * (CU - 1) < nvec; i += 32 * CU) {
+    uint4 v[CU];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcs(s4 + i + 32 * k);
+    for (int k = 0; k < CU; ++k) v[k] = __ldcs(s4 + i + 32 * k);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d4[i + 32 * k] = v[k];
+    for (int k = 0; k < CU; ++k) d4[i + 32 * k] = v[k];
   }
   for (; i < nvec; i += 32) d4[i] = __ldcs(s4 + i);
   const int64_t tail0 = head + (nvec << 4);
