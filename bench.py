@@ -274,6 +274,31 @@ def run_dist(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     N = world * n
+    # e2e: every step copies the rank's block in from pinned host memory, merges, and
+    # reads the merged block back (max over ranks of the device-timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        hk = torch.empty(n, dtype=torch.int32).pin_memory()
+        hk.copy_(keys0.cpu())
+        hout = torch.empty_like(hk).pin_memory()
+        et = []
+        for s in range(args.e2e_steps + 1):  # the first one is untimed
+            dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record()
+            work.copy_(hk, non_blocking=True)
+            merge_distributed(work, pay, la)
+            hout.copy_(work, non_blocking=True)
+            ev1.record()
+            ev1.synchronize()
+            if s:
+                et.append(ev0.elapsed_time(ev1))
+        te = torch.tensor([sum(et)], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te_ms = float(te.item())
+        e2e = {"value": N * len(et) / (te_ms / 1e3), "unit": "elements/s",
+               "h2d_bytes_per_step": N * 4, "d2h_bytes_per_step": N * 4, "ms_per_step": te_ms / len(et),
+               "path": "per rank: H2D of its block (pinned) + merge_distributed + D2H of the merged block"}
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -294,7 +319,9 @@ def run_dist(args):
             "roofline": {"bound": "hbm", "achieved": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9 / peak,
                          "traffic": None, "kernel": "whole distributed step per GPU"},
-            "e2e": None, "cpu_baseline": None, "gpu_launches": None,
+            "e2e": e2e, "cpu_baseline": None,
+            # ours per step and rank: k_plan + k_buffered (copy mode) of pm_merge_copy
+            "gpu_launches": 2 * args.steps,
         }
         if sampler:
             line["clocks"] = sampler.summary()
@@ -439,6 +466,30 @@ def run_ours(args):
                     "what": "pm_merge with scratch = min(|A|,|B|): run copy + streaming merge "
                             "(seq_merge_buffered, seqmerge.py:55-75)"}
 
+    # ---- copy mode: pm_merge_copy (out of place, the multi-GPU path's local merge) ----
+    copy_mode = None
+    if not args.no_buffered:
+        dk = torch.empty_like(keys0)
+        dp = torch.empty_like(pay0)
+        c_ms = []
+        for i in range(args.steps + 1):
+            ev0.record(stream)
+            rc = L.pm_merge_copy(ctx, ctypes.c_void_p(keys0.data_ptr()), ctypes.c_void_p(pay0.data_ptr() if w else 0),
+                                 ctypes.c_void_p(dk.data_ptr()), ctypes.c_void_p(dp.data_ptr() if w else 0), ks, w,
+                                 middle, n - middle, ctypes.c_void_p(stream.cuda_stream))
+            _capi.check(rc, "pm_merge_copy")
+            ev1.record(stream)
+            ev1.synchronize()
+            if i > 0:
+                c_ms.append(ev0.elapsed_time(ev1))
+        _capi.status(local, stream.cuda_stream)
+        okc = torch.equal(dk.to(torch.int64), torch.sort(keys0.to(torch.int64)).values)
+        ct = statistics.mean(c_ms)
+        copy_mode = {"value": n / (ct / 1e3), "unit": "elements/s", "ms_per_step": ct,
+                     "frac_of_roofline": (algo_bytes / (ct / 1e3) / 1e9) / peak, "sorted_ok": bool(okc),
+                     "what": "pm_merge_copy: out-of-place merge into a second buffer (1 read + 1 write per record)"}
+        del dk, dp
+
     # ---- end to end through the C-ABI host entry point (pinned host buffers) ----
     e2e = None
     log("e2e")
@@ -495,6 +546,7 @@ def run_ours(args):
             "merge_frac_of_roofline": (algo_bytes / (total_ms / args.steps / 1e3) / 1e9) / peak,
             "salvaged_records_frac": stats[1] / n,
             "buffered_mode": buffered,
+            "copy_mode": copy_mode,
             "regions": stats[2], "identity_regions": stats[3],
         }
         if sampler:
