@@ -27,6 +27,9 @@ __device__ __forceinline__ int64_t ld_acquire64(const int64_t* p) {
 __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// release/acquire fence at GPU scope (cheaper than __threadfence's sequentially
+// consistent fence; every use here publishes data before a flag or acquires after one)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
   int32_t v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

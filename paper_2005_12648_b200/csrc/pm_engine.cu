@@ -24,6 +24,10 @@ namespace pm {
 #ifndef PM_STATS
 #define PM_STATS 0
 #endif
+// timing ablations (tuning builds only; results are wrong)
+#ifndef PM_ABLATE
+#define PM_ABLATE 0  // bit 0: tile merge, 1: salvage copies, 2: gather loads, 3: output stores
+#endif
 
 
 // ============================================================================
@@ -82,7 +86,7 @@ __device__ __forceinline__ void stack_push(unsigned long long* top, int32_t* nex
   unsigned long long old = *(volatile unsigned long long*)top, nw;
   do {
     next[idx] = (int32_t)(uint32_t)(old & 0xFFFFFFFFull);
-    __threadfence();
+    fence_acq_rel_gpu();
     nw = (((old >> 32) + 1ull) << 32) | (uint32_t)idx;
     unsigned long long seen = atomicCAS(top, old, nw);
     if (seen == old) break;
@@ -98,7 +102,7 @@ __device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* n
     unsigned long long nw = (((old >> 32) + 1ull) << 32) | (uint32_t)nxt;
     unsigned long long seen = atomicCAS(top, old, nw);
     if (seen == old) {
-      __threadfence();
+      fence_acq_rel_gpu();
       return (int32_t)idx;
     }
     old = seen;
@@ -218,7 +222,7 @@ __device__ __forceinline__ int32_t warp_pop(unsigned long long* tops, int32_t* n
         const unsigned long long nw = (((old >> 32) + 1ull) << 32) | (uint32_t)nxt;
         const unsigned long long seen = atomicCAS(&tops[sh * kTopStride], old, nw);
         if (seen == old) {
-          __threadfence();
+          fence_acq_rel_gpu();
           v = (int32_t)idx;
           break;
         }
@@ -619,14 +623,15 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
   const int64_t sbase = g.slot_base(slot);
   const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
   char* kd = dest >= 0 ? P.keys + (dbase + (x0 - hb)) * ks : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * ks;
-  copy_g2g_warp(reinterpret_cast<uint8_t*>(kd), reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks),
-                (x1 - x0) * ks, lane);
+  if (!(PM_ABLATE & 2))
+    copy_g2g_warp(reinterpret_cast<uint8_t*>(kd), reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks),
+                  (x1 - x0) * ks, lane);
   if (w) {
     uint8_t* pd = dest >= 0 ? P.pay + (dbase + (x0 - hb)) * w : P.scr_pay + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * w;
     copy_g2g_warp(pd, P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w, lane);
   }
   if (!publish) return;  // the caller fences and publishes later (publish_pending)
-  __threadfence();  // every lane's part is visible before the new home is published
+  fence_acq_rel_gpu();  // every lane's part is visible before the new home is published
   __syncwarp();
   if (lane == 0) st_release(&P.loc[u], dest);
 }
@@ -962,7 +967,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
         }
         uint8_t* kdst = kin + (isA ? R.offA + (x0 - R.xa) * ks : R.offB + (x0 - R.xb) * ks);
-        copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+        if (!(PM_ABLATE & 4)) copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
         if (w) {
           uint8_t* pdst = pin + (isA ? R.poffA + (x0 - R.xa) * w : R.poffB + (x0 - R.xb) * w);
           copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
@@ -1020,7 +1025,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         pj = isA ? R.ua0 + gt : R.ub0 + (gt - R.npa);
         const int64_t run0 = isA ? R.xa : R.xb, run1 = isA ? R.xa + R.alpha : R.xb + R.beta;
         pn = (int32_t)(min(run1, g.slot_hi(pj)) - max(run0, g.slot_lo(pj)));
-        __threadfence();
+        fence_acq_rel_gpu();
         pold = atomicAdd(&P.reads[pj], pn);
       }
       if (P.mode == MODE_MERGE && !w) write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, gt, GT);
@@ -1039,7 +1044,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       const uint8_t* PA = pin + R.poffA;
       const uint8_t* PB = pin + R.poffB;
       const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-      merge_tile<KT>(P.mode, As, Bs, R.alpha, R.beta, R.nout, ko, po, PA, PB, w, wq4, gt, GT);
+      if (!(PM_ABLATE & 1)) merge_tile<KT>(P.mode, As, Bs, R.alpha, R.beta, R.nout, ko, po, PA, PB, w, wq4, gt, GT);
       fence_proxy_async_smem();  // our smem writes -> visible to the TMA (async proxy)
       PM_TICK(3);
       // ---- the input tile is free: start the next entry's gather now ----
@@ -1094,7 +1099,8 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       if (!vc.abort) {
         // stream the tile back in place: TMA bulk store for the 16-byte-aligned body,
         // generic stores for the unaligned head and tail bytes
-        stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), R.nout * ks, gt, GT);
+        if (!(PM_ABLATE & 8))
+          stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), R.nout * ks, gt, GT);
         if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, R.nout * w, gt, GT);
       }
       if (gt == 0) {
@@ -1354,7 +1360,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
         // copy mode: nothing to announce or wait for
       } else if (ctrl) {
         if (leader && !s_early[cur]) {
-          __threadfence();
+          fence_acq_rel_gpu();
           st_release(&flags[R.r], 1);
         }
         // the records this region overwrites in the unbuffered run must have been read
@@ -1379,7 +1385,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
             if (tk < P.Q && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
               const BufRegion Rk = buf_region<KT>(g, P, tk, buf_a, s_a[sk][0], s_a[sk][1]);
               if (!Rk.identity) {
-                __threadfence();
+                fence_acq_rel_gpu();
                 st_release(&flags[Rk.r], 1);
                 s_early[sk] = 1;
               }
