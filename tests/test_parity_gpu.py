@@ -330,3 +330,31 @@ def test_merge_host_vs_oracle(width):
         _ops.merge_host(kk, pp, lo, lo + middle, lo + size)
         assert np.array_equal(kk, want_k), f"keys size={size}"
         assert np.array_equal(pp, want_p), f"payload size={size}"
+
+
+@pytest.mark.parametrize("dtype,width", [(np.int32, 4), (np.int64, 12), (np.int32, 0)])
+def test_large_jobs_vs_oracle(dtype, width):
+    """2^22..2^24-record jobs (multi-level salvage, several waves of the grid) vs the oracle,
+    through every device path: in place (bounded pool), buffered, copy, host."""
+    import torch
+
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(31337 + width)
+    for size, split, domain in ((1 << 22, 0.5, 2**31 - 1), (3 << 22, 0.3, 1000), (1 << 24, 0.6, 2**31 - 1)):
+        keys, payload, middle = random_instance(rng, size, split, domain, width)
+        keys = keys.astype(dtype)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+        for mode in ("inplace", "buffered"):
+            arr = to_gpu(keys, payload)
+            _ops.merge(arr, 0, middle, size, scratch_records=(min(middle, size - middle) if mode == "buffered" else 0))
+            assert_same(arr, want_k, want_p, f"{mode} size={size}")
+        sk, sp = torch.from_numpy(keys).cuda(), torch.from_numpy(payload).cuda()
+        dk, dp = torch.empty_like(sk), torch.empty_like(sp)
+        _ops.merge_copy(sk, sp, dk, dp, middle)
+        pm.synchronize()
+        assert np.array_equal(dk.cpu().numpy(), want_k) and np.array_equal(dp.cpu().numpy(), want_p)
+        hk, hp = keys.copy(), payload.copy()
+        _ops.merge_host(hk, hp, 0, middle, size)
+        assert np.array_equal(hk, want_k) and np.array_equal(hp, want_p)
