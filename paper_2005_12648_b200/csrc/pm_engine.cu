@@ -246,12 +246,22 @@ __device__ __forceinline__ void cta_unlock(Ctl& c) {
   __threadfence_block();
   atomicExch(&c.lock, 0);
 }
-// push a freed slot (v >= 0) or scratch unit (v = -(i+1)); overflow goes global
+// Make slot v FREE on the global lists: a cached slot may still record its last
+// occupant `expect` (released without a round trip); it is handed over only if
+// it still holds that occupant (its region may have closed it meanwhile).
+__device__ __forceinline__ void release_slot_global(const EngineParams& P, int32_t v, int32_t expect, int home) {
+  if (expect != ST_FREE && atomicCAS(&P.state[v], expect, ST_FREE) != expect) return;
+  stack_push(&P.free_top[home * kTopStride], P.next_free, v);
+}
+// push a freed slot (v >= 0; state still `expect`) or scratch unit (v = -(i+1));
+// overflow goes global
 template <class Ctl>
-__device__ __forceinline__ void cache_push(Ctl& c, const EngineParams& P, int32_t v, int home) {
+__device__ __forceinline__ void cache_push(Ctl& c, const EngineParams& P, int32_t v, int home,
+                                           int32_t expect = ST_FREE) {
   cta_lock(c);
   bool done = false;
   if (v >= 0 && c.n_fs < kCache) {
+    c.fx[c.n_fs] = expect;
     c.fs[c.n_fs++] = v;
     done = true;
   } else if (v < 0 && c.n_sc < kCache) {
@@ -260,7 +270,7 @@ __device__ __forceinline__ void cache_push(Ctl& c, const EngineParams& P, int32_
   }
   cta_unlock(c);
   if (!done) {
-    if (v >= 0) stack_push(&P.free_top[home * kTopStride], P.next_free, v);
+    if (v >= 0) release_slot_global(P, v, expect, home);
     else stack_push(&P.scr_top[home * kTopStride], P.next_scr, -v - 1);
   }
 }
@@ -271,11 +281,14 @@ __device__ __forceinline__ void cache_flush(Ctl& c, const EngineParams& P, int h
   const int nf = c.n_fs, ns = c.n_sc;
   c.n_fs = 0;
   c.n_sc = 0;
-  int32_t fs[kCache], sc[kCache];
-  for (int i = 0; i < nf; ++i) fs[i] = c.fs[i];
+  int32_t fs[kCache], fx[kCache], sc[kCache];
+  for (int i = 0; i < nf; ++i) {
+    fs[i] = c.fs[i];
+    fx[i] = c.fx[i];
+  }
   for (int i = 0; i < ns; ++i) sc[i] = c.sc[i];
   cta_unlock(c);
-  for (int i = 0; i < nf; ++i) stack_push(&P.free_top[home * kTopStride], P.next_free, fs[i]);
+  for (int i = 0; i < nf; ++i) release_slot_global(P, fs[i], fx[i], home);
   for (int i = 0; i < ns; ++i) stack_push(&P.scr_top[home * kTopStride], P.next_scr, sc[i]);
 }
 
@@ -295,7 +308,9 @@ __device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, i
   bool flagged = false;
   int32_t dest = INT32_MIN;
   const Geo g(P);
-  auto usable = [&](int32_t f) { return g.order(g.region_of_slot(f)) > t && atomicCAS(&P.state[f], ST_FREE, u) == ST_FREE; };
+  auto usable = [&](int32_t f, int32_t x) {
+    return g.order(g.region_of_slot(f)) > t && atomicCAS(&P.state[f], x, u) == x;
+  };
   for (uint32_t it = 0;; ++it) {
     // scratch first (cache, then the global lists): a unit parked in scratch is
     // final, one parked in a free slot moves again when that slot's region starts
@@ -325,8 +340,9 @@ __device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, i
       cta_lock(c);
       int32_t f = -1;
       while (c.n_fs > 0) {
-        f = c.fs[--c.n_fs];
-        if (usable(f)) break;
+        --c.n_fs;
+        f = c.fs[c.n_fs];
+        if (usable(f, c.fx[c.n_fs])) break;
         f = -1;  // its region started meanwhile (or precedes t)
       }
       cta_unlock(c);
@@ -344,7 +360,7 @@ __device__ __forceinline__ int32_t acquire_dest(Ctl& c, const EngineParams& P, i
     bool got = false;
     while ((f = warp_pop(P.free_top, P.next_free, home, lane)) >= 0) {
       int ok = 0;
-      if (lane == 0) ok = usable(f);
+      if (lane == 0) ok = usable(f, ST_FREE);
       if (__shfl_sync(0xffffffffu, ok, 0)) {
         got = true;
         break;
@@ -673,6 +689,7 @@ struct EngCtl {
   int32_t n_fs, n_sc;
   int32_t abort;
   int32_t fs[kCache];
+  int32_t fx[kCache];   // the occupant fs[i] still records (ST_FREE once released)
   int32_t sc[kCache];
 };
 
@@ -932,7 +949,12 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     };
     // wait until every piece sits where nobody moves it before it is read, then
     // issue its TMA bulk load (thread per piece) and arm the barrier
-    auto gather_issue = [&](const DataRegion& R) {
+    // returns the location this thread read its first piece from (INT32_MIN: none):
+    // if this region turns out to be the unit's last reader, the unit is still
+    // there (nobody moves a unit without a later consumer), so it is released
+    // without another round trip
+    auto gather_issue = [&](const DataRegion& R) -> int32_t {
+      int32_t mine = INT32_MIN;
       for (int p = gt; p < R.np; p += GT) {
         const bool isA = p < R.npa;
         const int64_t j = isA ? R.ua0 + p : R.ub0 + (p - R.npa);
@@ -972,17 +994,20 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           uint8_t* pdst = pin + (isA ? R.poffA + (x0 - R.xa) * w : R.poffB + (x0 - R.xb) * w);
           copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
         }
+        if (p == gt) mine = l;
       }
       named_barrier_sync(1, GT);  // every expect_tx registered before the single arrive
       if (gt == 0) mbar_arrive(&ctl.bar);
+      return mine;
     };
 
     DataRegion R;
     int32_t e = 0;
     open_and_describe(0, R);
     bool pending = false;  // a gather is in flight on ctl.bar
+    int32_t gl = INT32_MIN;  // where this thread read its piece of the current region
     if (R.t < P.Q && !R.identity && !vc.abort) {
-      gather_issue(R);
+      gl = gather_issue(R);
       pending = true;
     }
     while (true) {
@@ -1002,8 +1027,9 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           vc.d_done = e + 1;
         }
         open_and_describe(e + 1, Rn);
+        gl = INT32_MIN;
         if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
-          gather_issue(Rn);
+          gl = gather_issue(Rn);
           pending = true;
         }
         R = Rn;
@@ -1050,18 +1076,20 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       // ---- the input tile is free: start the next entry's gather now ----
       open_and_describe(e + 1, Rn);  // (its barrier also ends every thread's merge)
       PM_TICK(1);
+      int32_t gl_next = INT32_MIN;
       if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
-        gather_issue(Rn);
+        gl_next = gather_issue(Rn);
         pending = true;
       }
       PM_TICK(0);
       if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
-        // last reader: free the unit's location into the CTA cache
-        const int32_t l = ld_acquire(&P.loc[pj]);
+        // last reader: release the unit's location into the CTA cache (a slot keeps
+        // recording pj until a salvage worker claims it: no round trip here)
+        const int32_t l = gl;
         if (l < 0) {
           cache_push(ctl, P, l, home);
-        } else if (g.slot_full(l) && atomicCAS(&P.state[l], (int32_t)pj, ST_FREE) == (int32_t)pj) {
-          cache_push(ctl, P, l, home);
+        } else if (g.slot_full(l)) {
+          cache_push(ctl, P, l, home, (int32_t)pj);
         }
       }
       open_ahead(e + 2);
@@ -1110,6 +1138,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       }
       PM_TICK(5);
       R = Rn;
+      gl = gl_next;
       ++e;
     }
     if (gt == 0) {
