@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     };
     // open entries up to e ahead of need (thread gt == 0, while the team waits anyway)
     auto open_ahead = [&](int32_t e) {
-      if (gt == 0 && vc.filled <= e && !vc.abort) {
+      if (gt == 0 && vc.filled <= e && e - vc.d_done < kRing && !vc.abort) {
         claim_lock(ctl);
         while (vc.filled <= e && vc.filled - vc.d_done < kRing) {
           const int32_t f = vc.filled;
