@@ -953,15 +953,23 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     // if this region turns out to be the unit's last reader, the unit is still
     // there (nobody moves a unit without a later consumer), so it is released
     // without another round trip
-    auto gather_issue = [&](const DataRegion& R) -> int32_t {
+    // pl: this thread's piece location loaded (relaxed) one merge earlier, or
+    // INT32_MIN.  A location of order >= t (or scratch) seen then is still safe to
+    // read: the unit only moves up, and its old slot is not overwritten before
+    // this region's read is counted.
+    auto gather_issue = [&](const DataRegion& R, int32_t pl) -> int32_t {
       int32_t mine = INT32_MIN;
       for (int p = gt; p < R.np; p += GT) {
         const bool isA = p < R.npa;
         const int64_t j = isA ? R.ua0 + p : R.ub0 + (p - R.npa);
         const int64_t run0 = isA ? R.xa : R.xb, run1 = isA ? R.xa + R.alpha : R.xb + R.beta;
         const int64_t x0 = max(run0, g.slot_lo(j)), x1 = min(run1, g.slot_hi(j));
-        int32_t l;
+        int32_t l = p == gt ? pl : INT32_MIN;
         for (uint32_t it = 0;; ++it) {
+          if (l != INT32_MIN && (l < 0 || g.order(g.region_of_slot(l)) >= R.t)) {
+            fence_acq_rel_gpu();  // (the prefetch was relaxed: acquire the unit's data)
+            break;
+          }
           l = ld_acquire(&P.loc[j]);
           if (l < 0 || g.order(g.region_of_slot(l)) >= R.t) break;
           if ((it & 255) == 255 && ld_relaxed(P.err)) {
@@ -1007,7 +1015,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     bool pending = false;  // a gather is in flight on ctl.bar
     int32_t gl = INT32_MIN;  // where this thread read its piece of the current region
     if (R.t < P.Q && !R.identity && !vc.abort) {
-      gl = gather_issue(R);
+      gl = gather_issue(R, INT32_MIN);
       pending = true;
     }
     while (true) {
@@ -1029,7 +1037,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         open_and_describe(e + 1, Rn);
         gl = INT32_MIN;
         if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
-          gl = gather_issue(Rn);
+          gl = gather_issue(Rn, INT32_MIN);
           pending = true;
         }
         R = Rn;
@@ -1042,6 +1050,17 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       phase ^= 1;
       pending = false;
       PM_TICK(1);
+      // prefetch (relaxed) the locations of the next entry's pieces for its gather
+      int32_t pl = INT32_MIN;
+      if (vc.filled > e + 1) {
+        __threadfence_block();
+        const TInfo& tn = ctl.ring[(e + 1) % kRing].ti;
+        if (tn.t < P.Q) {
+          DataRegion Rp;
+          Rp.init(g, P, tn, la);
+          if (!Rp.identity && gt < Rp.np) pl = ld_relaxed(&P.loc[gt < Rp.npa ? Rp.ua0 + gt : Rp.ub0 + (gt - Rp.npa)]);
+        }
+      }
       // publish the reads (one piece per thread; np <= GT): the atomics stay in
       // flight during the merge, deaths are handled after it
       int64_t pj = -1;
@@ -1078,7 +1097,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       PM_TICK(1);
       int32_t gl_next = INT32_MIN;
       if (Rn.t < P.Q && !Rn.identity && !vc.abort) {
-        gl_next = gather_issue(Rn);
+        gl_next = gather_issue(Rn, pl);
         pending = true;
       }
       PM_TICK(0);
