@@ -1101,6 +1101,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         pending = true;
       }
       PM_TICK(0);
+      const long long q0 = prof.now();
       if (pj >= 0 && pold + pn == (int32_t)(g.slot_hi(pj) - g.slot_lo(pj))) {
         // last reader: release the unit's location into the CTA cache (a slot keeps
         // recording pj until a salvage worker claims it: no round trip here)
@@ -1111,7 +1112,9 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           cache_push(ctl, P, l, home, (int32_t)pj);
         }
       }
+      const long long q1 = prof.now();
       open_ahead(e + 2);
+      const long long q2 = prof.now();
       // ---- every slot of the region must be cleared before the tile lands there:
       //      all slot items are done, and every consumer of order <= t has read
       //      each occupant (t's own reads are published by now) ----
@@ -1119,6 +1122,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         while (vc.ring[e % kRing].items_done < re.nslot && !vc.abort) {
         }
       named_barrier_sync(1, GT);
+      const long long q3 = prof.now();
       if (gt < re.nslot) {
         const int32_t u = re.occ[gt];
         if (u >= 0) {
@@ -1142,6 +1146,15 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         }
       }
       named_barrier_sync(1, GT);
+#if PM_STATS
+      if (gt == 0) {  // stats[24..27]: free, open-ahead, items wait, consumer wait
+        const long long q4 = prof.now();
+        atomicAdd(&P.stats[24], (unsigned long long)(q1 - q0));
+        atomicAdd(&P.stats[25], (unsigned long long)(q2 - q1));
+        atomicAdd(&P.stats[26], (unsigned long long)(q3 - q2));
+        atomicAdd(&P.stats[27], (unsigned long long)(q4 - q3));
+      }
+#endif
       PM_TICK(4);
       if (!vc.abort) {
         // stream the tile back in place: TMA bulk store for the 16-byte-aligned body,
