@@ -142,11 +142,14 @@ __global__ void k_plan(EngineParams P) {
     P.loc[j] = (int32_t)j;
     P.reads[j] = 0;
   }
-  // scratch unit i starts on shard i % kShards
-  for (int64_t i = tid; i < P.S; i += nthr) P.next_scr[i] = (i + kShards < P.S) ? (int32_t)(i + kShards) : (int32_t)kEmpty32;
+  // scratch units [0, G) start in the engine CTAs' caches (s_per each, k_engine);
+  // unit i >= G starts on shard (i - G) % kShards
+  const int64_t G = (int64_t)P.grid * P.s_per;
+  for (int64_t i = G + tid; i < P.S; i += nthr)
+    P.next_scr[i] = (i + kShards < P.S) ? (int32_t)(i + kShards) : (int32_t)kEmpty32;
   for (int64_t sh = tid; sh < kShards; sh += nthr) {
     P.free_top[sh * kTopStride] = (unsigned long long)kEmpty32;
-    P.scr_top[sh * kTopStride] = sh < P.S ? (unsigned long long)sh : (unsigned long long)kEmpty32;
+    P.scr_top[sh * kTopStride] = G + sh < P.S ? (unsigned long long)(G + sh) : (unsigned long long)kEmpty32;
   }
   if (tid == 0) {
     *P.scr_count = (int32_t)P.S;
@@ -790,6 +793,9 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     ctl.cur_e = 0;
     ctl.cur_i = 0;
     ctl.next_t = atomicAdd(P.ticket, 1);
+    // this CTA's share of the scratch pool starts in its cache (k_plan)
+    ctl.n_sc = (int32_t)P.s_per;
+    for (int32_t k = 0; k < (int32_t)P.s_per; ++k) ctl.sc[k] = (int32_t)(blockIdx.x * P.s_per + k);
   }
   __syncthreads();
   volatile EngCtl& vc = ctl;
