@@ -167,7 +167,10 @@ __global__ void k_plan(EngineParams P) {
 // k_engine
 // ============================================================================
 
-constexpr int kCache = 64;   // CTA-local caches of free slots / free scratch units
+#ifndef PM_CACHE
+#define PM_CACHE 64
+#endif
+constexpr int kCache = PM_CACHE;  // CTA-local caches of free slots / free scratch units
 
 // Splits a ticket's salvage and data phases need, loaded once (one round trip of
 // independent loads) an iteration ahead: region q = region_of_ticket(t) has
@@ -1076,7 +1079,8 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         pj = isA ? R.ua0 + gt : R.ub0 + (gt - R.npa);
         const int64_t run0 = isA ? R.xa : R.xb, run1 = isA ? R.xa + R.alpha : R.xb + R.beta;
         pn = (int32_t)(min(run1, g.slot_hi(pj)) - max(run0, g.slot_lo(pj)));
-        fence_acq_rel_gpu();
+        // (no fence: the bulk loads have completed -- the mbarrier said so -- so a
+        // writer that sees this count cannot change what this region read)
         pold = atomicAdd(&P.reads[pj], pn);
       }
       if (P.mode == MODE_MERGE && !w) write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, gt, GT);
