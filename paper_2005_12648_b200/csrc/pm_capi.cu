@@ -47,7 +47,6 @@ struct Ctl {
   unsigned long long free_top;
   unsigned long long scr_top;
   unsigned long long stats[64];  // [0,16): pm_status; [16,64): tuning histograms (PM_STATS builds)
-  Line32 scr_count_;
   Line32 ticket_;
   Line32 err_;
   Line32 noop_;
@@ -139,7 +138,6 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   if ((1ll << P.lT) != T || (1 << P.lmu) != mu) return fail(PM_ERR_INTERNAL, "unit geometry must be powers of two");
   P.mu = mu;
   if (mu > 8) return fail(PM_ERR_INTERNAL, "too many slots per region");
-  P.nthreads = kEngineThreads;
   P.M = M;
   P.k0 = s / T;
   P.K = (e - 1) / T - P.k0 + 1;
@@ -176,7 +174,6 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   S = std::min<int64_t>(S, P.K + P.reserve);
   P.S = S;
   P.grid = grid;
-  P.look = std::max<int64_t>(64, 2 * (int64_t)grid);
   // half of the pool starts in the CTAs' caches (<= 32 each, the cache holds 64)
   P.s_per = buffered ? 0 : std::min<int64_t>(S / (2 * (int64_t)grid), 32);
   // workspace
@@ -203,7 +200,6 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.free_top = reinterpret_cast<unsigned long long*>(ws + off_tops);  // [64] shard tops
   P.scr_top = P.free_top + kShards * kTopStride;
   P.stats = ctx->ctl->stats;
-  P.scr_count = &ctx->ctl->scr_count_.v;
   P.ticket = &ctx->ctl->ticket_.v;
   P.err = &ctx->ctl->err_.v;
   P.noop = &ctx->ctl->noop_.v;

@@ -152,7 +152,6 @@ __global__ void k_plan(EngineParams P) {
     P.scr_top[sh * kTopStride] = G + sh < P.S ? (unsigned long long)(G + sh) : (unsigned long long)kEmpty32;
   }
   if (tid == 0) {
-    *P.scr_count = (int32_t)P.S;
     *P.ticket = 0;
     bool nothing = (la == 0 || lb == 0);
     if (P.out_keys) nothing = false;  // out of place: every record still moves

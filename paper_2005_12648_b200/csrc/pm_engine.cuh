@@ -126,7 +126,6 @@ struct EngineParams {
   int64_t T;           // unit (slot) size, records
   int32_t mu;          // slots per region
   int32_t lT, lmu;     // log2 T, log2 mu (both powers of two)
-  int32_t nthreads;    // CTA size used by the launch
   int64_t M;           // region size = mu*T
   int64_t k0, K;       // first absolute slot, number of slots
   int64_t R0, Q;       // first absolute region, number of regions
@@ -139,12 +138,10 @@ struct EngineParams {
   int32_t* next_scr;   // [S] scratch stack links
   unsigned long long* free_top;  // tagged stack tops (tag<<32 | index)
   unsigned long long* scr_top;
-  int32_t* scr_count;  // free scratch units (heuristic only)
   int64_t S;           // scratch units
   int32_t grid;        // engine CTAs
-  int64_t look;        // split lookahead distance in tickets (merge mode)
-  int64_t s_per;
-  int64_t reserve;     // keep this many scratch units for the no-free-slot case
+  int64_t s_per;       // scratch units each engine CTA starts with in its cache
+  int64_t reserve;     // minimum pool: units the CTAs may hold moved-but-unread at once
   char* scr_keys;      // phase-matched scratch bases
   uint8_t* scr_pay;
   int32_t* ticket;
