@@ -523,17 +523,22 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
       int32_t i = lo, jb = o - lo;
       const int32_t amax = al > 0 ? al - 1 : 0, bmax = bl > 0 ? bl - 1 : 0;
       KT va = As[min(i, amax)], vb = Bs[min(jb, bmax)];
-      if (!w) {
-        // branch-free: both candidates are reloaded every step (two independent LDS per
-        // element instead of the warp diverging on every element)
+      // with payload (stability visible): bound-checked, branch-free steps -- the
+      // taken record's payload row is copied, then only the taken side reloads
+      if (wq4 && w == 4) {
+        const uint32_t* pa = reinterpret_cast<const uint32_t*>(PA);
+        const uint32_t* pb = reinterpret_cast<const uint32_t*>(PB);
+        uint32_t* pd = reinterpret_cast<uint32_t*>(po);
 #pragma unroll 4
         for (; o < oe; ++o) {
           const bool takeA = (jb >= bl) | ((i < al) & (va <= vb));
           ko[o] = takeA ? va : vb;
+          pd[o] = *(takeA ? pa + i : pb + jb);
           i += takeA;
           jb += !takeA;
-          va = As[min(i, amax)];
-          vb = Bs[min(jb, bmax)];
+          const KT v = *(takeA ? As + min(i, amax) : Bs + min(jb, bmax));
+          va = takeA ? v : va;
+          vb = takeA ? vb : v;
         }
       } else {
         for (; o < oe; ++o) {
@@ -547,13 +552,11 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
           } else {
             for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
           }
-          if (takeA) {
-            ++i;
-            va = As[min(i, amax)];
-          } else {
-            ++jb;
-            vb = Bs[min(jb, bmax)];
-          }
+          i += takeA;
+          jb += !takeA;
+          const KT v = *(takeA ? As + min(i, amax) : Bs + min(jb, bmax));
+          va = takeA ? v : va;
+          vb = takeA ? vb : v;
         }
       }
     } else {  // rotation: B piece then A piece
