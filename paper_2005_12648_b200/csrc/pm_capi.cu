@@ -183,7 +183,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   const size_t off_nf = off_reads + (size_t)align_up(P.K * 4, 256);
   const size_t off_ns = off_nf + (size_t)align_up(P.K * 4, 256);
   const size_t off_tops = off_ns + (size_t)align_up(S * 4, 256);
-  const size_t ws_need = off_tops + 2 * kShards * kTopStride * sizeof(unsigned long long);
+  const size_t off_tlist = off_tops + 2 * kShards * kTopStride * sizeof(unsigned long long);
+  const size_t ws_need = off_tlist + (size_t)align_up((2 * P.Q + 16) * 4 + 16, 256);  // list | flags | count
   int rc = ensure(&ctx->ws, &ctx->ws_bytes, ws_need);
   if (rc) return rc;
   const size_t scr_k = (size_t)align_up(S * T * ks + 32, 256);
@@ -198,6 +199,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.next_free = reinterpret_cast<int32_t*>(ws + off_nf);
   P.next_scr = reinterpret_cast<int32_t*>(ws + off_ns);
   P.free_top = reinterpret_cast<unsigned long long*>(ws + off_tops);  // [64] shard tops
+  P.tlist = buffered ? nullptr : reinterpret_cast<int32_t*>(ws + off_tlist);  // engine tickets (k_compact)
+  P.ntick = buffered ? nullptr : P.tlist + 2 * P.Q + 12;
   P.scr_top = P.free_top + kShards * kTopStride;
   P.stats = ctx->ctl->stats;
   P.ticket = &ctx->ctl->ticket_.v;

@@ -24,6 +24,9 @@ namespace pm {
 #ifndef PM_STATS
 #define PM_STATS 0
 #endif
+#ifndef PM_TLIST
+#define PM_TLIST 1  // tune: engine tickets skip identity regions
+#endif
 // timing ablations (tuning builds only; results are wrong)
 #ifndef PM_ABLATE
 #define PM_ABLATE 0  // bit 0: tile merge, 1: salvage copies, 2: gather loads, 3: output stores
@@ -158,6 +161,7 @@ __global__ void k_plan(EngineParams P) {
     else if (!nothing && P.mode == MODE_MERGE) nothing = keys[P.m - 1] <= keys[P.m];  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
     *P.need_space = 0;
+    if (P.ntick) P.ntick[1] = 0;  // identity regions (k_flags)
     for (int i = 0; i < 64; ++i) P.stats[i] = 0;
   }
 }
@@ -699,6 +703,7 @@ struct EngCtl {
   int32_t fs[kCache];
   int32_t fx[kCache];   // the occupant fs[i] still records (ST_FREE once released)
   int32_t sc[kCache];
+  int32_t ntick;        // tickets with work (k_compact; kept last: the layout above is register-sensitive)
 };
 
 // The data team's view of one region: its input pieces and staging offsets.
@@ -736,6 +741,13 @@ struct DataRegion {
   }
 };
 
+// Tickets with work are tlist[k] for k = 0, 1, ... (identity regions -- inputs
+// already on their outputs -- never get one); Q marks the end.
+__device__ __forceinline__ int32_t resolve_ticket(const EngineParams& P, int32_t k, int32_t ntick) {
+  if (ntick == P.Q) return k < ntick ? k : (int32_t)P.Q;  // nothing left out: the identity map
+  return k < ntick ? __ldg(&P.tlist[k]) : (int32_t)P.Q;
+}
+
 // Fill ring entry e with the prefetched ticket (caller holds the claim lock and
 // has checked that the entry is free: e - d_done < kRing).
 __device__ __forceinline__ void open_entry(EngCtl& c, const Geo& g, const EngineParams& P, int32_t e) {
@@ -746,7 +758,8 @@ __device__ __forceinline__ void open_entry(EngCtl& c, const Geo& g, const Engine
     load_tinfo(g, t, re.ti);
     const int64_t q = g.region_of_ticket(t);
     re.nslot = (int32_t)(g.region_end_slot(q) - g.region_first_slot(q));
-    vc.next_t = atomicAdd(P.ticket, 1);
+    vc.next_t = resolve_ticket(P, atomicAdd(P.ticket, 1), vc.ntick);  // (a load only if tickets were left out)
+
   } else {
     re.ti.t = P.Q;
     re.nslot = 0;
@@ -797,7 +810,8 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
     ctl.d_done = 0;
     ctl.cur_e = 0;
     ctl.cur_i = 0;
-    ctl.next_t = atomicAdd(P.ticket, 1);
+    ctl.ntick = PM_TLIST ? *P.ntick : (int32_t)P.Q;
+    ctl.next_t = resolve_ticket(P, atomicAdd(P.ticket, 1), ctl.ntick);
     // this CTA's share of the scratch pool starts in its cache (k_plan)
     ctl.n_sc = (int32_t)P.s_per;
     for (int32_t k = 0; k < (int32_t)P.s_per; ++k) ctl.sc[k] = (int32_t)(blockIdx.x * P.s_per + k);
@@ -1502,10 +1516,73 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
 #undef OUTB
 }
 
+// The engine's ticket list: every ticket (two-front order) whose region is not an
+// identity region, in order.  k_flags marks them (grid-wide, into tlist), then
+// one CTA compacts: per-thread chunk counts, a block scan, chunk writes.
+__global__ void __launch_bounds__(256) k_flags(EngineParams P) {
+  Geo g(P);
+  const int64_t la = g.LA();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P.Q; t += (int64_t)gridDim.x * blockDim.x) {
+    bool work = true;
+    if (P.mode == MODE_MERGE) {
+      const int64_t q = g.region_of_ticket(t);
+      const int64_t d0 = g.diag(q), d1 = g.diag(q + 1), a0 = g.split(q), a1 = g.split(q + 1);
+      work = !((a0 == d0 && a1 == d1) || (a0 == la && a1 == la));
+    }
+    P.tlist[P.Q + 8 + t] = work ? 1 : 0;  // flags live after the list
+    const unsigned idle = __ballot_sync(__activemask(), !work);
+    if (idle && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(&P.ntick[1], __popc(idle));
+  }
+}
+__global__ void __launch_bounds__(1024) k_compact(EngineParams P) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int32_t* flag = P.tlist + P.Q + 8;
+  if (*(volatile int32_t*)&P.ntick[1] == 0) {  // no identity region: tickets map to themselves
+    if (tid == 0) P.ntick[0] = (int32_t)P.Q;
+    return;
+  }
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < P.Q; t0 += blockDim.x) {  // coalesced tiles, running offset
+    const int64_t t = t0 + tid;
+    const int32_t f = t < P.Q ? flag[t] : 0;
+    int32_t x = f;  // warp inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int32_t s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      if (lane < nw) wsum[lane] = s;  // inclusive warp prefix sums
+    }
+    __syncthreads();
+    const int32_t pos = base + (wid ? wsum[wid - 1] : 0) + x - f;
+    if (f) P.tlist[pos] = (int32_t)t;
+    __syncthreads();
+    if (tid == 0) base += wsum[nw - 1];
+    __syncthreads();
+  }
+  if (tid == 0) *P.ntick = base;
+}
+
 // ---- host launchers (called from pm_capi.cu) --------------------------------
 template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
   k_plan<KT><<<grid, 256, 0, st>>>(P);
+  if (P.tlist && PM_TLIST) {
+    k_flags<<<(int)std::min<int64_t>((P.Q + 255) / 256, 1184), 256, 0, st>>>(P);
+    k_compact<<<1, 1024, 0, st>>>(P);
+  }
   return cudaGetLastError();
 }
 template <typename KT>

@@ -134,6 +134,8 @@ struct EngineParams {
   int32_t* state;      // [K] slot state: occupant unit, ST_FREE or ST_CLOSED
   int32_t* loc;        // [K] unit location: slot index or -(scratch index + 1)
   int32_t* reads;      // [K] records of the unit already gathered by consumers
+  int32_t* tlist;      // engine: [Q] the tickets with work (identity regions left out), k_compact
+  int32_t* ntick;      // engine: number of entries in tlist
   int32_t* next_free;  // [K] free-slot stack links
   int32_t* next_scr;   // [S] scratch stack links
   unsigned long long* free_top;  // tagged stack tops (tag<<32 | index)
