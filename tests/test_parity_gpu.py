@@ -358,3 +358,26 @@ def test_large_jobs_vs_oracle(dtype, width):
         hk, hp = keys.copy(), payload.copy()
         _ops.merge_host(hk, hp, 0, middle, size)
         assert np.array_equal(hk, want_k) and np.array_equal(hp, want_p)
+
+
+@pytest.mark.parametrize("width", [16, 32, 64, 100])
+def test_wide_payload_rows(width):
+    """Wide payload rows shrink the tiles (pick_tiles); every device path stays exact."""
+    import torch
+
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(777 + width)
+    for size, split, domain in ((5000, 0.5, 50), (300_000, 0.35, 2**31 - 1)):
+        keys, payload, middle = random_instance(rng, size, split, domain, width)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+        for scratch in (0, min(middle, size - middle)):
+            arr = to_gpu(keys, payload)
+            _ops.merge(arr, 0, middle, size, scratch_records=scratch)
+            assert_same(arr, want_k, want_p, f"w={width} size={size} scratch={scratch}")
+        sk, sp = torch.from_numpy(keys).cuda(), torch.from_numpy(payload).cuda()
+        dk, dp = torch.empty_like(sk), torch.empty_like(sp)
+        _ops.merge_copy(sk, sp, dk, dp, middle)
+        pm.synchronize()
+        assert np.array_equal(dk.cpu().numpy(), want_k) and np.array_equal(dp.cpu().numpy(), want_p)
