@@ -97,7 +97,10 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
   while (m > 16 && m * 2 * (ks + w) + 256 > budget) m >>= 1;
   if (m * 2 * (ks + w) + 256 > budget + 64 * 1024) return false;  // records too wide
   *M = m;
-  *T = std::max<int64_t>(16, m / 4);
+#ifndef PM_MU
+#define PM_MU 1
+#endif
+  *T = std::max<int64_t>(16, m / PM_MU);
   *mu = (int32_t)(m / *T);
   return true;
 }

@@ -24,6 +24,9 @@ namespace pm {
 #ifndef PM_STATS
 #define PM_STATS 0
 #endif
+#ifndef PM_PREFETCH_MOVE
+#define PM_PREFETCH_MOVE 0
+#endif
 #ifndef PM_TLIST
 #define PM_TLIST 1  // tune: engine tickets skip identity regions
 #endif
@@ -651,6 +654,13 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
   const int64_t sbase = g.slot_base(slot);
   const int64_t dbase = dest >= 0 ? g.slot_base(dest) : 0;
   char* kd = dest >= 0 ? P.keys + (dbase + (x0 - hb)) * ks : P.scr_keys + ((-(int64_t)dest - 1) * P.T + (x0 - hb)) * ks;
+#if PM_PREFETCH_MOVE
+  // pull the whole unit toward L2 at once: the warp's batched loads then mostly hit L2
+  if (lane == 0) {
+    prefetch_l2(P.keys + (sbase + (x0 - hb)) * ks, (x1 - x0) * ks);
+    if (w) prefetch_l2(P.pay + (sbase + (x0 - hb)) * w, (x1 - x0) * w);
+  }
+#endif
   if (!(PM_ABLATE & 2))
     copy_g2g_warp(reinterpret_cast<uint8_t*>(kd), reinterpret_cast<const uint8_t*>(P.keys + (sbase + (x0 - hb)) * ks),
                   (x1 - x0) * ks, lane);

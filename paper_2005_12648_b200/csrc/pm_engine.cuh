@@ -69,7 +69,7 @@ constexpr int kShards = 64;
 constexpr int kTopStride = 32;  // unsigned long long words between shard tops
 // tickets a k_engine CTA holds at once (its salvage workers run ahead of its data team)
 #ifndef PM_RING
-#define PM_RING 2
+#define PM_RING 4
 #endif
 constexpr int kRing = PM_RING;
 

@@ -13,7 +13,8 @@ from oracle import oracle as orc
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("inflight", [1, 3, 12])
-def test_model_merge_matches_oracle(seed, inflight):
+@pytest.mark.parametrize("mu", [1, 4])
+def test_model_merge_matches_oracle(seed, inflight, mu):
     rng = np.random.default_rng(seed)
     size = int(rng.integers(200, 3000))
     split = float(rng.choice([0.1, 0.5, 0.9, rng.random()]))
@@ -24,7 +25,7 @@ def test_model_merge_matches_oracle(seed, inflight):
     pp = np.concatenate([np.zeros((lo, 2), np.uint8), payload, np.ones((7, 2), np.uint8)])
     want_k, want_p = kk.copy(), pp.copy()
     orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
-    T, mu = 16, 4
+    T = 64 // mu
     scratch = inflight * (mu + 4) + 16  # the device's O(grid * tile) pool rule
     m = EngineModel(kk.copy(), pp.copy(), lo, lo + middle, lo + size, T, mu, scratch)
     m.run(inflight, random.Random(seed * 31 + inflight))
