@@ -29,10 +29,10 @@ constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 // kEngineMinBlocks resident CTAs per SM, staging tiles sized to kTileBudget bytes
 // of shared memory per CTA.
 #ifndef PM_ENGINE_TEAM
-#define PM_ENGINE_TEAM 4
+#define PM_ENGINE_TEAM 2
 #endif
 #ifndef PM_DATA_WARPS
-#define PM_DATA_WARPS PM_ENGINE_TEAM
+#define PM_DATA_WARPS 6
 #endif
 #ifndef PM_ENGINE_MINB
 #define PM_ENGINE_MINB 3
@@ -69,9 +69,10 @@ constexpr int kShards = 64;
 constexpr int kTopStride = 32;  // unsigned long long words between shard tops
 // tickets a k_engine CTA holds at once (its salvage workers run ahead of its data team)
 #ifndef PM_RING
-#define PM_RING 4
+#define PM_RING 2
 #endif
 constexpr int kRing = PM_RING;
+static_assert(kRing >= 2, "the data team opens the next entry before finishing the current one");
 
 // Two-front ticket order around the centre region qc (regions 0..Q-1): ticket 0
 // is qc, then qc-1, qc+1, qc-2, qc+2, ... until one side runs out, then the
