@@ -24,6 +24,9 @@ namespace pm {
 #ifndef PM_STATS
 #define PM_STATS 0
 #endif
+#ifndef PM_PREFETCH_ITEM
+#define PM_PREFETCH_ITEM 1
+#endif
 #ifndef PM_PREFETCH_MOVE
 #define PM_PREFETCH_MOVE 0
 #endif
@@ -909,6 +912,13 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           int64_t cwl, cwr;
           g.window(t, cwl, cwr);
           alive = g.consumed_in(u, cwl, cwr, re.ti.clo, re.ti.chi) < g.slot_hi(u) - g.slot_lo(u) && !vc.abort;
+#if PM_PREFETCH_ITEM
+          if (alive) {  // the copy comes after the destination search: warm L2 now
+            const int64_t ux0 = g.slot_lo(u), src = g.slot_base(slot) + (ux0 - g.slot_base(u));
+            prefetch_l2(P.keys + src * (int64_t)sizeof(KT), (g.slot_hi(u) - ux0) * (int64_t)sizeof(KT));
+            if (w) prefetch_l2(P.pay + src * w, (g.slot_hi(u) - ux0) * w);
+          }
+#endif
         }
         alive = __shfl_sync(0xffffffffu, alive, 0);
         const long long c2 = prof.now();
