@@ -463,8 +463,8 @@ def run_ours(args):
         buffered = {"value": n / (bt / 1e3), "unit": "elements/s", "ms_per_step": bt,
                     "kernels_ms": statistics.mean(be_ms), "extra_bytes": min(middle, n - middle) * rec,
                     "frac_of_roofline": (algo_bytes / (bt / 1e3) / 1e9) / peak, "sorted_ok": bool(okb),
-                    "what": "pm_merge with scratch = min(|A|,|B|): run copy + streaming merge "
-                            "(seq_merge_buffered, seqmerge.py:55-75)"}
+                    "what": "pm_merge with scratch = min(|A|,|B|) (seq_merge_buffered's budget, "
+                            "seqmerge.py:55-75): the engine with that salvage pool"}
 
     # ---- copy mode: pm_merge_copy (out of place, the multi-GPU path's local merge) ----
     copy_mode = None

@@ -117,7 +117,10 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   int32_t mu;
   // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
   // half-size regions, two staging + two output tiles (72 KB of shared memory)
-  const bool buffered = copy || (mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
+#ifndef PM_USE_BUFFERED
+#define PM_USE_BUFFERED 0  // tune: the streaming buffered pipeline for scratch >= min(|A|,|B|) (measured slower than the engine with that pool)
+#endif
+  const bool buffered = copy || (PM_USE_BUFFERED && mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
   // (the engine stages one input and one output tile; the buffered pipeline
   //  kBufStages inputs and two outputs)
   if (!pick_tiles(ks, w, buffered ? kBufBudget * 2 / (kBufStages + 2) : kTileBudget, &M, &T, &mu))
