@@ -181,7 +181,10 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.S = S;
   P.grid = grid;
   // half of the pool starts in the CTAs' caches (<= 32 each, the cache holds 64)
-  P.s_per = buffered ? 0 : std::min<int64_t>(S / (2 * (int64_t)grid), 32);
+#ifndef PM_SPER_DIV
+#define PM_SPER_DIV 2
+#endif
+  P.s_per = buffered ? 0 : std::min<int64_t>(S / (PM_SPER_DIV * (int64_t)grid), 32);
   // workspace
   const size_t off_state = (size_t)align_up((P.Q + 1) * 8, 256);
   const size_t off_loc = off_state + (size_t)align_up(P.K * 4, 256);
