@@ -121,22 +121,59 @@ __device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* n
 // ============================================================================
 // k_plan: merge-path splits + workspace reset
 // ============================================================================
+constexpr int kCoarse = 64;  // k_plan_coarse searches every kCoarse-th region boundary
+// Full-range merge-path searches at every kCoarse-th boundary (and the last);
+// k_plan then searches the boundaries in between inside these brackets.
+template <typename KT>
+__global__ void __launch_bounds__(256) k_plan_coarse(EngineParams P) {
+  Geo g(P);
+  const KT* keys = reinterpret_cast<const KT*>(P.keys);
+  const int64_t la = g.LA(), lb = g.LB();
+  const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
+  const int64_t nc = P.Q / kCoarse + 1;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nc; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = min(c * kCoarse, P.Q);
+    const int64_t d = g.diag(q);
+    int64_t a;
+    if (P.mode == MODE_MERGE) {
+      a = merge_path_thread<KT>(keys + P.s, la, B, lb, d);
+    } else {
+      a = d - lb;
+      a = a < 0 ? 0 : (a > la ? la : a);
+    }
+    P.split_a[q] = a;
+  }
+}
+
 template <typename KT>
 __global__ void k_plan(EngineParams P) {
   Geo g(P);
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
-  // one thread per region boundary: plain binary search of the stable merge path
-  // (2 independent loads per step, every search in flight at once -- far fewer
-  // DRAM sectors than a 33-ary warp search)
+  // one thread per region boundary: binary search of the stable merge path
+  // (2 independent loads per step, every search in flight at once), bounded by
+  // the coarse splits k_plan_coarse found every kCoarse boundaries
   {
     const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthr0 = (int64_t)gridDim.x * blockDim.x;
+    const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
     for (int64_t q = tid0; q <= P.Q; q += nthr0) {
+      if ((q & (kCoarse - 1)) == 0 || q == P.Q) continue;  // (coarse boundary: done)
       const int64_t d = g.diag(q);
       int64_t a;
       if (P.mode == MODE_MERGE) {
-        a = merge_path_thread<KT>(keys + P.s, la, P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m, lb, d);
+        const int64_t q0 = q & ~(int64_t)(kCoarse - 1), q1 = min(q0 + kCoarse, P.Q);
+        const int64_t a0 = P.split_a[q0], a1 = P.split_a[q1];
+        const int64_t b0 = g.diag(q0) - a0, b1 = g.diag(q1) - a1;
+        // a is monotone in d and so is b = d - a: both stay between the coarse splits
+        int64_t lo = max(max(a0, d - b1), max(d - lb, (int64_t)0));
+        int64_t hi = min(min(a1, d - b0), min(d, la));
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(keys + P.s + mid) <= __ldg(B + d - 1 - mid)) lo = mid + 1;
+          else hi = mid;
+        }
+        a = lo;
       } else {  // rotation: outputs are B then A
         a = d - lb;
         a = a < 0 ? 0 : (a > la ? la : a);
@@ -1598,6 +1635,7 @@ __global__ void __launch_bounds__(1024) k_compact(EngineParams P) {
 // ---- host launchers (called from pm_capi.cu) --------------------------------
 template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
+  k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 256) / 256, 1024), 256, 0, st>>>(P);
   k_plan<KT><<<grid, 256, 0, st>>>(P);
   if (P.tlist && PM_TLIST) {
     k_flags<<<(int)std::min<int64_t>((P.Q + 255) / 256, 1184), 256, 0, st>>>(P);
