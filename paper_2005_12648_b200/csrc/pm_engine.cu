@@ -130,18 +130,22 @@ __global__ void __launch_bounds__(256) k_plan_coarse(EngineParams P) {
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
   const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
+  // one warp per coarse boundary: 33-ary ballot search, ~6 dependent probes at 2^29
+  const int lane = threadIdx.x & 31;
   const int64_t nc = P.Q / kCoarse + 1;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nc; c += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0; c <= nc; c += nw) {
     const int64_t q = min(c * kCoarse, P.Q);
     const int64_t d = g.diag(q);
     int64_t a;
     if (P.mode == MODE_MERGE) {
-      a = merge_path_thread<KT>(keys + P.s, la, B, lb, d);
+      a = merge_path_warp<KT>(keys + P.s, la, B, lb, d, lane);
     } else {
       a = d - lb;
       a = a < 0 ? 0 : (a > la ? la : a);
     }
-    P.split_a[q] = a;
+    if (lane == 0) P.split_a[q] = a;
   }
 }
 
@@ -1635,7 +1639,7 @@ __global__ void __launch_bounds__(1024) k_compact(EngineParams P) {
 // ---- host launchers (called from pm_capi.cu) --------------------------------
 template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
-  k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 256) / 256, 1024), 256, 0, st>>>(P);
+  k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 8) / 8, 2048), 256, 0, st>>>(P);
   k_plan<KT><<<grid, 256, 0, st>>>(P);
   if (P.tlist && PM_TLIST) {
     k_flags<<<(int)std::min<int64_t>((P.Q + 255) / 256, 1184), 256, 0, st>>>(P);
