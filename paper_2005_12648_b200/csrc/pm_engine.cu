@@ -24,6 +24,9 @@ namespace pm {
 #ifndef PM_STATS
 #define PM_STATS 0
 #endif
+#ifndef PM_ITEM_RESAMPLE
+#define PM_ITEM_RESAMPLE 0
+#endif
 #ifndef PM_PREFETCH_ITEM
 #define PM_PREFETCH_ITEM 1
 #endif
@@ -992,6 +995,14 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           }
         }
       }
+#if PM_ITEM_RESAMPLE
+      // refresh the occupant's reads sample for the store-time check
+      if (lane == 0 && u >= 0 && !identity) {
+        int64_t cwl, cwr;
+        g.window(t, cwl, cwr);
+        if (early_r < g.consumed_in(u, cwl, cwr, re.ti.clo, re.ti.chi)) re.occ_r[i] = ld_acquire(&P.reads[u]);
+      }
+#endif
       __syncwarp();
       if (lane == 0) atomicAdd(&re.items_done, 1);
       cw = prof.now();
