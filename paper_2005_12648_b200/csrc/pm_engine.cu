@@ -1,11 +1,14 @@
-// pm_engine.cu -- plan + in-place merge/rotation engine kernels (sm_100a).
+// pm_engine.cu -- plan + in-place merge engine + streaming pipeline kernels (sm_100a).
 //
-// k_plan   : stable merge-path splits at every region diagonal (one warp per
-//            split, 33-ary search with warp ballots) + workspace reset.
-// k_engine : persistent kernel; each CTA repeatedly takes a ticket, gathers the
-//            region's A/B ranges into shared memory with TMA bulk copies,
-//            salvages still-needed units out of the region's slots, merges in
-//            shared memory and streams the region back in place.
+// k_plan_coarse / k_plan : stable merge-path splits at every region diagonal
+//            (a warp per coarse boundary, bracketed per-thread searches between)
+//            + workspace reset; k_flags / k_compact: the engine's ticket list.
+// k_engine : persistent kernel; salvage workers close each
+//            region's slot and move still-needed units out, the data team
+//            gathers the region's A/B pieces into shared memory with TMA bulk
+//            copies, merges there and streams the region back in place.
+// k_buffered : streaming TMA pipeline -- the out-of-place merge (pm_merge_copy)
+//            and, behind PM_USE_BUFFERED, the min-side-buffered in-place mode.
 //
 // Reference behaviour being reproduced (bit-exact): the stable merge of
 // seq_merge_buffered (seqmerge.py:55-75 / _kernels.py:227-313, A wins ties)
@@ -724,14 +727,15 @@ __device__ __forceinline__ void move_unit(const Geo& g, const EngineParams& P, i
 // Decoupled persistent engine.  A CTA holds a ring of up to kRing tickets:
 //   salvage workers (warps 0..kTeam-1) each take the next (ticket, slot) item in
 //     ticket order and run its chain on their own: close the slot and sample its
-//     occupant, wait for the occupant to land and for every earlier consumer to
-//     read it, then move it (scratch first, else a free slot) if a later region
-//     still needs it.  No space -> wait for the ticket's reads to be published,
-//     then block for space (the region's own reads free space first).
-//   data team (warps kTeam..2*kTeam-1) takes the ring's tickets in order: gathers
-//     the A/B pieces into shared memory (TMA bulk), publishes the reads, merges in
-//     shared memory, waits until every slot item of the ticket is done, and
-//     streams the output tile back in place (TMA bulk store).
+//     occupant, wait for the occupant to land, then move it (scratch first, else
+//     a free slot of a higher-order region) if a later region still needs it.
+//     No space -> wait for the ticket's reads to be published, then block for
+//     space (the region's own reads free space first).
+//   data team (the other kDataWarps warps) takes the ring's tickets in order:
+//     gathers the A/B pieces into shared memory (TMA bulk), publishes the reads,
+//     merges in shared memory, issues the next ticket's gather, waits until every
+//     slot item of the ticket is done and every consumer of order <= t has read
+//     each occupant, and streams the output tile back in place (TMA bulk store).
 // The teams meet only on shared-memory counters, so a worker's long chain
 // (waits on other CTAs, round trips of the copy) overlaps the other workers'
 // chains and the data team's work on earlier tickets.
