@@ -1068,7 +1068,9 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
         int32_t l = p == gt ? pl : INT32_MIN;
         for (uint32_t it = 0;; ++it) {
           if (l != INT32_MIN && (l < 0 || g.order(g.region_of_slot(l)) >= R.t)) {
-            fence_acq_rel_gpu();  // (the prefetch was relaxed: acquire the unit's data)
+            // the prefetch was relaxed: acquire a moved unit's data (a unit still
+            // in its home slot holds the caller's original records)
+            if (l != (int32_t)j) fence_acq_rel_gpu();
             break;
           }
           l = ld_acquire(&P.loc[j]);
