@@ -278,17 +278,17 @@ def run_dist(args):
     # reads the merged block back (max over ranks of the device-timed region)
     e2e = None
     if args.e2e_steps > 0:
+        # one pinned buffer per rank: the step reads it in, then writes the merged block back
         hk = torch.empty(n, dtype=torch.int32).pin_memory()
-        hk.copy_(keys0.cpu())
-        hout = torch.empty_like(hk).pin_memory()
         et = []
         for s in range(args.e2e_steps + 1):  # the first one is untimed
+            hk.copy_(keys0)  # restore the rank's host block (outside the timed region)
             dist.barrier()
             torch.cuda.synchronize()
             ev0.record()
             work.copy_(hk, non_blocking=True)
             merge_distributed(work, pay, la)
-            hout.copy_(work, non_blocking=True)
+            hk.copy_(work, non_blocking=True)
             ev1.record()
             ev1.synchronize()
             if s:
