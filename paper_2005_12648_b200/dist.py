@@ -53,10 +53,15 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
     lo = torch.clamp(diags - lb, min=0)
     hi = torch.clamp(diags, max=la)
     k = torch.arange(1, _PROBES + 1, dtype=torch.int64, device=dev)
-    while True:
+    # each round cuts a span s to <= s // 33 + 1 and resolves spans <= 32 exactly, so
+    # the round count is known up front: no host synchronisation inside the loop
+    s = max(min(d, la) - max(d - lb, 0) for d in offsets)  # widest initial span (host side)
+    rounds = 0 if s == 0 else 1
+    while s > _PROBES:
+        s = s // (_PROBES + 1) + 1
+        rounds += 1
+    for _ in range(rounds):
         span = hi - lo
-        if int(span.max().item()) == 0:
-            break
         small = span <= _PROBES
         # probes: evenly spaced when the interval is wide, every index when it is small
         p_wide = lo[:, None] + (k[None, :] * span[:, None]) // (_PROBES + 1)
@@ -79,7 +84,9 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
         last_valid = torch.where(valid, p, lo[:, None] - 1).max(dim=1).values
         new_lo = torch.where(has, torch.where(first > 0, last_true + 1, lo), last_valid + 1)
         lo, hi = torch.where(span > 0, new_lo, lo), torch.where(span > 0, new_hi, hi)
-    return [int(x) for x in lo.tolist()]
+    res = torch.cat([lo, hi - lo]).tolist()
+    assert not any(res[len(offsets):]), "global_splits: search did not converge"
+    return [int(x) for x in res[:len(offsets)]]
 
 
 def _default_local_merge(src_k: torch.Tensor, src_p: torch.Tensor, len_a: int, dst_k: torch.Tensor,
