@@ -306,6 +306,13 @@ def test_distributed_merge_single_rank_nccl():
         orc.seq_merge_buffered(want_k, want_p, 0, middle, len(keys))
         k = torch.from_numpy(keys).cuda()
         p = torch.from_numpy(payload).cuda()
+        # the split search itself (its rounds run only when a diagonal is interior)
+        from paper_2005_12648_b200.dist import global_splits
+
+        diags = [0, 1, 777, 150000, middle, len(keys) - 5, len(keys)]
+        got = global_splits(k, diags, middle)
+        want = [int(orc.merge_path(keys[:middle], keys[middle:], d)) for d in diags]
+        assert got == want
         rk, rp = merge_distributed(k, p, middle)
         assert np.array_equal(rk.cpu().numpy(), want_k) and np.array_equal(rp.cpu().numpy(), want_p)
     finally:
