@@ -42,24 +42,13 @@ def _owned_values(keys_local: torch.Tensor, off: int, positions: torch.Tensor) -
     return torch.where(mine, vals, torch.zeros_like(vals))
 
 
-def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: int, group=None) -> list[int]:
-    """A-count of the stable merge at every rank boundary diagonal (A wins ties)."""
-    rank = dist.get_rank(group)
-    off = offsets[rank]
-    N = offsets[-1]
-    la, lb = global_len_a, N - global_len_a
+def _split_search(keys_local: torch.Tensor, off: int, diags: torch.Tensor, la: int, lb: int, rounds: int,
+                  group) -> tuple[torch.Tensor, torch.Tensor]:
+    """The probe rounds of global_splits on device tensors; returns (lo, hi)."""
     dev = keys_local.device
-    diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
     lo = torch.clamp(diags - lb, min=0)
     hi = torch.clamp(diags, max=la)
     k = torch.arange(1, _PROBES + 1, dtype=torch.int64, device=dev)
-    # each round cuts a span s to <= s // 33 + 1 and resolves spans <= 32 exactly, so
-    # the round count is known up front: no host synchronisation inside the loop
-    s = max(min(d, la) - max(d - lb, 0) for d in offsets)  # widest initial span (host side)
-    rounds = 0 if s == 0 else 1
-    while s > _PROBES:
-        s = s // (_PROBES + 1) + 1
-        rounds += 1
     for _ in range(rounds):
         span = hi - lo
         small = span <= _PROBES
@@ -84,6 +73,52 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
         last_valid = torch.where(valid, p, lo[:, None] - 1).max(dim=1).values
         new_lo = torch.where(has, torch.where(first > 0, last_true + 1, lo), last_valid + 1)
         lo, hi = torch.where(span > 0, new_lo, lo), torch.where(span > 0, new_hi, hi)
+    return lo, hi
+
+
+# CUDA graphs of the probe rounds, per (keys buffer, geometry): ~30 small ops and a
+# collective per round are replayed without host dispatch (NCCL supports capture)
+_graphs: dict = {}
+
+
+def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: int, group=None) -> list[int]:
+    """A-count of the stable merge at every rank boundary diagonal (A wins ties)."""
+    rank = dist.get_rank(group)
+    off = offsets[rank]
+    N = offsets[-1]
+    la, lb = global_len_a, N - global_len_a
+    dev = keys_local.device
+    # each round cuts a span s to <= s // 33 + 1 and resolves spans <= 32 exactly, so
+    # the round count is known up front: no host synchronisation inside the loop
+    s = max(min(d, la) - max(d - lb, 0) for d in offsets)  # widest initial span (host side)
+    rounds = 0 if s == 0 else 1
+    while s > _PROBES:
+        s = s // (_PROBES + 1) + 1
+        rounds += 1
+    if rounds == 0:
+        return [min(max(d - lb, 0), la) for d in offsets]
+    key = (keys_local.data_ptr(), keys_local.numel(), keys_local.dtype, off, tuple(offsets), la, rounds,
+           id(group)) if keys_local.is_cuda and dist.get_backend(group) == "nccl" else None
+    ent = _graphs.get(key) if key else None
+    if ent is None:
+        diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
+        lo, hi = _split_search(keys_local, off, diags, la, lb, rounds, group)
+        if key is not None:
+            try:  # capture for the next call with the same buffers and geometry
+                g = torch.cuda.CUDAGraph()
+                sd = diags.clone()
+                torch.cuda.synchronize(dev)
+                with torch.cuda.graph(g):
+                    slo, shi = _split_search(keys_local, off, sd, la, lb, rounds, group)
+                _graphs[key] = (g, slo, shi)
+            except Exception:  # (capture unsupported here: stay eager)
+                _graphs[key] = False
+    elif ent is False:
+        diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
+        lo, hi = _split_search(keys_local, off, diags, la, lb, rounds, group)
+    else:
+        g, lo, hi = ent
+        g.replay()
     res = torch.cat([lo, hi - lo]).tolist()
     assert not any(res[len(offsets):]), "global_splits: search did not converge"
     return [int(x) for x in res[:len(offsets)]]
