@@ -1,6 +1,6 @@
 import sys, time
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 from paper_2005_12648_b200.workloads import config_input_device

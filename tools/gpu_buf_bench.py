@@ -1,7 +1,7 @@
 """Tuning: buffered-mode pm_merge (scratch = min run) and pm_merge_copy at 2^L per side."""
 import sys
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 from paper_2005_12648_b200.workloads import config_input_device

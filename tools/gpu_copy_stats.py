@@ -1,7 +1,7 @@
 """Tuning: per-region phase cycles of the streaming pipeline (PM_LIB=libparmerge_b200_stats.so)."""
 import ctypes, sys
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops, _capi
 from paper_2005_12648_b200.workloads import config_input_device

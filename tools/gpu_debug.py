@@ -1,7 +1,7 @@
 """Quick GPU bring-up script: small merges with progressively larger sizes."""
 import sys, time
 import numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from oracle import oracle as orc
 rng = np.random.default_rng(0)

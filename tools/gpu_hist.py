@@ -2,7 +2,7 @@
 import ctypes, sys
 import numpy as np
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops, _capi
 from paper_2005_12648_b200.workloads import config_input_device

@@ -1,7 +1,7 @@
 """Tuning: salvage destination paths (needs PM_LIB=libparmerge_b200_stats.so)."""
 import ctypes, sys
 import numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops, _capi
 from paper_2005_12648_b200.workloads import config_input_device

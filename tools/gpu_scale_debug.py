@@ -1,7 +1,7 @@
 """Bring-up: time each size with status checks; prints as it goes."""
 import sys, time, ctypes
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _capi
 from paper_2005_12648_b200.workloads import config_input_device

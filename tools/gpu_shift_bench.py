@@ -1,7 +1,7 @@
 """Tuning: pm_shift (block exchange A|B -> B|A) throughput at n records."""
 import sys
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 L = int(sys.argv[1]); frac = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5

@@ -2,7 +2,7 @@
 import os, sys, time
 import torch
 import torch.distributed as dist
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 from paper_2005_12648_b200.dist import global_splits
 from paper_2005_12648_b200.workloads import config_input_device
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29641")

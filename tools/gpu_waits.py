@@ -1,6 +1,6 @@
 """Tuning: split of the data team's wait stage (PM_LIB=libparmerge_b200_stats.so)."""
 import ctypes, sys
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops, _capi
 from paper_2005_12648_b200.workloads import config_input_device

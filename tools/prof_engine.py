@@ -1,7 +1,7 @@
 """Profiling driver: a few merges of BASELINE config 2 (or 3/4) at 2^L per side."""
 import sys
 import torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.')  # run from the repo root
 import paper_2005_12648_b200 as pm
 from paper_2005_12648_b200 import _ops
 from paper_2005_12648_b200.workloads import config_input_device
