@@ -816,10 +816,12 @@ __device__ __forceinline__ void open_entry(EngCtl& c, const Geo& g, const Engine
   RingEntry& re = c.ring[e % kRing];
   const int64_t t = vc.next_t;
   if (t < P.Q) {
+    // the next ticket's fetch and this ticket's split loads share one round trip
+    const int32_t k_next = atomicAdd(P.ticket, 1);
     load_tinfo(g, t, re.ti);
     const int64_t q = g.region_of_ticket(t);
     re.nslot = (int32_t)(g.region_end_slot(q) - g.region_first_slot(q));
-    vc.next_t = resolve_ticket(P, atomicAdd(P.ticket, 1), vc.ntick);  // (a load only if tickets were left out)
+    vc.next_t = resolve_ticket(P, k_next, vc.ntick);  // (a load only if tickets were left out)
 
   } else {
     re.ti.t = P.Q;
