@@ -74,6 +74,89 @@ __global__ void __launch_bounds__(256) k_reverse(KT* keys, uint8_t* pay, int64_t
   }
 }
 
+// Keys only, 16-byte vectors: block job b of a segment swaps the aligned left
+// chunk [x0, x0+C) with its mirror [S-x0-C+1, S-x0] (S = 2 lo + len - 1).  Both
+// ranges are read into shared memory with aligned vector loads (the right one
+// as an aligned superset), then written back reversed -- aligned vector stores,
+// element stores only for the right range's partial edge vectors.  The pairs
+// before the first aligned chunk and after the last full one are swapped by one
+// extra job per segment, element by element.  Jobs never share a record.
+template <typename KT, int C>
+__global__ void __launch_bounds__(256) k_reverse_vec(KT* keys, int64_t lo0, int64_t len0, int64_t lo1, int64_t len1) {
+  constexpr int V = 16 / sizeof(KT);
+  __shared__ __align__(16) KT Lb[C];
+  __shared__ __align__(16) KT Rb[C + 2 * V];
+  auto plan = [&](int64_t lo, int64_t len, int64_t& L0, int64_t& nfull) {
+    const int64_t half = len >> 1;
+    L0 = (lo + V - 1) / V * V;
+    nfull = L0 < lo + half ? (lo + half - L0) / C : 0;
+  };
+  int64_t L00, nf0, L01, nf1;
+  plan(lo0, len0, L00, nf0);
+  plan(lo1, len1, L01, nf1);
+  const int64_t njobs = nf0 + nf1 + 2;
+  for (int64_t job = blockIdx.x; job < njobs; job += gridDim.x) {
+    // job order: full chunks of segment 0, of segment 1, then the two scalar jobs
+    const bool s1 = job >= nf0 && job != nf0 + nf1;
+    const int64_t lo = s1 ? lo1 : lo0, len = s1 ? len1 : len0, L0 = s1 ? L01 : L00, nf = s1 ? nf1 : nf0;
+    const int64_t S = 2 * lo + len - 1, half = len >> 1;
+    if (job >= nf0 + nf1) {  // scalar pairs of segment 0 (job nf0+nf1) or 1 (last job)
+      const int64_t head_end = min(L0, lo + half), tail0 = max(L0 + nf * C, head_end);
+      for (int64_t x = lo + threadIdx.x; x < head_end; x += blockDim.x) {
+        const KT a = keys[x], b = keys[S - x];
+        keys[x] = b;
+        keys[S - x] = a;
+      }
+      for (int64_t x = tail0 + threadIdx.x; x < lo + half; x += blockDim.x) {
+        const KT a = keys[x], b = keys[S - x];
+        keys[x] = b;
+        keys[S - x] = a;
+      }
+      continue;
+    }
+    const int64_t b = s1 ? job - nf0 : job;
+    const int64_t x0 = L0 + b * C;
+    const int64_t ylo = S - x0 - C + 1, yhi = S - x0;  // inclusive
+    const int64_t r0 = ylo / V * V, r1 = (yhi + V) / V * V;  // aligned superset [r0, r1)
+    const uint4* L4 = reinterpret_cast<const uint4*>(keys + x0);
+    const uint4* R4 = reinterpret_cast<const uint4*>(keys + r0);
+    for (int i = threadIdx.x; i < C / V; i += blockDim.x) reinterpret_cast<uint4*>(Lb)[i] = L4[i];
+    for (int i = threadIdx.x; i < (int)((r1 - r0) / V); i += blockDim.x) {
+      const int64_t yb = r0 + (int64_t)i * V;
+      if (yb + V <= lo + len) {
+        reinterpret_cast<uint4*>(Rb)[i] = R4[i];
+      } else {  // (the segment's last partial vector: stay inside the caller's array)
+        for (int c = 0; c < V && yb + c < lo + len; ++c) Rb[i * V + c] = keys[yb + c];
+      }
+    }
+    __syncthreads();
+    // left chunk <- mirror (reversed)
+    uint4* Lo4 = reinterpret_cast<uint4*>(keys + x0);
+    for (int i = threadIdx.x; i < C / V; i += blockDim.x) {
+      KT v[V];
+#pragma unroll
+      for (int c = 0; c < V; ++c) v[c] = Rb[(S - (x0 + i * V + c)) - r0];
+      Lo4[i] = *reinterpret_cast<const uint4*>(v);
+    }
+    // right range <- left chunk (reversed); partial edge vectors element by element
+    for (int64_t i = threadIdx.x; i < (r1 - r0) / V; i += blockDim.x) {
+      const int64_t yb = r0 + i * V;
+      if (yb >= ylo && yb + V - 1 <= yhi) {
+        KT v[V];
+#pragma unroll
+        for (int c = 0; c < V; ++c) v[c] = Lb[(S - (yb + c)) - x0];
+        *reinterpret_cast<uint4*>(keys + yb) = *reinterpret_cast<const uint4*>(v);
+      } else {
+        for (int c = 0; c < V; ++c) {
+          const int64_t y = yb + c;
+          if (y >= ylo && y <= yhi) keys[y] = Lb[(S - y) - x0];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st) {
@@ -84,6 +167,16 @@ cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int6
   auto grid_for = [&](int64_t np) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((np + 1023) / 1024, (int64_t)num_sms * 8));
   };
+  if (!w && (((uintptr_t)keys) & 15) == 0) {
+    // keys only: vectorised block jobs (the array base must be 16-byte aligned)
+    constexpr int C = 8192 / sizeof(KT);
+    auto jobs = [&](int64_t a, int64_t b) { return (a / 2) / C + (b / 2) / C + 2; };
+    const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(jobs(la, lb), (int64_t)num_sms * 8));
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(jobs(la + lb, 0), (int64_t)num_sms * 8));
+    if (pairs > 0) k_reverse_vec<KT, C><<<g1, 256, 0, st>>>(k, lo, la, lo + la, lb);
+    if (all > 0) k_reverse_vec<KT, C><<<g2, 256, 0, st>>>(k, lo, la + lb, 0, 0);
+    return cudaGetLastError();
+  }
   if (pairs > 0) k_reverse<KT><<<grid_for(pairs), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);
   if (all > 0) k_reverse<KT><<<grid_for(all), 256, 0, st>>>(k, p, w, lo, la + lb, 0, 0);
   return cudaGetLastError();

@@ -388,3 +388,26 @@ def test_wide_payload_rows(width):
         _ops.merge_copy(sk, sp, dk, dp, middle)
         pm.synchronize()
         assert np.array_equal(dk.cpu().numpy(), want_k) and np.array_equal(dp.cpu().numpy(), want_p)
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_shift_offsets_and_alignment(dtype):
+    """pm_shift on sub-ranges at every 16-byte phase, odd and even lengths, both key sizes
+    (vectorised block jobs + element-wise edge jobs)."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(4040)
+    n = 300_003
+    base = rng.integers(-10**6, 10**6, n).astype(dtype)
+    pay = np.zeros((n, 0), np.uint8)
+    for lo in (0, 1, 2, 3, 5, 17):
+        for la, lb in ((70_001, 90_000), (1, 150_000), (150_001, 3), (40_000, 40_000), (2, 2), (0, 10)):
+            keys = base.copy()
+            want = keys.copy()
+            seg = np.concatenate([want[lo + la:lo + la + lb], want[lo:lo + la]])
+            want[lo:lo + la + lb] = seg
+            arr = to_gpu(keys, pay)
+            _ops.shift(arr, lo, la, lb)
+            pm.synchronize()
+            got, _ = arr.numpy()
+            assert np.array_equal(got, want), f"lo={lo} la={la} lb={lb} {dtype.__name__}"
