@@ -534,11 +534,13 @@ __device__ __forceinline__ void write_sentinels(uint8_t* kin, int64_t offA, int6
   for (int k = gt; k < 2 * kSent; k += GT) (k < kSent ? a[k] : b[k - kSent]) = mx;
 }
 
-template <typename KT>
+// GT (the merging threads) is a compile-time constant: the per-thread span E is
+// then a multiply-shift, not a division, on every region
+template <typename KT, int GT>
 __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT* Bs, int64_t alpha, int64_t beta,
                                            int64_t nout, KT* ko, uint8_t* po, const uint8_t* PA, const uint8_t* PB,
-                                           int64_t w, bool wq4, int gt, int GT) {
-  int32_t E = ((int32_t)nout + GT - 1) / GT;  // 32-bit: nout <= M
+                                           int64_t w, bool wq4, int gt) {
+  int32_t E = (int32_t)(((uint32_t)nout + GT - 1) / (uint32_t)GT);  // 32-bit: nout <= M
   E |= 1;
   {
     // region-local indices fit in 32 bits (nout <= M)
@@ -553,22 +555,24 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
       // exhausted run offers +max, which loses to every real key except +max
       // itself -- and then either choice emits the same value.  No bound checks.
       int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
+      const KT* Bq = Bs + (o - 1);  // Bs[o - 1 - mid] == Bq[-mid]
       while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
-        if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+        if (As[mid] <= *(Bq - mid)) lo = mid + 1;
         else hi = mid;
       }
-      int32_t i = lo, jb = o - lo;
-      KT va = As[i], vb = Bs[jb];
+      // run cursors as pointers: a step is compare, min, store, one predicated
+      // advance per side, the candidate address select, load, and the refill
+      const KT* pa = As + lo;
+      const KT* pb = Bs + (o - lo);
+      KT va = *pa, vb = *pb;
 #pragma unroll 4
       for (; o < oe; ++o) {
         const bool takeA = va <= vb;
         ko[o] = takeA ? va : vb;
-        i += takeA;
-        jb += !takeA;
-        const KT v = *(takeA ? As + i : Bs + jb);
-        va = takeA ? v : va;
-        vb = takeA ? vb : v;
+        if (takeA) ++pa; else ++pb;
+        const KT v = *(takeA ? pa : pb);
+        if (takeA) va = v; else vb = v;
       }
     } else if (mode == MODE_MERGE) {
       int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
@@ -848,7 +852,7 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
   __shared__ EngCtl ctl;
   Geo g(P);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int NT = blockDim.x;
+  constexpr int NT = kEngineThreads;  // (launched with exactly this many)
   const int64_t ks = sizeof(KT);
   const int64_t w = P.w;
   if (*(volatile int32_t*)P.noop) return;
@@ -1195,7 +1199,8 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
       const uint8_t* PA = pin + R.poffA;
       const uint8_t* PB = pin + R.poffB;
       const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-      if (!(PM_ABLATE & 1)) merge_tile<KT>(P.mode, As, Bs, R.alpha, R.beta, R.nout, ko, po, PA, PB, w, wq4, gt, GT);
+      if (!(PM_ABLATE & 1))
+        merge_tile<KT, kEngineThreads - kTeam * 32>(P.mode, As, Bs, R.alpha, R.beta, R.nout, ko, po, PA, PB, w, wq4, gt);
       fence_proxy_async_smem();  // our smem writes -> visible to the TMA (async proxy)
       PM_TICK(3);
       // ---- the input tile is free: start the next entry's gather now ----
@@ -1374,6 +1379,25 @@ struct BufRegion {
   int64_t offA, offB, poffA, poffB;
   bool identity;
 };
+// What the merging warps need of a staged region: the leader derives it once
+// when it issues the region's loads and leaves it in shared memory (the
+// region-local quantities fit in 32 bits: nout <= M).
+struct BufDesc {
+  int64_t d0, r;
+  int32_t alpha, beta, nout, offA, offB, poffA, poffB, identity;
+  __device__ void set(const BufRegion& R) {
+    d0 = R.d0;
+    r = R.r;
+    alpha = (int32_t)R.alpha;
+    beta = (int32_t)R.beta;
+    nout = (int32_t)R.nout;
+    offA = (int32_t)R.offA;
+    offB = (int32_t)R.offB;
+    poffA = (int32_t)R.poffA;
+    poffB = (int32_t)R.poffB;
+    identity = R.identity;
+  }
+};
 
 // region of ticket t; its boundary splits a0/a1 are passed in when already at hand
 // (a0 < 0: load them)
@@ -1440,10 +1464,11 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
   extern __shared__ __align__(128) uint8_t dyn[];
   __shared__ uint64_t bar[NS];
   __shared__ int64_t s_t[NS];
-  __shared__ int64_t s_a[NS][2];   // the region's splits (loaded once, by the leader)
+  __shared__ BufDesc s_d[NS];      // the staged region's geometry (set by the leader)
   __shared__ int32_t s_early[NS];  // the region's read flag was already raised
   Geo g(P);
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
+  constexpr int NT = kBufferedThreads;  // (launched with exactly this many)
+  const int tid = threadIdx.x, lane = tid & 31;
   const int NW = NT >> 5;
   const bool ctrl = (tid >> 5) == NW - 1;
   const bool leader = ctrl && lane == 0;  // issues every TMA op of the CTA
@@ -1472,8 +1497,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
       s_t[k] = t0 < P.Q ? t0 : P.Q;
       if (t0 < P.Q) {
         const BufRegion R = buf_region<KT>(g, P, t0, buf_a);
-        s_a[k][0] = R.a0;
-        s_a[k][1] = R.a1;
+        s_d[k].set(R);
         if (!R.identity) buf_issue<KT>(P, R, buf_a, STAGE(k), STAGE(k) + P.smem_keys, &bar[k]);
       } else {
         break;
@@ -1496,7 +1520,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
     const int cur = it % NS, ob = it & 1;
     const int64_t t = s_t[cur];
     if (t >= P.Q) break;
-    const BufRegion R = buf_region<KT>(g, P, t, buf_a, s_a[cur][0], s_a[cur][1]);
+    const BufDesc R = s_d[cur];
     if (leader) {  // (writes only the previous iteration's stage slot: no race with R above)
       // keep NS-1 regions in flight: the stage of the previous iteration is free
       const int nx = (it + NS - 1) % NS;
@@ -1506,8 +1530,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
       s_early[nx] = 0;
       if (tn < P.Q) {
         const BufRegion Rn = buf_region<KT>(g, P, tn, buf_a);
-        s_a[nx][0] = Rn.a0;
-        s_a[nx][1] = Rn.a1;
+        s_d[nx].set(Rn);
         if (!Rn.identity) buf_issue<KT>(P, Rn, buf_a, STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
       }
     }
@@ -1550,10 +1573,9 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
             const int sk = (it + k) % NS;
             const int64_t tk = s_t[sk];
             if (tk < P.Q && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
-              const BufRegion Rk = buf_region<KT>(g, P, tk, buf_a, s_a[sk][0], s_a[sk][1]);
-              if (!Rk.identity) {
+              if (!s_d[sk].identity) {
                 fence_acq_rel_gpu();
-                st_release(&flags[Rk.r], 1);
+                st_release(&flags[s_d[sk].r], 1);
                 s_early[sk] = 1;
               }
             }
@@ -1567,10 +1589,10 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
           named_barrier_sync(1, MT);
         }
         const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-        merge_tile<KT>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
-                       reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
-                       reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA, pin + R.poffB, w, wq4,
-                       tid, MT);
+        merge_tile<KT, kBufferedThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
+                                              reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                                              reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                              pin + R.poffB, w, wq4, tid);
         PB_TICK(2);
         fence_proxy_async_smem();
       }
@@ -1668,6 +1690,7 @@ cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
 }
 template <typename KT>
 cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+  if (block != kEngineThreads) return cudaErrorInvalidValue;  // the kernel's team split is compile-time
   k_engine<KT><<<grid, block, smem, st>>>(P);
   return cudaGetLastError();
 }
