@@ -45,7 +45,7 @@ def log(msg):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cfg", type=int, default=2, help="BASELINE config number (2: int32 uniform, 3: int64 skew, 4: KV dup)")
@@ -76,6 +76,14 @@ def default_log_len(cfg):
     return {2: 29, 3: 28, 4: 26}[cfg]
 
 
+def launch_count():
+    """Kernels the library has launched so far in this process (pm_launch_count)."""
+    from paper_2005_12648_b200 import _capi
+    v = ctypes.c_int64()
+    _capi.check(_capi.lib().pm_launch_count(ctypes.byref(v)), "pm_launch_count")
+    return v.value
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
@@ -87,26 +95,37 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []      # samples taken while a timed region was open
+        self.idle = 0        # samples outside (start-up, restores)
+        self.active = False  # set around the timed regions (the reader tags samples)
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start on a fresh box: wait for its first sample
+            # so that the timed region is actually sampled
+            t0 = time.time()
+            while not self.idle and not self.lines and time.time() - t0 < 20 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            if self.active:
+                self.lines.append(line.strip())
+            else:
+                self.idle += 1
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.15)
+            time.sleep(0.03)  # the sample in flight at the end of the region
+            self.active = False
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -259,6 +278,8 @@ def run_dist(args):
     sampler = ClockSampler(local) if not args.quick else None
     if sampler:
         sampler.__enter__()
+        sampler.active = True
+    lc0 = launch_count()
     for _ in range(args.steps):
         work.copy_(keys0)
         dist.barrier()
@@ -268,6 +289,7 @@ def run_dist(args):
         ev1.synchronize()
         times.append(ev0.elapsed_time(ev1))
     torch.cuda.synchronize()
+    launches = launch_count() - lc0
     if sampler:
         sampler.__exit__()
     t = torch.tensor([sum(times)], device="cuda")
@@ -321,7 +343,7 @@ def run_dist(args):
                          "traffic": None, "kernel": "whole distributed step per GPU"},
             "e2e": e2e, "cpu_baseline": None,
             # ours per step and rank: k_plan + k_buffered (copy mode) of pm_merge_copy
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches,
         }
         if sampler:
             line["clocks"] = sampler.summary()
@@ -394,6 +416,8 @@ def run_ours(args):
     sampler = ClockSampler(local) if not args.quick else None
     if sampler:
         sampler.__enter__()
+        sampler.active = True
+    lc0 = launch_count()
     for _ in range(args.steps):
         restore()  # outside the timed region (pristine input for every step)
         ev0.record(stream)
@@ -405,6 +429,7 @@ def run_ours(args):
         plan_ms.append(pf.value)
         eng_ms.append(ef.value)
     torch.cuda.synchronize()
+    launches = launch_count() - lc0
     if sampler:
         sampler.__exit__()
     if world > 1:
@@ -464,7 +489,7 @@ def run_ours(args):
                     "kernels_ms": statistics.mean(be_ms), "extra_bytes": min(middle, n - middle) * rec,
                     "frac_of_roofline": (algo_bytes / (bt / 1e3) / 1e9) / peak, "sorted_ok": bool(okb),
                     "what": "pm_merge with scratch = min(|A|,|B|) (seq_merge_buffered's budget, "
-                            "seqmerge.py:55-75): the engine with that salvage pool"}
+                            "seqmerge.py:55-75): the min run copied out, then the streaming in-place merge (k_copy_run + k_buffered)"}
 
     # ---- copy mode: pm_merge_copy (out of place, the multi-GPU path's local merge) ----
     copy_mode = None
@@ -541,7 +566,7 @@ def run_ours(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peaks else "fallback 6650"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches,
             "kernel_ms": {"plan": statistics.mean(plan_ms), "engine": eng_avg, "merge": total_ms / args.steps},
             "merge_frac_of_roofline": (algo_bytes / (total_ms / args.steps / 1e3) / 1e9) / peak,
             "salvaged_records_frac": stats[1] / n,

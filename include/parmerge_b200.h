@@ -148,6 +148,9 @@ int pm_debug_splits(pm_ctx *ctx, int64_t *host_out, int64_t n);
  * per-ticket-range histograms filled only by -DPM_STATS=1 tuning builds). */
 int pm_debug_stats(pm_ctx *ctx, uint64_t *host_out64);
 int pm_kernel_ms(pm_ctx *ctx, float *plan_ms, float *engine_ms);
+/* Kernels this library has launched in this process (all contexts, since load):
+ * the bench's gpu_launches claim is the difference around its timed region. */
+int pm_launch_count(int64_t *out);
 
 #ifdef __cplusplus
 }

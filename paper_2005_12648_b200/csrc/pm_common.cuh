@@ -29,6 +29,9 @@ __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
 }
 // release/acquire fence at GPU scope (cheaper than __threadfence's sequentially
 // consistent fence; every use here publishes data before a flag or acquires after one)
+__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
   int32_t v;

@@ -8,7 +8,7 @@
 //            gathers the region's A/B pieces into shared memory with TMA bulk
 //            copies, merges there and streams the region back in place.
 // k_buffered : streaming TMA pipeline -- the out-of-place merge (pm_merge_copy)
-//            and, behind PM_USE_BUFFERED, the min-side-buffered in-place mode.
+//            and the min-side-buffered in-place mode (seq_merge_buffered budget).
 //
 // Reference behaviour being reproduced (bit-exact): the stable merge of
 // seq_merge_buffered (seqmerge.py:55-75 / _kernels.py:227-313, A wins ties)
@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "pm_common.cuh"
+#include "pm_launch.h"
 #include "pm_engine.cuh"
 #include "pm_search.cuh"
 
@@ -1507,6 +1508,12 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
   }
   __syncthreads();
   uint32_t phmask = 0;  // bit k: parity of stage k's barrier
+  // control warp: consumer range of the region one iteration ahead (in-place mode)
+  int64_t cn_lo = 1, cn_hi = 0;
+  if (ctrl && !oop && s_t[0] < P.Q && !s_d[0].identity) {
+    cn_lo = __ldg(&P.state[s_d[0].r]);
+    cn_hi = __ldg(&P.loc[s_d[0].r]);
+  }
   unsigned long long n_reg = 0;
   Prof prof;
   long long tb = prof.now();
@@ -1535,8 +1542,22 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
       }
     }
     PB_TICK(0);
+    // in-place mode, control warp: this region's consumer range (loaded one iteration
+    // ago), and the next region's, loaded now -- only the flag round trip is left
+    // to overlap the merge
+    const int64_t c_lo = cn_lo, c_hi = cn_hi;
+    if (ctrl && !oop) {
+      __syncwarp();  // (the leader's stage writes above)
+      const int sn = (it + 1) % NS;
+      cn_lo = 1;
+      cn_hi = 0;
+      if (s_t[sn] < P.Q && !s_d[sn].identity) {
+        cn_lo = __ldg(&P.state[s_d[sn].r]);
+        cn_hi = __ldg(&P.loc[s_d[sn].r]);
+      }
+    }
     if (R.identity) {  // records already on their outputs and read by r only
-      if (leader) st_release(&flags[R.r], 1);
+      if (leader) st_relaxed(&flags[R.r], 1);
     } else {
       while (!mbar_try_wait(&bar[cur], (phmask >> cur) & 1)) {
       }
@@ -1549,13 +1570,12 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
       if (ctrl && oop) {
         // copy mode: nothing to announce or wait for
       } else if (ctrl) {
-        if (leader && !s_early[cur]) {
-          fence_acq_rel_gpu();
-          st_release(&flags[R.r], 1);
-        }
+        // (a relaxed flag: the region's loads have completed -- its barrier said so --
+        // so a writer that sees the flag cannot change what the region read; a
+        // release here would be a full GPU membar behind this CTA's bulk stores)
+        if (leader && !s_early[cur]) st_relaxed(&flags[R.r], 1);
         // the records this region overwrites in the unbuffered run must have been read
         // by their consumers (regions c_lo..c_hi, precomputed by k_consumers)
-        const int64_t c_lo = __ldg(&P.state[R.r]), c_hi = __ldg(&P.loc[R.r]);
         for (int64_t c = c_lo + lane; c <= c_hi; c += 32) {
           if (c == R.r) continue;
           for (uint32_t it2 = 0; ld_acquire(&flags[c]) == 0; ++it2) {
@@ -1574,8 +1594,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, i
             const int64_t tk = s_t[sk];
             if (tk < P.Q && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
               if (!s_d[sk].identity) {
-                fence_acq_rel_gpu();
-                st_release(&flags[s_d[sk].r], 1);
+                st_relaxed(&flags[s_d[sk].r], 1);
                 s_early[sk] = 1;
               }
             }
@@ -1682,9 +1701,11 @@ template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
   k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 8) / 8, 2048), 256, 0, st>>>(P);
   k_plan<KT><<<grid, 256, 0, st>>>(P);
+  count_launches(2);
   if (P.tlist && PM_TLIST) {
     k_flags<<<(int)std::min<int64_t>((P.Q + 255) / 256, 1184), 256, 0, st>>>(P);
     k_compact<<<1, 1024, 0, st>>>(P);
+    count_launches(2);
   }
   return cudaGetLastError();
 }
@@ -1692,6 +1713,7 @@ template <typename KT>
 cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st) {
   if (block != kEngineThreads) return cudaErrorInvalidValue;  // the kernel's team split is compile-time
   k_engine<KT><<<grid, block, smem, st>>>(P);
+  count_launches(1);
   return cudaGetLastError();
 }
 template <typename KT>
@@ -1713,11 +1735,13 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
                                            (int64_t)grid * 4);
   k_copy_run<KT><<<cgrid, 256, 0, st>>>(P, x0, x1);
   k_consumers<<<(int)std::min<int64_t>((P.Q + 255) / 256, 4096), 256, 0, st>>>(P, buf_a);
+  count_launches(2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, buf_a);
+  count_launches(1);
   return cudaGetLastError();
 }
 template <typename KT>
@@ -1725,6 +1749,7 @@ cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cuda
   cudaError_t e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, 1);
+  count_launches(1);
   return cudaGetLastError();
 }
 template cudaError_t launch_merge_copy<int32_t>(const EngineParams&, int, size_t, cudaStream_t);

@@ -7,6 +7,8 @@
 #include "pm_engine.cuh"
 
 namespace pm {
+// every kernel launch of the library bumps this process-wide count (pm_launch_count)
+void count_launches(int n);
 template <typename KT> cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st);
 template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "pm_common.cuh"
+#include "pm_launch.h"
 #include "pm_search.cuh"
 
 namespace pm {
@@ -63,6 +64,7 @@ __global__ void k_plan_intervals(const KT* keys, int64_t s, int64_t m, int64_t e
 template <typename KT>
 cudaError_t launch_find_median(const void* a, const void* b, int64_t la, int64_t lb, int64_t* out, cudaStream_t st) {
   k_find_median<KT><<<1, 32, 0, st>>>(reinterpret_cast<const KT*>(a), reinterpret_cast<const KT*>(b), la, lb, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 template <typename KT>
@@ -70,6 +72,7 @@ cudaError_t launch_find_splits(const void* a, const void* b, int64_t la, int64_t
                                int64_t* out_a, int grid, cudaStream_t st) {
   k_find_splits<KT><<<grid, 256, 0, st>>>(reinterpret_cast<const KT*>(a), reinterpret_cast<const KT*>(b), la, lb,
                                           diags, nd, out_a);
+  count_launches(1);
   return cudaGetLastError();
 }
 template <typename KT>
@@ -77,6 +80,7 @@ cudaError_t launch_plan_intervals(const void* keys, int64_t s, int64_t m, int64_
                                   cudaStream_t st) {
   int block = levels >= 8 ? 256 : (1 << (levels > 5 ? levels : 5));
   k_plan_intervals<KT><<<1, block, 0, st>>>(reinterpret_cast<const KT*>(keys), s, m, e, levels, nodes);
+  count_launches(1);
   return cudaGetLastError();
 }
 template cudaError_t launch_find_median<int32_t>(const void*, const void*, int64_t, int64_t, int64_t*, cudaStream_t);

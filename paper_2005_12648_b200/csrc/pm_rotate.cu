@@ -175,10 +175,12 @@ cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int6
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(jobs(la + lb, 0), (int64_t)num_sms * 8));
     if (pairs > 0) k_reverse_vec<KT, C><<<g1, 256, 0, st>>>(k, lo, la, lo + la, lb);
     if (all > 0) k_reverse_vec<KT, C><<<g2, 256, 0, st>>>(k, lo, la + lb, 0, 0);
+    count_launches((pairs > 0) + (all > 0));
     return cudaGetLastError();
   }
   if (pairs > 0) k_reverse<KT><<<grid_for(pairs), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);
   if (all > 0) k_reverse<KT><<<grid_for(all), 256, 0, st>>>(k, p, w, lo, la + lb, 0, 0);
+  count_launches((pairs > 0) + (all > 0));
   return cudaGetLastError();
 }
 template cudaError_t launch_rotate<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
