@@ -141,6 +141,11 @@ int pm_set_timing(pm_ctx *ctx, int on);
 /* Host evaluation of the engine's two-front ticket order (same source as the
  * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
+/* Debug: the wide-record path's in-place row permutation on its own:
+ * row p of payload (DEVICE, n rows of width bytes) becomes old row idx[p]
+ * (idx: DEVICE int32[n], a permutation), cycles cut every cut_every rows. */
+int pm_debug_permute_rows(pm_ctx *ctx, void *payload, int64_t width, const int32_t *idx, int64_t n,
+                          int32_t cut_every, void *stream);
 /* Copy the first n entries of the last job's split table to host memory (debug). */
 int pm_debug_splits(pm_ctx *ctx, int64_t *host_out, int64_t n);
 

@@ -176,3 +176,14 @@ def plan_nodes(arr: KeyedArray, start: int, middle: int, end: int, threads: int)
     _capi.check(rc, "pm_plan_intervals")
     v = out.view(-1, 4).tolist()
     return [tuple(int(x) for x in r) for r in v]
+
+
+def permute_rows(payload: torch.Tensor, idx: torch.Tensor, cut_every: int):
+    """Debug: the wide-record path's in-place row permutation, payload[p] <- old payload[idx[p]]
+    (pm_debug_permute_rows).  payload: CUDA uint8 [n, w]; idx: CUDA int32 [n], a permutation."""
+    if not (payload.is_cuda and idx.is_cuda) or idx.dtype != torch.int32 or not payload.is_contiguous():
+        raise ValueError("permute_rows needs contiguous CUDA tensors (uint8 rows, int32 indices)")
+    dev = payload.device.index
+    rc = _capi.lib().pm_debug_permute_rows(_capi.context(dev), _ptr(payload), payload.shape[1], _ptr(idx),
+                                           payload.shape[0], cut_every, _stream(dev))
+    _capi.check(rc, "pm_debug_permute_rows")

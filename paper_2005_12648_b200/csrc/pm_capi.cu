@@ -72,6 +72,10 @@ struct pm_ctx {
   cudaEvent_t hev[33] = {};                          // [0]: joins; then per-chunk events (ring)
   void* buf = nullptr;    // min-side buffer of the buffered mode
   size_t buf_bytes = 0;
+  void* wide = nullptr;   // wide records: row indices, merged keys
+  size_t wide_bytes = 0;
+  void* wperm = nullptr;  // in-place row permutation: cycle tables, uncut heads, saved cut rows
+  size_t wperm_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   bool ev_recorded = false;
@@ -106,16 +110,85 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
   return true;
 }
 
+static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
+                      int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
+                      void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr);
+
+// Payload rows of at least PM_WIDE_MIN bytes (or too wide for the staging tiles)
+// take the wide-record path (pm_wide.cu): the stable merge of (key, row index)
+// pairs in copy mode, then the row permutation -- a gather into the destination
+// (copy mode) or the in-place cycle walk over segments cut every G rows.
+#ifndef PM_WIDE_MIN
+#define PM_WIDE_MIN 256  // tune: bytes per payload row from which the wide path runs
+#endif
+#ifndef PM_WIDE_SAVE_BYTES
+#define PM_WIDE_SAVE_BYTES (256ll << 20)  // bound on the saved cut rows (G grows past 16 to respect it)
+#endif
+// In-place row permutation new_row[p] = old_row[idx[p]] (idx: DEVICE int32[n], a
+// permutation of [0, n)), cycles cut every G rows (pm_wide.cu).
+static int permute_rows(pm_ctx* ctx, uint8_t* pay, int64_t w, const int32_t* idx, int64_t n, int32_t G,
+                        cudaStream_t st) {
+  const int64_t ncut = (n + G - 1) / G;
+  const size_t o_d1 = (size_t)align_up(n * 8, 256);
+  const size_t o_heads = o_d1 + (size_t)align_up(n * 8, 256);
+  const size_t o_unres = o_heads + (size_t)align_up(n * 4, 256);
+  const size_t o_ctl = o_unres + (size_t)align_up(n, 256);
+  const size_t o_save = o_ctl + 256;
+  int rc = ensure(&ctx->wperm, &ctx->wperm_bytes, o_save + (size_t)(ncut * w));
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->wperm);
+  cudaError_t ce = launch_cycle_permute(pay, w, idx, n, G, reinterpret_cast<int2*>(base), reinterpret_cast<int2*>(base + o_d1),
+                                        reinterpret_cast<int32_t*>(base + o_heads), reinterpret_cast<int32_t*>(base + o_ctl),
+                                        reinterpret_cast<uint8_t*>(base + o_unres), reinterpret_cast<uint8_t*>(base + o_save),
+                                        ctx->num_sms, st);
+  return ce == cudaSuccess ? PM_OK : cuda_fail(ce, "cycle permutation launch");
+}
+
+static int run_wide(pm_ctx* ctx, char* keys, int ks, uint8_t* pay, int64_t w, int64_t s, int64_t m, int64_t e,
+                    cudaStream_t st, char* out_keys, uint8_t* out_pay, const char* keys_b, const uint8_t* pay_b) {
+  const bool copy = out_keys != nullptr;
+  const int64_t n = e - s, la = m - s;
+  if (n >= INT32_MAX) return fail(PM_ERR_UNSUPPORTED, "wide-record merges index rows with 32 bits");
+  const size_t o_idx = (size_t)align_up(n * 4, 256);
+  const size_t o_tmpk = o_idx + (size_t)align_up(n * 4, 256);
+  const size_t need = o_tmpk + (size_t)(copy ? 0 : align_up(n * ks, 256));
+  int rc = ensure(&ctx->wide, &ctx->wide_bytes, need);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->wide);
+  int32_t* idx0 = reinterpret_cast<int32_t*>(base);
+  int32_t* idx = reinterpret_cast<int32_t*>(base + o_idx);
+  cudaError_t ce = launch_iota(idx0, n, ctx->num_sms, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_iota launch");
+  // (1) merged keys + the source row of every output position
+  rc = run_engine(ctx, keys + s * ks, ks, idx0, 4, 0, la, n, MODE_MERGE, 0, st, copy ? out_keys + s * ks : base + o_tmpk,
+                  idx, keys_b, keys_b ? idx0 + la : nullptr);
+  if (rc) return rc;
+  uint8_t* a = pay + s * w;
+  if (copy) {  // (2) gather
+    ce = launch_gather_rows(out_pay + s * w, a, pay_b ? pay_b : a + la * w, idx, n, la, w, ctx->num_sms, st);
+    return ce == cudaSuccess ? PM_OK : cuda_fail(ce, "k_gather_rows launch");
+  }
+  PM_CUDA(cudaMemcpyAsync(keys + s * ks, base + o_tmpk, (size_t)(n * ks), cudaMemcpyDeviceToDevice, st));
+  // (2) in-place cycle permutation of the rows; cut every G rows, G >= 16 bounded by the save budget
+  int32_t G = 16;
+  while (G < n && ((n + G - 1) / G) * w > PM_WIDE_SAVE_BYTES) G *= 2;
+  return permute_rows(ctx, a, w, idx, n, G, st);
+}
+
 // out_keys / out_payload non-null: copy mode -- merge keys[s,m) and keys[m,e) into
 // out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
 // keys_b / pay_b (copy mode only): the B run lives there instead of at keys + m.
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                      int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
-                      void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr) {
+                      int mode, int64_t scratch_records, cudaStream_t st, void* out_keys, void* out_payload,
+                      const void* keys_b, const void* pay_b) {
   const bool copy = out_keys != nullptr;
   if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
   int32_t mu;
+  if (mode == MODE_MERGE && w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &M, &T, &mu)))
+    return run_wide(ctx, static_cast<char*>(keys), ks, static_cast<uint8_t*>(payload), w, s, m, e, st,
+                    static_cast<char*>(out_keys), static_cast<uint8_t*>(out_payload),
+                    static_cast<const char*>(keys_b), static_cast<const uint8_t*>(pay_b));
   // buffered mode (the caller granted a min(|A|,|B|) buffer, seq_merge_buffered):
   // half-size regions, two staging + two output tiles (72 KB of shared memory)
 #ifndef PM_USE_BUFFERED
@@ -309,6 +382,15 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   return PM_OK;
 }
 
+int pm_debug_permute_rows(pm_ctx* ctx, void* payload, int64_t width, const int32_t* idx, int64_t n, int32_t cut_every,
+                          void* stream) {
+  if (!ctx || (n && (!payload || !idx)) || width <= 0 || n < 0 || n >= INT32_MAX || cut_every < 1)
+    return fail(PM_ERR_ARG, "bad pm_debug_permute_rows arguments");
+  if (n == 0) return PM_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return permute_rows(ctx, static_cast<uint8_t*>(payload), width, idx, n, cut_every, static_cast<cudaStream_t>(stream));
+}
+
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t* out4) {
   if (Q < 1 || qc < 0 || qc >= Q || t < 0 || t >= Q || !out4) return fail(PM_ERR_ARG, "bad order arguments");
   TwoFront tf{Q, qc};
@@ -351,6 +433,8 @@ int pm_ctx_destroy(pm_ctx* ctx) {
   if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->buf) cudaFree(ctx->buf);
+  if (ctx->wide) cudaFree(ctx->wide);
+  if (ctx->wperm) cudaFree(ctx->wperm);
   for (auto& x : ctx->hs)
     if (x) cudaStreamDestroy(x);
   for (auto& x : ctx->hev)

@@ -27,4 +27,11 @@ cudaError_t launch_find_splits(const void* a, const void* b, int64_t la, int64_t
 template <typename KT>
 cudaError_t launch_plan_intervals(const void* keys, int64_t s, int64_t m, int64_t e, int32_t levels, int64_t* nodes,
                                   cudaStream_t st);
+// wide records (pm_wide.cu): row index fill, out-of-place row gather, in-place cycle permutation
+cudaError_t launch_iota(int32_t* idx, int64_t n, int num_sms, cudaStream_t st);
+cudaError_t launch_gather_rows(uint8_t* out, const uint8_t* a, const uint8_t* b, const int32_t* idx, int64_t n,
+                               int64_t la, int64_t w, int num_sms, cudaStream_t st);
+cudaError_t launch_cycle_permute(uint8_t* pay, int64_t w, const int32_t* idx, int64_t n, int32_t G, int2* dbl0,
+                                 int2* dbl1, int32_t* heads, int32_t* ctl, uint8_t* unres, uint8_t* save, int num_sms,
+                                 cudaStream_t st);
 }  // namespace pm

@@ -411,3 +411,86 @@ def test_shift_offsets_and_alignment(dtype):
             pm.synchronize()
             got, _ = arr.numpy()
             assert np.array_equal(got, want), f"lo={lo} la={la} lb={lb} {dtype.__name__}"
+
+
+def _wide_cases(rng, width):
+    """Wide-row instances: random, heavy duplicates, exact interleave (many short
+    cycles), B entirely before A (one rotation), all-equal keys (identity).
+    Sizes shrink with the row width (at most ~150 MB of rows per case)."""
+    big = width > 4096
+    out = []
+    for size, split, domain in ((3000, 0.5, 40), (2000 if big else 20_000, 0.3, 2**31 - 1)):
+        out.append(random_instance(rng, size, split, domain, width))
+    n = 1024 if big else 4096
+    pay = lambda k: rng.integers(0, 256, (k, width), dtype=np.uint8)  # noqa: E731
+    ev = np.arange(0, 2 * n, 2, dtype=np.int32)
+    out.append((np.concatenate([ev, ev + 1]), pay(2 * n), n))           # perfect shuffle
+    out.append((np.concatenate([ev + 10 * n, ev]), pay(2 * n), n))      # rotation
+    out.append((np.zeros(2 * n, np.int32), pay(2 * n), n // 3))          # identity
+    return out
+
+
+@pytest.mark.parametrize("width", [252, 301, 508, 1020, 16380, 65536])
+def test_wide_records_vs_oracle(width):
+    """Rows up to the reference's 65 540-byte elements (bench.py:22): the wide-record
+    path (key+index merge, then gather / in-place cycle permutation) is exact."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(9000 + width)
+    cases = _wide_cases(rng, width)
+    for keys, payload, middle in cases:
+        size = len(keys)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+        arr = to_gpu(keys, payload)
+        _ops.merge(arr, 0, middle, size)
+        assert_same(arr, want_k, want_p, f"in place w={width} size={size} m={middle}")
+        sk, sp = torch.from_numpy(keys).cuda(), torch.from_numpy(payload).cuda()
+        dk, dp = torch.empty_like(sk), torch.empty_like(sp)
+        _ops.merge_copy(sk, sp, dk, dp, middle)
+        pm.synchronize()
+        assert np.array_equal(dk.cpu().numpy(), want_k) and np.array_equal(dp.cpu().numpy(), want_p)
+        if size <= 20_000 and width <= 1020:
+            hk, hp = keys.copy(), payload.copy()
+            _ops.merge_host(hk, hp, 0, middle, size)
+            assert np.array_equal(hk, want_k) and np.array_equal(hp, want_p)
+
+
+@pytest.mark.parametrize("width", [508, 16380])
+def test_wide_records_offset_jobs_public_api(width):
+    """Sub-range jobs (start > 0) through merge_srecpar / merge_soptmov with wide rows;
+    the rows outside the job are untouched."""
+    rng = np.random.default_rng(31 + width)
+    n = 6000 if width < 4096 else 1500
+    keys, payload, _ = random_instance(rng, n, 0.5, 1000, width)
+    s, e = 137, n - 91
+    m = (s + e) // 2 + 7
+    keys[s:m].sort()
+    keys[m:e].sort()
+    want_k, want_p = keys.copy(), payload.copy()
+    orc.seq_merge_buffered(want_k, want_p, s, m, e)
+    for fn in (pm.merge_srecpar, pm.merge_soptmov):
+        arr = to_gpu(keys, payload)
+        fn(arr, pm.MergeJob(s, m, e), 8)
+        assert_same(arr, want_k, want_p, f"{fn.__name__} w={width}")
+
+
+@pytest.mark.parametrize("cut_every", [1, 16, 1 << 30])
+@pytest.mark.parametrize("width", [4, 60, 4096 + 16, 333])
+def test_wide_row_permutation_cycles(cut_every, width):
+    """The in-place cycle walk on arbitrary permutations: random (long cycles; with no
+    cuts they exceed the bounded walk and take the pointer-doubling fallback), many
+    2-cycles, identity, one n-cycle."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(width * 7 + cut_every % 97)
+    n = 20_000 if width < 1000 else 3000
+    perms = [rng.permutation(n), np.arange(n), np.roll(np.arange(n), 1),
+             np.arange(n).reshape(-1, 2)[:, ::-1].reshape(-1)]
+    for perm in perms:
+        perm = perm.astype(np.int32)
+        rows = rng.integers(0, 256, (n, width), dtype=np.uint8)
+        dp = torch.from_numpy(rows).cuda()
+        _ops.permute_rows(dp, torch.from_numpy(perm).cuda(), cut_every)
+        pm.synchronize()
+        assert np.array_equal(dp.cpu().numpy(), rows[perm]), f"cut_every={cut_every} width={width}"
