@@ -157,6 +157,74 @@ __global__ void __launch_bounds__(256) k_reverse_vec(KT* keys, int64_t lo0, int6
   }
 }
 
+// Wide payload rows: one warp per (mirrored pair, column chunk) swaps the two
+// rows with V-byte vector words (lane 0 of chunk 0 also swaps the keys), so a
+// row pair moves coalesced instead of one thread walking a whole row.
+template <int V> struct RowWord;
+template <> struct RowWord<16> { using T = uint4; };
+template <> struct RowWord<8> { using T = uint2; };
+template <> struct RowWord<4> { using T = uint32_t; };
+template <> struct RowWord<2> { using T = uint16_t; };
+template <> struct RowWord<1> { using T = uint8_t; };
+
+template <typename KT, int V>
+__global__ void __launch_bounds__(256) k_reverse_wide(KT* keys, uint8_t* pay, int64_t w, int64_t lo0, int64_t len0,
+                                                      int64_t lo1, int64_t len1) {
+  using T = typename RowWord<V>::T;
+  constexpr int CW = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = w / V, span = 32 * CW, nch = (W + span - 1) / span;
+  const int64_t p0 = len0 >> 1, np = p0 + (len1 >> 1), items = np * nch;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += nw) {
+    const int64_t p = it / nch, c0 = (it - p * nch) * span;
+    const bool s0 = p < p0;
+    const int64_t i = s0 ? p : p - p0, lo = s0 ? lo0 : lo1, len = s0 ? len0 : len1;
+    const int64_t xl = lo + i, xr = lo + len - 1 - i;
+    if (c0 == 0 && lane == 0) {
+      const KT a = keys[xl];
+      keys[xl] = keys[xr];
+      keys[xr] = a;
+    }
+    T* L = reinterpret_cast<T*>(pay + xl * w);
+    T* R = reinterpret_cast<T*>(pay + xr * w);
+    T a[CW], b[CW];
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+      const int64_t x = c0 + u * 32 + lane;
+      if (x < W) {
+        a[u] = L[x];
+        b[u] = R[x];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+      const int64_t x = c0 + u * 32 + lane;
+      if (x < W) {
+        L[x] = b[u];
+        R[x] = a[u];
+      }
+    }
+  }
+}
+
+template <typename KT, int V>
+static void reverse_wide_pair(KT* k, uint8_t* p, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
+                              cudaStream_t st) {
+  const int64_t nch = (w / V + 127) / 128;
+  const int64_t pairs = (la >> 1) + (lb >> 1), all = (la + lb) >> 1;
+  auto grid_for = [&](int64_t items) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)num_sms * 8));
+  };
+  if (pairs > 0) k_reverse_wide<KT, V><<<grid_for(pairs * nch), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);
+  if (all > 0) k_reverse_wide<KT, V><<<grid_for(all * nch), 256, 0, st>>>(k, p, w, lo, la + lb, 0, 0);
+  count_launches((pairs > 0) + (all > 0));
+}
+
+#ifndef PM_ROTATE_WIDE_MIN
+#define PM_ROTATE_WIDE_MIN 32  // payload bytes per row from which rows move warp-wide
+#endif
+
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st) {
@@ -176,6 +244,15 @@ cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int6
     if (pairs > 0) k_reverse_vec<KT, C><<<g1, 256, 0, st>>>(k, lo, la, lo + la, lb);
     if (all > 0) k_reverse_vec<KT, C><<<g2, 256, 0, st>>>(k, lo, la + lb, 0, 0);
     count_launches((pairs > 0) + (all > 0));
+    return cudaGetLastError();
+  }
+  if (w >= PM_ROTATE_WIDE_MIN) {
+    const uintptr_t al = (uintptr_t)p | (uintptr_t)w;
+    if ((al & 15) == 0) reverse_wide_pair<KT, 16>(k, p, w, lo, la, lb, num_sms, st);
+    else if ((al & 7) == 0) reverse_wide_pair<KT, 8>(k, p, w, lo, la, lb, num_sms, st);
+    else if ((al & 3) == 0) reverse_wide_pair<KT, 4>(k, p, w, lo, la, lb, num_sms, st);
+    else if ((al & 1) == 0) reverse_wide_pair<KT, 2>(k, p, w, lo, la, lb, num_sms, st);
+    else reverse_wide_pair<KT, 1>(k, p, w, lo, la, lb, num_sms, st);
     return cudaGetLastError();
   }
   if (pairs > 0) k_reverse<KT><<<grid_for(pairs), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);

@@ -494,3 +494,20 @@ def test_wide_row_permutation_cycles(cut_every, width):
         _ops.permute_rows(dp, torch.from_numpy(perm).cuda(), cut_every)
         pm.synchronize()
         assert np.array_equal(dp.cpu().numpy(), rows[perm]), f"cut_every={cut_every} width={width}"
+
+
+@pytest.mark.parametrize("width", [32, 60, 301, 508, 16380])
+def test_shift_wide_rows(width):
+    """Block exchange with wide payload rows (warp-wide row swaps), both shift kinds and
+    sub-range regions, against the oracle's rotation."""
+    rng = np.random.default_rng(500 + width)
+    sizes = [(1, 777), (777, 1), (1000, 333), (5, 7)] if width < 4096 else [(100, 33), (1, 64), (7, 5)]
+    for la, lb in sizes:
+        keys = rng.integers(-1000, 1000, la + lb + 10).astype(np.int32)
+        payload = rng.integers(0, 256, (la + lb + 10, width), dtype=np.uint8)
+        wk, wp = keys.copy(), payload.copy()
+        wk[3:3 + la + lb], wp[3:3 + la + lb] = orc.rotate_oracle(keys[3:3 + la + lb], payload[3:3 + la + lb], la)
+        for kind in ("linear", "circular"):
+            arr = to_gpu(keys, payload)
+            pm.shift_region(arr, 3, la, lb, kind)
+            assert_same(arr, wk, wp, f"shift_region {kind} {la},{lb},w={width}")
