@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e/cpu/clock legs (profiling runs)")
     ap.add_argument("--no-buffered", action="store_true", help="skip the buffered-mode leg")
     ap.add_argument("--dist", action="store_true", help="distributed block merge even at one rank")
+    ap.add_argument("--no-sweep", action="store_true", help="skip config 2's size sweep leg")
     return ap.parse_args()
 
 
@@ -515,6 +516,45 @@ def run_ours(args):
                      "what": "pm_merge_copy: out-of-place merge into a second buffer (1 read + 1 write per record)"}
         del dk, dp
 
+    # ---- config 2's size sweep (L_A = L_B = 2^10 ... 2^28 in powers of 4): in place + copy ----
+    sweep = None
+    if rank == 0 and args.cfg == 2 and not args.quick and not args.no_sweep:
+        log("size sweep")
+        sweep = []
+        for lg in range(10, 29, 2):
+            k0, p0, mid = config_input_device(2, seed=2000 + lg, log_len=lg)
+            nn = k0.numel()
+            a = pm.KeyedArray(k0.clone(), p0.clone())
+            dk = torch.empty_like(k0)
+            ti, tc = [], []
+            for i in range(8):
+                a.keys.copy_(k0)
+                ev0.record(stream)
+                rc = L.pm_merge(ctx, ctypes.c_void_p(a.keys.data_ptr()), 4, ctypes.c_void_p(0), 0, 0, mid, nn, 0,
+                                ctypes.c_void_p(stream.cuda_stream))
+                _capi.check(rc, "pm_merge(sweep)")
+                ev1.record(stream)
+                ev1.synchronize()
+                ti.append(ev0.elapsed_time(ev1))
+                ev0.record(stream)
+                rc = L.pm_merge_copy(ctx, ctypes.c_void_p(k0.data_ptr()), ctypes.c_void_p(0),
+                                     ctypes.c_void_p(dk.data_ptr()), ctypes.c_void_p(0), 4, 0, mid, nn - mid,
+                                     ctypes.c_void_p(stream.cuda_stream))
+                _capi.check(rc, "pm_merge_copy(sweep)")
+                ev1.record(stream)
+                ev1.synchronize()
+                tc.append(ev0.elapsed_time(ev1))
+            _capi.status(local, stream.cuda_stream)
+            srt = torch.sort(k0).values
+            ok = torch.equal(a.keys, srt) and torch.equal(dk, srt)
+            mi, mc = statistics.median(ti[1:]), statistics.median(tc[1:])
+            sweep.append({"log_len_per_side": lg, "n": nn, "inplace_ms": round(mi, 4),
+                          "inplace_rec_per_s": nn / (mi / 1e3), "inplace_frac": (8 * nn / (mi / 1e3) / 1e9) / peak,
+                          "copy_ms": round(mc, 4), "copy_rec_per_s": nn / (mc / 1e3),
+                          "copy_frac": (8 * nn / (mc / 1e3) / 1e9) / peak, "sorted_ok": bool(ok),
+                          "l2": "warm (input restored just before)" if 8 * nn < 96 << 20 else "exceeds L2"})
+            del k0, p0, a, dk, srt
+
     # ---- end to end through the C-ABI host entry point (pinned host buffers) ----
     e2e = None
     log("e2e")
@@ -572,6 +612,7 @@ def run_ours(args):
             "salvaged_records_frac": stats[1] / n,
             "buffered_mode": buffered,
             "copy_mode": copy_mode,
+            "size_sweep": sweep,
             "regions": stats[2], "identity_regions": stats[3],
         }
         if sampler:

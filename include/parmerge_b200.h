@@ -141,6 +141,10 @@ int pm_set_timing(pm_ctx *ctx, int on);
 /* Host evaluation of the engine's two-front ticket order (same source as the
  * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
+/* Debug: on != 0 routes every in-place merge of this context through the
+ * bounded-scratch engine (no one-CTA small-job or staged shortcut), so tests
+ * exercise it at small sizes. */
+int pm_debug_engine_only(pm_ctx *ctx, int on);
 /* Debug: the wide-record path's in-place row permutation on its own:
  * row p of payload (DEVICE, n rows of width bytes) becomes old row idx[p]
  * (idx: DEVICE int32[n], a permutation), cycles cut every cut_every rows. */

@@ -187,3 +187,10 @@ def permute_rows(payload: torch.Tensor, idx: torch.Tensor, cut_every: int):
     rc = _capi.lib().pm_debug_permute_rows(_capi.context(dev), _ptr(payload), payload.shape[1], _ptr(idx),
                                            payload.shape[0], cut_every, _stream(dev))
     _capi.check(rc, "pm_debug_permute_rows")
+
+
+def set_engine_only(on: bool, device: int | None = None):
+    """Debug: route in-place merges through the bounded-scratch engine even for small
+    jobs (pm_debug_engine_only); tests use it to cover the engine at small sizes."""
+    dev = torch.cuda.current_device() if device is None else device
+    _capi.check(_capi.lib().pm_debug_engine_only(_capi.context(dev), int(bool(on))), "pm_debug_engine_only")

@@ -77,6 +77,7 @@ struct pm_ctx {
   void* wperm = nullptr;  // in-place row permutation: cycle tables, uncut heads, saved cut rows
   size_t wperm_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
+  bool engine_only = false;  // debug: no small-job / staged shortcuts (pm_debug_engine_only)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   bool ev_recorded = false;
 };
@@ -113,6 +114,19 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
                       void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr);
+
+#ifndef PM_SMALL_BYTES
+#define PM_SMALL_BYTES (200 * 1024)  // records staged by the one-CTA small merge (shared memory)
+#endif
+#ifndef PM_STAGE_BYTES
+#define PM_STAGE_BYTES (256ll << 20)  // in-place jobs up to this size merge via a staging buffer (a constant, below the engine pool)
+#endif
+static int launch_merge_small_(int ks, void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
+                               cudaStream_t st) {
+  cudaError_t ce = ks == 4 ? launch_merge_small<int32_t>(keys, payload, w, s, m, e, st)
+                           : launch_merge_small<int64_t>(keys, payload, w, s, m, e, st);
+  return ce == cudaSuccess ? PM_OK : cuda_fail(ce, "k_merge_small launch");
+}
 
 // Payload rows of at least PM_WIDE_MIN bytes (or too wide for the staging tiles)
 // take the wide-record path (pm_wide.cu): the stable merge of (key, row index)
@@ -185,6 +199,26 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
   int32_t mu;
+  // small in-place jobs: one CTA with both runs in shared memory
+  if (mode == MODE_MERGE && !copy && !ctx->engine_only && small_merge_smem(ks, w, e - s) <= PM_SMALL_BYTES)
+    return launch_merge_small_(ks, keys, payload, w, s, m, e, st);
+  // medium in-place jobs (at most PM_STAGE_BYTES of records): the streaming merge
+  // into a staging buffer, then one copy back -- both passes mostly in L2
+  if (mode == MODE_MERGE && !copy && !ctx->engine_only && (e - s) * (ks + w) <= PM_STAGE_BYTES && w < PM_WIDE_MIN) {
+    const int64_t n = e - s;
+    const size_t kb = (size_t)align_up(n * ks + 16, 256);  // + the phase offset below
+    int rc = ensure(&ctx->buf, &ctx->buf_bytes, kb + (size_t)(n * w) + 256);
+    if (rc) return rc;
+    char* sk = static_cast<char*>(ctx->buf) + (((uintptr_t)keys + s * ks) & 15);
+    uint8_t* sp = reinterpret_cast<uint8_t*>(static_cast<char*>(ctx->buf) + kb + (w ? (((uintptr_t)payload + s * w) & 15) : 0));
+    char* k0 = static_cast<char*>(keys) + s * ks;
+    uint8_t* p0 = w ? static_cast<uint8_t*>(payload) + s * w : nullptr;
+    rc = run_engine(ctx, k0, ks, p0, w, 0, m - s, n, MODE_MERGE, 0, st, sk, w ? sp : nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    PM_CUDA(cudaMemcpyAsync(k0, sk, (size_t)(n * ks), cudaMemcpyDeviceToDevice, st));
+    if (w) PM_CUDA(cudaMemcpyAsync(p0, sp, (size_t)(n * w), cudaMemcpyDeviceToDevice, st));
+    return PM_OK;
+  }
   if (mode == MODE_MERGE && w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &M, &T, &mu)))
     return run_wide(ctx, static_cast<char*>(keys), ks, static_cast<uint8_t*>(payload), w, s, m, e, st,
                     static_cast<char*>(out_keys), static_cast<uint8_t*>(out_payload),
@@ -379,6 +413,13 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   if (!ctx || !host_out || n < 0) return fail(PM_ERR_ARG, "bad arguments");
   PM_CUDA(cudaDeviceSynchronize());
   PM_CUDA(cudaMemcpy(host_out, ctx->ws, (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return PM_OK;
+}
+
+int pm_debug_engine_only(pm_ctx* ctx, int on) {
+  if (!ctx) return fail(PM_ERR_ARG, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->engine_only = on != 0;
   return PM_OK;
 }
 

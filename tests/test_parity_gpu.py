@@ -22,6 +22,18 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 
+@pytest.fixture(autouse=True, params=["auto", "engine"])
+def route(request):
+    """Every parity test runs twice: with the library's own routing (one-CTA small
+    jobs, staged medium jobs, wide-record path) and with in-place merges forced
+    through the bounded-scratch engine."""
+    from paper_2005_12648_b200 import _ops
+
+    _ops.set_engine_only(request.param == "engine")
+    yield request.param
+    _ops.set_engine_only(False)
+
+
 def sha(*arrays):
     h = hashlib.sha256()
     for a in arrays:
