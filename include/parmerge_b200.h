@@ -79,7 +79,9 @@ int pm_merge_copy(pm_ctx *ctx, const void *src_keys, const void *src_payload, vo
 
 /*
  * In-place block exchange A|B -> B|A of [lo, lo+len_a) and [lo+len_a,
- * lo+len_a+len_b).  Replaces _kernels.linear_shift (_kernels.py:92-150) and
+ * lo+len_a+len_b).  When the smaller block fits a 64 MB stash it is staged and
+ * the larger block slides over it in one pass (the reference's staged exchange,
+ * _kernels.py:46-90); otherwise three streaming reversals (two passes).  Replaces _kernels.linear_shift (_kernels.py:92-150) and
  * _kernels.circular_shift (_kernels.py:154-197) behind shift_region /
  * linear_shift / circular_shift (shift.py:38-55); both kinds produce the same
  * array (tests/test_srecpar.py:70-80 of the reference).
@@ -142,8 +144,9 @@ int pm_set_timing(pm_ctx *ctx, int on);
  * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
 /* Debug: on != 0 routes every in-place merge of this context through the
- * bounded-scratch engine (no one-CTA small-job or staged shortcut), so tests
- * exercise it at small sizes. */
+ * bounded-scratch engine (no one-CTA small-job or staged shortcut) and every
+ * block exchange through the three reversals (no one-pass slide), so tests
+ * exercise those paths at small sizes. */
 int pm_debug_engine_only(pm_ctx *ctx, int on);
 /* Debug: the wide-record path's in-place row permutation on its own:
  * row p of payload (DEVICE, n rows of width bytes) becomes old row idx[p]

@@ -115,6 +115,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
                       void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr);
 
+#ifndef PM_SLIDE_STASH
+#define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
+#endif
 #ifndef PM_SMALL_BYTES
 #define PM_SMALL_BYTES (200 * 1024)  // records staged by the one-CTA small merge (shared memory)
 #endif
@@ -541,8 +544,40 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
   if (rc) return rc;
   if (lo < 0 || len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "lengths must be non-negative");  // shift.py:157
   if (len_a == 0 || len_b == 0) return PM_OK;
-  // three reversals (pm_rotate.cu): two streaming passes, no workspace
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // one small block: stash it, slide the big block over it in one pass, land the
+  // stash at the far end (the reference's staged exchange, _kernels.py:46-90)
+  const int64_t small = std::min(len_a, len_b), big = std::max(len_a, len_b);
+  const int64_t rb = key_bytes + width;
+  if (small * rb <= PM_SLIDE_STASH && !ctx->engine_only) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const int64_t ntk = (big * key_bytes + 32767) / 32768, ntp = (big * width + 32767) / 32768;
+    const size_t sk = (size_t)align_up(small * key_bytes, 256), sp = (size_t)align_up(small * width, 256);
+    const size_t fl = (size_t)align_up((ntk + ntp + 2) * 4, 256);
+    rc = ensure(&ctx->buf, &ctx->buf_bytes, sk + sp + fl);
+    if (rc) return rc;
+    char* stash_k = static_cast<char*>(ctx->buf);
+    char* stash_p = stash_k + sk;
+    int32_t* flags = reinterpret_cast<int32_t*>(stash_p + sp);
+    char* K = static_cast<char*>(keys);
+    char* Pp = static_cast<char*>(payload);
+    const bool a_small = len_a <= len_b;
+    // the small block's first record, the big block's first record, where the stash lands
+    const int64_t xs = a_small ? lo : lo + len_a, xb = a_small ? lo + len_a : lo;
+    const int64_t xdst = a_small ? lo + len_b : lo;
+    PM_CUDA(cudaMemcpyAsync(stash_k, K + xs * key_bytes, (size_t)(small * key_bytes), cudaMemcpyDeviceToDevice, st));
+    if (width) PM_CUDA(cudaMemcpyAsync(stash_p, Pp + xs * width, (size_t)(small * width), cudaMemcpyDeviceToDevice, st));
+    cudaError_t e = launch_slide(K, xb * key_bytes, big * key_bytes, small * key_bytes, !a_small, flags,
+                                 flags + ntk + ntp, &ctx->ctl->err_.v, ctx->num_sms, st);
+    if (e == cudaSuccess && width)
+      e = launch_slide(Pp, xb * width, big * width, small * width, !a_small, flags + ntk, flags + ntk + ntp + 1,
+                       &ctx->ctl->err_.v, ctx->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_slide launch");
+    PM_CUDA(cudaMemcpyAsync(K + xdst * key_bytes, stash_k, (size_t)(small * key_bytes), cudaMemcpyDeviceToDevice, st));
+    if (width) PM_CUDA(cudaMemcpyAsync(Pp + xdst * width, stash_p, (size_t)(small * width), cudaMemcpyDeviceToDevice, st));
+    return PM_OK;
+  }
+  // three reversals (pm_rotate.cu): two streaming passes, no workspace
   const cudaError_t e = key_bytes == 4
                             ? launch_rotate<int32_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st)
                             : launch_rotate<int64_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "pm_common.cuh"
 #include "pm_launch.h"
 
 namespace pm {
@@ -224,6 +225,108 @@ static void reverse_wide_pair(KT* k, uint8_t* p, int64_t w, int64_t lo, int64_t 
 #ifndef PM_ROTATE_WIDE_MIN
 #define PM_ROTATE_WIDE_MIN 32  // payload bytes per row from which rows move warp-wide
 #endif
+
+// ---- one-pass block exchange when one block is small (the reference's staged
+// exchange, _kernels.py:46-90, for blocks of up to PM_SLIDE_STASH bytes) ----
+// The small block is stashed (stream-ordered copies on the host side), the big
+// block slides over it in one pass, the stash lands at the far end.  The slide
+// is an overlapping move: plane bytes [S0, S0+L) move by -D (left) or +D
+// (right).  A persistent grid claims kSlideTile-byte source tiles in the
+// direction of the move (ascending for left), stages a tile in shared memory,
+// publishes "read" for it, waits until every earlier-claimed tile whose source
+// the tile's destination overlaps has been read, then writes the destination
+// (16-byte stores; bytewise at the range edges).  Waits only ever target tiles
+// claimed earlier by resident CTAs, so they always resolve.
+constexpr int kSlideTile = 32768;
+constexpr int kSlideThreads = 256;
+
+__global__ void __launch_bounds__(kSlideThreads) k_slide(uint8_t* plane, int64_t S0, int64_t L, int64_t D, int right,
+                                                         int32_t* flags, int32_t* ticket, int32_t* err) {
+  __shared__ __align__(16) uint8_t tile[kSlideTile + 32];
+  __shared__ int64_t s_i;
+  const int64_t ntiles = (L + kSlideTile - 1) / kSlideTile;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int64_t t = atomicAdd(ticket, 1);
+      s_i = t < ntiles ? (right ? ntiles - 1 - t : t) : -1;
+    }
+    __syncthreads();
+    const int64_t i = s_i;
+    __syncthreads();
+    if (i < 0) break;
+    const int64_t s0 = S0 + i * kSlideTile, s1 = min(S0 + L, s0 + kSlideTile);
+    // stage the 16-byte-aligned superset of [s0, s1)
+    const uintptr_t sb = (uintptr_t)(plane + s0) & ~(uintptr_t)15;
+    const uintptr_t se = ((uintptr_t)(plane + s1) + 15) & ~(uintptr_t)15;
+    const int nv = (int)((se - sb) >> 4);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x)
+      reinterpret_cast<uint4*>(tile)[v] = __ldcs(reinterpret_cast<const uint4*>(sb) + v);
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(&flags[i], 1);  // this tile's source is read
+    // source tiles the destination overlaps (other than i): wait until read
+    const int64_t d0 = right ? s0 + D : s0 - D, d1 = right ? s1 + D : s1 - D;
+    const int64_t lo = max(d0, S0), hi = min(d1, S0 + L);  // the part over the big block's source
+    if (hi > lo) {
+      const int64_t j0 = (lo - S0) / kSlideTile, j1 = (hi - 1 - S0) / kSlideTile;
+      for (int64_t j = j0 + threadIdx.x; j <= j1; j += blockDim.x) {
+        if (j == i) continue;
+        for (uint32_t it = 0; ld_acquire(&flags[j]) == 0; ++it) {
+          if (it > kSpinLimit) {
+            raise_error(err, PM_ERR_TIMEOUT);
+            break;
+          }
+          backoff(it);
+        }
+      }
+    }
+    __syncthreads();
+    // destination [d0, d1): aligned 16-byte chunks from the staged bytes at +/-D
+    const int64_t shift = right ? -D : D;  // smem byte for destination x: x + shift - (sb - plane)
+    const int64_t base = (int64_t)(sb - (uintptr_t)plane);
+    const uintptr_t c0 = ((uintptr_t)(plane + d0) + 15) & ~(uintptr_t)15;
+    const uintptr_t c1 = (uintptr_t)(plane + d1) & ~(uintptr_t)15;
+    const bool w4 = (D & 3) == 0;
+    if (c1 > c0) {
+      const int64_t nc = (int64_t)((c1 - c0) >> 4);
+      for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) {
+        const int64_t x = (int64_t)(c0 - (uintptr_t)plane) + c * 16;  // plane offset of the chunk
+        const int64_t off = x + shift - base;
+        uint4 v;
+        if (w4) {
+          const uint32_t* q = reinterpret_cast<const uint32_t*>(tile + off);
+          v = make_uint4(q[0], q[1], q[2], q[3]);
+        } else {
+          uint8_t* b = reinterpret_cast<uint8_t*>(&v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) b[k] = tile[off + k];
+        }
+        *reinterpret_cast<uint4*>(plane + x) = v;
+      }
+      // unaligned head [d0, c0) and tail [c1, d1)
+      const int64_t h = (int64_t)(c0 - (uintptr_t)(plane + d0)), tl = (int64_t)((uintptr_t)(plane + d1) - c1);
+      for (int64_t b = threadIdx.x; b < h + tl; b += blockDim.x) {
+        const int64_t x = b < h ? d0 + b : (int64_t)(c1 - (uintptr_t)plane) + (b - h);
+        plane[x] = tile[x + shift - base];
+      }
+    } else {
+      for (int64_t x = d0 + threadIdx.x; x < d1; x += blockDim.x) plane[x] = tile[x + shift - base];
+    }
+  }
+}
+
+cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool right, int32_t* flags, int32_t* ticket,
+                         int32_t* err, int num_sms, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  const int64_t ntiles = (L + kSlideTile - 1) / kSlideTile;
+  cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ntiles * sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ticket, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms * 6);
+  k_slide<<<grid, kSlideThreads, 0, st>>>(static_cast<uint8_t*>(plane), S0, L, D, right ? 1 : 0, flags, ticket, err);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
