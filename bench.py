@@ -25,6 +25,9 @@ import argparse
 import ctypes
 import json
 import os
+
+# NCCL's own messages (its version banner, NCCL_DEBUG output) go to stderr: stdout carries the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 import statistics
 import subprocess
 import sys
@@ -57,6 +60,8 @@ def parse():
     ap.add_argument("--no-buffered", action="store_true", help="skip the buffered-mode leg")
     ap.add_argument("--dist", action="store_true", help="distributed block merge even at one rank")
     ap.add_argument("--no-sweep", action="store_true", help="skip config 2's size sweep leg")
+    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="distributed path: NCCL all-to-all + local merge, or the merge reading peer blocks (IPC/NVLink)")
     return ap.parse_args()
 
 
@@ -249,7 +254,10 @@ def run_dist(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2005_12648_b200.dist import merge_distributed
+    from paper_2005_12648_b200.dist import merge_distributed, merge_distributed_p2p
+
+    if args.exchange == "p2p":
+        merge_distributed = merge_distributed_p2p  # noqa: F811
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -337,7 +345,10 @@ def run_dist(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"cfg5: int32 uniform sorted runs, block-distributed A|B, {n} records per GPU "
                                    f"(N = {N})", "key": "int32", "payload_bytes": 0, "L_A": la, "L_B": N - la,
-                       "parallelism": f"dist{world}: global stable splits + NCCL all-to-all + local copy merge (pm_merge_copy)",
+                       "parallelism": (f"dist{world}: global stable splits + NCCL all-to-all + local copy merge (pm_merge_copy)"
+                                       if args.exchange == "nccl" else
+                                       f"dist{world}: pm_merge_peers (merge reads peer blocks over NVLink via CUDA IPC) "
+                                       "+ barrier + copy into the block"),
                        "l2": "per-GPU blocks exceed the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": 2 * n * 4 / (total_ms / args.steps / 1e3) / 1e9 / peak,

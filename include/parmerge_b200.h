@@ -116,6 +116,32 @@ int pm_plan_intervals(pm_ctx *ctx, const void *keys, int key_bytes, int64_t star
                       int64_t end, int32_t threads, int64_t *nodes, void *stream);
 
 /*
+ * Multi-GPU merge with the partition exchange fused into the merge's loads.
+ * The global array X = A|B (A = X[0, len_a), B = X[len_a, N), N = world*block)
+ * is block-distributed: block k (records [k*block, (k+1)*block)) at
+ * peer_keys[k] / peer_payload[k] -- a HOST array of `world` DEVICE pointers,
+ * valid in this process (this GPU's own block, and the others' mapped through
+ * pm_ipc_open with NVLink peer access).  Writes rank `rank`'s share of the
+ * stable merge, X'[rank*block, (rank+1)*block), to out_keys / out_payload
+ * (this GPU; must not alias any block).  The global splits and the output
+ * positions of the block boundaries inside the rank's pieces come from merge
+ * path searches over the peer table (the median/split search of srecpar.py:
+ * 63-84 across GPUs); each resulting sub-range is one streaming merge whose
+ * TMA loads read the remote pieces over NVLink.  The caller keeps every block
+ * unmodified until all ranks have returned (a barrier), then may copy out
+ * into its block.  Synchronises `stream` (the searches are read back).
+ * the dist variant taking a peer-pointer table.
+ */
+int pm_merge_peers(pm_ctx *ctx, const void *const *peer_keys, const void *const *peer_payload, int world,
+                   int rank, int64_t block, int64_t len_a, int key_bytes, int64_t width, void *out_keys,
+                   void *out_payload, void *stream);
+/* CUDA IPC for the peer table: a 64-byte handle of a device allocation's base,
+ * its mapping in another process (NVLink peer access enabled lazily), unmap. */
+int pm_ipc_handle(void *device_ptr, void *out_handle64);
+int pm_ipc_open(const void *handle64, void **out_ptr);
+int pm_ipc_close(void *ptr);
+
+/*
  * Synchronise `stream`, then return (and clear) the sticky device status of the
  * context's last merges/shifts.  stats (host uint64[16], may be NULL) receives
  * the last job's counters: [0] salvaged units, [1] salvaged records, [2] merged

@@ -28,7 +28,8 @@ EXPORTED = (
     "pm_version", "pm_last_error", "pm_ctx_create", "pm_ctx_destroy", "pm_merge", "pm_shift",
     "pm_find_median", "pm_find_splits", "pm_plan_intervals", "pm_status", "pm_merge_host",
     "pm_set_timing", "pm_kernel_ms", "pm_debug_order", "pm_debug_splits", "pm_debug_stats", "pm_merge_copy", "pm_launch_count",
-    "pm_debug_permute_rows", "pm_debug_engine_only",
+    "pm_debug_permute_rows", "pm_debug_engine_only", "pm_merge_peers", "pm_ipc_handle", "pm_ipc_open",
+    "pm_ipc_close",
 )
 
 _lib = None
@@ -71,6 +72,10 @@ def lib() -> ctypes.CDLL:
         L.pm_debug_stats.argtypes = [vp, vp]
         L.pm_launch_count.argtypes = [vp]
         L.pm_debug_engine_only.argtypes = [vp, i32]
+        L.pm_merge_peers.argtypes = [vp, vp, vp, i32, i32, i64, i64, i32, i64, vp, vp, vp]
+        L.pm_ipc_handle.argtypes = [vp, vp]
+        L.pm_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+        L.pm_ipc_close.argtypes = [vp]
         L.pm_debug_permute_rows.argtypes = [vp, vp, i64, vp, i64, ctypes.c_int32, vp]
         L.pm_merge_copy.argtypes = [vp, vp, vp, vp, vp, i32, i64, i64, i64, vp]
         L.pm_kernel_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]

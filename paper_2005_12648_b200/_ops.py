@@ -194,3 +194,44 @@ def set_engine_only(on: bool, device: int | None = None):
     jobs (pm_debug_engine_only); tests use it to cover the engine at small sizes."""
     dev = torch.cuda.current_device() if device is None else device
     _capi.check(_capi.lib().pm_debug_engine_only(_capi.context(dev), int(bool(on))), "pm_debug_engine_only")
+
+
+def merge_peers(peer_keys: list, peer_payload: list | None, len_a: int, rank: int, out_keys: torch.Tensor,
+                out_payload: torch.Tensor | None = None, ptrs: tuple[list[int], list[int]] | None = None):
+    """pm_merge_peers: rank ``rank``'s block of the stable merge of the block-distributed
+    A|B (blocks ``peer_keys[k]`` of equal length, A = the first ``len_a`` global records).
+
+    ``ptrs`` optionally gives the (keys, payload) device addresses of the blocks directly
+    (mapped peer memory from pm_ipc_open); otherwise the tensors' own addresses are used.
+    """
+    world = len(peer_keys)
+    block = out_keys.numel()
+    w = out_payload.shape[1] if out_payload is not None else 0
+    kp = ptrs[0] if ptrs else [t.data_ptr() for t in peer_keys]
+    pp = ptrs[1] if ptrs else ([t.data_ptr() for t in peer_payload] if w else [0] * world)
+    tk = (ctypes.c_void_p * world)(*kp)
+    tp = (ctypes.c_void_p * world)(*pp)
+    dev = out_keys.device.index
+    rc = _capi.lib().pm_merge_peers(_capi.context(dev), tk, tp if w else None, world, rank, block, len_a,
+                                    out_keys.element_size(), w, _ptr(out_keys), _ptr(out_payload) if w else None,
+                                    _stream(dev))
+    _capi.check(rc, "pm_merge_peers")
+
+
+def ipc_handle(t: torch.Tensor) -> bytes:
+    """64-byte CUDA IPC handle of the allocation holding ``t`` (pm_ipc_handle) and t's offset in it."""
+    base = t.untyped_storage().data_ptr()
+    h = ctypes.create_string_buffer(64)
+    _capi.check(_capi.lib().pm_ipc_handle(ctypes.c_void_p(base), h), "pm_ipc_handle")
+    return h.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer's allocation (pm_ipc_open); returns the device address in this process."""
+    p = ctypes.c_void_p()
+    _capi.check(_capi.lib().pm_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)), "pm_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(addr: int):
+    _capi.check(_capi.lib().pm_ipc_close(ctypes.c_void_p(addr)), "pm_ipc_close")

@@ -76,6 +76,8 @@ struct pm_ctx {
   size_t wide_bytes = 0;
   void* wperm = nullptr;  // in-place row permutation: cycle tables, uncut heads, saved cut rows
   size_t wperm_bytes = 0;
+  void* peer = nullptr;   // pm_merge_peers: device copy of the peer table + queries + answers
+  size_t peer_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
   bool engine_only = false;  // debug: no small-job / staged shortcuts (pm_debug_engine_only)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -419,6 +421,108 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   return PM_OK;
 }
 
+int pm_merge_peers(pm_ctx* ctx, const void* const* peer_keys, const void* const* peer_payload, int world, int rank,
+                   int64_t block, int64_t len_a, int key_bytes, int64_t width, void* out_keys, void* out_payload,
+                   void* stream) {
+  if (!ctx || !peer_keys || world < 1 || rank < 0 || rank >= world || block < 0 || (key_bytes != 4 && key_bytes != 8) ||
+      width < 0 || !out_keys || (width && (!peer_payload || !out_payload)))
+    return fail(PM_ERR_ARG, "bad pm_merge_peers arguments");
+  const int64_t N = (int64_t)world * block;
+  if (len_a < 0 || len_a > N) return fail(PM_ERR_ARG, "len_a outside [0, world*block]");
+  for (int k = 0; k < world; ++k)
+    if (block && (!peer_keys[k] || (width && !peer_payload[k]))) return fail(PM_ERR_ARG, "null peer block");
+  if (block == 0) return PM_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t la = len_a, lb = N - len_a, d0 = (int64_t)rank * block, d1 = d0 + block;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int maxq = 2 + 2 * (world + 1);
+  const size_t o_q = (size_t)align_up((int64_t)world * 8, 256), o_out = o_q + (size_t)maxq * 16;
+  int rc = ensure(&ctx->peer, &ctx->peer_bytes, o_out + (size_t)maxq * 8);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->peer);
+  const void** dtab = reinterpret_cast<const void**>(base);
+  int64_t* dq = reinterpret_cast<int64_t*>(base + o_q);
+  int64_t* dout = reinterpret_cast<int64_t*>(base + o_out);
+  PM_CUDA(cudaMemcpyAsync(dtab, peer_keys, (size_t)world * sizeof(void*), cudaMemcpyHostToDevice, st));
+  auto run = [&](const std::vector<int64_t>& q, std::vector<int64_t>& ans) -> int {
+    const int nq = (int)(q.size() / 2);
+    ans.assign(nq, 0);
+    if (!nq) return PM_OK;
+    PM_CUDA(cudaMemcpyAsync(dq, q.data(), q.size() * 8, cudaMemcpyHostToDevice, st));
+    cudaError_t ce = key_bytes == 4 ? launch_peer_queries<int32_t>(dtab, block, la, lb, dq, nq, dout, st)
+                                    : launch_peer_queries<int64_t>(dtab, block, la, lb, dq, nq, dout, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "k_peer_queries launch");
+    PM_CUDA(cudaMemcpyAsync(ans.data(), dout, (size_t)nq * 8, cudaMemcpyDeviceToHost, st));
+    PM_CUDA(cudaStreamSynchronize(st));
+    return PM_OK;
+  };
+  // (1) rank r's pieces: A[a0, a1), B[b0, b1)
+  std::vector<int64_t> ans;
+  rc = run({0, d0, 0, d1}, ans);
+  if (rc) return rc;
+  const int64_t a0 = ans[0], a1 = ans[1], b0 = d0 - a0, b1 = d1 - a1;
+  // (2) the output position of every block boundary strictly inside a piece:
+  //     A[i] lands at i + #(B < A[i]); B[j] at j + #(A <= B[j])
+  std::vector<int64_t> q, ai, bj;
+  for (int64_t g = (a0 / block + 1) * block; g < a1; g += block) {
+    ai.push_back(g);
+    q.insert(q.end(), {1, g});
+  }
+  for (int64_t g = ((la + b0) / block + 1) * block; g < la + b1; g += block) {
+    bj.push_back(g - la);
+    q.insert(q.end(), {2, g - la});
+  }
+  rc = run(q, ans);
+  if (rc) return rc;
+  struct Cut { int64_t d, a; };
+  std::vector<Cut> cuts{{d0, a0}, {d1, a1}};
+  for (size_t k = 0; k < ai.size(); ++k) cuts.push_back({ai[k] + ans[k], ai[k]});
+  for (size_t k = 0; k < bj.size(); ++k) cuts.push_back({bj[k] + ans[ai.size() + k], ans[ai.size() + k]});
+  std::sort(cuts.begin(), cuts.end(), [](const Cut& x, const Cut& y) { return x.d < y.d; });
+  // (3) one copy-mode merge per sub-range: each piece inside one block
+  auto at = [&](const void* const* tab, int64_t g, int64_t rb) -> const char* {
+    const int64_t k = std::min<int64_t>(g / block, world - 1);
+    return static_cast<const char*>(tab[k]) + (g - k * block) * rb;
+  };
+  for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+    const int64_t c0 = cuts[k].d, c1 = cuts[k + 1].d;
+    if (c1 <= c0) continue;
+    const int64_t sa0 = cuts[k].a, sa1 = cuts[k + 1].a, nA = sa1 - sa0, nB = (c1 - c0) - nA;
+    const int64_t sb0 = c0 - sa0;
+    const char* ka = at(peer_keys, nA ? sa0 : 0, key_bytes);
+    const char* kb = at(peer_keys, nB ? la + sb0 : 0, key_bytes);
+    const char* pa = width ? at(peer_payload, nA ? sa0 : 0, width) : nullptr;
+    const char* pb = width ? at(peer_payload, nB ? la + sb0 : 0, width) : nullptr;
+    rc = run_engine(ctx, const_cast<char*>(ka), key_bytes, const_cast<char*>(pa), width, 0, nA, nA + nB, MODE_MERGE, 0,
+                    st, static_cast<char*>(out_keys) + (c0 - d0) * key_bytes,
+                    width ? static_cast<char*>(out_payload) + (c0 - d0) * width : nullptr, kb, pb);
+    if (rc) return rc;
+  }
+  return PM_OK;
+}
+
+int pm_ipc_handle(void* device_ptr, void* out_handle) {
+  if (!device_ptr || !out_handle) return fail(PM_ERR_ARG, "bad pm_ipc_handle arguments");
+  cudaIpcMemHandle_t h;
+  PM_CUDA(cudaIpcGetMemHandle(&h, device_ptr));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return PM_OK;
+}
+
+int pm_ipc_open(const void* handle, void** out_ptr) {
+  if (!handle || !out_ptr) return fail(PM_ERR_ARG, "bad pm_ipc_open arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  PM_CUDA(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PM_OK;
+}
+
+int pm_ipc_close(void* ptr) {
+  if (!ptr) return fail(PM_ERR_ARG, "null pointer");
+  PM_CUDA(cudaIpcCloseMemHandle(ptr));
+  return PM_OK;
+}
+
 int pm_debug_engine_only(pm_ctx* ctx, int on) {
   if (!ctx) return fail(PM_ERR_ARG, "null context");
   std::lock_guard<std::mutex> lk(ctx->mu);
@@ -479,6 +583,7 @@ int pm_ctx_destroy(pm_ctx* ctx) {
   if (ctx->buf) cudaFree(ctx->buf);
   if (ctx->wide) cudaFree(ctx->wide);
   if (ctx->wperm) cudaFree(ctx->wperm);
+  if (ctx->peer) cudaFree(ctx->peer);
   for (auto& x : ctx->hs)
     if (x) cudaStreamDestroy(x);
   for (auto& x : ctx->hev)

@@ -37,6 +37,10 @@ cudaError_t launch_cycle_permute(uint8_t* pay, int64_t w, const int32_t* idx, in
 // one-pass overlapping move of a byte plane by D bytes (pm_rotate.cu); flags: one int32 per 32 KB tile
 cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool right, int32_t* flags, int32_t* ticket,
                          int32_t* err, int num_sms, cudaStream_t st);
+// block-distributed searches through a peer-pointer table (pm_peers.cu)
+template <typename KT>
+cudaError_t launch_peer_queries(const void* const* tab, int64_t block, int64_t la, int64_t lb, const int64_t* q, int nq,
+                                int64_t* out, cudaStream_t st);
 // small jobs (pm_small.cu): one CTA, both runs staged in shared memory
 int64_t small_merge_smem(int ks, int64_t w, int64_t n);
 template <typename KT>

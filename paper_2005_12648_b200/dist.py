@@ -186,3 +186,73 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
         keys_local.copy_(out_k)
         payload_local.copy_(out_p)
     return keys_local, payload_local
+
+
+# ---------------------------------------------------------------------------------------------
+# Exchange fused with the merge: every rank maps the others' blocks (CUDA IPC, NVLink peer
+# access) and pm_merge_peers streams its A and B pieces straight out of peer memory into a
+# staging block -- no all-to-all pass, no send/receive copies.
+_PEER_CACHE: dict = {}
+
+
+def _peer_view(meta, numel: int, dtype, shape_tail, elem_off: int) -> torch.Tensor:
+    """A tensor over a peer's block (torch's CUDA IPC storage sharing), cached per handle."""
+    key = (bytes(meta[1]), int(meta[3]))
+    st = _PEER_CACHE.get(key)
+    if st is None:
+        st = torch.UntypedStorage._new_shared_cuda(*meta)
+        _PEER_CACHE[key] = st
+    t = torch.empty(0, dtype=dtype, device=st.device)
+    t.set_(st, elem_off, (numel, *shape_tail))
+    return t
+
+
+def merge_distributed_p2p(keys_local: torch.Tensor, payload_local: torch.Tensor | None, global_len_a: int,
+                          group=None):
+    """merge_distributed with the exchange fused into the merge (pm_merge_peers).
+
+    Every rank holds an equal-length block.  Blocks are shared once through CUDA IPC
+    (``all_gather_object`` of the storage handles); each rank's merge reads its pieces
+    from the peers' blocks over NVLink into a staging block, all ranks meet at a
+    barrier (no block changes while a peer may still read it), and the staging block
+    is copied into the rank's own block.
+    """
+    from . import _ops
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = keys_local.numel()
+    if payload_local is None:
+        payload_local = torch.empty((n, 0), dtype=torch.uint8, device=keys_local.device)
+    w = payload_local.shape[1]
+    if world == 1:  # nothing to map: the table is this block
+        out_k = torch.empty_like(keys_local)
+        out_p = torch.empty_like(payload_local)
+        _ops.merge_peers([keys_local], [payload_local] if w else None, global_len_a, 0, out_k, out_p if w else None)
+        keys_local.copy_(out_k)
+        if w:
+            payload_local.copy_(out_p)
+        return keys_local, payload_local
+    sizes = [None] * world
+    mine = (n, keys_local.untyped_storage()._share_cuda_(), keys_local.storage_offset(),
+            payload_local.untyped_storage()._share_cuda_() if w else None, payload_local.storage_offset() if w else 0)
+    dist.all_gather_object(sizes, mine, group=group)
+    if any(s[0] != n for s in sizes):
+        raise ValueError("merge_distributed_p2p needs equal blocks on every rank")
+    pk, pp = [], []
+    for r, (_, mk, ok, mp, op) in enumerate(sizes):
+        if r == rank:
+            pk.append(keys_local)
+            pp.append(payload_local)
+        else:
+            pk.append(_peer_view(mk, n, keys_local.dtype, (), ok))
+            pp.append(_peer_view(mp, n, torch.uint8, (w,), op) if w else payload_local)
+    out_k = torch.empty_like(keys_local)
+    out_p = torch.empty_like(payload_local)
+    _ops.merge_peers(pk, pp if w else None, global_len_a, rank, out_k, out_p if w else None)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)  # every peer has finished reading this block
+    keys_local.copy_(out_k)
+    if w:
+        payload_local.copy_(out_p)
+    return keys_local, payload_local

@@ -523,3 +523,65 @@ def test_shift_wide_rows(width):
             arr = to_gpu(keys, payload)
             pm.shift_region(arr, 3, la, lb, kind)
             assert_same(arr, wk, wp, f"shift_region {kind} {la},{lb},w={width}")
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("width", [0, 4, 300])
+def test_merge_peers_block_distributed(dtype, width):
+    """pm_merge_peers over a peer-pointer table, every rank of a simulated world on one
+    GPU (separate allocations stand in for the peers' blocks; no kernel waits on another
+    rank).  Rank outputs concatenated == the oracle's stable merge of the global A|B."""
+    import torch
+
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(4242 + width + (1 if dtype == np.int64 else 0))
+    for world, block, afrac, domain in ((1, 5000, 0.5, 1000), (2, 4096, 0.5, 2**31 - 1), (3, 3001, 0.37, 50),
+                                         (5, 2000, 0.71, 2**31 - 1), (4, 8192, 0.5, 7), (3, 1000, 0.0, 10),
+                                         (3, 1000, 1.0, 10)):
+        n = world * block
+        la = int(n * afrac)
+        keys = np.concatenate([np.sort(rng.integers(0, domain, la)), np.sort(rng.integers(0, domain, n - la))])
+        keys = keys.astype(dtype)
+        pay = rng.integers(0, 256, (n, width), dtype=np.uint8)
+        want_k, want_p = keys.copy(), pay.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, la, n)
+        bk = [torch.from_numpy(keys[k * block:(k + 1) * block].copy()).cuda() for k in range(world)]
+        bp = [torch.from_numpy(pay[k * block:(k + 1) * block].copy()).cuda() for k in range(world)]
+        for r in range(world):
+            ok = torch.empty_like(bk[0])
+            op = torch.empty_like(bp[0]) if width else None
+            _ops.merge_peers(bk, bp if width else None, la, r, ok, op)
+            pm.synchronize()
+            sl = slice(r * block, (r + 1) * block)
+            assert np.array_equal(ok.cpu().numpy(), want_k[sl]), f"world={world} rank={r} keys"
+            if width:
+                assert np.array_equal(op.cpu().numpy(), want_p[sl]), f"world={world} rank={r} payload"
+
+
+def test_distributed_merge_p2p_single_rank_nccl():
+    """merge_distributed_p2p over a 1-rank NCCL group (the peer table holds this block)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_12648_b200.dist import merge_distributed_p2p
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29637"
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(78)
+        for width in (0, 4):
+            keys, payload, middle = random_instance(rng, 300000, 0.4, 1000, width)
+            want_k, want_p = keys.copy(), payload.copy()
+            orc.seq_merge_buffered(want_k, want_p, 0, middle, len(keys))
+            k = torch.from_numpy(keys).cuda()
+            p = torch.from_numpy(payload).cuda()
+            rk, rp = merge_distributed_p2p(k, p if width else None, middle)
+            assert np.array_equal(rk.cpu().numpy(), want_k)
+            if width:
+                assert np.array_equal(rp.cpu().numpy(), want_p)
+    finally:
+        dist.destroy_process_group()
