@@ -585,3 +585,22 @@ def test_distributed_merge_p2p_single_rank_nccl():
                 assert np.array_equal(rp.cpu().numpy(), want_p)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("width", [256, 1020])
+def test_wide_records_int64_keys(width):
+    """int64 keys with wide rows (the key+row-index merge runs with 12-byte records)."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(1234 + width)
+    for size, split in ((7000, 0.5), (20_001, 0.81)):
+        m = int(size * split)
+        keys = np.concatenate([np.sort(rng.integers(-2**62, 2**62, m)), np.sort(rng.integers(-2**62, 2**62, size - m))])
+        keys[: m // 3] = np.sort(rng.integers(-5, 5, m // 3))  # duplicates in A's prefix
+        keys[:m].sort()
+        payload = rng.integers(0, 256, (size, width), dtype=np.uint8)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, m, size)
+        arr = to_gpu(keys, payload)
+        _ops.merge(arr, 0, m, size)
+        assert_same(arr, want_k, want_p, f"int64 wide w={width} size={size}")
