@@ -120,6 +120,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #ifndef PM_SLIDE_STASH
 #define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
 #endif
+#ifndef PM_CLUSTER_MERGE
+#define PM_CLUSTER_MERGE 1  // tune: in-place jobs of up to ~3 MB in one thread-block cluster
+#endif
 #ifndef PM_SMALL_BYTES
 #define PM_SMALL_BYTES (200 * 1024)  // records staged by the one-CTA small merge (shared memory)
 #endif
@@ -207,6 +210,17 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // small in-place jobs: one CTA with both runs in shared memory
   if (mode == MODE_MERGE && !copy && !ctx->engine_only && small_merge_smem(ks, w, e - s) <= PM_SMALL_BYTES)
     return launch_merge_small_(ks, keys, payload, w, s, m, e, st);
+  // up to ~3 MB: one thread-block cluster, both runs in distributed shared memory
+  if (mode == MODE_MERGE && !copy && !ctx->engine_only && w <= 64 && PM_CLUSTER_MERGE) {
+    int lchunk = 0;
+    const int C = cluster_merge_plan(ks, w, e - s, &lchunk);
+    if (C > 0) {
+      cudaError_t ce = ks == 4 ? launch_merge_cluster<int32_t>(keys, payload, w, s, m, e, C, lchunk, st)
+                               : launch_merge_cluster<int64_t>(keys, payload, w, s, m, e, C, lchunk, st);
+      if (ce != cudaSuccess) return cuda_fail(ce, "k_merge_cluster launch");
+      return PM_OK;
+    }
+  }
   // medium in-place jobs (at most PM_STAGE_BYTES of records): the streaming merge
   // into a staging buffer, then one copy back -- both passes mostly in L2
   if (mode == MODE_MERGE && !copy && !ctx->engine_only && (e - s) * (ks + w) <= PM_STAGE_BYTES && w < PM_WIDE_MIN) {

@@ -46,4 +46,9 @@ int64_t small_merge_smem(int ks, int64_t w, int64_t n);
 template <typename KT>
 cudaError_t launch_merge_small(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                                cudaStream_t st);
+// cluster size (0: does not fit) and log2 chunk of the cluster merge; its launcher
+int cluster_merge_plan(int ks, int64_t w, int64_t n, int* lchunk);
+template <typename KT>
+cudaError_t launch_merge_cluster(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int C,
+                                 int lchunk, cudaStream_t st);
 }  // namespace pm

@@ -7,9 +7,11 @@
 // caller's arrays -- everything was read before anything is written, so the
 // in-place semantics hold with no scratch.  One launch, a few microseconds:
 // the persistent engine's plan + ticket machinery costs ~50 us at these sizes.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "pm_launch.h"
@@ -19,6 +21,7 @@ namespace pm {
 namespace {
 
 constexpr int kSmallThreads = 1024;
+constexpr int64_t kClusterSmem = 216 * 1024;  // shared memory per CTA of the cluster merge (staging + window)
 
 // stable merge-path split: number of A records among the first d outputs
 template <typename KT>
@@ -41,39 +44,28 @@ __device__ __forceinline__ void block_copy(void* dst, const void* src, int64_t b
   for (int64_t i = threadIdx.x; i < bytes / (int64_t)sizeof(W); i += blockDim.x) d[i] = s[i];
 }
 
+// merged records of a thread's output span go to a shared-memory output tile
+// first (per-thread spans written straight to global memory would scatter every
+// warp store over 32 lines); the tile then leaves with coalesced stores
 template <typename KT>
-__global__ void __launch_bounds__(kSmallThreads) k_merge_small(KT* keys, uint8_t* pay, int64_t w, int la, int lb) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  const int n = la + lb;
-  KT* sk = reinterpret_cast<KT*>(sm);
-  uint8_t* sp = sm + ((n * sizeof(KT) + 15) & ~(size_t)15);
-  // stage keys (and payload rows) -- word size chosen by alignment
-  if ((((uintptr_t)keys) & 15) == 0 && ((n * sizeof(KT)) & 15) == 0) block_copy<uint4>(sk, keys, n * sizeof(KT));
-  else block_copy<KT>(sk, keys, n * sizeof(KT));
-  const bool w4 = w && ((((uintptr_t)pay) | (uintptr_t)w) & 3) == 0;
-  if (w) {
-    if (((((uintptr_t)pay) | (uintptr_t)(n * w)) & 15) == 0) block_copy<uint4>(sp, pay, n * w);
-    else if (w4) block_copy<uint32_t>(sp, pay, n * w);
-    else block_copy<uint8_t>(sp, pay, n * w);
-  }
-  __syncthreads();
-  const KT* A = sk;
-  const KT* B = sk + la;
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int d0 = min(n, (int)threadIdx.x * per), d1 = min(n, d0 + per);
+__device__ __forceinline__ void merge_spans_to_tile(const KT* A, int la, const KT* B, int lb, const uint8_t* PA,
+                                                    const uint8_t* PB, int64_t w, KT* ok, uint8_t* op) {
+  const int no = la + lb;
+  const int per = (no + blockDim.x - 1) / blockDim.x;
+  const int d0 = min(no, (int)threadIdx.x * per), d1 = min(no, d0 + per);
   if (d0 >= d1) return;
   int i = split_smem(A, la, B, lb, d0), j = d0 - i;
+  const bool w4 = w && ((uintptr_t)w & 3) == 0;
   for (int d = d0; d < d1; ++d) {
     const bool ta = j >= lb || (i < la && A[i] <= B[j]);
-    const int src = ta ? i : la + j;
-    keys[d] = sk[src];
+    ok[d] = ta ? A[i] : B[j];
     if (w) {
+      const uint8_t* rs = ta ? PA + (int64_t)i * w : PB + (int64_t)j * w;
+      uint8_t* rd = op + (int64_t)d * w;
       if (w4) {
-        const uint32_t* s = reinterpret_cast<const uint32_t*>(sp + (int64_t)src * w);
-        uint32_t* o = reinterpret_cast<uint32_t*>(pay + (int64_t)d * w);
-        for (int64_t c = 0; c < (w >> 2); ++c) o[c] = s[c];
+        for (int64_t c = 0; c < w; c += 4) *reinterpret_cast<uint32_t*>(rd + c) = *reinterpret_cast<const uint32_t*>(rs + c);
       } else {
-        for (int64_t c = 0; c < w; ++c) pay[(int64_t)d * w + c] = sp[(int64_t)src * w + c];
+        for (int64_t c = 0; c < w; ++c) rd[c] = rs[c];
       }
     }
     if (ta) ++i;
@@ -81,17 +73,179 @@ __global__ void __launch_bounds__(kSmallThreads) k_merge_small(KT* keys, uint8_t
   }
 }
 
+// coalesced copy of a tile (keys ok[0, n), rows op) to keys / pay
+template <typename KT>
+__device__ __forceinline__ void tile_out(KT* keys, uint8_t* pay, const KT* ok, const uint8_t* op, int n, int64_t w) {
+  for (int t = threadIdx.x; t < n; t += blockDim.x) keys[t] = ok[t];
+  if (w) {
+    if (((((uintptr_t)pay) | (uintptr_t)w) & 3) == 0) {
+      const int64_t nw = (int64_t)n * (w >> 2);
+      for (int64_t t = threadIdx.x; t < nw; t += blockDim.x)
+        reinterpret_cast<uint32_t*>(pay)[t] = reinterpret_cast<const uint32_t*>(op)[t];
+    } else {
+      for (int64_t t = threadIdx.x; t < (int64_t)n * w; t += blockDim.x) pay[t] = op[t];
+    }
+  }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kSmallThreads) k_merge_small(KT* keys, uint8_t* pay, int64_t w, int la, int lb) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int n = la + lb;
+  const int64_t kreg = ((int64_t)n * sizeof(KT) + 15) & ~(int64_t)15, preg = ((int64_t)n * w + 15) & ~(int64_t)15;
+  KT* sk = reinterpret_cast<KT*>(sm);
+  uint8_t* sp = sm + kreg;
+  KT* ok = reinterpret_cast<KT*>(sm + kreg + preg);
+  uint8_t* op = sm + 2 * kreg + preg;
+  // stage keys (and payload rows) -- word size chosen by alignment
+  if ((((uintptr_t)keys) & 15) == 0 && ((n * sizeof(KT)) & 15) == 0) block_copy<uint4>(sk, keys, n * sizeof(KT));
+  else block_copy<KT>(sk, keys, n * sizeof(KT));
+  if (w) {
+    if (((((uintptr_t)pay) | (uintptr_t)(n * w)) & 15) == 0) block_copy<uint4>(sp, pay, n * w);
+    else if (((((uintptr_t)pay) | (uintptr_t)w) & 3) == 0) block_copy<uint32_t>(sp, pay, n * w);
+    else block_copy<uint8_t>(sp, pay, n * w);
+  }
+  __syncthreads();
+  merge_spans_to_tile<KT>(sk, la, sk + la, lb, sp, sp + (int64_t)la * w, w, ok, op);
+  __syncthreads();
+  tile_out<KT>(keys, pay, ok, op, n, w);
+}
+
+// ---- cluster merge: both runs spread over the shared memory of a thread-block
+// cluster (up to 16 CTAs, ~1.7 MB), read across CTAs through distributed shared
+// memory.  CTA k stages records [k*chunk, (k+1)*chunk) of A|B (chunk a power of
+// two: a record's CTA is a shift away); after a cluster barrier two threads
+// find the merge-path splits of the CTA's output range [k*chunk, (k+1)*chunk)
+// over the cluster, the CTA copies its A and B windows in (consecutive threads
+// read consecutive remote records), a second cluster barrier releases the
+// staging, and the CTA merges the windows in local shared memory straight into
+// the caller's arrays (everything was read before anything is written).
+namespace cg = cooperative_groups;
+
+// distributed shared memory: this CTA's shared address -> the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+template <typename KT>
+__device__ __forceinline__ KT ld_dsmem(uint32_t a) {
+  if constexpr (sizeof(KT) == 4) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return (KT)(int32_t)v;
+  } else {
+    unsigned long long v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return (KT)(long long)v;
+  }
+}
+__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint8_t ld_dsmem_u8(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return (uint8_t)v;
+}
+
+// record x of A|B: key / payload-row addresses in the cluster's shared memory
+template <typename KT>
+struct ClusterRuns {
+  uint32_t sk, sp;  // this CTA's key / payload staging (shared addresses)
+  int lchunk;
+  __device__ __forceinline__ KT k(int x) const {
+    return ld_dsmem<KT>(dsmem_addr(sk + (uint32_t)(x & ((1 << lchunk) - 1)) * (uint32_t)sizeof(KT), (uint32_t)(x >> lchunk)));
+  }
+  __device__ __forceinline__ uint32_t row(int x, int64_t w) const {
+    return dsmem_addr(sp + (uint32_t)((int64_t)(x & ((1 << lchunk) - 1)) * w), (uint32_t)(x >> lchunk));
+  }
+};
+
+template <typename KT>
+__global__ void __launch_bounds__(kSmallThreads) k_merge_cluster(KT* keys, uint8_t* pay, int64_t w, int la, int lb,
+                                                                 int lchunk) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int s_split[2];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int n = la + lb, chunk = 1 << lchunk;
+  const int x0 = min(n, rank * chunk), x1 = min(n, x0 + chunk);
+  const int64_t kreg = ((int64_t)chunk * sizeof(KT) + 15) & ~(int64_t)15, preg = ((int64_t)chunk * w + 15) & ~(int64_t)15;
+  KT* sk = reinterpret_cast<KT*>(sm);  // staged records [x0, x1) of A|B
+  uint8_t* sp = sm + kreg;
+  KT* wk = reinterpret_cast<KT*>(sm + kreg + preg);  // this CTA's A window then B window
+  uint8_t* wp = sm + 2 * kreg + preg;
+  if (x1 > x0) {
+    const int64_t kb = (int64_t)(x1 - x0) * sizeof(KT);
+    if ((((uintptr_t)(keys + x0)) & 15) == 0 && (kb & 15) == 0) block_copy<uint4>(sk, keys + x0, kb);
+    else block_copy<KT>(sk, keys + x0, kb);
+    if (w) {
+      const int64_t pb = (int64_t)(x1 - x0) * w;
+      const uint8_t* src = pay + (int64_t)x0 * w;
+      if (((((uintptr_t)src) | (uintptr_t)pb) & 15) == 0) block_copy<uint4>(sp, src, pb);
+      else if (((((uintptr_t)src) | (uintptr_t)pb) & 3) == 0) block_copy<uint32_t>(sp, src, pb);
+      else block_copy<uint8_t>(sp, src, pb);
+    }
+  }
+  ClusterRuns<KT> R;
+  R.lchunk = lchunk;
+  R.sk = (uint32_t)__cvta_generic_to_shared(sk);
+  R.sp = (uint32_t)__cvta_generic_to_shared(sp);
+  cluster.sync();  // every CTA's records are staged
+  // this CTA's output range [x0, x1): its A and B windows (merge-path splits over the cluster)
+  if (threadIdx.x < 2) {
+    const int d = threadIdx.x ? x1 : x0;
+    int lo = max(0, d - lb), hi = min(d, la);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (R.k(mid) <= R.k(la + d - 1 - mid)) lo = mid + 1;
+      else hi = mid;
+    }
+    s_split[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  const int a0 = s_split[0], a1 = s_split[1], b0 = x0 - a0, b1 = x1 - a1;
+  const int alpha = a1 - a0, beta = b1 - b0;
+  // copy both windows in from distributed shared memory (consecutive threads, consecutive records)
+  for (int t = threadIdx.x; t < alpha + beta; t += blockDim.x) wk[t] = R.k(t < alpha ? a0 + t : la + b0 + (t - alpha));
+  if (w) {
+    const bool w4 = ((uintptr_t)w & 3) == 0;
+    const int64_t words = w4 ? w >> 2 : w;
+    for (int64_t t = threadIdx.x; t < (int64_t)(alpha + beta) * words; t += blockDim.x) {
+      const int r = (int)(t / words);
+      const int64_t c = t - (int64_t)r * words;
+      const uint32_t src = R.row(r < alpha ? a0 + r : la + b0 + (r - alpha), w);
+      if (w4) reinterpret_cast<uint32_t*>(wp)[t] = ld_dsmem_u32(src + (uint32_t)(c * 4));
+      else wp[t] = ld_dsmem_u8(src + (uint32_t)c);
+    }
+  }
+  cluster.sync();  // every window is copied: the staging may go away
+  // merge the windows into this CTA's output tile, then write it back coalesced
+  KT* ok = reinterpret_cast<KT*>(sm + 2 * (kreg + preg));
+  uint8_t* op = sm + 3 * kreg + 2 * preg;
+  merge_spans_to_tile<KT>(wk, alpha, wk + alpha, beta, wp, wp + (int64_t)alpha * w, w, ok, op);
+  __syncthreads();
+  tile_out<KT>(keys + x0, w ? pay + (int64_t)x0 * w : pay, ok, op, x1 - x0, w);
+}
+
 }  // namespace
 
-int64_t small_merge_smem(int ks, int64_t w, int64_t n) { return ((n * ks + 15) & ~15ll) + n * w; }
+int64_t small_merge_smem(int ks, int64_t w, int64_t n) { return 2 * (((n * ks + 15) & ~15ll) + ((n * w + 15) & ~15ll)); }
 
 template <typename KT>
 cudaError_t launch_merge_small(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                                cudaStream_t st) {
   const int64_t n = e - s;
   const size_t smem = (size_t)small_merge_smem(sizeof(KT), w, n);
-  cudaError_t ce = cudaFuncSetAttribute(k_merge_small<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (ce != cudaSuccess) return ce;
+  static std::atomic<int> attrs_set{0};
+  if (!attrs_set.load(std::memory_order_acquire)) {
+    cudaError_t ce = cudaFuncSetAttribute(k_merge_small<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (ce != cudaSuccess) return ce;
+    attrs_set.store(1, std::memory_order_release);
+  }
   k_merge_small<KT><<<1, kSmallThreads, smem, st>>>(static_cast<KT*>(keys) + s,
                                                     w ? static_cast<uint8_t*>(payload) + s * w : nullptr, w,
                                                     (int)(m - s), (int)(e - m));
@@ -100,5 +254,58 @@ cudaError_t launch_merge_small(void* keys, void* payload, int64_t w, int64_t s, 
 }
 template cudaError_t launch_merge_small<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_merge_small<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
+
+// Cluster size and chunk for n records of (ks + w) bytes: the smallest
+// power-of-two cluster (2..16) whose CTAs hold a power-of-two chunk each
+// within kClusterSmem; 0 when n does not fit.
+int cluster_merge_plan(int ks, int64_t w, int64_t n, int* lchunk) {
+  for (int C = 2; C <= 16; C *= 2) {
+    int lc = 0;
+    while ((int64_t)C << lc < n) ++lc;
+    const int64_t chunk = (int64_t)1 << lc;
+    if (3 * (((chunk * ks + 15) & ~15ll) + ((chunk * w + 15) & ~15ll)) <= kClusterSmem) {
+      *lchunk = lc;
+      return C;
+    }
+  }
+  return 0;
+}
+
+template <typename KT>
+cudaError_t launch_merge_cluster(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int C,
+                                 int lchunk, cudaStream_t st) {
+  const int64_t chunk = (int64_t)1 << lchunk;
+  const size_t smem = (size_t)(3 * (((chunk * (int64_t)sizeof(KT) + 15) & ~15ll) + ((chunk * w + 15) & ~15ll)));
+  // function attributes are set once per process (each call costs host time on the launch path)
+  static std::atomic<int> attrs_set{0};
+  cudaError_t ce = cudaSuccess;
+  if (!attrs_set.load(std::memory_order_acquire)) {
+    ce = cudaFuncSetAttribute(k_merge_cluster<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kClusterSmem));
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_merge_cluster<KT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ce != cudaSuccess) return ce;
+    attrs_set.store(1, std::memory_order_release);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ce = cudaLaunchKernelEx(&cfg, k_merge_cluster<KT>, static_cast<KT*>(keys) + s,
+                          w ? static_cast<uint8_t*>(payload) + s * w : static_cast<uint8_t*>(nullptr), w,
+                          (int)(m - s), (int)(e - m), lchunk);
+  count_launches(1);
+  return ce != cudaSuccess ? ce : cudaGetLastError();
+}
+template cudaError_t launch_merge_cluster<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, int,
+                                                   cudaStream_t);
+template cudaError_t launch_merge_cluster<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, int,
+                                                   cudaStream_t);
 
 }  // namespace pm
