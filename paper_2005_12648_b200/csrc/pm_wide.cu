@@ -36,6 +36,9 @@ namespace pm {
 namespace {
 
 constexpr int kWideThreads = 256;
+#ifndef PM_CYC_MINB
+#define PM_CYC_MINB 3  // tune: resident CTAs per SM the cycle walk is compiled for (1: 1.94 ms, 3: 1.67, 4: 2.62 at 508-byte rows)
+#endif
 constexpr int kChunkWords = 4;  // vector words per lane per chunk step
 
 template <int V> struct VecT;
@@ -191,7 +194,7 @@ template <int V> __host__ __device__ constexpr int chains() { return V >= 8 ? 2 
 // the next step writes row s: every row is read before it is written.  Each
 // warp runs kC chains side by side, refilling a slot from its item sequence.
 template <int V>
-__global__ void __launch_bounds__(kWideThreads) k_cyc_move(uint8_t* pay, const uint8_t* __restrict__ save,
+__global__ void __launch_bounds__(kWideThreads, PM_CYC_MINB) k_cyc_move(uint8_t* pay, const uint8_t* __restrict__ save,
                                                            const int32_t* __restrict__ idx,
                                                            const int32_t* __restrict__ heads, const int32_t* cnt,
                                                            int64_t n, int64_t w, int32_t G) {
