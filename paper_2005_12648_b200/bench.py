@@ -20,7 +20,9 @@ the work runs:
 
 from __future__ import annotations
 
+import collections
 import csv
+import itertools
 import time
 from dataclasses import dataclass, replace
 
@@ -47,16 +49,20 @@ QUALITY_HEADER = "t,size,rel_diff_findmedian"
 
 
 class ValidationFailure(Exception):
-    """A merge under measurement produced an unsorted or altered key multiset."""
+    """A measured merge left unsorted keys or changed the key multiset."""
 
 
 class ConfigError(Exception):
-    """The benchmark configuration is inconsistent."""
+    """An inconsistent measurement grid."""
+
+
+def _is_pow2(t: int) -> bool:
+    return t >= 1 and t & (t - 1) == 0
 
 
 @dataclass(frozen=True)
 class BenchConfig:
-    """One measurement campaign (bench.py:41-80): the grid plus run controls."""
+    """A measurement campaign: the grid (sizes x widths x splits x methods x threads) plus controls."""
 
     sizes: tuple[int, ...] = DEFAULT_SIZES
     elem_bytes: tuple[int, ...] = DEFAULT_ELEM_BYTES
@@ -70,37 +76,32 @@ class BenchConfig:
     device: str = "cuda"
 
     def validate(self) -> "BenchConfig":
-        """Reject inconsistent grids with ConfigError; splits are quantised to 2 decimals."""
-        problems = []
-        if any(s < 0 for s in self.sizes):
-            problems.append("sizes must be >= 0")
-        if any(eb < 4 for eb in self.elem_bytes):
-            problems.append("elem_bytes must be >= 4")
-        if any(not 0.0 < sp < 1.0 for sp in self.splits):
-            problems.append("splits must lie in the open interval (0, 1)")
-        if self.reps < 1:
-            problems.append("reps must be >= 1")
-        bad = [m for m in self.methods if m not in METHODS]
-        if bad:
-            problems.append(f"unknown methods {bad}; choose from {METHODS}")
-        if any(t < 1 or (t & (t - 1)) for t in self.threads):
-            problems.append("thread counts must be powers of two >= 1")
-        if self.device != "cuda":
-            problems.append(f"device must be 'cuda' (this build has no CPU path), got {self.device!r}")
-        if problems:
-            raise ConfigError(problems[0])
-        # the CSV keeps two decimals: round now so written records read back equal
-        q = tuple(round(sp, 2) for sp in self.splits)
-        if any(not 0.0 < sp < 1.0 for sp in q):
+        """ConfigError on the first inconsistency; returns a copy with splits quantised to 2 decimals."""
+        unknown = [m for m in self.methods if m not in METHODS]
+        checks = (
+            (all(x >= 0 for x in self.sizes), "sizes must be >= 0"),
+            (all(x >= 4 for x in self.elem_bytes), "elem_bytes must be >= 4"),
+            (all(0.0 < x < 1.0 for x in self.splits), "splits must lie in the open interval (0, 1)"),
+            (self.reps >= 1, "reps must be >= 1"),
+            (not unknown, f"unknown methods {unknown}; choose from {METHODS}"),
+            (all(map(_is_pow2, self.threads)), "thread counts must be powers of two >= 1"),
+            (self.device == "cuda", f"device must be 'cuda' (this build has no CPU path), got {self.device!r}"),
+        )
+        for ok, why in checks:
+            if not ok:
+                raise ConfigError(why)
+        # the CSV keeps two decimals: quantise now so written records read back equal
+        q = tuple(round(x, 2) for x in self.splits)
+        if not all(0.0 < x < 1.0 for x in q):
             raise ConfigError("splits must stay inside (0, 1) at 2-decimal precision")
-        if len(set(q)) != len(q):
+        if len(set(q)) < len(q):
             raise ConfigError("splits collide after 2-decimal rounding")
         return replace(self, splits=q)
 
 
 @dataclass(frozen=True)
 class BenchRecord:
-    """One measured grid cell, nanoseconds aggregated over the repetitions."""
+    """One grid cell's timing (nanoseconds over the repetitions)."""
 
     method: str
     threads: int
@@ -112,7 +113,7 @@ class BenchRecord:
     max_ns: float
 
     def __post_init__(self):
-        if not (self.min_ns <= self.mean_ns <= self.max_ns):
+        if self.min_ns > self.mean_ns or self.mean_ns > self.max_ns:
             raise ValueError("need min_ns <= mean_ns <= max_ns")
 
 
@@ -133,155 +134,151 @@ class QualityRow:
 
 
 def generate_input(size: int, split: float, seed: int, elem_bytes: int = 4) -> tuple[KeyedArray, int]:
-    """The reference's random-walk runs (bench.py:110-146) as a device KeyedArray + middle."""
+    """The reference harness's random-walk runs (bench.py:110-146), as a device KeyedArray, and the middle."""
     keys, payload, middle = _generate_host(size, split, seed, elem_bytes)
     return KeyedArray(keys, payload if payload.shape[1] else None), middle
 
 
-def _method_call(name: str):
-    calls = {
-        "seq-rotation": lambda arr, job, t: seq_merge_rotation(arr, job),
-        "seq-buffered": lambda arr, job, t: seq_merge_buffered(arr, job),
-        "soptmov": lambda arr, job, t: merge_soptmov(arr, job, t),
-        "srecpar-ls": lambda arr, job, t: merge_srecpar(arr, job, t, shift_kind=LINEAR),
-        "srecpar-cs": lambda arr, job, t: merge_srecpar(arr, job, t, shift_kind=CIRCULAR),
-    }
-    if name not in calls:
-        raise ConfigError(f"unknown method {name!r}")
-    return calls[name]
+# method name -> device call (arr, job, t); the sequential ones ignore t
+_CALLS = {
+    "seq-rotation": lambda arr, job, t: seq_merge_rotation(arr, job),
+    "seq-buffered": lambda arr, job, t: seq_merge_buffered(arr, job),
+    "soptmov": lambda arr, job, t: merge_soptmov(arr, job, t),
+    "srecpar-ls": lambda arr, job, t: merge_srecpar(arr, job, t, shift_kind=LINEAR),
+    "srecpar-cs": lambda arr, job, t: merge_srecpar(arr, job, t, shift_kind=CIRCULAR),
+}
 
 
 def threads_for(method: str, config: BenchConfig) -> tuple[int, ...]:
-    """Sequential methods run once with t = 1; the parallel ones once per worker count."""
+    """t = 1 for the sequential methods, every configured worker count for the parallel ones."""
     return (1,) if method in SEQ_METHODS else tuple(config.threads)
 
 
 def iter_cells(config: BenchConfig):
-    """(method, threads, elem_bytes, size, split) in emission order, skipping cells over max_bytes."""
+    """Grid cells (method, threads, elem_bytes, size, split) in emission order, within max_bytes."""
+    cap = config.max_bytes
     for method in config.methods:
-        for t in threads_for(method, config):
-            for eb in config.elem_bytes:
-                for size in config.sizes:
-                    if config.max_bytes is not None and size * eb > config.max_bytes:
-                        continue
-                    for split in config.splits:
-                        yield method, t, eb, size, split
+        for t, eb, size, split in itertools.product(threads_for(method, config), config.elem_bytes, config.sizes,
+                                                     config.splits):
+            if cap is None or size * eb <= cap:
+                yield method, t, eb, size, split
+
+
+def _time_cell(call, arr, job, t, pristine, want, reps: int, label: str) -> list[int]:
+    import torch
+
+    pk, pp = pristine
+    samples = []
+    for rep in range(reps + 1):  # repetition 0 warms up
+        arr.keys.copy_(pk)
+        if pp.shape[1]:
+            arr.payload.copy_(pp)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter_ns()
+        call(arr, job, t)
+        torch.cuda.synchronize()
+        dt = time.perf_counter_ns() - t0
+        if not torch.equal(arr.keys, want):
+            raise ValidationFailure(f"unsorted or corrupted output in cell [{label}]")
+        samples.append(dt)
+    return samples[1:]
 
 
 def run_grid(config: BenchConfig, *, validate_only: bool = False, progress=None) -> list[BenchRecord]:
-    """Measure every cell: restore the input, merge on the device, verify, aggregate.
+    """Measure every cell on the device: restore the input, merge, check against a device sort.
 
-    One warm-up repetition per cell is discarded; an unsorted result or a
-    changed key multiset raises ValidationFailure naming the cell.
+    validate_only runs each cell once and returns no records.
     """
     import torch
 
     config = config.validate()
-    out = []
+    records = []
     for method, t, eb, size, split in iter_cells(config):
         label = f"{method} t={t} elem_bytes={eb} size={size} split={split:.2f}"
         arr, middle = generate_input(size, split, config.seed, eb)
-        pristine_k = arr.keys.clone()
-        pristine_p = arr.payload.clone()
-        want = torch.sort(pristine_k).values
-        job = MergeJob(0, middle, size)
-        call = _method_call(method)
-        reps = 1 if validate_only else config.reps
-        samples = []
-        for rep in range(reps + 1):
-            arr.keys.copy_(pristine_k)
-            if pristine_p.shape[1]:
-                arr.payload.copy_(pristine_p)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter_ns()
-            call(arr, job, t)
-            torch.cuda.synchronize()
-            dt = time.perf_counter_ns() - t0
-            if not torch.equal(arr.keys, want):
-                raise ValidationFailure(f"unsorted or corrupted output in cell [{label}]")
-            if rep:
-                samples.append(dt)
-            if validate_only:
-                break
+        pristine = (arr.keys.clone(), arr.payload.clone())
+        want = torch.sort(pristine[0]).values
+        samples = _time_cell(_CALLS[method], arr, MergeJob(0, middle, size), t, pristine, want,
+                             0 if validate_only else config.reps, label)
         if progress is not None:
             progress(label)
-        if not validate_only:
-            out.append(BenchRecord(method, t, eb, size, split, mean_ns=float(np.mean(samples)),
-                                   min_ns=float(min(samples)), max_ns=float(max(samples))))
-    return out
+        if samples:
+            records.append(BenchRecord(method, t, eb, size, split, mean_ns=float(np.mean(samples)),
+                                       min_ns=float(min(samples)), max_ns=float(max(samples))))
+    return records
 
 
 def speedup_table(records: list[BenchRecord], baseline_method: str) -> list[SpeedupRow]:
-    """baseline mean / method mean per (elem_bytes, size, split), averaged over splits.
+    """Per (method, threads, elem_bytes, size): mean over splits of baseline_ns / method_ns.
 
-    Every cell present must have a baseline record (ConfigError otherwise).
+    Every cell needs a baseline record with the same (elem_bytes, size, split).
     """
     base = {(r.elem_bytes, r.size, r.split): r.mean_ns for r in records if r.method == baseline_method}
     if not base:
         raise ConfigError(f"baseline method {baseline_method!r} has no records")
-    ratios: dict[tuple, list[float]] = {}
+    groups: dict[tuple, list[float]] = collections.defaultdict(list)
     for r in records:
-        cell = (r.elem_bytes, r.size, r.split)
-        if cell not in base:
+        ref = base.get((r.elem_bytes, r.size, r.split))
+        if ref is None:
             raise ConfigError(f"baseline {baseline_method!r} missing cell elem_bytes={r.elem_bytes} "
                               f"size={r.size} split={r.split:.2f}")
-        ratios.setdefault((r.method, r.threads, r.elem_bytes, r.size), []).append(base[cell] / r.mean_ns)
-    return [SpeedupRow(m, t, eb, size, float(np.mean(v))) for (m, t, eb, size), v in ratios.items()]
+        groups[(r.method, r.threads, r.elem_bytes, r.size)].append(ref / r.mean_ns)
+    return [SpeedupRow(*key, speedup=float(np.mean(v))) for key, v in groups.items()]
 
 
 def largest_leaf_pair(keys, middle: int, t: int, median_fn) -> int:
-    """Largest of the t leaf pairs left by log2(t) levels of recursive division with median_fn."""
-    if t < 1 or (t & (t - 1)):
+    """Size of the largest of the t leaf pairs that log2(t) levels of division by median_fn leave."""
+    if not _is_pow2(t):
         raise ConfigError("t must be a power of two >= 1")
-    level = [(keys[:middle], keys[middle:])]
-    while len(level) < t:
-        split_level = []
-        for a, b in level:
-            p_a, p_b = median_fn(a, b)
-            split_level += [(a[:p_a], b[:p_b]), (a[p_a:], b[p_b:])]
-        level = split_level
-    return max(len(a) + len(b) for a, b in level)
+    pairs = [(keys[:middle], keys[middle:])]
+    for _ in range(t.bit_length() - 1):
+        pairs = [half for a, b in pairs for half in _halves(a, b, median_fn)]
+    return max(len(a) + len(b) for a, b in pairs)
+
+
+def _halves(a, b, median_fn):
+    p_a, p_b = median_fn(a, b)
+    return (a[:p_a], b[:p_b]), (a[p_a:], b[p_b:])
 
 
 def median_quality_study(config: BenchConfig) -> list[QualityRow]:
-    """Worst leaf of find_median vs find_median_optimal, relative, averaged over splits.
-
-    Both searches run on the device over the same generated runs (bench.py's
-    study, Fig. 5 of the paper): (max_heuristic - max_optimal) / max_optimal.
-    """
+    """Fig. 5 study on the device: (worst leaf of find_median - worst of find_median_optimal) / the
+    latter, averaged over the splits, for t in QUALITY_THREADS and every size."""
     config = config.validate()
-    rows = []
-    for t in QUALITY_THREADS:
-        for size in config.sizes:
-            diffs = []
-            for split in config.splits:
-                arr, middle = generate_input(size, split, config.seed)
-                heur = largest_leaf_pair(arr.keys, middle, t, find_median)
-                best = largest_leaf_pair(arr.keys, middle, t, find_median_optimal)
-                diffs.append(0.0 if best == 0 else (heur - best) / best)
-            rows.append(QualityRow(t, size, float(np.mean(diffs))))
-    return rows
+
+    def rel(size, split, t):
+        arr, middle = generate_input(size, split, config.seed)
+        best = largest_leaf_pair(arr.keys, middle, t, find_median_optimal)
+        return 0.0 if best == 0 else (largest_leaf_pair(arr.keys, middle, t, find_median) - best) / best
+
+    return [QualityRow(t, size, float(np.mean([rel(size, sp, t) for sp in config.splits])))
+            for t in QUALITY_THREADS for size in config.sizes]
+
+
+_RECORD_FIELDS = RECORD_HEADER.split(",")
 
 
 def write_records_csv(path, records: list[BenchRecord]) -> None:
     with open(path, "w", encoding="utf-8", newline="") as fh:
-        w = csv.writer(fh, lineterminator="\n")
-        w.writerow(RECORD_HEADER.split(","))
-        w.writerows([r.method, r.threads, r.elem_bytes, r.size, f"{r.split:.2f}", repr(r.mean_ns), repr(r.min_ns),
-                     repr(r.max_ns)] for r in records)
+        out = csv.DictWriter(fh, _RECORD_FIELDS, lineterminator="\n")
+        out.writeheader()
+        for r in records:
+            row = {f: getattr(r, f) for f in _RECORD_FIELDS}
+            row.update(split=f"{r.split:.2f}", mean_ns=repr(r.mean_ns), min_ns=repr(r.min_ns), max_ns=repr(r.max_ns))
+            out.writerow(row)
 
 
 def read_records_csv(path) -> list[BenchRecord]:
     with open(path, encoding="utf-8", newline="") as fh:
-        rows = list(csv.reader(fh))
-    if not rows or rows[0] != RECORD_HEADER.split(","):
-        raise ConfigError(f"unexpected CSV header {rows[0] if rows else None}")
-    return [BenchRecord(m, int(t), int(eb), int(sz), float(sp), float(a), float(lo), float(hi))
-            for m, t, eb, sz, sp, a, lo, hi in rows[1:]]
+        rd = csv.reader(fh)
+        header = next(rd, None)
+        if header != _RECORD_FIELDS:
+            raise ConfigError(f"unexpected CSV header {header}")
+        casts = (str, int, int, int, float, float, float, float)
+        return [BenchRecord(*(c(v) for c, v in zip(casts, row))) for row in rd]
 
 
 def write_quality_csv(path, rows: list[QualityRow]) -> None:
     with open(path, "w", encoding="utf-8", newline="") as fh:
-        w = csv.writer(fh, lineterminator="\n")
-        w.writerow(QUALITY_HEADER.split(","))
-        w.writerows([r.t, r.size, repr(r.rel_diff)] for r in rows)
+        fh.write(QUALITY_HEADER + "\n")
+        fh.writelines(f"{r.t},{r.size},{r.rel_diff!r}\n" for r in rows)

@@ -77,10 +77,9 @@ def pivot_invariants_hold(a, b, pivots, *, key=None) -> bool:
     p_a, p_b = pivots
     a = a.tolist() if isinstance(a, (torch.Tensor, np.ndarray)) else a
     b = b.tolist() if isinstance(b, (torch.Tensor, np.ndarray)) else b
-    if not (0 <= p_a <= len(a) and 0 <= p_b <= len(b)):
-        return False
-    if p_a > 0 and p_b < len(b) and k(a[p_a - 1]) > k(b[p_b]):
-        return False
-    if p_b > 0 and p_a < len(a) and k(b[p_b - 1]) > k(a[p_a]):
-        return False
-    return True
+    la, lb = len(a), len(b)
+    in_range = 0 <= p_a <= la and 0 <= p_b <= lb
+    # left part of each run <= right part of the other (where both sides exist)
+    a_left_ok = not (in_range and 0 < p_a and p_b < lb) or k(a[p_a - 1]) <= k(b[p_b])
+    b_left_ok = not (in_range and 0 < p_b and p_a < la) or k(b[p_b - 1]) <= k(a[p_a])
+    return in_range and a_left_ok and b_left_ok
