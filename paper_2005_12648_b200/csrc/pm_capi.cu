@@ -807,7 +807,10 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   // order after the caller's stream
   PM_CUDA(cudaEventRecord(ctx->hev[0], st));
   PM_CUDA(cudaStreamWaitEvent(sH, ctx->hev[0], 0));
-  const int64_t chunk = std::max<int64_t>((int64_t)1 << 21, (n + 95) / 96);
+#ifndef PM_HOST_CHUNKS
+#define PM_HOST_CHUNKS 96  // tune: output chunks of the host-buffer pipeline
+#endif
+  const int64_t chunk = std::max<int64_t>((int64_t)1 << 21, (n + PM_HOST_CHUNKS - 1) / PM_HOST_CHUNKS);
   const int nch = (int)((n + chunk - 1) / chunk);
   auto split = [&](int64_t d) -> int64_t {
     if (key_bytes == 4)
