@@ -185,9 +185,11 @@ def _device_stable_check(arr, keys_in_sorted_ref=None):
     assert bool(torch.all(k[1:] >= k[:-1]).item())
 
 
-@pytest.mark.parametrize("cfg,log_len", [(2, 24), (4, 24), (3, 26)])
+@pytest.mark.parametrize("cfg,log_len", [(2, 24), (4, 24), (3, 26), (2, 29), (4, 26), (3, 28)])
 def test_full_size_properties(cfg, log_len):
-    """Size-independent properties at large sizes: sorted, multiset kept, stable payload."""
+    """Size-independent properties at large sizes, up to BASELINE.json's full configs
+    (config 2: 2^30 int32; config 4: 2^27 key+index records; config 3: 2^28 + 2^16
+    int64): equal to a stable device sort, and for config 4 payload == stable argsort."""
     from paper_2005_12648_b200.workloads import config_input_device
 
     kw = {"log_len_b": 16} if cfg == 3 else {}
