@@ -301,6 +301,21 @@ def run_dist(args):
     launches = launch_count() - lc0
     if sampler:
         sampler.__exit__()
+    # one more (untimed) step with phase events: split search / exchange / local merge
+    phases = None
+    if args.exchange == "nccl":
+        ph = {}
+        work.copy_(keys0)
+        dist.barrier()
+        merge_distributed(work, pay, la, phases=ph)
+        torch.cuda.synchronize()
+        if "events" in ph:
+            e = ph["events"]
+            ex_ms = e[1].elapsed_time(e[2])
+            phases = {"splits_ms": e[0].elapsed_time(e[1]), "exchange_ms": ex_ms, "merge_ms": e[2].elapsed_time(e[3]),
+                      "bytes_in_remote": ph["bytes_in_remote"],
+                      "exchange_in_gbs": ph["bytes_in_remote"] / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None,
+                      "what": "rank 0, one extra step; exchange = two NCCL all_to_all_single (A part, B part)"}
     t = torch.tensor([sum(times)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -356,6 +371,7 @@ def run_dist(args):
             "e2e": e2e, "cpu_baseline": None,
             # ours per step and rank: k_plan + k_buffered (copy mode) of pm_merge_copy
             "gpu_launches": launches,
+            "phases": phases,
         }
         if sampler:
             line["clocks"] = sampler.summary()

@@ -133,13 +133,20 @@ def _default_local_merge(src_k: torch.Tensor, src_p: torch.Tensor, len_a: int, d
 
 
 def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | None, global_len_a: int,
-                      group=None, local_merge: Callable | None = None):
+                      group=None, local_merge: Callable | None = None, phases: dict | None = None):
     """Stable merge of the block-distributed A|B; returns this rank's output block.
 
     ``keys_local`` / ``payload_local`` are this rank's block (device tensors for
     NCCL).  Returns (keys, payload) of the same length, holding the merged
     records for this rank's block; the input tensors are overwritten too.
+    ``phases`` (optional dict, CUDA tensors only) receives CUDA events around the
+    split search, the exchange and the local merge, and the bytes this rank
+    received from other ranks.
     """
+    timed = phases is not None and keys_local.is_cuda
+    if timed:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        evs[0].record()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = keys_local.device
@@ -174,13 +181,22 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
     split_at = max(0, min(n, la - off))
     out_k = torch.empty_like(keys_local)
     out_p = torch.empty_like(payload_local)
+    if timed:
+        evs[1].record()
+        rec = keys_local.element_size() + payload_local.shape[1]
+        phases["bytes_in_remote"] = sum(recv_a[r] + recv_b[r] for r in range(world) if r != rank) * rec
     dist.all_to_all_single(out_k[:na], keys_local[:split_at].contiguous(), recv_a, send_a, group=group)
     dist.all_to_all_single(out_k[na:], keys_local[split_at:].contiguous(), recv_b, send_b, group=group)
     if payload_local.shape[1]:
         dist.all_to_all_single(out_p[:na], payload_local[:split_at].contiguous(), recv_a, send_a, group=group)
         dist.all_to_all_single(out_p[na:], payload_local[split_at:].contiguous(), recv_b, send_b, group=group)
+    if timed:
+        evs[2].record()
     if local_merge is None:
         _default_local_merge(out_k, out_p, na, keys_local, payload_local)
+        if timed:
+            evs[3].record()
+            phases["events"] = evs
     else:  # (host-logic tests: any in-place merge of the received pair)
         local_merge(out_k, out_p, na)
         keys_local.copy_(out_k)
