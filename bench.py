@@ -28,6 +28,17 @@ import os
 
 # NCCL's own messages (its version banner, NCCL_DEBUG output) go to stderr: stdout carries the one JSON line
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_FD = None  # the real stdout once main() has pointed fd 1 at stderr (libraries print there)
+
+
+def emit(line: dict) -> None:
+    """Write the result line to the real stdout (fd 1 carries library chatter to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 import statistics
 import subprocess
 import sys
@@ -212,7 +223,7 @@ def run_reference(args):
         "cpu_baseline": {"value": rate, "unit": "elements/s", "cores": t, "kind": "port", "sample": sample},
         "e2e": {"value": rate, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -375,7 +386,7 @@ def run_dist(args):
         }
         if sampler:
             line["clocks"] = sampler.summary()
-        print(json.dumps(line))
+        emit(line)
     dist.destroy_process_group()
     return 0
 
@@ -644,14 +655,20 @@ def run_ours(args):
         }
         if sampler:
             line["clocks"] = sampler.summary()
-        print(json.dumps(line))
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
 def main():
+    global _JSON_FD
     args = parse()
+    # native libraries (NCCL's version banner, ...) write to fd 1 directly: send fd 1 to
+    # stderr and keep the real stdout for the single JSON line
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     if os.environ.get("BENCH_VERBOSE"):
         import faulthandler
 
