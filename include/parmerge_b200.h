@@ -174,6 +174,14 @@ int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);
  * block exchange through the three reversals (no one-pass slide), so tests
  * exercise those paths at small sizes. */
 int pm_debug_engine_only(pm_ctx *ctx, int on);
+
+/* In-place merge engine selection (debug/benchmark control; default 1).
+ *   0: the bounded-pool engine only (k_engine: a fixed ~175 MB salvage pool);
+ *   1: the scheduled engine (pm_flow.cu), order chosen per job, falling back on
+ *      the device to the bounded-pool engine if the salvage exceeds its pool;
+ *   2 / 3: the scheduled engine with the two-front / itinerary-angle order forced;
+ *   4: run the scheduled plan, then force the device-side fallback (tests). */
+int pm_debug_flow(pm_ctx *ctx, int mode);
 /* Debug: the wide-record path's in-place row permutation on its own:
  * row p of payload (DEVICE, n rows of width bytes) becomes old row idx[p]
  * (idx: DEVICE int32[n], a permutation), cycles cut every cut_every rows. */

@@ -196,6 +196,20 @@ def set_engine_only(on: bool, device: int | None = None):
     _capi.check(_capi.lib().pm_debug_engine_only(_capi.context(dev), int(bool(on))), "pm_debug_engine_only")
 
 
+FLOW_MODES = {"bounded": 0, "auto": 1, "two_front": 2, "angle": 3, "fallback": 4}
+
+
+def set_flow_mode(mode: str, device: int | None = None):
+    """Debug/benchmark: which in-place engine pm_merge uses (pm_debug_flow).
+
+    "auto" (default): the scheduled engine, order chosen per job, with the device-side
+    fallback to the bounded-pool engine; "bounded": the bounded-pool engine only;
+    "two_front" / "angle": the scheduled engine with that order forced; "fallback":
+    plan, then force the fallback."""
+    dev = torch.cuda.current_device() if device is None else device
+    _capi.check(_capi.lib().pm_debug_flow(_capi.context(dev), FLOW_MODES[mode]), "pm_debug_flow")
+
+
 def merge_peers(peer_keys: list, peer_payload: list | None, len_a: int, rank: int, out_keys: torch.Tensor,
                 out_payload: torch.Tensor | None = None, ptrs: tuple[list[int], list[int]] | None = None):
     """pm_merge_peers: rank ``rank``'s block of the stable merge of the block-distributed

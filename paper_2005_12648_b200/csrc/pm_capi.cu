@@ -80,6 +80,11 @@ struct pm_ctx {
   size_t peer_bytes = 0;
   bool timing = false;  // record events around the plan and engine kernels
   bool engine_only = false;  // debug: no small-job / staged shortcuts (pm_debug_engine_only)
+  int flow_mode = 1;  // scheduled engine: 0 off (bounded-pool engine), 1 auto, 2 two-front, 3 angle, 4 force fallback
+  void* fws = nullptr;  // scheduled engine: plan arrays + tickets + control words
+  size_t fws_bytes = 0;
+  void* fpool = nullptr;  // scheduled engine: salvage pool (keys + payload, phase matched)
+  size_t fpool_bytes = 0;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   bool ev_recorded = false;
 };
@@ -115,7 +120,8 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
 
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
-                      void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr);
+                      void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr,
+                      const int32_t* gate = nullptr);
 
 #ifndef PM_SLIDE_STASH
 #define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
@@ -203,18 +209,23 @@ static int run_wide(pm_ctx* ctx, char* keys, int ks, uint8_t* pay, int64_t w, in
 // out_keys / out_payload non-null: copy mode -- merge keys[s,m) and keys[m,e) into
 // out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
 // keys_b / pay_b (copy mode only): the B run lives there instead of at keys + m.
+static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
+                    cudaStream_t st);
+
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys, void* out_payload,
-                      const void* keys_b, const void* pay_b) {
+                      const void* keys_b, const void* pay_b, const int32_t* gate) {
   const bool copy = out_keys != nullptr;
   if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
   int32_t mu;
+  // the fallback behind the scheduled engine goes straight to the bounded-pool engine
+  const bool direct = gate != nullptr;
   // small in-place jobs: one CTA with both runs in shared memory
-  if (mode == MODE_MERGE && !copy && !ctx->engine_only && small_merge_smem(ks, w, e - s) <= PM_SMALL_BYTES)
+  if (mode == MODE_MERGE && !copy && !direct && !ctx->engine_only && small_merge_smem(ks, w, e - s) <= PM_SMALL_BYTES)
     return launch_merge_small_(ks, keys, payload, w, s, m, e, st);
   // up to ~3 MB: one thread-block cluster, both runs in distributed shared memory
-  if (mode == MODE_MERGE && !copy && !ctx->engine_only && w <= 64 && PM_CLUSTER_MERGE) {
+  if (mode == MODE_MERGE && !copy && !direct && !ctx->engine_only && w <= 64 && PM_CLUSTER_MERGE) {
     int lchunk = 0;
     const int C = cluster_merge_plan(ks, w, e - s, &lchunk);
     if (C > 0) {
@@ -226,7 +237,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   }
   // medium in-place jobs (at most PM_STAGE_BYTES of records): the streaming merge
   // into a staging buffer, then one copy back -- both passes mostly in L2
-  if (mode == MODE_MERGE && !copy && !ctx->engine_only && (e - s) * (ks + w) <= PM_STAGE_BYTES && (PM_STAGE_WIDE || w < PM_WIDE_MIN)) {
+  if (mode == MODE_MERGE && !copy && !direct && !ctx->engine_only && (e - s) * (ks + w) <= PM_STAGE_BYTES && (PM_STAGE_WIDE || w < PM_WIDE_MIN)) {
     const int64_t n = e - s;
     const size_t kb = (size_t)align_up(n * ks + 16, 256);  // + the phase offset below
     int rc = ensure(&ctx->buf, &ctx->buf_bytes, kb + (size_t)(n * w) + 256);
@@ -250,7 +261,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #ifndef PM_USE_BUFFERED
 #define PM_USE_BUFFERED 1  // tune: the streaming buffered pipeline when scratch >= min(|A|,|B|) (2^30 int32: 2.6 ms vs 3.0 for the engine with that pool)
 #endif
-  const bool buffered = copy || (PM_USE_BUFFERED && mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
+  // the scheduled engine (pm_flow.cu) for in-place merges; it needs 16-byte aligned
+  // bases (slot boundaries are then 16-byte aligned in the array and the pool)
+  if (mode == MODE_MERGE && !copy && !direct && ctx->flow_mode != 0 && ((uintptr_t)keys & 15) == 0 &&
+      (w == 0 || ((uintptr_t)payload & 15) == 0))
+    return run_flow(ctx, keys, ks, payload, w, s, m, e, st);
+  const bool buffered = copy || (!direct && PM_USE_BUFFERED && mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
   // (the engine stages one input and one output tile; the buffered pipeline
   //  kBufStages inputs and two outputs)
   if (!pick_tiles(ks, w, buffered ? kBufBudget * 2 / (kBufStages + 2) : kTileBudget, &M, &T, &mu))
@@ -262,6 +278,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.out_pay = static_cast<uint8_t*>(out_payload);
   P.keys_b = static_cast<const char*>(keys_b);
   P.pay_b = static_cast<const uint8_t*>(pay_b);
+  P.gate = gate;
   P.w = w;
   P.ks = ks;
   P.mode = mode;
@@ -364,10 +381,11 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   // plan (splits + reset) then engine
   int64_t plan_work = std::max<int64_t>(P.Q + 1, P.K);
   int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((plan_work + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
-  if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
+  const bool timed = ctx->timing && !direct;
+  if (timed) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
   ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
-  if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[1], st));
+  if (timed) PM_CUDA(cudaEventRecord(ctx->ev[1], st));
   if (copy) {
     ce = ks == 4 ? launch_merge_copy<int32_t>(P, grid, smem, st) : launch_merge_copy<int64_t>(P, grid, smem, st);
   } else if (buffered) {
@@ -377,11 +395,123 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
                  : launch_engine<int64_t>(P, grid, kEngineThreads, smem, st);
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "k_engine launch");
-  if (ctx->timing) {
+  if (timed) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_recorded = true;
   }
   return PM_OK;
+}
+
+#ifndef PM_FLOW_POOL_DIV
+#define PM_FLOW_POOL_DIV 4  // scheduled engine: salvage pool capacity N / PM_FLOW_POOL_DIV records (+ slack)
+#endif
+#ifndef PM_FLOW_BITS
+#define PM_FLOW_BITS 12  // itinerary length of the angle order
+#endif
+#ifndef PM_FLOW_BINS
+#define PM_FLOW_BINS 16384  // angle bins of the counting sort
+#endif
+// Scheduled in-place merge (pm_flow.cu), with the bounded-pool engine queued
+// behind it on the device: it runs only if the plan's salvage exceeds the pool
+// (FC_FAIL), so the whole call stays asynchronous.
+static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
+                    cudaStream_t st) {
+  int64_t M, T;
+  int32_t mu;
+  if (!pick_tiles(ks, w, kBufBudget * 2 / (kBufStages + 2), &M, &T, &mu) || mu != 1)
+    return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
+  FlowParams F{};
+  EngineParams& P = F.P;
+  P.keys = static_cast<char*>(keys);
+  P.pay = static_cast<uint8_t*>(payload);
+  P.w = w;
+  P.ks = ks;
+  P.mode = MODE_MERGE;
+  P.s = s;
+  P.m = m;
+  P.e = e;
+  P.T = T;
+  P.M = M;
+  P.mu = 1;
+  P.lT = 63 - __builtin_clzll((unsigned long long)T);
+  P.lmu = 0;
+  P.k0 = s / T;
+  P.K = (e - 1) / T - P.k0 + 1;
+  P.R0 = P.k0;
+  P.Q = P.K;
+  P.qc = std::min<int64_t>(std::max<int64_t>(m / M - P.R0, 0), P.Q - 1);
+  if (P.K >= INT32_MAX / 2) return fail(PM_ERR_UNSUPPORTED, "job too large for 32-bit region indices");
+  P.smem_keys = (size_t)align_up((M + 2 * kSent) * ks + 64, 128);
+  if ((((M + kBufferedThreads - 32 - 1) / (kBufferedThreads - 32)) | 1) + 1 > kSent)
+    return fail(PM_ERR_INTERNAL, "tile merge span exceeds the sentinel gap");
+  P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
+  const size_t smem = (kBufStages + 2) * (P.smem_keys + P.smem_pay);
+  int bps = 0;
+  cudaError_t ce = ks == 4 ? flow_occupancy<int32_t>(smem, &bps) : flow_occupancy<int64_t>(smem, &bps);
+  if (ce != cudaSuccess) return cuda_fail(ce, "flow occupancy");
+  if (bps < 1) return fail(PM_ERR_UNSUPPORTED, "scheduled engine does not fit on an SM");
+  const int grid = (int)std::min<int64_t>((int64_t)bps * ctx->num_sms, P.Q);
+  P.grid = grid;
+  // workspace: splits | D | key | order | rank | slo | shi | pend | pdelta | tickets | hist | chunk | idn | fc
+  const int64_t K = P.K;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (size_t)align_up((int64_t)bytes, 256);
+    return o;
+  };
+  const size_t o_split = take((size_t)(P.Q + 1) * 8), o_D = take(K * 4), o_key = take(K * 4), o_order = take(K * 4),
+               o_rank = take(K * 4), o_slo = take(K * 4), o_shi = take(K * 4), o_pend = take(K * 4),
+               o_pd = take(K * 8), o_tk = take(K * sizeof(FlowTicket)), o_hist = take((PM_FLOW_BINS + 1) * 4),
+               o_chunk = take((P.Q / 1024 + 2) * 4), o_idn = take(K), o_fc = take(FC_WORDS * 8);
+  int rc = ensure(&ctx->fws, &ctx->fws_bytes, off);
+  if (rc) return rc;
+  char* b = static_cast<char*>(ctx->fws);
+  P.split_a = reinterpret_cast<int64_t*>(b + o_split);
+  F.D = reinterpret_cast<int32_t*>(b + o_D);
+  F.key = reinterpret_cast<uint32_t*>(b + o_key);
+  F.order = reinterpret_cast<int32_t*>(b + o_order);
+  F.rank = reinterpret_cast<int32_t*>(b + o_rank);
+  F.slo = reinterpret_cast<int32_t*>(b + o_slo);
+  F.shi = reinterpret_cast<int32_t*>(b + o_shi);
+  F.pend = reinterpret_cast<int32_t*>(b + o_pend);
+  F.pdelta = reinterpret_cast<int64_t*>(b + o_pd);
+  F.tk = reinterpret_cast<FlowTicket*>(b + o_tk);
+  F.hist = reinterpret_cast<int32_t*>(b + o_hist);
+  F.chunk = reinterpret_cast<int32_t*>(b + o_chunk);
+  F.idn = reinterpret_cast<uint8_t*>(b + o_idn);
+  F.fc = reinterpret_cast<long long*>(b + o_fc);
+  F.nbits = PM_FLOW_BITS;
+  F.nb = PM_FLOW_BINS;
+  F.force = ctx->flow_mode == 2 ? 0 : ctx->flow_mode == 3 ? 1 : ctx->flow_mode == 4 ? 2 : -1;
+  // salvage pool, phase matched to the caller's (16-byte aligned) arrays
+  const int64_t n = e - s;
+  F.pool_cap = n / PM_FLOW_POOL_DIV + 32 * T;
+  const size_t pk = (size_t)align_up(F.pool_cap * ks, 256);
+  rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w : 0));
+  if (rc) return rc;
+  F.pool_keys = static_cast<char*>(ctx->fpool);
+  F.pool_pay = reinterpret_cast<uint8_t*>(static_cast<char*>(ctx->fpool) + pk);
+  P.stats = ctx->ctl->stats;
+  P.ticket = &ctx->ctl->ticket_.v;
+  P.err = &ctx->ctl->err_.v;
+  P.noop = &ctx->ctl->noop_.v;
+  P.need_space = &ctx->ctl->need_space_.v;
+  // splits (k_plan_coarse / k_plan; no engine bookkeeping), then the flow plan and merge
+  const int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((P.Q + 256) / 256, 1), (int64_t)ctx->num_sms * 8);
+  if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
+  ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
+  ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr)
+               : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_flow launch");
+  if (ctx->timing) {
+    PM_CUDA(cudaEventRecord(ctx->ev[2], st));
+    ctx->ev_recorded = true;
+  }
+  // the bounded-pool engine, gated on the plan's overflow word
+  return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, 0, st, nullptr, nullptr, nullptr, nullptr,
+                    reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
 }
 
 static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* payload, int64_t w) {
@@ -601,12 +731,21 @@ int pm_ctx_destroy(pm_ctx* ctx) {
   if (ctx->wide) cudaFree(ctx->wide);
   if (ctx->wperm) cudaFree(ctx->wperm);
   if (ctx->peer) cudaFree(ctx->peer);
+  if (ctx->fws) cudaFree(ctx->fws);
+  if (ctx->fpool) cudaFree(ctx->fpool);
   for (auto& x : ctx->hs)
     if (x) cudaStreamDestroy(x);
   for (auto& x : ctx->hev)
     if (x) cudaEventDestroy(x);
   if (ctx->ctl) cudaFree(ctx->ctl);
   delete ctx;
+  return PM_OK;
+}
+
+int pm_debug_flow(pm_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 4) return fail(PM_ERR_ARG, "bad pm_debug_flow arguments");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->flow_mode = mode;
   return PM_OK;
 }
 

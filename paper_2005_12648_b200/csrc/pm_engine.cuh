@@ -158,6 +158,53 @@ struct EngineParams {
   uint8_t* out_pay;
   const char* keys_b;  // copy mode: B run base (record j at keys_b + j*ks), else null (B = keys + m)
   const uint8_t* pay_b;
+  // device-side routing: when non-null the kernel runs only if *gate != 0 (the
+  // bounded-pool engine behind the scheduled engine, taken when the latter's plan
+  // does not fit its pool -- pm_flow.cu)
+  const int32_t* gate;
+};
+
+// Scheduled in-place merge (pm_flow.cu).  Per region ("ticket") of the plan's
+// processing order, what the streaming kernel needs in one 80-byte load: the
+// region, its splits, and for each of its (at most two) A and B pieces whether it
+// is read from the original slot or from the slot's salvage entry in the pool
+// (pool address of record x = pool + (x + delta) * bytes).
+struct FlowTicket {
+  int32_t r;      // region (== slot it writes)
+  int32_t flags;  // bit 1+k: A piece k from the pool; bit 3+k: B piece k from the pool
+  int32_t ja[2];  // slot of A piece k (-1: none)
+  int32_t jb[2];  // slot of B piece k
+  int32_t pad_[2];
+  int64_t a0, a1;  // A-local split at the region's two diagonals
+  int64_t dA[2], dB[2];
+};
+static_assert(sizeof(FlowTicket) == 80, "FlowTicket is loaded as five 16-byte vectors");
+
+// flow control words (int64, one 256-byte line)
+enum : int { FC_SAL_ANGLE = 0, FC_SAL_TF = 1, FC_POOL = 2, FC_NIDENT = 3, FC_MODE = 4, FC_FAIL = 5, FC_NTICK = 6,
+             FC_NSALV = 7, FC_WORDS = 32 };
+
+struct FlowParams {
+  EngineParams P;       // geometry (T == M, one slot per region, Q == K), splits, ticket/err/noop/stats
+  int32_t* D;           // [K] region reading the slot's middle record | (record in B) << 31
+  uint8_t* idn;         // [K] identity region (inputs already on its outputs)
+  uint32_t* key;        // [K] angle-order key (bin)
+  int32_t* order;       // [K] ticket -> region
+  int32_t* rank;        // [K] region -> ticket (INT32_MAX: identity, never processed)
+  int32_t* hist;        // [nb + 1] angle bins: counts, then cursors
+  int32_t* chunk;       // [Q / 1024 + 2] identity regions per 1024 two-front tickets, then prefix
+  int32_t* slo;         // [K] salvage hull of the slot (record offsets in the slot), slo >= shi: none
+  int32_t* shi;
+  int32_t* pend;        // [K] lower-ranked readers of the slot that have not read it yet
+  int64_t* pdelta;      // [K] pool delta of the slot's salvage entry
+  FlowTicket* tk;       // [K]
+  long long* fc;        // control words (FC_*)
+  char* pool_keys;      // phase-matched to keys (16-byte) / payload
+  uint8_t* pool_pay;
+  int64_t pool_cap;     // records
+  int32_t nbits;        // itinerary length of the angle key
+  int32_t nb;           // angle bins
+  int32_t force;        // -1: choose per job, 0: two-front, 1: angle order, 2: force the fallback
 };
 
 }  // namespace pm

@@ -1,0 +1,665 @@
+// pm_flow.cu -- the scheduled in-place merge ("flow" engine, sm_100a).
+//
+// Same job as k_engine (pm_engine.cu): the stable merge (A wins ties) of the
+// adjacent sorted runs A = [s, m) and B = [m, e) in place, bit-exact to the
+// reference's stable core (seqmerge.py:55-75 / _kernels.py:227-313; the t >= 1
+// drivers srecpar.py:33-84, soptmov.py:146-192 produce the same records).  The
+// difference is WHEN the work is decided: k_engine discovers at run time, region
+// by region, which units must be moved out of the way (a chain of dependent
+// global round trips per region); here a plan computed on the device before the
+// merge fixes the whole schedule, so the merge itself is a streaming pipeline
+// whose only synchronisation is one counter per region.
+//
+// Output region q (M records) == slot q of the array.  Writing region q destroys
+// slot q's input records; every other region that reads some of them ("reader")
+// must have read them first, or they must have been saved ("salvaged") into the
+// pool.  For a processing order (rank), reader c of slot j reads
+//   * the original slot when rank(c) < rank(j)  (j's store waits for c's read:
+//     pend[j] counts those readers, each decrements it once its loads landed),
+//   * the slot's salvage entry otherwise (copied before the merge starts).
+// So the salvage volume is the weight of the order's backward edges in the
+// reader graph.  For two uniform runs that graph is the binary de Bruijn graph
+// (slot j is read by regions 2j, 2j+1 mod K), whose cycles force some salvage.
+// Two orders are evaluated per job and the cheaper one is taken:
+//   * two fronts out of the A/B boundary (k_engine's order): 1/3 of N for uniform
+//     runs, near zero for skewed/translated inputs;
+//   * the itinerary angle: slot j's symbolic orbit (side of j, side of the region
+//     reading j's middle record, side of the region reading that slot, ...) b_1..b_n
+//     gives z_j = sum_i b_i exp(2 pi i k / n); a reader's z is z_j rotated by
+//     -2 pi / n up to a +-1 perturbation, so processing in increasing arg(z) puts
+//     readers first except across the cut and where the perturbation wins (the
+//     circle-valued potential behind Mykkeltveit's de Bruijn feedback sets):
+//     ~0.20 N salvaged for uniform runs (tools/sim_flow.py).
+//
+// Plan kernels (one pass each, all on the device, no host round trip):
+//   k_plan_coarse/k_plan (pm_engine.cu) : merge-path split at every region boundary
+//   k_flow_readers : identity regions; the reader of each slot's middle record
+//   k_flow_angle   : itinerary angle key per slot, angle histogram
+//   k_flow_choose  : salvage volume of both orders (per region, its <= 4 pieces)
+//   k_flow_decide  : pick the order; scan the histogram / identity counts
+//   k_flow_rank    : order[] / rank[] (counting sort / two-front compaction)
+//   k_flow_hull    : per slot the hull of records later readers need; pend[] counts
+//   k_flow_alloc   : pool entries (16-record aligned, phase-matched)
+//   k_flow_tickets : the 80-byte per-ticket descriptor
+// Merge:
+//   k_flow_save    : copy every salvage entry into the pool
+//   k_flow         : persistent streaming pipeline (k_buffered's shape): TMA
+//                    gathers of the next region while the current one merges in
+//                    shared memory, TMA bulk store in place once pend[r] == 0.
+// If the salvage does not fit the pool the plan raises FC_FAIL; k_flow then
+// exits at once and the bounded-pool engine (gated on that word) runs instead.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "pm_common.cuh"
+#include "pm_engine.cuh"
+#include "pm_launch.h"
+#include "pm_tile.cuh"
+
+namespace pm {
+
+constexpr int kFlowChunk = 1024;  // two-front tickets per compaction block
+
+struct FlowGeo : Geo {
+  __device__ explicit FlowGeo(const EngineParams& p) : Geo(p) {}
+  __device__ int64_t bsplit(int64_t q) const { return diag(q) - split(q); }
+  // smallest region q whose A range ends after A-local index v (0 <= v < LA)
+  __device__ int64_t reader_a(int64_t v) const {
+    int64_t lo = 0, hi = P.Q - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (split(mid + 1) > v) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  }
+  __device__ int64_t reader_b(int64_t v) const {
+    int64_t lo = 0, hi = P.Q - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (bsplit(mid + 1) > v) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  }
+  __device__ bool identity(int64_t q, int64_t a0, int64_t a1) const {
+    const int64_t la = LA();
+    return (a0 == diag(q) && a1 == diag(q + 1)) || (a0 == la && a1 == la);
+  }
+};
+
+// The pieces of region q: A records [s+a0, s+a1) and B records [m+b0, m+b1), each
+// cut at slot boundaries (at most two pieces per run: a run of a region holds at
+// most M == T records).  f(slot, lo, hi, k, is_b): absolute record range [lo, hi).
+template <class F>
+__device__ __forceinline__ void for_pieces(const EngineParams& P, int64_t xa0, int64_t xa1, int64_t xb0, int64_t xb1,
+                                           F&& f) {
+  for (int side = 0; side < 2; ++side) {
+    int64_t x = side ? xb0 : xa0;
+    const int64_t xe = side ? xb1 : xa1;
+    for (int k = 0; x < xe && k < 2; ++k) {
+      const int64_t y = min(xe, ((x >> P.lT) + 1) << P.lT);
+      f((x >> P.lT) - P.k0, x, y, k, side);
+      x = y;
+    }
+  }
+}
+
+__device__ __forceinline__ bool flow_off(const FlowParams& F) {
+  return *(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_FAIL];
+}
+
+// ---- k_flow_readers: identity flags, middle-record reader, resets -------------
+__global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  if (tid < FC_WORDS) F.fc[tid] = 0;
+  if (*(volatile int32_t*)P.noop) return;
+  for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;
+  for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
+  for (int64_t j = tid; j < P.K; j += nthr) {
+    const int64_t x0 = g.slot_lo(j), x1 = g.slot_hi(j);
+    const int64_t y = (x0 + x1 - 1) >> 1;
+    const int32_t side = y >= P.m;
+    const int64_t dj = side ? g.reader_b(y - P.m) : g.reader_a(y - P.s);
+    F.D[j] = (int32_t)dj | (side ? (int32_t)0x80000000 : 0);
+    F.idn[j] = g.identity(j, g.split(j), g.split(j + 1)) ? 1 : 0;
+    F.rank[j] = INT32_MAX;
+    F.slo[j] = (int32_t)P.T;
+    F.shi[j] = 0;
+    F.pend[j] = 0;
+  }
+}
+
+// ---- k_flow_angle: itinerary angle key per slot --------------------------------
+__global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
+  const EngineParams& P = F.P;
+  if (flow_off(F)) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const int n = F.nbits;
+  const float step = 6.283185307179586f / (float)n;
+  TwoFront tf{P.Q, P.qc};
+  for (int64_t j = tid; j < P.K; j += nthr) {
+    uint32_t key = (uint32_t)F.nb;  // identity: the last bin (never ranked)
+    if (!F.idn[j]) {
+      float zr = 0.f, zi = 0.f;
+      int32_t x = (int32_t)j;
+      for (int i = 1; i <= n; ++i) {
+        const int32_t v = __ldg(&F.D[x]);
+        if (v < 0) {
+          float sn, cs;
+          __sincosf(step * (float)i, &sn, &cs);
+          zr += cs;
+          zi += sn;
+        }
+        x = v & 0x7fffffff;
+      }
+      float ang = atan2f(zi, zr);
+      if (ang < 0.f) ang += 6.283185307179586f;
+      key = min((uint32_t)(ang * (float)F.nb * 0.15915494309189535f), (uint32_t)F.nb - 1);
+      atomicAdd(&F.hist[key], 1);
+    } else {
+      atomicAdd(&F.chunk[tf.order(j) / kFlowChunk], 1);
+      atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], 1ull);
+    }
+    F.key[j] = key;
+  }
+}
+
+// ---- k_flow_choose: salvage volume of both orders ------------------------------
+// Region q reads piece (slot j, n records); it reads the salvage entry iff it
+// comes after j.  Angle order ties (same bin) are broken by region index here
+// (the counting sort breaks them arbitrarily -- an estimate suffices).
+__global__ void __launch_bounds__(256) k_flow_choose(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  if (flow_off(F) || F.force >= 0) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  TwoFront tf{P.Q, P.qc};
+  unsigned long long sa = 0, st = 0;
+  for (int64_t q = tid; q < P.Q; q += nthr) {
+    if (F.idn[q]) continue;
+    const int64_t a0 = g.split(q), a1 = g.split(q + 1), d0 = g.diag(q), d1 = g.diag(q + 1);
+    const uint32_t kq = F.key[q];
+    const int64_t oq = tf.order(q);
+    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t j, int64_t lo, int64_t hi, int, int) {
+      if (j == q) return;
+      const uint32_t kj = __ldg(&F.key[j]);
+      if (kq > kj || (kq == kj && q > j)) sa += (unsigned long long)(hi - lo);
+      if (oq > tf.order(j)) st += (unsigned long long)(hi - lo);
+    });
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (sa | st)) {
+    atomicAdd((unsigned long long*)&F.fc[FC_SAL_ANGLE], sa);
+    atomicAdd((unsigned long long*)&F.fc[FC_SAL_TF], st);
+  }
+}
+
+// block-wide exclusive scan of one int32 per thread (blockDim.x <= 1024); returns
+// the exclusive prefix, *total the block sum
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* total) {
+  __shared__ int32_t ws[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();  // (ws reuse across calls)
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t s = lane < nw ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) ws[lane] = s;
+  }
+  __syncthreads();
+  *total = ws[nw - 1];
+  return (wid ? ws[wid - 1] : 0) + x - v;
+}
+
+// ---- k_flow_decide (one CTA): the order, then its scan ------------------------
+__global__ void __launch_bounds__(1024) k_flow_decide(FlowParams F) {
+  const EngineParams& P = F.P;
+  if (flow_off(F)) return;
+  __shared__ int32_t s_mode;
+  if (threadIdx.x == 0) {
+    int32_t mode = F.force;
+    if (mode < 0) mode = F.fc[FC_SAL_ANGLE] < F.fc[FC_SAL_TF] ? 1 : 0;
+    if (mode == 2) {  // debug: exercise the device-side fallback
+      F.fc[FC_FAIL] = 1;
+      mode = 0;
+    }
+    s_mode = mode;
+    F.fc[FC_MODE] = mode;
+    F.fc[FC_NTICK] = (long long)P.Q - F.fc[FC_NIDENT];
+  }
+  __syncthreads();
+  if (s_mode == 1) {  // exclusive scan of the angle histogram, in place (cursors)
+    int32_t base = 0;
+    for (int64_t b0 = 0; b0 < F.nb; b0 += blockDim.x) {
+      const int64_t b = b0 + threadIdx.x;
+      const int32_t v = b < F.nb ? F.hist[b] : 0;
+      int32_t tot;
+      const int32_t ex = block_excl_scan(v, &tot);
+      if (b < F.nb) F.hist[b] = base + ex;
+      base += tot;
+    }
+  } else {  // exclusive scan of the per-chunk identity counts
+    int32_t base = 0;
+    const int64_t nc = P.Q / kFlowChunk + 1;
+    for (int64_t c0 = 0; c0 < nc; c0 += blockDim.x) {
+      const int64_t c = c0 + threadIdx.x;
+      const int32_t v = c < nc ? F.chunk[c] : 0;
+      int32_t tot;
+      const int32_t ex = block_excl_scan(v, &tot);
+      if (c < nc) F.chunk[c] = base + ex;
+      base += tot;
+    }
+  }
+}
+
+// ---- k_flow_rank: order[] / rank[] -------------------------------------------
+// angle order: counting-sort scatter (ties in arrival order); two-front: block b
+// compacts tickets [1024 b, 1024 b + 1024) minus identity regions.
+__global__ void __launch_bounds__(kFlowChunk) k_flow_rank(FlowParams F) {
+  const EngineParams& P = F.P;
+  if (flow_off(F)) return;
+  const int32_t mode = (int32_t)F.fc[FC_MODE];
+  if (mode == 1) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = tid; j < P.Q; j += nthr) {
+      if (F.idn[j]) continue;
+      const int32_t t = atomicAdd(&F.hist[F.key[j]], 1);
+      F.order[t] = (int32_t)j;
+      F.rank[j] = t;
+    }
+  } else {
+    TwoFront tf{P.Q, P.qc};
+    for (int64_t b = blockIdx.x; b * kFlowChunk < P.Q; b += gridDim.x) {
+      const int64_t t = b * kFlowChunk + threadIdx.x;
+      int32_t q = -1, f = 0;
+      if (t < P.Q) {
+        q = (int32_t)tf.region_of_ticket(t);
+        f = F.idn[q] ? 0 : 1;
+      }
+      int32_t tot;
+      const int32_t ex = block_excl_scan(f, &tot);
+      if (f) {
+        const int32_t pos = (int32_t)(b * kFlowChunk - F.chunk[b]) + ex;
+        F.order[pos] = q;
+        F.rank[q] = pos;
+      }
+    }
+  }
+}
+
+// ---- k_flow_hull: salvage hulls and pending-reader counts ----------------------
+__global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  if (flow_off(F)) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = tid; q < P.Q; q += nthr) {
+    if (F.idn[q]) continue;
+    const int64_t a0 = g.split(q), a1 = g.split(q + 1), d0 = g.diag(q), d1 = g.diag(q + 1);
+    const int32_t rq = F.rank[q];
+    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t j, int64_t lo, int64_t hi, int, int) {
+      if (j == q) return;
+      if (rq > __ldg(&F.rank[j])) {  // j is written first: q reads its salvage entry
+        const int64_t base = g.slot_base(j);
+        atomicMin(&F.slo[j], (int32_t)(lo - base));
+        atomicMax(&F.shi[j], (int32_t)(hi - base));
+      } else {
+        atomicAdd(&F.pend[j], 1);  // j's store waits for this read
+      }
+    });
+  }
+}
+
+// ---- k_flow_alloc: pool entries ------------------------------------------------
+// Entry of slot j: records [L, H) of the slot, L/H its salvage hull rounded to
+// multiples of 16 records (so an entry keeps the caller's 16-byte phase and every
+// superset TMA load of a piece stays inside it).  One atomic per block.
+__global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  if (flow_off(F)) return;
+  __shared__ long long s_base;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < P.K; j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    int32_t sz = 0, L = 0;
+    if (j < P.K) {
+      const int32_t lo = F.slo[j], hi = F.shi[j];
+      if (hi > lo) {
+        L = lo & ~15;
+        sz = ((hi + 15) & ~15) - L;
+      }
+    }
+    int32_t tot;
+    const int32_t ex = block_excl_scan(sz, &tot);
+    if (threadIdx.x == 0) {
+      s_base = tot ? atomicAdd((unsigned long long*)&F.fc[FC_POOL], (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    const long long base = s_base;
+    __syncthreads();
+    if (sz) {
+      const long long off = base + ex;  // multiple of 16 records
+      if (off + sz > F.pool_cap) {
+        atomicExch((unsigned long long*)&F.fc[FC_FAIL], 1ull);
+      } else {
+        F.pdelta[j] = off - (g.slot_base(j) + L);
+        atomicAdd((unsigned long long*)&F.fc[FC_NSALV], 1ull);
+      }
+    }
+  }
+}
+
+// ---- k_flow_tickets: per-ticket descriptors ------------------------------------
+__global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  if (flow_off(F)) return;
+  const int64_t nt = F.fc[FC_NTICK];
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) {  // pm_status: salvaged slots / records, identity regions, order, both salvage estimates
+    P.stats[0] = (unsigned long long)F.fc[FC_NSALV];
+    P.stats[1] = (unsigned long long)F.fc[FC_POOL];
+    P.stats[3] = (unsigned long long)F.fc[FC_NIDENT];
+    P.stats[4] = (unsigned long long)(F.fc[FC_MODE] + 1);
+    P.stats[5] = (unsigned long long)F.fc[FC_SAL_ANGLE];
+    P.stats[6] = (unsigned long long)F.fc[FC_SAL_TF];
+  }
+  for (int64_t t = tid; t < nt; t += nthr) {
+    const int32_t q = F.order[t];
+    FlowTicket T;
+    T.r = q;
+    T.flags = 0;
+    T.ja[0] = T.ja[1] = T.jb[0] = T.jb[1] = -1;
+    T.pad_[0] = T.pad_[1] = 0;
+    T.a0 = g.split(q);
+    T.a1 = g.split(q + 1);
+    T.dA[0] = T.dA[1] = T.dB[0] = T.dB[1] = 0;
+    const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+    for_pieces(P, P.s + T.a0, P.s + T.a1, P.m + d0 - T.a0, P.m + d1 - T.a1,
+               [&](int64_t j, int64_t, int64_t, int k, int side) {
+                 const bool pool = j != q && __ldg(&F.rank[j]) < (int32_t)t;
+                 if (side == 0) {
+                   T.ja[k] = (int32_t)j;
+                   if (pool) {
+                     T.flags |= 1 << (1 + k);
+                     T.dA[k] = F.pdelta[j];
+                   }
+                 } else {
+                   T.jb[k] = (int32_t)j;
+                   if (pool) {
+                     T.flags |= 1 << (3 + k);
+                     T.dB[k] = F.pdelta[j];
+                   }
+                 }
+               });
+    F.tk[t] = T;
+  }
+}
+
+// ---- k_flow_save: copy the salvage entries into the pool ------------------------
+// One warp per slot (grid-stride); 16-byte vectors, identical phase on both sides.
+__global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  if (flow_off(F)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t ks = P.ks, w = P.w;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w0; j < P.K; j += nw) {
+    const int32_t lo = F.slo[j], hi = F.shi[j];
+    if (hi <= lo) continue;
+    const int64_t base = g.slot_base(j);
+    // copy the records of the hull that belong to the job
+    const int64_t x0 = max(base + lo, g.slot_lo(j)), x1 = min(base + hi, g.slot_hi(j));
+    if (x1 <= x0) continue;
+    const int64_t dl = F.pdelta[j];
+    copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (x0 + dl) * ks),
+                  reinterpret_cast<const uint8_t*>(P.keys + x0 * ks), (x1 - x0) * ks, lane);
+    if (w) copy_g2g_warp(F.pool_pay + (x0 + dl) * w, P.pay + x0 * w, (x1 - x0) * w, lane);
+  }
+}
+
+// ---- k_flow: the streaming in-place merge ---------------------------------------
+struct FlowDesc {
+  int64_t d0;
+  int32_t r, alpha, beta, nout, offA, offB, poffA, poffB;
+  int32_t rd[4];  // slots read from their original place (pend[] to release), -1: none
+};
+
+__device__ __forceinline__ FlowTicket load_ticket(const FlowTicket* p) {
+  FlowTicket T;
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&T);
+#pragma unroll
+  for (int i = 0; i < 5; ++i) d[i] = __ldg(s + i);
+  return T;
+}
+
+// leader: the region's geometry, then TMA loads of its pieces into the stage
+template <typename KT>
+__device__ __forceinline__ void flow_issue(const FlowParams& F, const FlowGeo& g, const FlowTicket& T,
+                                           FlowDesc& D, uint8_t* kin, uint8_t* pin, uint64_t* bar) {
+  const EngineParams& P = F.P;
+  const int64_t ks = sizeof(KT), w = P.w;
+  const int64_t q = T.r;
+  const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
+  const int64_t a0 = T.a0, a1 = T.a1, b0 = d0 - a0, b1 = d1 - a1;
+  const int64_t alpha = a1 - a0, beta = b1 - b0;
+  const int64_t xa = P.s + a0, xb = P.m + b0;
+  D.d0 = d0;
+  D.r = (int32_t)q;
+  D.alpha = (int32_t)alpha;
+  D.beta = (int32_t)beta;
+  D.nout = (int32_t)(d1 - d0);
+  const int64_t offA = ((uintptr_t)(P.keys + xa * ks)) & 15;
+  const int64_t offB = ((offA + (alpha + kSent) * ks + 15) & ~(int64_t)15) + (((uintptr_t)(P.keys + xb * ks)) & 15);
+  int64_t poffA = 0, poffB = 0;
+  if (w) {
+    poffA = ((uintptr_t)(P.pay + xa * w)) & 15;
+    poffB = ((poffA + alpha * w + 15) & ~(int64_t)15) + (((uintptr_t)(P.pay + xb * w)) & 15);
+  }
+  D.offA = (int32_t)offA;
+  D.offB = (int32_t)offB;
+  D.poffA = (int32_t)poffA;
+  D.poffB = (int32_t)poffB;
+  int nrd = 0;
+  D.rd[0] = D.rd[1] = D.rd[2] = D.rd[3] = -1;
+  for_pieces(P, xa, xa + alpha, xb, xb + beta, [&](int64_t j, int64_t x, int64_t y, int k, int side) {
+    const bool pool = (T.flags >> (side ? 3 + k : 1 + k)) & 1;
+    const int64_t dl = pool ? (side ? T.dB[k] : T.dA[k]) : 0;
+    const int64_t o = side ? x - xb : x - xa;  // records already staged on this side
+    const char* ksrc = (pool ? F.pool_keys : P.keys) + (x + dl) * ks;
+    copy_g2s_superset(kin + (side ? offB : offA) + o * ks, reinterpret_cast<const uint8_t*>(ksrc), (y - x) * ks, bar);
+    if (w) {
+      const uint8_t* psrc = (pool ? F.pool_pay : P.pay) + (x + dl) * w;
+      copy_g2s_superset(pin + (side ? poffB : poffA) + o * w, psrc, (y - x) * w, bar);
+    }
+    if (!pool && j != q) D.rd[nrd++] = (int32_t)j;
+  });
+  mbar_arrive(bar);
+}
+
+// the region's reads have landed: release the original slots it read
+__device__ __forceinline__ void flow_release(const FlowParams& F, const FlowDesc& D) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (D.rd[i] >= 0) atomicSub(&F.pend[D.rd[i]], 1);
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
+  constexpr int NS = kBufStages;
+  extern __shared__ __align__(128) uint8_t dyn[];
+  __shared__ uint64_t bar[NS];
+  __shared__ int64_t s_t[NS];
+  __shared__ FlowDesc s_d[NS];
+  __shared__ int32_t s_early[NS];
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  constexpr int NT = kBufferedThreads;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int NW = NT >> 5;
+  const bool ctrl = (tid >> 5) == NW - 1;
+  const bool leader = ctrl && lane == 0;
+  const int MT = NT - 32;
+  const int64_t ks = sizeof(KT), w = P.w;
+  if (flow_off(F)) return;
+  const int64_t ntick = F.fc[FC_NTICK];
+  const size_t tile = P.smem_keys + P.smem_pay;
+#define STAGE(b) (dyn + (size_t)(b) * tile)
+#define OUTB(b) (dyn + (size_t)(NS + (b)) * tile)
+  int32_t t_pref = 0;
+  if (leader) {
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&bar[k], 1);
+      s_early[k] = 0;
+      s_t[k] = ntick;
+    }
+    for (int k = 0; k < NS - 1; ++k) {
+      const int64_t t0 = (*(volatile int32_t*)P.err) ? ntick : atomicAdd(P.ticket, 1);
+      s_t[k] = t0 < ntick ? t0 : ntick;
+      if (t0 >= ntick) break;
+      flow_issue<KT>(F, g, load_ticket(F.tk + t0), s_d[k], STAGE(k), STAGE(k) + P.smem_keys, &bar[k]);
+    }
+    t_pref = atomicAdd(P.ticket, 1);
+  }
+  __syncthreads();
+  uint32_t phmask = 0;
+  unsigned long long n_reg = 0;
+  for (int it = 0;; ++it) {
+    const int cur = it % NS, ob = it & 1;
+    const int64_t t = s_t[cur];
+    if (t >= ntick) break;
+    const FlowDesc R = s_d[cur];
+    if (leader) {  // keep NS-1 regions in flight: the previous iteration's stage is free
+      const int nx = (it + NS - 1) % NS;
+      const int64_t tn = (*(volatile int32_t*)P.err) ? ntick : (t_pref < ntick ? t_pref : ntick);
+      if (t_pref < ntick) t_pref = atomicAdd(P.ticket, 1);
+      s_t[nx] = tn;
+      s_early[nx] = 0;
+      if (tn < ntick)
+        flow_issue<KT>(F, g, load_ticket(F.tk + tn), s_d[nx], STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
+    }
+    while (!mbar_try_wait(&bar[cur], (phmask >> cur) & 1)) {
+    }
+    phmask ^= 1u << cur;
+    const int64_t phk = ((uintptr_t)(P.keys + (P.s + R.d0) * ks)) & 15;
+    const int64_t php = w ? (((uintptr_t)(P.pay + (P.s + R.d0) * w)) & 15) : 0;
+    uint8_t* kout_s = OUTB(ob);
+    uint8_t* pout_s = OUTB(ob) + P.smem_keys;
+    if (ctrl) {
+      // (relaxed releases: the loads have completed -- the barrier said so -- so a
+      // writer that sees the count drop cannot change what this region read)
+      if (leader && !s_early[cur]) flow_release(F, R);
+      // every lower-ranked reader of this slot has read it
+      if (leader) {
+        for (uint32_t it2 = 0; ld_acquire(&F.pend[R.r]) != 0; ++it2) {
+          if ((it2 & 255) == 255 && ld_relaxed(P.err)) break;
+          if (it2 > kSpinLimit) {
+            raise_error(P.err, PM_ERR_TIMEOUT);
+            break;
+          }
+          backoff(it2);
+        }
+        // regions in flight whose loads have landed: release their reads early
+        for (int k = 1; k < NS; ++k) {
+          const int sk = (it + k) % NS;
+          if (s_t[sk] < ntick && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
+            flow_release(F, s_d[sk]);
+            s_early[sk] = 1;
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+      uint8_t* kin = STAGE(cur);
+      uint8_t* pin = STAGE(cur) + P.smem_keys;
+      if (!w) {
+        write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, tid, MT);
+        named_barrier_sync(1, MT);
+      }
+      const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
+      merge_tile<KT, kBufferedThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
+                                            reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                                            reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                            pin + R.poffB, w, wq4, tid);
+      fence_proxy_async_smem();
+    }
+    __syncthreads();  // tile complete, slot clear
+    const int gt = (tid + 32) % NT;
+    stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), (int64_t)R.nout * ks, gt, NT);
+    if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, (int64_t)R.nout * w, gt, NT);
+    ++n_reg;
+    if (leader) bulk_wait_read<1>();  // the store that used the other output buffer has read it
+    __syncthreads();
+  }
+  if (leader) {
+    bulk_wait_all();
+    atomicAdd(&P.stats[2], n_reg);
+  }
+#undef STAGE
+#undef OUTB
+}
+
+// ---- host launcher ---------------------------------------------------------------
+template <typename KT>
+cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_flow<KT>, kBufferedThreads, smem);
+}
+
+// plan kernels (after launch_plan's splits); ev (may be null) is recorded between
+// the plan and the merge
+template <typename KT>
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev) {
+  const EngineParams& P = F.P;
+  const int g1 = (int)std::min<int64_t>((P.Q + 255) / 256, (int64_t)num_sms * 8);
+  k_flow_readers<<<g1, 256, 0, st>>>(F);
+  k_flow_angle<<<g1, 256, 0, st>>>(F);
+  k_flow_choose<<<g1, 256, 0, st>>>(F);
+  k_flow_decide<<<1, 1024, 0, st>>>(F);
+  k_flow_rank<<<(int)std::min<int64_t>((P.Q + kFlowChunk - 1) / kFlowChunk, (int64_t)num_sms * 2), kFlowChunk, 0, st>>>(F);
+  k_flow_hull<<<g1, 256, 0, st>>>(F);
+  k_flow_alloc<<<g1, 256, 0, st>>>(F);
+  k_flow_tickets<<<g1, 256, 0, st>>>(F);
+  count_launches(8);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (ev) {
+    e = cudaEventRecord(ev, st);
+    if (e != cudaSuccess) return e;
+  }
+  k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
+  e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_flow<KT><<<grid, kBufferedThreads, smem, st>>>(F);
+  count_launches(2);
+  return cudaGetLastError();
+}
+
+template cudaError_t flow_occupancy<int32_t>(size_t, int*);
+template cudaError_t flow_occupancy<int64_t>(size_t, int*);
+template cudaError_t launch_flow<int32_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t);
+template cudaError_t launch_flow<int64_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t);
+
+}  // namespace pm

@@ -13,6 +13,10 @@ template <typename KT> cudaError_t launch_plan(const EngineParams& P, int grid, 
 template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);
 template <typename KT> cudaError_t buffered_occupancy(size_t smem, int* blocks_per_sm);
+// scheduled in-place merge (pm_flow.cu): plan kernels + pool copy + streaming merge
+template <typename KT> cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm);
+template <typename KT>
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev);
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st);
