@@ -408,6 +408,12 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #ifndef PM_FLOW_BITS
 #define PM_FLOW_BITS 12  // itinerary length of the angle order
 #endif
+#ifndef PM_FLOW_SYNC
+#define PM_FLOW_SYNC 4  // angular-synchronisation steps refining the angle order
+#endif
+#ifndef PM_FLOW_SYNC_DIV
+#define PM_FLOW_SYNC_DIV 10  // their phase step 2 pi / PM_FLOW_SYNC_DIV
+#endif
 #ifndef PM_FLOW_BINS
 #define PM_FLOW_BINS 16384  // angle bins of the counting sort
 #endif
@@ -418,8 +424,12 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
                     cudaStream_t st) {
   int64_t M, T;
   int32_t mu;
-  if (!pick_tiles(ks, w, kBufBudget * 2 / (kBufStages + 2), &M, &T, &mu) || mu != 1)
-    return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
+  // regions: the largest power of two <= 8192 records whose keys + rows fit a tile
+  M = 8192;
+  while (M > 16 && M * (ks + w) > PM_FLOW_TILE) M >>= 1;
+  if (M * (ks + w) > PM_FLOW_TILE) return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
+  T = M;
+  (void)mu;
   FlowParams F{};
   EngineParams& P = F.P;
   P.keys = static_cast<char*>(keys);
@@ -442,10 +452,10 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   P.qc = std::min<int64_t>(std::max<int64_t>(m / M - P.R0, 0), P.Q - 1);
   if (P.K >= INT32_MAX / 2) return fail(PM_ERR_UNSUPPORTED, "job too large for 32-bit region indices");
   P.smem_keys = (size_t)align_up((M + 2 * kSent) * ks + 64, 128);
-  if ((((M + kBufferedThreads - 32 - 1) / (kBufferedThreads - 32)) | 1) + 1 > kSent)
+  if ((((M + kFlowThreads - 32 - 1) / (kFlowThreads - 32)) | 1) + 1 > kSent)
     return fail(PM_ERR_INTERNAL, "tile merge span exceeds the sentinel gap");
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
-  const size_t smem = (kBufStages + 2) * (P.smem_keys + P.smem_pay);
+  const size_t smem = (kFlowStages + kFlowOut) * (P.smem_keys + P.smem_pay);
   int bps = 0;
   cudaError_t ce = ks == 4 ? flow_occupancy<int32_t>(smem, &bps) : flow_occupancy<int64_t>(smem, &bps);
   if (ce != cudaSuccess) return cuda_fail(ce, "flow occupancy");
@@ -464,6 +474,17 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
                o_rank = take(K * 4), o_slo = take(K * 4), o_shi = take(K * 4), o_pend = take(K * 4),
                o_pd = take(K * 8), o_tk = take(K * sizeof(FlowTicket)), o_hist = take((PM_FLOW_BINS + 1) * 4),
                o_chunk = take((P.Q / 1024 + 2) * 4), o_idn = take(K), o_fc = take(FC_WORDS * 8);
+  // split-search samples (stride S = min(256, M); S divides M)
+#ifndef PM_FLOW_SAMPLE
+#define PM_FLOW_SAMPLE 1024  // split-search sample stride (records)
+#endif
+  const int64_t S = std::min<int64_t>(PM_FLOW_SAMPLE, M);
+  F.lS = 63 - __builtin_clzll((unsigned long long)S);
+  F.phi = (int32_t)(((-(s + 1)) % S + S) % S);
+  F.nsa = (m - s + S - 1) / S;
+  F.nsb = (e - m) > F.phi ? (e - m - F.phi + S - 1) / S : 0;
+  const size_t o_sa = take((size_t)(F.nsa + 1) * ks), o_sb = take((size_t)(F.nsb + 1) * ks);
+  const size_t o_pc = take((size_t)K * 64), o_z = take((size_t)K * 24);
   int rc = ensure(&ctx->fws, &ctx->fws_bytes, off);
   if (rc) return rc;
   char* b = static_cast<char*>(ctx->fws);
@@ -481,6 +502,12 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.chunk = reinterpret_cast<int32_t*>(b + o_chunk);
   F.idn = reinterpret_cast<uint8_t*>(b + o_idn);
   F.fc = reinterpret_cast<long long*>(b + o_fc);
+  F.samp_a = b + o_sa;
+  F.samp_b = b + o_sb;
+  F.pieces = reinterpret_cast<int4*>(b + o_pc);
+  F.z = reinterpret_cast<float2*>(b + o_z);
+  F.nsync = PM_FLOW_SYNC;
+  F.nsync_div = PM_FLOW_SYNC_DIV;
   F.nbits = PM_FLOW_BITS;
   F.nb = PM_FLOW_BINS;
   F.force = ctx->flow_mode == 2 ? 0 : ctx->flow_mode == 3 ? 1 : ctx->flow_mode == 4 ? 2 : -1;
@@ -497,11 +524,8 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   P.err = &ctx->ctl->err_.v;
   P.noop = &ctx->ctl->noop_.v;
   P.need_space = &ctx->ctl->need_space_.v;
-  // splits (k_plan_coarse / k_plan; no engine bookkeeping), then the flow plan and merge
-  const int plan_grid = (int)std::min<int64_t>(std::max<int64_t>((P.Q + 256) / 256, 1), (int64_t)ctx->num_sms * 8);
+  // plan (splits, order, salvage, tickets) and merge
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
-  ce = ks == 4 ? launch_plan<int32_t>(P, plan_grid, st) : launch_plan<int64_t>(P, plan_grid, st);
-  if (ce != cudaSuccess) return cuda_fail(ce, "k_plan launch");
   ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr)
                : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr);
   if (ce != cudaSuccess) return cuda_fail(ce, "k_flow launch");

@@ -202,9 +202,18 @@ struct FlowParams {
   char* pool_keys;      // phase-matched to keys (16-byte) / payload
   uint8_t* pool_pay;
   int64_t pool_cap;     // records
+  int4* pieces;         // [4 K] per region: (slot, lo, hi, 2 side + k) of each piece, slot -1: none
+  float2* z;            // [3 K] itinerary vectors / synchronisation buffers
+  int32_t nsync;        // synchronisation steps
+  int32_t nsync_div;    // their phase step delta = 2 pi / nsync_div
   int32_t nbits;        // itinerary length of the angle key
   int32_t nb;           // angle bins
   int32_t force;        // -1: choose per job, 0: two-front, 1: angle order, 2: force the fallback
+  int32_t lS;           // log2 of the split-search sample stride S (S divides M)
+  int32_t phi;          // B samples sit at B[k S + phi], phi = (-s - 1) mod S
+  void* samp_a;         // A[k S]            k < ceil(LA / S)
+  void* samp_b;         // B[k S + phi]      k S + phi < LB
+  int64_t nsa, nsb;
 };
 
 }  // namespace pm

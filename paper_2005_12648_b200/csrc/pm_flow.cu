@@ -59,7 +59,10 @@
 
 namespace pm {
 
-constexpr int kFlowChunk = 1024;  // two-front tickets per compaction block
+constexpr int kFlowChunk = 1024;
+#ifndef PM_FLOW_ABLATE
+#define PM_FLOW_ABLATE 0  // k_flow timing ablations (tuning builds; results are wrong): 1 no pend wait, 2 no merge, 4 no store
+#endif  // two-front tickets per compaction block
 
 struct FlowGeo : Geo {
   __device__ explicit FlowGeo(const EngineParams& p) : Geo(p) {}
@@ -110,12 +113,81 @@ __device__ __forceinline__ bool flow_off(const FlowParams& F) {
   return *(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_FAIL];
 }
 
-// ---- k_flow_readers: identity flags, middle-record reader, resets -------------
+// ---- k_flow_sample / k_flow_split: the stable merge path at every region boundary
+// Two levels instead of one long binary search per boundary (whose ~17 probes are
+// mostly DRAM misses): the predicate A[i] <= B[d-1-i] at i = k S only touches
+// A[k S] and B[d-1-k S] = B[k' S + phi] (every diagonal d = (R0+q) M - s is
+// congruent mod S), so a search over the two sample arrays (L2-resident) brackets
+// the split within S, and a last search of log2 S steps in the arrays finishes it.
+template <typename KT>
+__global__ void __launch_bounds__(256) k_flow_sample(FlowParams F) {
+  const EngineParams& P = F.P;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const KT* A = reinterpret_cast<const KT*>(P.keys) + P.s;
+  const KT* B = reinterpret_cast<const KT*>(P.keys) + P.m;
+  KT* sa = reinterpret_cast<KT*>(F.samp_a);
+  KT* sb = reinterpret_cast<KT*>(F.samp_b);
+  if (tid < FC_WORDS) F.fc[tid] = 0;
+  if (tid == 0) {
+    *P.ticket = 0;
+    const bool nothing = P.m == P.s || P.m == P.e || A[P.m - P.s - 1] <= B[0];  // srecpar.py:56-57
+    *P.noop = nothing ? 1 : 0;
+    for (int i = 0; i < 16; ++i) P.stats[i] = 0;
+  }
+  for (int64_t k = tid; k < F.nsa; k += nthr) sa[k] = __ldcs(A + (k << F.lS));
+  for (int64_t k = tid; k < F.nsb; k += nthr) sb[k] = __ldcs(B + (k << F.lS) + F.phi);
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256) k_flow_split(FlowParams F) {
+  const EngineParams& P = F.P;
+  Geo g(P);
+  if (*(volatile int32_t*)P.noop) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const KT* A = reinterpret_cast<const KT*>(P.keys) + P.s;
+  const KT* B = reinterpret_cast<const KT*>(P.keys) + P.m;
+  const KT* sa = reinterpret_cast<const KT*>(F.samp_a);
+  const KT* sb = reinterpret_cast<const KT*>(F.samp_b);
+  const int64_t la = g.LA(), lb = g.LB(), S = (int64_t)1 << F.lS;
+  for (int64_t q = tid; q <= P.Q; q += nthr) {
+    const int64_t d = g.diag(q);
+    const int64_t lo = max(d - lb, (int64_t)0), hi = min(d, la);
+    int64_t a;
+    if (q == 0 || q == P.Q || lo == hi) {
+      a = q == 0 ? 0 : q == P.Q ? la : lo;
+    } else {
+      // largest k with k S in [lo, hi) and A[k S] <= B[d-1-k S]  (B index = (c - k) S + phi)
+      int64_t klo = (lo + S - 1) >> F.lS, khi = (hi - 1) >> F.lS;
+      const int64_t c = (d - 1 - F.phi) >> F.lS;  // exact: d - 1 - phi is a multiple of S
+      int64_t wlo = lo, whi = min(hi, klo << F.lS);  // window if no sample point passes
+      if (klo <= khi && __ldg(&sa[klo]) <= __ldg(&sb[c - klo])) {
+        while (klo < khi) {  // invariant: the predicate holds at klo
+          const int64_t mid = (klo + khi + 1) >> 1;
+          if (__ldg(&sa[mid]) <= __ldg(&sb[c - mid])) klo = mid;
+          else khi = mid - 1;
+        }
+        wlo = (klo << F.lS) + 1;
+        whi = min(hi, wlo - 1 + S);
+      }
+      while (wlo < whi) {
+        const int64_t mid = (wlo + whi) >> 1;
+        if (__ldg(A + mid) <= __ldg(B + d - 1 - mid)) wlo = mid + 1;
+        else whi = mid;
+      }
+      a = wlo;
+    }
+    P.split_a[q] = a;
+  }
+}
+
+// ---- k_flow_readers: pieces, identity flags, middle-record reader, resets -------
+// Region q's pieces (FlowPiece[4 q .. 4 q + 3]): slot j, the record offsets
+// [lo, hi) it reads in that slot, and 2 * side + k (side 0: A, 1: B; k: piece of
+// the side).  j == -1: no piece.
 __global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
   const EngineParams& P = F.P;
   FlowGeo g(P);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
-  if (tid < FC_WORDS) F.fc[tid] = 0;
   if (*(volatile int32_t*)P.noop) return;
   for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;
   for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
@@ -125,7 +197,22 @@ __global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
     const int32_t side = y >= P.m;
     const int64_t dj = side ? g.reader_b(y - P.m) : g.reader_a(y - P.s);
     F.D[j] = (int32_t)dj | (side ? (int32_t)0x80000000 : 0);
-    F.idn[j] = g.identity(j, g.split(j), g.split(j + 1)) ? 1 : 0;
+    const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
+    const bool idn = g.identity(j, a0, a1);
+    F.idn[j] = idn ? 1 : 0;
+    int4 pc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
+    if (!idn) {
+      int i = 0;
+      for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1,
+                 [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
+                   const int64_t base = g.slot_base(jj);
+                   pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
+                 });
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) F.pieces[4 * j + i] = pc[i];
     F.rank[j] = INT32_MAX;
     F.slo[j] = (int32_t)P.T;
     F.shi[j] = 0;
@@ -133,7 +220,7 @@ __global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
   }
 }
 
-// ---- k_flow_angle: itinerary angle key per slot --------------------------------
+// ---- k_flow_angle: itinerary vector per slot --------------------------------------
 __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
   const EngineParams& P = F.P;
   if (flow_off(F)) return;
@@ -142,9 +229,8 @@ __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
   const float step = 6.283185307179586f / (float)n;
   TwoFront tf{P.Q, P.qc};
   for (int64_t j = tid; j < P.K; j += nthr) {
-    uint32_t key = (uint32_t)F.nb;  // identity: the last bin (never ranked)
+    float zr = 0.f, zi = 0.f;
     if (!F.idn[j]) {
-      float zr = 0.f, zi = 0.f;
       int32_t x = (int32_t)j;
       for (int i = 1; i <= n; ++i) {
         const int32_t v = __ldg(&F.D[x]);
@@ -156,13 +242,75 @@ __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
         }
         x = v & 0x7fffffff;
       }
-      float ang = atan2f(zi, zr);
-      if (ang < 0.f) ang += 6.283185307179586f;
-      key = min((uint32_t)(ang * (float)F.nb * 0.15915494309189535f), (uint32_t)F.nb - 1);
-      atomicAdd(&F.hist[key], 1);
     } else {
       atomicAdd(&F.chunk[tf.order(j) / kFlowChunk], 1);
       atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], 1ull);
+    }
+    F.z[j] = make_float2(zr, zi);
+    F.z[P.K + j] = make_float2(0.f, 0.f);
+    F.z[2 * P.K + j] = make_float2(0.f, 0.f);
+  }
+}
+
+// ---- k_flow_sync: one step of angular synchronisation on the reader graph ------
+// The angle order wants arg z(reader) = arg z(slot) - delta on every edge; one
+// power-iteration step of the edge-weighted phase-synchronisation matrix moves
+// each slot's phase to the weighted circular mean of what its readers and the
+// slots it reads imply (tools/sim_flow.py: salvage 0.20 N -> 0.15 N in 4 steps).
+// z[(it % 3) K ..] is read (normalised on the fly), z[((it + 1) % 3) K ..]
+// accumulated, z[((it + 2) % 3) K ..] zeroed for the next step.
+__global__ void __launch_bounds__(256) k_flow_sync(FlowParams F, int it) {
+  const EngineParams& P = F.P;
+  if (flow_off(F) || F.force >= 0 && F.force != 1) return;
+  const int64_t K = P.K;
+  const float2* zin = F.z + (it % 3) * K;
+  float2* zout = F.z + ((it + 1) % 3) * K;
+  float2* zclr = F.z + ((it + 2) % 3) * K;
+  float cd, sd;
+  __sincosf(6.283185307179586f / (float)F.nsync_div, &sd, &cd);
+  auto unit = [](float2 v) {
+    const float r = rsqrtf(fmaxf(v.x * v.x + v.y * v.y, 1e-30f));
+    return make_float2(v.x * r, v.y * r);
+  };
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = tid; q < P.Q; q += nthr) {
+    zclr[q] = make_float2(0.f, 0.f);
+    if (F.idn[q]) continue;
+    const float2 zq = unit(zin[q]);
+    float ar = 0.f, ai = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int4 pc = F.pieces[4 * q + i];
+      if (pc.x < 0 || pc.x == q) continue;
+      const float wgt = (float)(pc.z - pc.y);
+      const float2 zj = unit(zin[pc.x]);
+      // slot j (writer) wants zq * e^{+i delta}; region q (reader) wants zj * e^{-i delta}
+      atomicAdd(&zout[pc.x].x, wgt * (zq.x * cd - zq.y * sd));
+      atomicAdd(&zout[pc.x].y, wgt * (zq.x * sd + zq.y * cd));
+      ar += wgt * (zj.x * cd + zj.y * sd);
+      ai += wgt * (zj.y * cd - zj.x * sd);
+    }
+    if (ar != 0.f || ai != 0.f) {
+      atomicAdd(&zout[q].x, ar);
+      atomicAdd(&zout[q].y, ai);
+    }
+  }
+}
+
+// ---- k_flow_key: angle bin per slot, histogram ----------------------------------
+__global__ void __launch_bounds__(256) k_flow_key(FlowParams F, int zbuf) {
+  const EngineParams& P = F.P;
+  if (flow_off(F)) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  const float2* z = F.z + zbuf * P.K;
+  for (int64_t j = tid; j < P.K; j += nthr) {
+    uint32_t key = (uint32_t)F.nb;  // identity: the last bin (never ranked)
+    if (!F.idn[j]) {
+      const float2 v = z[j];
+      float ang = atan2f(v.y, v.x);
+      if (ang < 0.f) ang += 6.283185307179586f;
+      key = min((uint32_t)(ang * (float)F.nb * 0.15915494309189535f), (uint32_t)F.nb - 1);
+      atomicAdd(&F.hist[key], 1);
     }
     F.key[j] = key;
   }
@@ -174,22 +322,22 @@ __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
 // (the counting sort breaks them arbitrarily -- an estimate suffices).
 __global__ void __launch_bounds__(256) k_flow_choose(FlowParams F) {
   const EngineParams& P = F.P;
-  FlowGeo g(P);
   if (flow_off(F) || F.force >= 0) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   TwoFront tf{P.Q, P.qc};
   unsigned long long sa = 0, st = 0;
   for (int64_t q = tid; q < P.Q; q += nthr) {
     if (F.idn[q]) continue;
-    const int64_t a0 = g.split(q), a1 = g.split(q + 1), d0 = g.diag(q), d1 = g.diag(q + 1);
     const uint32_t kq = F.key[q];
     const int64_t oq = tf.order(q);
-    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t j, int64_t lo, int64_t hi, int, int) {
-      if (j == q) return;
-      const uint32_t kj = __ldg(&F.key[j]);
-      if (kq > kj || (kq == kj && q > j)) sa += (unsigned long long)(hi - lo);
-      if (oq > tf.order(j)) st += (unsigned long long)(hi - lo);
-    });
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int4 pc = F.pieces[4 * q + i];
+      if (pc.x < 0 || pc.x == q) continue;
+      const uint32_t kj = __ldg(&F.key[pc.x]);
+      if (kq > kj || (kq == kj && q > pc.x)) sa += (unsigned long long)(pc.z - pc.y);
+      if (oq > tf.order(pc.x)) st += (unsigned long long)(pc.z - pc.y);
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -230,6 +378,22 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* total) {
   return (wid ? ws[wid - 1] : 0) + x - v;
 }
 
+// one CTA: exclusive scan of v[0, n) in place; each thread scans a contiguous
+// segment serially around a single block scan of the segment sums
+__device__ __forceinline__ void cta_scan_inplace(int32_t* v, int64_t n) {
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t i0 = min(n, (int64_t)threadIdx.x * per), i1 = min(n, i0 + per);
+  int32_t sum = 0;
+  for (int64_t i = i0; i < i1; ++i) sum += v[i];
+  int32_t tot;
+  int32_t run = block_excl_scan(sum, &tot);
+  for (int64_t i = i0; i < i1; ++i) {
+    const int32_t x = v[i];
+    v[i] = run;
+    run += x;
+  }
+}
+
 // ---- k_flow_decide (one CTA): the order, then its scan ------------------------
 __global__ void __launch_bounds__(1024) k_flow_decide(FlowParams F) {
   const EngineParams& P = F.P;
@@ -247,28 +411,8 @@ __global__ void __launch_bounds__(1024) k_flow_decide(FlowParams F) {
     F.fc[FC_NTICK] = (long long)P.Q - F.fc[FC_NIDENT];
   }
   __syncthreads();
-  if (s_mode == 1) {  // exclusive scan of the angle histogram, in place (cursors)
-    int32_t base = 0;
-    for (int64_t b0 = 0; b0 < F.nb; b0 += blockDim.x) {
-      const int64_t b = b0 + threadIdx.x;
-      const int32_t v = b < F.nb ? F.hist[b] : 0;
-      int32_t tot;
-      const int32_t ex = block_excl_scan(v, &tot);
-      if (b < F.nb) F.hist[b] = base + ex;
-      base += tot;
-    }
-  } else {  // exclusive scan of the per-chunk identity counts
-    int32_t base = 0;
-    const int64_t nc = P.Q / kFlowChunk + 1;
-    for (int64_t c0 = 0; c0 < nc; c0 += blockDim.x) {
-      const int64_t c = c0 + threadIdx.x;
-      const int32_t v = c < nc ? F.chunk[c] : 0;
-      int32_t tot;
-      const int32_t ex = block_excl_scan(v, &tot);
-      if (c < nc) F.chunk[c] = base + ex;
-      base += tot;
-    }
-  }
+  if (s_mode == 1) cta_scan_inplace(F.hist, F.nb);  // angle bins -> cursors
+  else cta_scan_inplace(F.chunk, P.Q / kFlowChunk + 1);  // identity regions before each chunk
 }
 
 // ---- k_flow_rank: order[] / rank[] -------------------------------------------
@@ -309,23 +453,22 @@ __global__ void __launch_bounds__(kFlowChunk) k_flow_rank(FlowParams F) {
 // ---- k_flow_hull: salvage hulls and pending-reader counts ----------------------
 __global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
   const EngineParams& P = F.P;
-  FlowGeo g(P);
   if (flow_off(F)) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = tid; q < P.Q; q += nthr) {
     if (F.idn[q]) continue;
-    const int64_t a0 = g.split(q), a1 = g.split(q + 1), d0 = g.diag(q), d1 = g.diag(q + 1);
     const int32_t rq = F.rank[q];
-    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t j, int64_t lo, int64_t hi, int, int) {
-      if (j == q) return;
-      if (rq > __ldg(&F.rank[j])) {  // j is written first: q reads its salvage entry
-        const int64_t base = g.slot_base(j);
-        atomicMin(&F.slo[j], (int32_t)(lo - base));
-        atomicMax(&F.shi[j], (int32_t)(hi - base));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int4 pc = F.pieces[4 * q + i];
+      if (pc.x < 0 || pc.x == q) continue;
+      if (rq > __ldg(&F.rank[pc.x])) {  // j is written first: q reads its salvage entry
+        atomicMin(&F.slo[pc.x], pc.y);
+        atomicMax(&F.shi[pc.x], pc.z);
       } else {
-        atomicAdd(&F.pend[j], 1);  // j's store waits for this read
+        atomicAdd(&F.pend[pc.x], 1);  // j's store waits for this read
       }
-    });
+    }
   }
 }
 
@@ -335,7 +478,7 @@ __global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
 // superset TMA load of a piece stays inside it).  One atomic per block.
 __global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
   const EngineParams& P = F.P;
-  FlowGeo g(P);
+  Geo g(P);
   if (flow_off(F)) return;
   __shared__ long long s_base;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < P.K; j0 += (int64_t)gridDim.x * blockDim.x) {
@@ -350,9 +493,8 @@ __global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
     }
     int32_t tot;
     const int32_t ex = block_excl_scan(sz, &tot);
-    if (threadIdx.x == 0) {
-      s_base = tot ? atomicAdd((unsigned long long*)&F.fc[FC_POOL], (unsigned long long)tot) : 0;
-    }
+    if (threadIdx.x == 0)
+      s_base = tot ? (long long)atomicAdd((unsigned long long*)&F.fc[FC_POOL], (unsigned long long)tot) : 0ll;
     __syncthreads();
     const long long base = s_base;
     __syncthreads();
@@ -371,7 +513,7 @@ __global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
 // ---- k_flow_tickets: per-ticket descriptors ------------------------------------
 __global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
   const EngineParams& P = F.P;
-  FlowGeo g(P);
+  Geo g(P);
   if (flow_off(F)) return;
   const int64_t nt = F.fc[FC_NTICK];
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
@@ -393,24 +535,26 @@ __global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
     T.a0 = g.split(q);
     T.a1 = g.split(q + 1);
     T.dA[0] = T.dA[1] = T.dB[0] = T.dB[1] = 0;
-    const int64_t d0 = g.diag(q), d1 = g.diag(q + 1);
-    for_pieces(P, P.s + T.a0, P.s + T.a1, P.m + d0 - T.a0, P.m + d1 - T.a1,
-               [&](int64_t j, int64_t, int64_t, int k, int side) {
-                 const bool pool = j != q && __ldg(&F.rank[j]) < (int32_t)t;
-                 if (side == 0) {
-                   T.ja[k] = (int32_t)j;
-                   if (pool) {
-                     T.flags |= 1 << (1 + k);
-                     T.dA[k] = F.pdelta[j];
-                   }
-                 } else {
-                   T.jb[k] = (int32_t)j;
-                   if (pool) {
-                     T.flags |= 1 << (3 + k);
-                     T.dB[k] = F.pdelta[j];
-                   }
-                 }
-               });
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int4 pc = F.pieces[4 * q + i];
+      if (pc.x < 0) continue;
+      const int k = pc.w & 1;
+      const bool pool = pc.x != q && __ldg(&F.rank[pc.x]) < (int32_t)t;
+      if (pc.w < 2) {
+        T.ja[k] = pc.x;
+        if (pool) {
+          T.flags |= 1 << (1 + k);
+          T.dA[k] = F.pdelta[pc.x];
+        }
+      } else {
+        T.jb[k] = pc.x;
+        if (pool) {
+          T.flags |= 1 << (3 + k);
+          T.dB[k] = F.pdelta[pc.x];
+        }
+      }
+    }
     F.tk[t] = T;
   }
 }
@@ -505,9 +649,13 @@ __device__ __forceinline__ void flow_release(const FlowParams& F, const FlowDesc
     if (D.rd[i] >= 0) atomicSub(&F.pend[D.rd[i]], 1);
 }
 
+// Persistent, software-pipelined (k_buffered's shape).  The control warp's lane 0
+// ("leader") claims tickets two ahead and loads each ticket's descriptor one
+// iteration before it issues the region's TMA loads, so the only round trips left
+// on its path are the pend[] polls, which are issued before the stage wait.
 template <typename KT>
-__global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
-  constexpr int NS = kBufStages;
+__global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
+  constexpr int NS = kFlowStages;
   extern __shared__ __align__(128) uint8_t dyn[];
   __shared__ uint64_t bar[NS];
   __shared__ int64_t s_t[NS];
@@ -515,7 +663,7 @@ __global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
   __shared__ int32_t s_early[NS];
   const EngineParams& P = F.P;
   FlowGeo g(P);
-  constexpr int NT = kBufferedThreads;
+  constexpr int NT = kFlowThreads;
   const int tid = threadIdx.x, lane = tid & 31;
   const int NW = NT >> 5;
   const bool ctrl = (tid >> 5) == NW - 1;
@@ -527,7 +675,8 @@ __global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
   const size_t tile = P.smem_keys + P.smem_pay;
 #define STAGE(b) (dyn + (size_t)(b) * tile)
 #define OUTB(b) (dyn + (size_t)(NS + (b)) * tile)
-  int32_t t_pref = 0;
+  int64_t t_next = ntick;  // leader: the next ticket to issue, its descriptor loaded ahead
+  FlowTicket T_next;
   if (leader) {
     for (int k = 0; k < NS; ++k) {
       mbar_init(&bar[k], 1);
@@ -540,24 +689,32 @@ __global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
       if (t0 >= ntick) break;
       flow_issue<KT>(F, g, load_ticket(F.tk + t0), s_d[k], STAGE(k), STAGE(k) + P.smem_keys, &bar[k]);
     }
-    t_pref = atomicAdd(P.ticket, 1);
+    t_next = atomicAdd(P.ticket, 1);
+    if (t_next < ntick) T_next = load_ticket(F.tk + t_next);
+    else t_next = ntick;
   }
   __syncthreads();
   uint32_t phmask = 0;
   unsigned long long n_reg = 0;
   for (int it = 0;; ++it) {
-    const int cur = it % NS, ob = it & 1;
+    const int cur = it % NS, ob = kFlowOut == 2 ? (it & 1) : 0;
     const int64_t t = s_t[cur];
     if (t >= ntick) break;
     const FlowDesc R = s_d[cur];
-    if (leader) {  // keep NS-1 regions in flight: the previous iteration's stage is free
+    int32_t pv = 0;
+    if (leader) {
+      pv = ld_relaxed(&F.pend[R.r]);  // first poll of this region's store condition, in flight now
+      // keep NS-1 regions in flight: the previous iteration's stage is free
       const int nx = (it + NS - 1) % NS;
-      const int64_t tn = (*(volatile int32_t*)P.err) ? ntick : (t_pref < ntick ? t_pref : ntick);
-      if (t_pref < ntick) t_pref = atomicAdd(P.ticket, 1);
+      const int64_t tn = (*(volatile int32_t*)P.err) ? ntick : t_next;
       s_t[nx] = tn;
       s_early[nx] = 0;
-      if (tn < ntick)
-        flow_issue<KT>(F, g, load_ticket(F.tk + tn), s_d[nx], STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
+      if (tn < ntick) {
+        flow_issue<KT>(F, g, T_next, s_d[nx], STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
+        t_next = atomicAdd(P.ticket, 1);
+        if (t_next < ntick) T_next = load_ticket(F.tk + t_next);  // used next iteration
+        else t_next = ntick;
+      }
     }
     while (!mbar_try_wait(&bar[cur], (phmask >> cur) & 1)) {
     }
@@ -567,26 +724,33 @@ __global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
     uint8_t* kout_s = OUTB(ob);
     uint8_t* pout_s = OUTB(ob) + P.smem_keys;
     if (ctrl) {
-      // (relaxed releases: the loads have completed -- the barrier said so -- so a
-      // writer that sees the count drop cannot change what this region read)
-      if (leader && !s_early[cur]) flow_release(F, R);
-      // every lower-ranked reader of this slot has read it
       if (leader) {
-        for (uint32_t it2 = 0; ld_acquire(&F.pend[R.r]) != 0; ++it2) {
+        // (relaxed: the loads have completed -- the barrier said so -- so a writer that
+        // sees the count drop cannot change what this region read)
+        if (!s_early[cur]) flow_release(F, R);
+        // regions in flight whose loads have landed: release their reads now -- other
+        // CTAs' stores may be waiting for them (checked again while this one waits)
+        auto release_landed = [&]() {
+          for (int k = 1; k < NS; ++k) {
+            const int sk = (it + k) % NS;
+            if (s_t[sk] < ntick && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
+              flow_release(F, s_d[sk]);
+              s_early[sk] = 1;
+            }
+          }
+        };
+        release_landed();
+        // every lower-ranked reader of this slot has read it
+        if (PM_FLOW_ABLATE & 1) pv = 0;  // (timing ablation: results are wrong)
+        for (uint32_t it2 = 0; pv != 0; ++it2) {
           if ((it2 & 255) == 255 && ld_relaxed(P.err)) break;
           if (it2 > kSpinLimit) {
             raise_error(P.err, PM_ERR_TIMEOUT);
             break;
           }
           backoff(it2);
-        }
-        // regions in flight whose loads have landed: release their reads early
-        for (int k = 1; k < NS; ++k) {
-          const int sk = (it + k) % NS;
-          if (s_t[sk] < ntick && !s_early[sk] && mbar_try_wait(&bar[sk], (phmask >> sk) & 1)) {
-            flow_release(F, s_d[sk]);
-            s_early[sk] = 1;
-          }
+          release_landed();
+          pv = ld_relaxed(&F.pend[R.r]);
         }
       }
       __syncwarp();
@@ -598,18 +762,24 @@ __global__ void __launch_bounds__(kBufferedThreads) k_flow(FlowParams F) {
         named_barrier_sync(1, MT);
       }
       const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-      merge_tile<KT, kBufferedThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
-                                            reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
-                                            reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
-                                            pin + R.poffB, w, wq4, tid);
+      if (!(PM_FLOW_ABLATE & 2))
+      merge_tile<KT, kFlowThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
+                                        reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                                        reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                        pin + R.poffB, w, wq4, tid);
       fence_proxy_async_smem();
     }
     __syncthreads();  // tile complete, slot clear
     const int gt = (tid + 32) % NT;
-    stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), (int64_t)R.nout * ks, gt, NT);
-    if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, (int64_t)R.nout * w, gt, NT);
+    if (!(PM_FLOW_ABLATE & 4)) {
+      stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), (int64_t)R.nout * ks, gt, NT);
+      if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, (int64_t)R.nout * w, gt, NT);
+    }
     ++n_reg;
-    if (leader) bulk_wait_read<1>();  // the store that used the other output buffer has read it
+    if (leader) {
+      if (kFlowOut == 2) bulk_wait_read<1>();  // the store that used the other output buffer has read it
+      else bulk_wait_read<0>();                // one output tile: this store has read it
+    }
     __syncthreads();
   }
   if (leader) {
@@ -625,7 +795,7 @@ template <typename KT>
 cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_flow<KT>, kBufferedThreads, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_flow<KT>, kFlowThreads, smem);
 }
 
 // plan kernels (after launch_plan's splits); ev (may be null) is recorded between
@@ -634,15 +804,21 @@ template <typename KT>
 cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev) {
   const EngineParams& P = F.P;
   const int g1 = (int)std::min<int64_t>((P.Q + 255) / 256, (int64_t)num_sms * 8);
+  k_flow_sample<KT><<<(int)std::min<int64_t>((std::max(F.nsa, F.nsb) + 255) / 256 + 1, (int64_t)num_sms * 8), 256, 0,
+                      st>>>(F);
+  k_flow_split<KT><<<(int)std::min<int64_t>((P.Q + 256) / 256, (int64_t)num_sms * 8), 256, 0, st>>>(F);
+  count_launches(2);
   k_flow_readers<<<g1, 256, 0, st>>>(F);
   k_flow_angle<<<g1, 256, 0, st>>>(F);
+  for (int it = 0; it < F.nsync; ++it) k_flow_sync<<<g1, 256, 0, st>>>(F, it);
+  k_flow_key<<<g1, 256, 0, st>>>(F, F.nsync % 3);
   k_flow_choose<<<g1, 256, 0, st>>>(F);
   k_flow_decide<<<1, 1024, 0, st>>>(F);
   k_flow_rank<<<(int)std::min<int64_t>((P.Q + kFlowChunk - 1) / kFlowChunk, (int64_t)num_sms * 2), kFlowChunk, 0, st>>>(F);
   k_flow_hull<<<g1, 256, 0, st>>>(F);
   k_flow_alloc<<<g1, 256, 0, st>>>(F);
   k_flow_tickets<<<g1, 256, 0, st>>>(F);
-  count_launches(8);
+  count_launches(9 + F.nsync);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (ev) {
@@ -652,7 +828,7 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
   e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_flow<KT><<<grid, kBufferedThreads, smem, st>>>(F);
+  k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
   count_launches(2);
   return cudaGetLastError();
 }

@@ -14,6 +14,21 @@ template <typename KT> cudaError_t launch_engine(const EngineParams& P, int grid
 template <typename KT> cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm);
 template <typename KT> cudaError_t buffered_occupancy(size_t smem, int* blocks_per_sm);
 // scheduled in-place merge (pm_flow.cu): plan kernels + pool copy + streaming merge
+#ifndef PM_FLOW_STAGES
+#define PM_FLOW_STAGES 2  // k_flow input stages (regions whose loads are in flight + the one merging)
+#endif
+#ifndef PM_FLOW_THREADS
+#define PM_FLOW_THREADS 256  // k_flow CTA: one control warp + merge warps
+#endif
+#ifndef PM_FLOW_OUT
+#define PM_FLOW_OUT 1  // k_flow output tiles (1: the leader waits for each store to read its tile)
+#endif
+#ifndef PM_FLOW_TILE
+#define PM_FLOW_TILE (32 * 1024)  // k_flow tile bytes (keys + payload): regions of up to 8192 records
+#endif
+constexpr int kFlowStages = PM_FLOW_STAGES;
+constexpr int kFlowOut = PM_FLOW_OUT;
+constexpr int kFlowThreads = PM_FLOW_THREADS;
 template <typename KT> cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm);
 template <typename KT>
 cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev);
