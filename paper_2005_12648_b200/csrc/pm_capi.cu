@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -476,7 +477,7 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
                o_chunk = take((P.Q / 1024 + 2) * 4), o_idn = take(K), o_fc = take(FC_WORDS * 8);
   // split-search samples (stride S = min(256, M); S divides M)
 #ifndef PM_FLOW_SAMPLE
-#define PM_FLOW_SAMPLE 1024  // split-search sample stride (records)
+#define PM_FLOW_SAMPLE 2048  // split-search sample stride (records)
 #endif
   const int64_t S = std::min<int64_t>(PM_FLOW_SAMPLE, M);
   F.lS = 63 - __builtin_clzll((unsigned long long)S);
@@ -534,7 +535,7 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
     ctx->ev_recorded = true;
   }
   // the bounded-pool engine, gated on the plan's overflow word
-  return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, 0, st, nullptr, nullptr, nullptr, nullptr,
+    return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, 0, st, nullptr, nullptr, nullptr, nullptr,
                     reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
 }
 

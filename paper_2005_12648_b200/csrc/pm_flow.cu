@@ -51,21 +51,32 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "pm_common.cuh"
 #include "pm_engine.cuh"
 #include "pm_launch.h"
 #include "pm_tile.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace pm {
 
 constexpr int kFlowChunk = 1024;
+#ifndef PM_FLOW_WIN4
+#define PM_FLOW_WIN4 0  // tune: 4-ary window search in the split phase
+#endif
 #ifndef PM_FLOW_ABLATE
 #define PM_FLOW_ABLATE 0  // k_flow timing ablations (tuning builds; results are wrong): 1 no pend wait, 2 no merge, 4 no store
 #endif  // two-front tickets per compaction block
 
 struct FlowGeo : Geo {
   __device__ explicit FlowGeo(const EngineParams& p) : Geo(p) {}
+  // (plain load: the plan kernel writes split_a itself, so no read-only path)
+  __device__ int64_t split(int64_t q) const { return P.split_a[q]; }
+  __device__ int64_t diag(int64_t q) const { return Geo::diag(q); }
   __device__ int64_t bsplit(int64_t q) const { return diag(q) - split(q); }
   // smallest region q whose A range ends after A-local index v (0 <= v < LA)
   __device__ int64_t reader_a(int64_t v) const {
@@ -112,6 +123,17 @@ __device__ __forceinline__ void for_pieces(const EngineParams& P, int64_t xa0, i
 __device__ __forceinline__ bool flow_off(const FlowParams& F) {
   return *(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_FAIL];
 }
+// The same test inside the cooperative plan, where FC_FAIL may be raised during a
+// phase (k_flow_alloc / the forced fallback): one thread reads it for the whole
+// CTA, so every thread of a CTA takes the same branch around the phase's CTA
+// barriers.
+__device__ __forceinline__ bool block_flow_off(const FlowParams& F) {
+  __shared__ int32_t s_off;
+  __syncthreads();
+  if (threadIdx.x == 0) s_off = flow_off(F) ? 1 : 0;
+  __syncthreads();
+  return s_off != 0;
+}
 
 // ---- k_flow_sample / k_flow_split: the stable merge path at every region boundary
 // Two levels instead of one long binary search per boundary (whose ~17 probes are
@@ -120,7 +142,7 @@ __device__ __forceinline__ bool flow_off(const FlowParams& F) {
 // congruent mod S), so a search over the two sample arrays (L2-resident) brackets
 // the split within S, and a last search of log2 S steps in the arrays finishes it.
 template <typename KT>
-__global__ void __launch_bounds__(256) k_flow_sample(FlowParams F) {
+__device__ __forceinline__ void ph_sample(const FlowParams& F) {
   const EngineParams& P = F.P;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const KT* A = reinterpret_cast<const KT*>(P.keys) + P.s;
@@ -134,14 +156,55 @@ __global__ void __launch_bounds__(256) k_flow_sample(FlowParams F) {
     *P.noop = nothing ? 1 : 0;
     for (int i = 0; i < 16; ++i) P.stats[i] = 0;
   }
-  for (int64_t k = tid; k < F.nsa; k += nthr) sa[k] = __ldcs(A + (k << F.lS));
-  for (int64_t k = tid; k < F.nsb; k += nthr) sb[k] = __ldcs(B + (k << F.lS) + F.phi);
+  // (four independent strided loads in flight per thread before their stores)
+  for (int64_t k0 = tid; k0 < F.nsa + F.nsb; k0 += 4 * nthr) {
+    KT v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * nthr;
+      v[u] = k < F.nsa ? __ldcs(A + (k << F.lS)) : k < F.nsa + F.nsb ? __ldcs(B + ((k - F.nsa) << F.lS) + F.phi) : (KT)0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * nthr;
+      if (k < F.nsa) sa[k] = v[u];
+      else if (k < F.nsa + F.nsb) sb[k - F.nsa] = v[u];
+    }
+  }
+}
+
+// Largest k in [lo, hi] with pred(k) true, for pred monotone (true, then false) and
+// pred(lo) true: an 8-ary search, seven independent probes per step, so a search
+// over 2^20 candidates is 7 dependent round trips instead of 20.
+template <class Pred>
+__device__ __forceinline__ int64_t last_true8(int64_t lo, int64_t hi, Pred&& pred) {
+  while (lo < hi) {
+    const int64_t span = hi - lo;
+    int64_t p[7];
+    bool f[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) p[i] = lo + (span * (i + 1) + 7) / 8;  // in (lo, hi], non-decreasing
+#pragma unroll
+    for (int i = 0; i < 7; ++i) f[i] = pred(p[i]);
+    int64_t nlo = lo, nhi = hi;
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+      if (f[i]) {
+        nlo = max(nlo, p[i]);
+      } else {
+        nhi = min(nhi, p[i] - 1);
+      }
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
 }
 
 template <typename KT>
-__global__ void __launch_bounds__(256) k_flow_split(FlowParams F) {
+__device__ __forceinline__ void ph_split(const FlowParams& F) {
   const EngineParams& P = F.P;
-  Geo g(P);
+  FlowGeo g(P);
   if (*(volatile int32_t*)P.noop) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const KT* A = reinterpret_cast<const KT*>(P.keys) + P.s;
@@ -157,19 +220,30 @@ __global__ void __launch_bounds__(256) k_flow_split(FlowParams F) {
       a = q == 0 ? 0 : q == P.Q ? la : lo;
     } else {
       // largest k with k S in [lo, hi) and A[k S] <= B[d-1-k S]  (B index = (c - k) S + phi)
-      int64_t klo = (lo + S - 1) >> F.lS, khi = (hi - 1) >> F.lS;
+      const int64_t klo = (lo + S - 1) >> F.lS, khi = (hi - 1) >> F.lS;
       const int64_t c = (d - 1 - F.phi) >> F.lS;  // exact: d - 1 - phi is a multiple of S
       int64_t wlo = lo, whi = min(hi, klo << F.lS);  // window if no sample point passes
-      if (klo <= khi && __ldg(&sa[klo]) <= __ldg(&sb[c - klo])) {
-        while (klo < khi) {  // invariant: the predicate holds at klo
-          const int64_t mid = (klo + khi + 1) >> 1;
-          if (__ldg(&sa[mid]) <= __ldg(&sb[c - mid])) klo = mid;
-          else khi = mid - 1;
-        }
-        wlo = (klo << F.lS) + 1;
+      if (klo <= khi && sa[klo] <= sb[c - klo]) {
+        const int64_t k = last_true8(klo, khi, [&](int64_t x) { return sa[x] <= sb[c - x]; });
+        wlo = (k << F.lS) + 1;
         whi = min(hi, wlo - 1 + S);
       }
-      while (wlo < whi) {
+      // the split is in [wlo, whi]
+#if PM_FLOW_WIN4
+      // 4-ary: three probes per step, half the dependent DRAM round trips
+      while (whi - wlo > 3) {
+        const int64_t span = whi - wlo;
+        const int64_t p1 = wlo + span / 4, p2 = wlo + span / 2, p3 = wlo + (3 * span) / 4;
+        const bool f1 = __ldg(A + p1) <= __ldg(B + d - 1 - p1);
+        const bool f2 = __ldg(A + p2) <= __ldg(B + d - 1 - p2);
+        const bool f3 = __ldg(A + p3) <= __ldg(B + d - 1 - p3);
+        if (f3) wlo = p3 + 1;
+        else if (f2) { wlo = p2 + 1; whi = p3; }
+        else if (f1) { wlo = p1 + 1; whi = p2; }
+        else whi = p1;
+      }
+#endif
+      while (wlo < whi) {  // binary (its late probes share DRAM lines)
         const int64_t mid = (wlo + whi) >> 1;
         if (__ldg(A + mid) <= __ldg(B + d - 1 - mid)) wlo = mid + 1;
         else whi = mid;
@@ -184,35 +258,33 @@ __global__ void __launch_bounds__(256) k_flow_split(FlowParams F) {
 // Region q's pieces (FlowPiece[4 q .. 4 q + 3]): slot j, the record offsets
 // [lo, hi) it reads in that slot, and 2 * side + k (side 0: A, 1: B; k: piece of
 // the side).  j == -1: no piece.
-__global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
+__device__ __forceinline__ void ph_readers(const FlowParams& F) {
   const EngineParams& P = F.P;
   FlowGeo g(P);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if (*(volatile int32_t*)P.noop) return;
   for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;
   for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
-  for (int64_t j = tid; j < P.K; j += nthr) {
-    const int64_t x0 = g.slot_lo(j), x1 = g.slot_hi(j);
-    const int64_t y = (x0 + x1 - 1) >> 1;
-    const int32_t side = y >= P.m;
-    const int64_t dj = side ? g.reader_b(y - P.m) : g.reader_a(y - P.s);
-    F.D[j] = (int32_t)dj | (side ? (int32_t)0x80000000 : 0);
+  for (int64_t j = tid; j < P.K; j += nthr) {  // (Q == K: region j writes slot j)
     const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
     const bool idn = g.identity(j, a0, a1);
     F.idn[j] = idn ? 1 : 0;
     int4 pc[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
-    if (!idn) {
-      int i = 0;
-      for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1,
-                 [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
-                   const int64_t base = g.slot_base(jj);
-                   pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
-                 });
-    }
+    int i = 0;
+    // every slot's middle record lies in exactly one region's A or B range: that
+    // region is the slot's reader D[] (the itinerary's next step)
+    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
+      const int64_t ymid = (g.slot_lo(jj) + g.slot_hi(jj) - 1) >> 1;
+      if (lo <= ymid && ymid < hi) F.D[jj] = (int32_t)j | (sd ? (int32_t)0x80000000 : 0);
+      if (!idn) {
+        const int64_t base = g.slot_base(jj);
+        pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
+      }
+    });
 #pragma unroll
-    for (int i = 0; i < 4; ++i) F.pieces[4 * j + i] = pc[i];
+    for (int k = 0; k < 4; ++k) F.pieces[4 * j + k] = pc[k];
     F.rank[j] = INT32_MAX;
     F.slo[j] = (int32_t)P.T;
     F.shi[j] = 0;
@@ -221,9 +293,9 @@ __global__ void __launch_bounds__(256) k_flow_readers(FlowParams F) {
 }
 
 // ---- k_flow_angle: itinerary vector per slot --------------------------------------
-__global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
+__device__ __forceinline__ void ph_angle(const FlowParams& F) {
   const EngineParams& P = F.P;
-  if (flow_off(F)) return;
+  if (block_flow_off(F)) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const int n = F.nbits;
   const float step = 6.283185307179586f / (float)n;
@@ -233,7 +305,7 @@ __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
     if (!F.idn[j]) {
       int32_t x = (int32_t)j;
       for (int i = 1; i <= n; ++i) {
-        const int32_t v = __ldg(&F.D[x]);
+        const int32_t v = F.D[x];
         if (v < 0) {
           float sn, cs;
           __sincosf(step * (float)i, &sn, &cs);
@@ -259,9 +331,9 @@ __global__ void __launch_bounds__(256) k_flow_angle(FlowParams F) {
 // slots it reads imply (tools/sim_flow.py: salvage 0.20 N -> 0.15 N in 4 steps).
 // z[(it % 3) K ..] is read (normalised on the fly), z[((it + 1) % 3) K ..]
 // accumulated, z[((it + 2) % 3) K ..] zeroed for the next step.
-__global__ void __launch_bounds__(256) k_flow_sync(FlowParams F, int it) {
+__device__ __forceinline__ void ph_sync(const FlowParams& F, int it) {
   const EngineParams& P = F.P;
-  if (flow_off(F) || F.force >= 0 && F.force != 1) return;
+  if (block_flow_off(F) || F.force >= 0 && F.force != 1) return;
   const int64_t K = P.K;
   const float2* zin = F.z + (it % 3) * K;
   float2* zout = F.z + ((it + 1) % 3) * K;
@@ -298,9 +370,9 @@ __global__ void __launch_bounds__(256) k_flow_sync(FlowParams F, int it) {
 }
 
 // ---- k_flow_key: angle bin per slot, histogram ----------------------------------
-__global__ void __launch_bounds__(256) k_flow_key(FlowParams F, int zbuf) {
+__device__ __forceinline__ void ph_key(const FlowParams& F, int zbuf) {
   const EngineParams& P = F.P;
-  if (flow_off(F)) return;
+  if (block_flow_off(F)) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const float2* z = F.z + zbuf * P.K;
   for (int64_t j = tid; j < P.K; j += nthr) {
@@ -320,9 +392,9 @@ __global__ void __launch_bounds__(256) k_flow_key(FlowParams F, int zbuf) {
 // Region q reads piece (slot j, n records); it reads the salvage entry iff it
 // comes after j.  Angle order ties (same bin) are broken by region index here
 // (the counting sort breaks them arbitrarily -- an estimate suffices).
-__global__ void __launch_bounds__(256) k_flow_choose(FlowParams F) {
+__device__ __forceinline__ void ph_choose(const FlowParams& F) {
   const EngineParams& P = F.P;
-  if (flow_off(F) || F.force >= 0) return;
+  if (block_flow_off(F) || F.force >= 0) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   TwoFront tf{P.Q, P.qc};
   unsigned long long sa = 0, st = 0;
@@ -334,7 +406,7 @@ __global__ void __launch_bounds__(256) k_flow_choose(FlowParams F) {
     for (int i = 0; i < 4; ++i) {
       const int4 pc = F.pieces[4 * q + i];
       if (pc.x < 0 || pc.x == q) continue;
-      const uint32_t kj = __ldg(&F.key[pc.x]);
+      const uint32_t kj = F.key[pc.x];
       if (kq > kj || (kq == kj && q > pc.x)) sa += (unsigned long long)(pc.z - pc.y);
       if (oq > tf.order(pc.x)) st += (unsigned long long)(pc.z - pc.y);
     }
@@ -395,9 +467,9 @@ __device__ __forceinline__ void cta_scan_inplace(int32_t* v, int64_t n) {
 }
 
 // ---- k_flow_decide (one CTA): the order, then its scan ------------------------
-__global__ void __launch_bounds__(1024) k_flow_decide(FlowParams F) {
+__device__ __forceinline__ void ph_decide(const FlowParams& F) {
   const EngineParams& P = F.P;
-  if (flow_off(F)) return;
+  if (block_flow_off(F)) return;
   __shared__ int32_t s_mode;
   if (threadIdx.x == 0) {
     int32_t mode = F.force;
@@ -411,16 +483,35 @@ __global__ void __launch_bounds__(1024) k_flow_decide(FlowParams F) {
     F.fc[FC_NTICK] = (long long)P.Q - F.fc[FC_NIDENT];
   }
   __syncthreads();
-  if (s_mode == 1) cta_scan_inplace(F.hist, F.nb);  // angle bins -> cursors
+  if (s_mode == 1 && F.nb == 16 * (int)blockDim.x) {  // angle bins -> cursors: 16 per thread, vector loads
+    int4* h4 = reinterpret_cast<int4*>(F.hist) + 4 * threadIdx.x;
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = h4[u];
+    int32_t sum = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sum += v[u].x + v[u].y + v[u].z + v[u].w;
+    int32_t tot;
+    int32_t run = block_excl_scan(sum, &tot);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int4 o;
+      o.x = run; run += v[u].x;
+      o.y = run; run += v[u].y;
+      o.z = run; run += v[u].z;
+      o.w = run; run += v[u].w;
+      h4[u] = o;
+    }
+  } else if (s_mode == 1) cta_scan_inplace(F.hist, F.nb);
   else cta_scan_inplace(F.chunk, P.Q / kFlowChunk + 1);  // identity regions before each chunk
 }
 
 // ---- k_flow_rank: order[] / rank[] -------------------------------------------
 // angle order: counting-sort scatter (ties in arrival order); two-front: block b
 // compacts tickets [1024 b, 1024 b + 1024) minus identity regions.
-__global__ void __launch_bounds__(kFlowChunk) k_flow_rank(FlowParams F) {
+__device__ __forceinline__ void ph_rank(const FlowParams& F) {
   const EngineParams& P = F.P;
-  if (flow_off(F)) return;
+  if (block_flow_off(F)) return;
   const int32_t mode = (int32_t)F.fc[FC_MODE];
   if (mode == 1) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
@@ -451,9 +542,9 @@ __global__ void __launch_bounds__(kFlowChunk) k_flow_rank(FlowParams F) {
 }
 
 // ---- k_flow_hull: salvage hulls and pending-reader counts ----------------------
-__global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
+__device__ __forceinline__ void ph_hull(const FlowParams& F) {
   const EngineParams& P = F.P;
-  if (flow_off(F)) return;
+  if (block_flow_off(F)) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = tid; q < P.Q; q += nthr) {
     if (F.idn[q]) continue;
@@ -462,7 +553,7 @@ __global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
     for (int i = 0; i < 4; ++i) {
       const int4 pc = F.pieces[4 * q + i];
       if (pc.x < 0 || pc.x == q) continue;
-      if (rq > __ldg(&F.rank[pc.x])) {  // j is written first: q reads its salvage entry
+      if (rq > F.rank[pc.x]) {  // j is written first: q reads its salvage entry
         atomicMin(&F.slo[pc.x], pc.y);
         atomicMax(&F.shi[pc.x], pc.z);
       } else {
@@ -476,10 +567,10 @@ __global__ void __launch_bounds__(256) k_flow_hull(FlowParams F) {
 // Entry of slot j: records [L, H) of the slot, L/H its salvage hull rounded to
 // multiples of 16 records (so an entry keeps the caller's 16-byte phase and every
 // superset TMA load of a piece stays inside it).  One atomic per block.
-__global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
+__device__ __forceinline__ void ph_alloc(const FlowParams& F) {
   const EngineParams& P = F.P;
-  Geo g(P);
-  if (flow_off(F)) return;
+  FlowGeo g(P);
+  if (block_flow_off(F)) return;
   __shared__ long long s_base;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < P.K; j0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = j0 + threadIdx.x;
@@ -511,10 +602,10 @@ __global__ void __launch_bounds__(256) k_flow_alloc(FlowParams F) {
 }
 
 // ---- k_flow_tickets: per-ticket descriptors ------------------------------------
-__global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
+__device__ __forceinline__ void ph_tickets(const FlowParams& F) {
   const EngineParams& P = F.P;
-  Geo g(P);
-  if (flow_off(F)) return;
+  FlowGeo g(P);
+  if (block_flow_off(F)) return;
   const int64_t nt = F.fc[FC_NTICK];
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if (tid == 0) {  // pm_status: salvaged slots / records, identity regions, order, both salvage estimates
@@ -540,7 +631,7 @@ __global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
       const int4 pc = F.pieces[4 * q + i];
       if (pc.x < 0) continue;
       const int k = pc.w & 1;
-      const bool pool = pc.x != q && __ldg(&F.rank[pc.x]) < (int32_t)t;
+      const bool pool = pc.x != q && F.rank[pc.x] < (int32_t)t;
       if (pc.w < 2) {
         T.ja[k] = pc.x;
         if (pool) {
@@ -557,6 +648,67 @@ __global__ void __launch_bounds__(256) k_flow_tickets(FlowParams F) {
     }
     F.tk[t] = T;
   }
+}
+
+// ---- k_flow_plan: every plan phase in one cooperative launch --------------------
+// One CTA of 1024 threads per SM; a grid-wide barrier between phases replaces a
+// kernel boundary (the phases are short and latency-bound: launch gaps and tails
+// dominated when they were separate kernels).  Every early exit (noop, FC_FAIL)
+// is taken by the whole grid, after a barrier, so no CTA is left waiting.
+#ifndef PM_FLOW_DEBUG
+#define PM_FLOW_DEBUG 0
+#endif
+// tuning builds (-DPM_FLOW_DEBUG=1): %globaltimer after each phase -> stats[32 + k]
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PM_FLOW_DBG(k) \
+  if (PM_FLOW_DEBUG && threadIdx.x == 0 && blockIdx.x == 0) F.P.stats[32 + (k)] = gtimer()
+template <typename KT>
+__global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
+  cg::grid_group grid = cg::this_grid();
+  PM_FLOW_DBG(0);
+  ph_sample<KT>(F);
+  PM_FLOW_DBG(1);
+  grid.sync();
+  if (*(volatile int32_t*)F.P.noop) return;
+  ph_split<KT>(F);
+  PM_FLOW_DBG(2);
+  grid.sync();
+  ph_readers(F);
+  PM_FLOW_DBG(3);
+  grid.sync();
+  ph_angle(F);
+  PM_FLOW_DBG(4);
+  grid.sync();
+  const bool angle = F.force < 0 || F.force == 1;
+  for (int it = 0; angle && it < F.nsync; ++it) {
+    ph_sync(F, it);
+  PM_FLOW_DBG(5);
+    grid.sync();
+  }
+  ph_key(F, angle ? F.nsync % 3 : 0);
+  PM_FLOW_DBG(6);
+  grid.sync();
+  ph_choose(F);
+  PM_FLOW_DBG(7);
+  grid.sync();
+  if (blockIdx.x == 0) ph_decide(F);
+  PM_FLOW_DBG(8);
+  grid.sync();
+  ph_rank(F);
+  PM_FLOW_DBG(9);
+  grid.sync();
+  ph_hull(F);
+  PM_FLOW_DBG(10);
+  grid.sync();
+  ph_alloc(F);
+  PM_FLOW_DBG(11);
+  grid.sync();
+  ph_tickets(F);
+  PM_FLOW_DBG(12);
 }
 
 // ---- k_flow_save: copy the salvage entries into the pool ------------------------
@@ -802,25 +954,16 @@ cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
 // the plan and the merge
 template <typename KT>
 cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev) {
-  const EngineParams& P = F.P;
-  const int g1 = (int)std::min<int64_t>((P.Q + 255) / 256, (int64_t)num_sms * 8);
-  k_flow_sample<KT><<<(int)std::min<int64_t>((std::max(F.nsa, F.nsb) + 255) / 256 + 1, (int64_t)num_sms * 8), 256, 0,
-                      st>>>(F);
-  k_flow_split<KT><<<(int)std::min<int64_t>((P.Q + 256) / 256, (int64_t)num_sms * 8), 256, 0, st>>>(F);
-  count_launches(2);
-  k_flow_readers<<<g1, 256, 0, st>>>(F);
-  k_flow_angle<<<g1, 256, 0, st>>>(F);
-  for (int it = 0; it < F.nsync; ++it) k_flow_sync<<<g1, 256, 0, st>>>(F, it);
-  k_flow_key<<<g1, 256, 0, st>>>(F, F.nsync % 3);
-  k_flow_choose<<<g1, 256, 0, st>>>(F);
-  k_flow_decide<<<1, 1024, 0, st>>>(F);
-  k_flow_rank<<<(int)std::min<int64_t>((P.Q + kFlowChunk - 1) / kFlowChunk, (int64_t)num_sms * 2), kFlowChunk, 0, st>>>(F);
-  k_flow_hull<<<g1, 256, 0, st>>>(F);
-  k_flow_alloc<<<g1, 256, 0, st>>>(F);
-  k_flow_tickets<<<g1, 256, 0, st>>>(F);
-  count_launches(9 + F.nsync);
-  cudaError_t e = cudaGetLastError();
+  int bps = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_flow_plan<KT>, kFlowChunk, 0);
   if (e != cudaSuccess) return e;
+  if (bps < 1) return cudaErrorInvalidConfiguration;
+  FlowParams Fa = F;
+  void* args[] = {&Fa};
+  e = cudaLaunchCooperativeKernel((const void*)k_flow_plan<KT>, dim3(num_sms * std::min(bps, 2)), dim3(kFlowChunk), args,
+                                  0, st);
+  if (e != cudaSuccess) return e;
+  count_launches(1);
   if (ev) {
     e = cudaEventRecord(ev, st);
     if (e != cudaSuccess) return e;
@@ -830,6 +973,7 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   if (e != cudaSuccess) return e;
   k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
   count_launches(2);
+
   return cudaGetLastError();
 }
 
