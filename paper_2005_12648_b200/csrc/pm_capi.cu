@@ -262,10 +262,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #ifndef PM_USE_BUFFERED
 #define PM_USE_BUFFERED 1  // tune: the streaming buffered pipeline when scratch >= min(|A|,|B|) (2^30 int32: 2.6 ms vs 3.0 for the engine with that pool)
 #endif
-  // the scheduled engine (pm_flow.cu) for in-place merges; it needs 16-byte aligned
-  // bases (slot boundaries are then 16-byte aligned in the array and the pool)
-  if (mode == MODE_MERGE && !copy && !direct && ctx->flow_mode != 0 && ((uintptr_t)keys & 15) == 0 &&
-      (w == 0 || ((uintptr_t)payload & 15) == 0))
+  // the scheduled engine (pm_flow.cu) for in-place merges
+  if (mode == MODE_MERGE && !copy && !direct && ctx->flow_mode != 0)
     return run_flow(ctx, keys, ks, payload, w, s, m, e, st);
   const bool buffered = copy || (!direct && PM_USE_BUFFERED && mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
   // (the engine stages one input and one output tile; the buffered pipeline
@@ -515,11 +513,12 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   // salvage pool, phase matched to the caller's (16-byte aligned) arrays
   const int64_t n = e - s;
   F.pool_cap = n / PM_FLOW_POOL_DIV + 32 * T;
-  const size_t pk = (size_t)align_up(F.pool_cap * ks, 256);
-  rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w : 0));
+  const size_t pk = (size_t)align_up(F.pool_cap * ks + 16, 256);
+  rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w + 16 : 0));
   if (rc) return rc;
-  F.pool_keys = static_cast<char*>(ctx->fpool);
-  F.pool_pay = reinterpret_cast<uint8_t*>(static_cast<char*>(ctx->fpool) + pk);
+  // same 16-byte phase as the caller's arrays (pool entries are 16-record aligned)
+  F.pool_keys = static_cast<char*>(ctx->fpool) + ((uintptr_t)keys & 15);
+  F.pool_pay = reinterpret_cast<uint8_t*>(static_cast<char*>(ctx->fpool) + pk + (w ? ((uintptr_t)payload & 15) : 0));
   P.stats = ctx->ctl->stats;
   P.ticket = &ctx->ctl->ticket_.v;
   P.err = &ctx->ctl->err_.v;

@@ -837,10 +837,13 @@ __global__ void __launch_bounds__(kEngineThreads, kEngineMinBlocks) k_engine(Eng
           psrc = P.scr_pay + (si * P.T + (x0 - hb)) * w;
         }
         uint8_t* kdst = kin + (isA ? R.offA + (x0 - R.xa) * ks : R.offB + (x0 - R.xb) * ks);
-        if (!(PM_ABLATE & 4)) copy_g2s_superset(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar);
+        // (unit boundaries are 16-byte aligned only when both bases are)
+        const bool exact = (((uintptr_t)P.keys) & 15) || (w && (((uintptr_t)P.pay) & 15));
+        if (!(PM_ABLATE & 4))
+          copy_g2s_piece(kdst, reinterpret_cast<const uint8_t*>(ksrc), (x1 - x0) * ks, &ctl.bar, exact);
         if (w) {
           uint8_t* pdst = pin + (isA ? R.poffA + (x0 - R.xa) * w : R.poffB + (x0 - R.xb) * w);
-          copy_g2s_superset(pdst, psrc, (x1 - x0) * w, &ctl.bar);
+          copy_g2s_piece(pdst, psrc, (x1 - x0) * w, &ctl.bar, exact);
         }
         if (p == gt) mine = l;
       }

@@ -779,15 +779,18 @@ __device__ __forceinline__ void flow_issue(const FlowParams& F, const FlowGeo& g
   D.poffB = (int32_t)poffB;
   int nrd = 0;
   D.rd[0] = D.rd[1] = D.rd[2] = D.rd[3] = -1;
+  // slot boundaries are 16-byte aligned only when both bases are (see copy_g2s_piece)
+  const bool exact = (((uintptr_t)P.keys) & 15) || (w && (((uintptr_t)P.pay) & 15));
   for_pieces(P, xa, xa + alpha, xb, xb + beta, [&](int64_t j, int64_t x, int64_t y, int k, int side) {
     const bool pool = (T.flags >> (side ? 3 + k : 1 + k)) & 1;
     const int64_t dl = pool ? (side ? T.dB[k] : T.dA[k]) : 0;
     const int64_t o = side ? x - xb : x - xa;  // records already staged on this side
     const char* ksrc = (pool ? F.pool_keys : P.keys) + (x + dl) * ks;
-    copy_g2s_superset(kin + (side ? offB : offA) + o * ks, reinterpret_cast<const uint8_t*>(ksrc), (y - x) * ks, bar);
+    copy_g2s_piece(kin + (side ? offB : offA) + o * ks, reinterpret_cast<const uint8_t*>(ksrc), (y - x) * ks, bar,
+                   exact);
     if (w) {
       const uint8_t* psrc = (pool ? F.pool_pay : P.pay) + (x + dl) * w;
-      copy_g2s_superset(pin + (side ? poffB : poffA) + o * w, psrc, (y - x) * w, bar);
+      copy_g2s_piece(pin + (side ? poffB : poffA) + o * w, psrc, (y - x) * w, bar, exact);
     }
     if (!pool && j != q) D.rd[nrd++] = (int32_t)j;
   });

@@ -111,6 +111,16 @@ __device__ __forceinline__ void copy_g2s_superset(uint8_t* dst, const uint8_t* s
   bulk_g2s(dst - ((uintptr_t)src - a), reinterpret_cast<const void*>(a), n, bar);
 }
 
+// One staged piece: the superset copy when the caller's slot boundaries are 16-byte
+// aligned (consecutive pieces then meet on aligned bytes), else the exact copy --
+// with an unaligned base two adjacent pieces from different sources would both
+// write the bytes around their common boundary.
+__device__ __forceinline__ void copy_g2s_piece(uint8_t* dst, const uint8_t* src, int64_t nbytes, uint64_t* bar,
+                                               bool exact) {
+  if (exact) copy_g2s_phased(dst, src, nbytes, bar);
+  else copy_g2s_superset(dst, src, nbytes, bar);
+}
+
 // warp copy global -> global, identical 16-byte phase on both sides; all loads of
 // a lane are issued before its stores (8 x 16 B in flight per lane)
 __device__ __forceinline__ void copy_g2g_warp(uint8_t* dst, const uint8_t* src, int64_t nbytes, int lane) {

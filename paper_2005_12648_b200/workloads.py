@@ -127,3 +127,46 @@ def config_input_device(cfg: int, seed: int = 0, log_len: int | None = None,
         idx = torch.arange(2 * L, dtype=torch.int32, device=device)
         return torch.cat([a, b]), idx.view(torch.uint8).reshape(2 * L, 4), L
     raise ValueError(f"unknown config {cfg}")
+
+
+def sorted_uniform_device(n: int, seed: int, out=None, hi: int = 2**31, chunk: int = 1 << 27, buckets: int = 1024,
+                          device="cuda"):
+    """``sort(uniform int32 in [0, hi))`` of ``n`` draws on the device, for runs too
+    large to sort in one piece (BASELINE config 5: 2^32 per run = 16 GiB).
+
+    Exactly the sorted multiset of the seeded draws: pass 1 counts the draws per
+    value bucket, pass 2 regenerates them chunk by chunk (same seed) and scatters
+    each sorted chunk's bucket segments behind the bucket's cursor, pass 3 sorts
+    each bucket in place.  Peak extra memory: a few chunks.
+    """
+    import torch
+
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=device)
+    shift = max(0, (hi - 1).bit_length() - (buckets - 1).bit_length())
+    nb = ((hi - 1) >> shift) + 1
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    counts = torch.zeros(nb, dtype=torch.int64, device=device)
+    for c0 in range(0, n, chunk):
+        v = torch.randint(0, hi, (min(chunk, n - c0),), generator=g, device=device, dtype=torch.int64)
+        counts += torch.bincount(v >> shift, minlength=nb)
+        del v
+    offs = torch.cumsum(counts, 0) - counts
+    cursor = offs.tolist()
+    edges = (torch.arange(nb, device=device, dtype=torch.int64) << shift).to(torch.int32)  # bucket starts
+    g.manual_seed(seed)
+    for c0 in range(0, n, chunk):
+        v = torch.randint(0, hi, (min(chunk, n - c0),), generator=g, device=device, dtype=torch.int64)
+        v = v.to(torch.int32).sort().values
+        bnd = torch.searchsorted(v, edges).tolist() + [v.numel()]
+        for b in range(nb):
+            k = bnd[b + 1] - bnd[b]
+            if k:
+                out[cursor[b]:cursor[b] + k] = v[bnd[b]:bnd[b + 1]]
+                cursor[b] += k
+        del v
+    for b, (o, c) in enumerate(zip(offs.tolist(), counts.tolist())):
+        if c > 1:
+            out[o:o + c] = out[o:o + c].sort().values
+    return out

@@ -1,4 +1,5 @@
-"""Adversarial layouts at 2^23 records through the bounded-scratch engine (and the
+"""Adversarial layouts at 2^23 records through every in-place engine route (the
+scheduled engine with each order and its fallback, the bounded-pool engine, the
 library's routing): one big rotation, perfect interleave, tiny runs, heavy
 duplicates, all-equal and already-sorted inputs, a 1/16 split.  Payload = original
 index, so stability is checked exactly (== stable argsort)."""
@@ -32,19 +33,24 @@ def _cases():
     }
 
 
-@pytest.mark.parametrize("engine_only", [True, False])
+@pytest.mark.parametrize("route", ["auto", "flow", "two_front", "angle", "fallback", "bounded"])
 @pytest.mark.parametrize("case", ["rotation", "interleave", "tiny_b", "tiny_a", "dups4", "equal", "sorted", "uneven"])
-def test_adversarial_layouts(case, engine_only):
+def test_adversarial_layouts(case, route):
+    """route: the library's routing; the scheduled engine with its order chosen per job,
+    or forced (two-front / angle), or its device-side fallback forced; the bounded-pool
+    engine."""
     from paper_2005_12648_b200 import _ops
 
     k0, m = _cases()[case]
     idx = torch.arange(k0.numel(), device="cuda", dtype=torch.int32)
     arr = pm.KeyedArray(k0.clone(), idx.view(torch.uint8).view(-1, 4).clone())
-    _ops.set_engine_only(engine_only)
+    _ops.set_engine_only(route != "auto")
+    _ops.set_flow_mode("auto" if route in ("auto", "flow") else route)
     try:
         _ops.merge(arr, 0, m, k0.numel())
     finally:
         _ops.set_engine_only(False)
+        _ops.set_flow_mode("auto")
     ref = torch.sort(k0.to(torch.int64), stable=True)
     assert torch.equal(arr.keys.to(torch.int64), ref.values)
     assert torch.equal(arr.payload.contiguous().view(torch.int32).view(-1).to(torch.int64), ref.indices)

@@ -1,0 +1,173 @@
+"""The scheduled in-place engine (pm_flow.cu) on its own: every order mode against the
+pinned oracle (oracle/, the reference's stable core _kernels.py:227-313), the
+device-side fallback, workspace reuse across geometries, and BASELINE config 5
+(L_A = L_B = 2^32 int32, 32 GiB) on one GPU."""
+import numpy as np
+import pytest
+import torch
+
+from gen import random_instance
+from oracle import oracle as orc
+
+pm = pytest.importorskip("paper_2005_12648_b200")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2005_12648_b200 import _ops  # noqa: E402
+
+MODE_OF = {"two_front": 1, "angle": 2}  # pm_status stats[4] after a scheduled merge
+
+
+@pytest.fixture
+def flow_mode():
+    def set_mode(mode):
+        _ops.set_engine_only(True)
+        _ops.set_flow_mode(mode)
+    yield set_mode
+    _ops.set_engine_only(False)
+    _ops.set_flow_mode("auto")
+
+
+def to_gpu(keys, payload):
+    return pm.KeyedArray(torch.from_numpy(np.ascontiguousarray(keys)).cuda(),
+                         torch.from_numpy(np.ascontiguousarray(payload)).cuda())
+
+
+@pytest.mark.parametrize("mode", ["auto", "two_front", "angle", "fallback"])
+@pytest.mark.parametrize("width,dtype", [(0, np.int32), (4, np.int32), (12, np.int32), (0, np.int64), (5, np.int64)])
+def test_modes_vs_oracle(flow_mode, mode, width, dtype):
+    flow_mode(mode)
+    rng = np.random.default_rng(31337 + width + (3 if dtype == np.int64 else 0))
+    for size in (9000, 70000, 300001, 1 << 21):
+        for domain in (5, 2**31 - 1):
+            split = float(rng.choice([0.02, 0.3, 0.5, 0.77, 0.99]))
+            keys, payload, middle = random_instance(rng, size, split, domain, width)
+            keys = keys.astype(dtype)
+            lo, hi = int(rng.integers(0, 5000)), int(rng.integers(0, 300))
+            kk = np.concatenate([np.full(lo, -3, dtype), keys, np.full(hi, -9, dtype)])
+            pp = np.concatenate([np.full((lo, width), 7, np.uint8), payload, np.full((hi, width), 8, np.uint8)])
+            want_k, want_p = kk.copy(), pp.copy()
+            orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
+            arr = to_gpu(kk, pp)
+            st = _ops.merge(arr, lo, lo + middle, lo + size)
+            k, p = arr.numpy()
+            assert np.array_equal(k, want_k), f"{mode} size={size} dom={domain} split={split} w={width}"
+            assert np.array_equal(p, want_p), f"{mode} payload size={size} dom={domain} split={split}"
+            if mode in MODE_OF and st[4]:
+                assert st[4] == MODE_OF[mode]
+
+
+@pytest.mark.parametrize("mode", ["auto", "two_front", "angle", "fallback", "bounded"])
+@pytest.mark.parametrize("koff,poff,width", [(1, 0, 4), (2, 3, 3), (3, 1, 8), (1, 1, 0)])
+def test_misaligned_bases(flow_mode, mode, koff, poff, width):
+    """Keys / payload views off the 16-byte grid (slot boundaries are then unaligned):
+    every engine stages the pieces exactly (no superset copies) and stays bit-exact."""
+    flow_mode(mode)
+    rng = np.random.default_rng(5 + koff + 7 * poff)
+    for size in (200001, 1 << 21):
+        keys, payload, middle = random_instance(rng, size, 0.4, 2**31 - 1, width)
+        dk = torch.from_numpy(np.concatenate([np.zeros(koff, np.int32), keys])).cuda()
+        pflat = np.concatenate([np.zeros(poff, np.uint8), payload.reshape(-1)])
+        dp = torch.from_numpy(pflat).cuda()[poff:].view(size, width) if width else torch.empty((size, 0), dtype=torch.uint8).cuda()
+        arr = pm.KeyedArray(dk[koff:], dp)
+        assert arr.keys.data_ptr() % 16 != 0
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+        _ops.merge(arr, 0, middle, size)
+        k, p = arr.numpy()
+        assert np.array_equal(k, want_k) and np.array_equal(p, want_p), (mode, koff, poff, width, size)
+
+
+def test_pool_overflow_falls_back(flow_mode):
+    """One big rotation needs half the job salvaged (> the pool's N/4): the plan
+    raises the overflow word and the gated bounded-pool engine merges instead."""
+    flow_mode("auto")
+    h = 1 << 22
+    ar = torch.arange(h, device="cuda", dtype=torch.int32)
+    k0 = torch.cat([ar + h, ar])
+    arr = pm.KeyedArray(k0.clone())
+    st = _ops.merge(arr, 0, h, 2 * h)
+    assert torch.equal(arr.keys, torch.sort(k0).values)
+    assert st[4] == 0  # no scheduled order reported: the bounded-pool engine ran
+
+
+def test_geometries_back_to_back(flow_mode):
+    """Workspace and pool reuse across shrinking / growing jobs and key widths."""
+    flow_mode("auto")
+    rng = np.random.default_rng(77)
+    for size, dtype, width in [(1 << 22, np.int32, 0), (3 << 18, np.int64, 0), (1 << 23, np.int32, 4),
+                               (12345, np.int32, 0), (1 << 22, np.int64, 8)]:
+        keys, payload, middle = random_instance(rng, size, 0.5, 2**31 - 1, width)
+        keys = keys.astype(dtype)
+        want_k, want_p = keys.copy(), payload.copy()
+        orc.seq_merge_buffered(want_k, want_p, 0, middle, size)
+        arr = to_gpu(keys, payload)
+        _ops.merge(arr, 0, middle, size)
+        k, p = arr.numpy()
+        assert np.array_equal(k, want_k) and np.array_equal(p, want_p), (size, dtype, width)
+
+
+def _mix(x, a, b):
+    """int64 hash of int64 keys (wrapping arithmetic): multiset fingerprints."""
+    y = x * a + b
+    y = y ^ (y >> 29)
+    return y * 0x5851F42D4C957F2D
+
+
+def test_config5_single_gpu_full_size():
+    """BASELINE config 5 on ONE B200: L_A = L_B = 2^32 uniform int32 (2^33 records,
+    32 GiB) merged in place by the scheduled engine (int64 record indices end to end).
+    Checks: sorted output; two multiset fingerprints of input == output; the exact
+    rank of 256 pivot values (records < v, from searchsorted on regenerated runs);
+    64 output windows equal to an independent merge of the regenerated runs."""
+    from paper_2005_12648_b200.workloads import sorted_uniform_device
+
+    L = 1 << 32
+    free = torch.cuda.mem_get_info()[0]
+    if free < (80 << 30):  # pragma: no cover
+        pytest.skip("needs ~80 GB of free device memory")
+    keys = torch.empty(2 * L, dtype=torch.int32, device="cuda")
+    sorted_uniform_device(L, 50, out=keys[:L])
+    sorted_uniform_device(L, 51, out=keys[L:])
+    fp_in = [0, 0]
+    C = 1 << 28
+    for c in range(0, 2 * L, C):
+        x = keys[c:c + C].to(torch.int64)
+        fp_in[0] += int(_mix(x, 0x9E3779B97F4A7C15, 7).sum().item())
+        fp_in[1] += int(_mix(x, 0xD1B54A32D192ED03, 11).sum().item())
+    arr = pm.KeyedArray(keys)
+    st = _ops.merge(arr, 0, L, 2 * L)
+    assert st[2] > 0 and st[4] in (1, 2)  # the scheduled engine ran
+    fp_out = [0, 0]
+    for c in range(0, 2 * L, C):
+        blk = keys[c:min(c + C + 1, 2 * L)]
+        assert bool(torch.all(blk[1:] >= blk[:-1]).item()), f"unsorted near {c}"
+        x = keys[c:c + C].to(torch.int64)
+        fp_out[0] += int(_mix(x, 0x9E3779B97F4A7C15, 7).sum().item())
+        fp_out[1] += int(_mix(x, 0xD1B54A32D192ED03, 11).sum().item())
+    M64 = (1 << 64) - 1
+    assert [v & M64 for v in fp_out] == [v & M64 for v in fp_in]
+    # regenerate the runs; exact ranks of pivot values and exact output windows
+    runs = torch.empty(2 * L, dtype=torch.int32, device="cuda")
+    A, B = sorted_uniform_device(L, 50, out=runs[:L]), sorted_uniform_device(L, 51, out=runs[L:])
+    g = torch.Generator(device="cuda").manual_seed(9)
+    piv = torch.randint(0, 2**31, (256,), generator=g, device="cuda", dtype=torch.int32)
+    want = torch.searchsorted(A, piv).to(torch.int64) + torch.searchsorted(B, piv).to(torch.int64)
+    got = torch.searchsorted(keys, piv).to(torch.int64)
+    assert torch.equal(got, want)
+    W = 4096
+    starts = torch.randint(0, 2 * L - W, (64,), generator=g, device="cuda", dtype=torch.int64).tolist()
+    for p in starts:
+        # stable merge path: i records of A among the first p outputs
+        lo, hi = max(0, p - L), min(p, L)
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if int(A[mid].item()) <= int(B[p - 1 - mid].item()):
+                lo = mid + 1
+            else:
+                hi = mid
+        a0, b0 = lo, p - lo
+        cand = torch.cat([A[a0:a0 + W], B[b0:b0 + W]]).sort(stable=True).values[:W]
+        assert torch.equal(keys[p:p + W], cand), f"window at {p}"

@@ -22,16 +22,20 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 
-@pytest.fixture(autouse=True, params=["auto", "engine"])
+@pytest.fixture(autouse=True, params=["auto", "flow", "bounded"])
 def route(request):
-    """Every parity test runs twice: with the library's own routing (one-CTA small
-    jobs, staged medium jobs, wide-record path) and with in-place merges forced
-    through the bounded-scratch engine."""
+    """Every parity test runs three times: with the library's own routing (one-CTA
+    small jobs, staged medium jobs, wide-record path, the scheduled engine for large
+    jobs), with every in-place merge forced through the scheduled engine (pm_flow.cu,
+    its order chosen per job, device-side fallback), and forced through the
+    bounded-pool engine (k_engine)."""
     from paper_2005_12648_b200 import _ops
 
-    _ops.set_engine_only(request.param == "engine")
+    _ops.set_engine_only(request.param != "auto")
+    _ops.set_flow_mode("bounded" if request.param == "bounded" else "auto")
     yield request.param
     _ops.set_engine_only(False)
+    _ops.set_flow_mode("auto")
 
 
 def sha(*arrays):
