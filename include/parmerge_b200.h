@@ -166,6 +166,9 @@ int pm_merge_host(pm_ctx *ctx, void *keys_host, int key_bytes, void *payload_hos
  * pm_kernel_ms() waits for the last one and returns their device durations.
  */
 int pm_set_timing(pm_ctx *ctx, int on);
+/* After a timed in-place merge: out4 = {plan, salvage copy, merge kernel, total} in
+ * ms (salvage copy 0 when the bounded-pool engine ran; its kernel is then "merge"). */
+int pm_kernel_ms_detail(pm_ctx *ctx, float *out4);
 /* Host evaluation of the engine's two-front ticket order (same source as the
  * device code): out4 = {region of ticket t, order(region), window lo, window hi}. */
 int pm_debug_order(int64_t Q, int64_t qc, int64_t t, int64_t *out4);

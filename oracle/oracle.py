@@ -56,6 +56,8 @@ def lib():
         L.orc_srecpar_buffered.argtypes = [
             _vp, ctypes.c_int, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _i64]
         L.orc_srecpar_buffered.restype = ctypes.c_int
+        L.orc_srecpar.argtypes = [_vp, ctypes.c_int, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _i64, ctypes.c_int]
+        L.orc_srecpar.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -131,6 +133,16 @@ def srecpar_buffered(keys, payload, start, middle, end, threads, size_limit=512)
     rc = lib().orc_srecpar_buffered(
         _ptr(keys), keys.dtype.itemsize, _ptr(payload), payload.shape[1],
         start, middle, end, threads, size_limit)
+    if rc != 0:
+        raise ValueError(f"worker count must be a power of two >= 1, got {threads}")
+
+
+def srecpar(keys, payload, start, middle, end, threads, size_limit=512, leaf="buffered") -> None:
+    """merge_srecpar(arr, job, threads) with the default rotation leaves (leaf="rotation",
+    srecpar.py:57) or seq_merge_buffered leaves (leaf="buffered"), on host threads."""
+    payload = _check(keys, payload)
+    rc = lib().orc_srecpar(_ptr(keys), keys.dtype.itemsize, _ptr(payload), payload.shape[1],
+                           start, middle, end, threads, size_limit, {"buffered": 0, "rotation": 1}[leaf])
     if rc != 0:
         raise ValueError(f"worker count must be a power of two >= 1, got {threads}")
 

@@ -184,6 +184,7 @@ DEFINE_ORACLE(int64_t, i64)
 typedef struct {
     void *k; uint8_t *p; int64_t w; int64_t s, m, e; int level, depth;
     int64_t size_limit; int key_bytes;
+    int leaf;  /* 0: seq_merge_buffered leaves; 1: the default rotation leaves (seqmerge.py:37-52) */
 } rp_task;
 
 static void *rp_core(void *arg);
@@ -214,7 +215,12 @@ static void rp_run(rp_task *t) {
         ++ns;
         end = rs; middle = start + piv[0]; ++level;
     }
-    if (t->key_bytes == 4)
+    if (t->leaf == 1) {  /* seq_merge_rotation(arr, job, LINEAR), srecpar.py:57 default leaf */
+        if (t->key_bytes == 4)
+            orc_rotation_merge_i32((int32_t *)t->k, t->p, t->w, start, middle, end, 0);
+        else
+            orc_rotation_merge_i64((int64_t *)t->k, t->p, t->w, start, middle, end, 0);
+    } else if (t->key_bytes == 4)
         orc_seq_merge_buffered_i32((int32_t *)t->k, t->p, t->w, start, middle, end);
     else
         orc_seq_merge_buffered_i64((int64_t *)t->k, t->p, t->w, start, middle, end);
@@ -223,16 +229,23 @@ static void rp_run(rp_task *t) {
 
 static void *rp_core(void *arg) { rp_run((rp_task *)arg); return NULL; }
 
-/* merge_srecpar(arr, job, threads, leaf_core=seq_merge_buffered), srecpar.py:33-60 */
-int orc_srecpar_buffered(void *keys, int key_bytes, uint8_t *payload, int64_t w,
-                         int64_t start, int64_t middle, int64_t end, int threads,
-                         int64_t size_limit) {
+/* merge_srecpar(arr, job, threads, leaf_core=...), srecpar.py:33-60; leaf 0 =
+ * seq_merge_buffered (the fastest reference path), 1 = the default rotation leaves */
+int orc_srecpar(void *keys, int key_bytes, uint8_t *payload, int64_t w,
+                int64_t start, int64_t middle, int64_t end, int threads,
+                int64_t size_limit, int leaf) {
     if (threads < 1 || (threads & (threads - 1))) return -1;
     if (start == middle || middle == end) return 0;
     if (key_bytes == 4) { int32_t *k = (int32_t *)keys; if (k[middle - 1] <= k[middle]) return 0; }
     else { int64_t *k = (int64_t *)keys; if (k[middle - 1] <= k[middle]) return 0; }
     int depth = 0; while ((1 << (depth + 1)) <= threads) ++depth;
-    rp_task t = {keys, payload, w, start, middle, end, 0, depth, size_limit, key_bytes};
+    rp_task t = {keys, payload, w, start, middle, end, 0, depth, size_limit, key_bytes, leaf};
     rp_run(&t);
     return 0;
+}
+
+int orc_srecpar_buffered(void *keys, int key_bytes, uint8_t *payload, int64_t w,
+                         int64_t start, int64_t middle, int64_t end, int threads,
+                         int64_t size_limit) {
+    return orc_srecpar(keys, key_bytes, payload, w, start, middle, end, threads, size_limit, 0);
 }

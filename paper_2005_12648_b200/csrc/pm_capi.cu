@@ -86,7 +86,8 @@ struct pm_ctx {
   size_t fws_bytes = 0;
   void* fpool = nullptr;  // scheduled engine: salvage pool (keys + payload, phase matched)
   size_t fpool_bytes = 0;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // plan | engine [| merge kernel] | end
+  bool ev_mid = false;  // ev[3] recorded (scheduled engine: between the salvage copy and k_flow)
   bool ev_recorded = false;
 };
 
@@ -397,6 +398,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   if (timed) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_recorded = true;
+    ctx->ev_mid = false;
   }
   return PM_OK;
 }
@@ -526,8 +528,11 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   P.need_space = &ctx->ctl->need_space_.v;
   // plan (splits, order, salvage, tickets) and merge
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
-  ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr)
-               : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr);
+  ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr,
+                                      ctx->timing ? ctx->ev[3] : nullptr)
+               : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr,
+                                      ctx->timing ? ctx->ev[3] : nullptr);
+  ctx->ev_mid = ctx->timing;
   if (ce != cudaSuccess) return cuda_fail(ce, "k_flow launch");
   if (ctx->timing) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
@@ -789,6 +794,22 @@ int pm_kernel_ms(pm_ctx* ctx, float* plan_ms, float* engine_ms) {
   PM_CUDA(cudaEventSynchronize(ctx->ev[2]));
   PM_CUDA(cudaEventElapsedTime(plan_ms, ctx->ev[0], ctx->ev[1]));
   PM_CUDA(cudaEventElapsedTime(engine_ms, ctx->ev[1], ctx->ev[2]));
+  return PM_OK;
+}
+
+int pm_kernel_ms_detail(pm_ctx* ctx, float* out4) {
+  if (!ctx || !out4) return fail(PM_ERR_ARG, "null argument");
+  if (!ctx->ev_recorded) return fail(PM_ERR_ARG, "no timed launch recorded (pm_set_timing first)");
+  PM_CUDA(cudaEventSynchronize(ctx->ev[2]));
+  PM_CUDA(cudaEventElapsedTime(&out4[0], ctx->ev[0], ctx->ev[1]));
+  PM_CUDA(cudaEventElapsedTime(&out4[3], ctx->ev[0], ctx->ev[2]));
+  if (ctx->ev_mid) {
+    PM_CUDA(cudaEventElapsedTime(&out4[1], ctx->ev[1], ctx->ev[3]));
+    PM_CUDA(cudaEventElapsedTime(&out4[2], ctx->ev[3], ctx->ev[2]));
+  } else {
+    out4[1] = 0.f;
+    PM_CUDA(cudaEventElapsedTime(&out4[2], ctx->ev[1], ctx->ev[2]));
+  }
   return PM_OK;
 }
 

@@ -956,7 +956,8 @@ cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
 // plan kernels (after launch_plan's splits); ev (may be null) is recorded between
 // the plan and the merge
 template <typename KT>
-cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev) {
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev,
+                        cudaEvent_t ev_merge) {
   int bps = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_flow_plan<KT>, kFlowChunk, 0);
   if (e != cudaSuccess) return e;
@@ -974,6 +975,10 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
   e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (ev_merge) {
+    e = cudaEventRecord(ev_merge, st);
+    if (e != cudaSuccess) return e;
+  }
   k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
   count_launches(2);
 
@@ -982,7 +987,7 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
 
 template cudaError_t flow_occupancy<int32_t>(size_t, int*);
 template cudaError_t flow_occupancy<int64_t>(size_t, int*);
-template cudaError_t launch_flow<int32_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t);
-template cudaError_t launch_flow<int64_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t);
+template cudaError_t launch_flow<int32_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t, cudaEvent_t);
+template cudaError_t launch_flow<int64_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t, cudaEvent_t);
 
 }  // namespace pm

@@ -31,7 +31,8 @@ constexpr int kFlowOut = PM_FLOW_OUT;
 constexpr int kFlowThreads = PM_FLOW_THREADS;
 template <typename KT> cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm);
 template <typename KT>
-cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev);
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev,
+                        cudaEvent_t ev_merge);
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st);
