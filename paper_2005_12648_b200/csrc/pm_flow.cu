@@ -65,6 +65,19 @@ namespace cg = cooperative_groups;
 namespace pm {
 
 constexpr int kFlowChunk = 1024;
+// -DPM_FLOW_CHECKED=1 (tools/checked.sh): device-side bounds and invariant checks
+// on every access of the scheduled engine -- a failed check prints and traps (the
+// substitute for compute-sanitizer, which this pool does not run)
+#ifndef PM_FLOW_CHECKED
+#define PM_FLOW_CHECKED 0
+#endif
+#define FLOW_CHECK(cond, ...)                                                      \
+  do {                                                                             \
+    if (PM_FLOW_CHECKED && !(cond)) {                                              \
+      printf("FLOW_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);         \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
 #ifndef PM_FLOW_WIN4
 #define PM_FLOW_WIN4 0  // tune: 4-ary window search in the split phase
 #endif
@@ -618,6 +631,7 @@ __device__ __forceinline__ void ph_tickets(const FlowParams& F) {
   }
   for (int64_t t = tid; t < nt; t += nthr) {
     const int32_t q = F.order[t];
+    FLOW_CHECK(q >= 0 && q < P.Q && F.rank[q] == (int32_t)t && !F.idn[q]);
     FlowTicket T;
     T.r = q;
     T.flags = 0;
@@ -728,6 +742,7 @@ __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
     const int64_t x0 = max(base + lo, g.slot_lo(j)), x1 = min(base + hi, g.slot_hi(j));
     if (x1 <= x0) continue;
     const int64_t dl = F.pdelta[j];
+    FLOW_CHECK(x0 + dl >= 0 && x1 + dl <= F.pool_cap && x0 >= P.s && x1 <= P.e);
     copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (x0 + dl) * ks),
                   reinterpret_cast<const uint8_t*>(P.keys + x0 * ks), (x1 - x0) * ks, lane);
     if (w) copy_g2g_warp(F.pool_pay + (x0 + dl) * w, P.pay + x0 * w, (x1 - x0) * w, lane);
@@ -784,6 +799,12 @@ __device__ __forceinline__ void flow_issue(const FlowParams& F, const FlowGeo& g
   for_pieces(P, xa, xa + alpha, xb, xb + beta, [&](int64_t j, int64_t x, int64_t y, int k, int side) {
     const bool pool = (T.flags >> (side ? 3 + k : 1 + k)) & 1;
     const int64_t dl = pool ? (side ? T.dB[k] : T.dA[k]) : 0;
+    FLOW_CHECK(x < y && (side ? (x >= P.m && y <= P.e) : (x >= P.s && y <= P.m)));
+    FLOW_CHECK(j == (x >> P.lT) - P.k0 && j == ((y - 1) >> P.lT) - P.k0 && j >= 0 && j < P.K);
+    FLOW_CHECK(!pool || (x + dl >= 0 && y + dl <= F.pool_cap));
+    FLOW_CHECK(!pool || (j != q && F.rank[j] < F.rank[q] && x - g.slot_base(j) >= F.slo[j] &&
+                         y - g.slot_base(j) <= F.shi[j]));
+    FLOW_CHECK(pool || j == q || F.rank[j] > F.rank[q]);
     const int64_t o = side ? x - xb : x - xa;  // records already staged on this side
     const char* ksrc = (pool ? F.pool_keys : P.keys) + (x + dl) * ks;
     copy_g2s_piece(kin + (side ? offB : offA) + o * ks, reinterpret_cast<const uint8_t*>(ksrc), (y - x) * ks, bar,
@@ -801,7 +822,11 @@ __device__ __forceinline__ void flow_issue(const FlowParams& F, const FlowGeo& g
 __device__ __forceinline__ void flow_release(const FlowParams& F, const FlowDesc& D) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (D.rd[i] >= 0) atomicSub(&F.pend[D.rd[i]], 1);
+    if (D.rd[i] >= 0) {
+      const int32_t old = atomicSub(&F.pend[D.rd[i]], 1);
+      FLOW_CHECK(old > 0);  // every release was counted by the plan
+      (void)old;
+    }
 }
 
 // Persistent, software-pipelined (k_buffered's shape).  The control warp's lane 0
@@ -926,6 +951,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
     }
     __syncthreads();  // tile complete, slot clear
     const int gt = (tid + 32) % NT;
+    FLOW_CHECK(R.d0 >= 0 && R.d0 + R.nout <= P.e - P.s && R.nout == g.slot_hi(R.r) - g.slot_lo(R.r) &&
+               P.s + R.d0 == g.slot_lo(R.r));
+    FLOW_CHECK(F.pend[R.r] == 0 || *(volatile int32_t*)P.err);
     if (!(PM_FLOW_ABLATE & 4)) {
       stream_out(kout_s + phk, reinterpret_cast<uint8_t*>(P.keys + (P.s + R.d0) * ks), (int64_t)R.nout * ks, gt, NT);
       if (w) stream_out(pout_s + php, P.pay + (P.s + R.d0) * w, (int64_t)R.nout * w, gt, NT);
