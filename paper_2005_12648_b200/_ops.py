@@ -108,8 +108,13 @@ def merge_host(keys, payload, start: int, middle: int, end: int, device: int = 0
 
 
 def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
-    """In-place block exchange A|B -> B|A on the device (pm_shift)."""
+    """In-place block exchange A|B -> B|A on the device (pm_shift).
+
+    The span must lie inside the array: pm_shift is not given the array length, and a
+    span past its end would write into neighbouring device allocations."""
     require_cuda(arr)
+    if lo < 0 or len_a < 0 or len_b < 0 or lo + len_a + len_b > len(arr):
+        raise IndexError(f"shift span [{lo}, {lo + len_a + len_b}) outside the array (length {len(arr)})")
     if len_a == 0 or len_b == 0:
         return None
     dev = arr.keys.device.index

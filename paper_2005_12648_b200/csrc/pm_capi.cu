@@ -88,8 +88,42 @@ struct pm_ctx {
   size_t fpool_bytes = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // plan | engine [| merge kernel] | end
   bool ev_mid = false;  // ev[3] recorded (scheduled engine: between the salvage copy and k_flow)
+  cudaStream_t last_stream = nullptr;  // the stream of the previous call (use_stream)
+  bool have_last = false;
+  cudaEvent_t xev = nullptr;
   bool ev_recorded = false;
 };
+
+// Every entry point runs on the context's device and restores the caller's current
+// device on return (tensors on cuda:1 while cuda:0 is current must not allocate or
+// launch on cuda:0).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      return;
+    }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// A context's workspace (splits, tickets, pools, control words) is shared by every
+// call on it: a call on another stream than the previous one first waits for the
+// previous stream's work (one event), so calls on different streams cannot race on it.
+static void use_stream(pm_ctx* ctx, cudaStream_t st) {
+  if (ctx->have_last && ctx->last_stream != st) {
+    if (!ctx->xev) cudaEventCreateWithFlags(&ctx->xev, cudaEventDisableTiming);
+    if (cudaEventRecord(ctx->xev, ctx->last_stream) == cudaSuccess) cudaStreamWaitEvent(st, ctx->xev, 0);
+    else cudaGetLastError();  // (the previous stream is gone: nothing left to wait for)
+  }
+  ctx->last_stream = st;
+  ctx->have_last = true;
+}
 
 static int ensure(void** p, size_t* have, size_t need) {
   if (*have >= need) return PM_OK;
@@ -582,6 +616,7 @@ int pm_launch_count(int64_t* out) {
 }
 
 int pm_debug_stats(pm_ctx* ctx, uint64_t* host_out64) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !host_out64) return fail(PM_ERR_ARG, "bad arguments");
   PM_CUDA(cudaDeviceSynchronize());
   Ctl h;
@@ -591,6 +626,7 @@ int pm_debug_stats(pm_ctx* ctx, uint64_t* host_out64) {
 }
 
 int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !host_out || n < 0) return fail(PM_ERR_ARG, "bad arguments");
   PM_CUDA(cudaDeviceSynchronize());
   PM_CUDA(cudaMemcpy(host_out, ctx->ws, (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -600,6 +636,7 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
 int pm_merge_peers(pm_ctx* ctx, const void* const* peer_keys, const void* const* peer_payload, int world, int rank,
                    int64_t block, int64_t len_a, int key_bytes, int64_t width, void* out_keys, void* out_payload,
                    void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !peer_keys || world < 1 || rank < 0 || rank >= world || block < 0 || (key_bytes != 4 && key_bytes != 8) ||
       width < 0 || !out_keys || (width && (!peer_payload || !out_payload)))
     return fail(PM_ERR_ARG, "bad pm_merge_peers arguments");
@@ -611,6 +648,7 @@ int pm_merge_peers(pm_ctx* ctx, const void* const* peer_keys, const void* const*
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t la = len_a, lb = N - len_a, d0 = (int64_t)rank * block, d1 = d0 + block;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, st);
   const int maxq = 2 + 2 * (world + 1);
   const size_t o_q = (size_t)align_up((int64_t)world * 8, 256), o_out = o_q + (size_t)maxq * 16;
   int rc = ensure(&ctx->peer, &ctx->peer_bytes, o_out + (size_t)maxq * 8);
@@ -700,6 +738,7 @@ int pm_ipc_close(void* ptr) {
 }
 
 int pm_debug_engine_only(pm_ctx* ctx, int on) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return fail(PM_ERR_ARG, "null context");
   std::lock_guard<std::mutex> lk(ctx->mu);
   ctx->engine_only = on != 0;
@@ -708,10 +747,12 @@ int pm_debug_engine_only(pm_ctx* ctx, int on) {
 
 int pm_debug_permute_rows(pm_ctx* ctx, void* payload, int64_t width, const int32_t* idx, int64_t n, int32_t cut_every,
                           void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || (n && (!payload || !idx)) || width <= 0 || n < 0 || n >= INT32_MAX || cut_every < 1)
     return fail(PM_ERR_ARG, "bad pm_debug_permute_rows arguments");
   if (n == 0) return PM_OK;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, static_cast<cudaStream_t>(stream));
   return permute_rows(ctx, static_cast<uint8_t*>(payload), width, idx, n, cut_every, static_cast<cudaStream_t>(stream));
 }
 
@@ -728,7 +769,10 @@ const char* pm_last_error(void) { return g_last_error.c_str(); }
 
 int pm_ctx_create(int device, pm_ctx** out) {
   if (!out) return fail(PM_ERR_ARG, "null out");
-  PM_CUDA(cudaSetDevice(device));
+  int ndev = 0;
+  PM_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(PM_ERR_ARG, "no such device");
+  DeviceGuard dg_(device);  // (the caller's current device is restored)
   pm_ctx* c = new pm_ctx();
   c->device = device;
   cudaDeviceProp prop;
@@ -749,10 +793,11 @@ int pm_ctx_create(int device, pm_ctx** out) {
 }
 
 int pm_ctx_destroy(pm_ctx* ctx) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return PM_OK;
-  cudaSetDevice(ctx->device);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->xev) cudaEventDestroy(ctx->xev);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->scr) cudaFree(ctx->scr);
   if (ctx->stage) cudaFree(ctx->stage);
@@ -772,6 +817,7 @@ int pm_ctx_destroy(pm_ctx* ctx) {
 }
 
 int pm_debug_flow(pm_ctx* ctx, int mode) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || mode < 0 || mode > 4) return fail(PM_ERR_ARG, "bad pm_debug_flow arguments");
   std::lock_guard<std::mutex> lk(ctx->mu);
   ctx->flow_mode = mode;
@@ -779,6 +825,7 @@ int pm_debug_flow(pm_ctx* ctx, int mode) {
 }
 
 int pm_set_timing(pm_ctx* ctx, int on) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return fail(PM_ERR_ARG, "null context");
   std::lock_guard<std::mutex> lk(ctx->mu);
   if (on && !ctx->ev[0])
@@ -789,6 +836,7 @@ int pm_set_timing(pm_ctx* ctx, int on) {
 }
 
 int pm_kernel_ms(pm_ctx* ctx, float* plan_ms, float* engine_ms) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !plan_ms || !engine_ms) return fail(PM_ERR_ARG, "null argument");
   if (!ctx->ev_recorded) return fail(PM_ERR_ARG, "no timed launch recorded (pm_set_timing first)");
   PM_CUDA(cudaEventSynchronize(ctx->ev[2]));
@@ -798,6 +846,7 @@ int pm_kernel_ms(pm_ctx* ctx, float* plan_ms, float* engine_ms) {
 }
 
 int pm_kernel_ms_detail(pm_ctx* ctx, float* out4) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !out4) return fail(PM_ERR_ARG, "null argument");
   if (!ctx->ev_recorded) return fail(PM_ERR_ARG, "no timed launch recorded (pm_set_timing first)");
   PM_CUDA(cudaEventSynchronize(ctx->ev[2]));
@@ -815,6 +864,7 @@ int pm_kernel_ms_detail(pm_ctx* ctx, float* out4) {
 
 int pm_merge_copy(pm_ctx* ctx, const void* src_keys, const void* src_payload, void* dst_keys, void* dst_payload,
                   int key_bytes, int64_t width, int64_t len_a, int64_t len_b, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   int rc = check_common(ctx, src_keys, key_bytes, src_payload, width);
   if (rc) return rc;
   rc = check_common(ctx, dst_keys, key_bytes, dst_payload, width);
@@ -829,23 +879,27 @@ int pm_merge_copy(pm_ctx* ctx, const void* src_keys, const void* src_payload, vo
     return fail(PM_ERR_ARG, "source and destination overlap (use pm_merge for in-place)");
   if (n == 0) return PM_OK;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, static_cast<cudaStream_t>(stream));
   return run_engine(ctx, const_cast<void*>(src_keys), key_bytes, const_cast<void*>(src_payload), width, 0, len_a, n,
                     MODE_MERGE, 0, static_cast<cudaStream_t>(stream), dst_keys, width ? dst_payload : nullptr);
 }
 
 int pm_merge(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t start, int64_t middle,
              int64_t end, int64_t scratch_records, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   int rc = check_common(ctx, keys, key_bytes, payload, width);
   if (rc) return rc;
   if (!(0 <= start && start <= middle && middle <= end))  // records.py:100-102
     return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, static_cast<cudaStream_t>(stream));
   return run_engine(ctx, keys, key_bytes, payload, width, start, middle, end, MODE_MERGE, scratch_records,
                     static_cast<cudaStream_t>(stream));
 }
 
 int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t lo, int64_t len_a,
              int64_t len_b, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   int rc = check_common(ctx, keys, key_bytes, payload, width);
   if (rc) return rc;
   if (lo < 0 || len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "lengths must be non-negative");  // shift.py:157
@@ -857,6 +911,7 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
   const int64_t rb = key_bytes + width;
   if (small * rb <= PM_SLIDE_STASH && !ctx->engine_only) {
     std::lock_guard<std::mutex> lk(ctx->mu);
+    use_stream(ctx, st);
     const int64_t ntk = (big * key_bytes + 32767) / 32768, ntp = (big * width + 32767) / 32768;
     const size_t sk = (size_t)align_up(small * key_bytes, 256), sp = (size_t)align_up(small * width, 256);
     const size_t fl = (size_t)align_up((ntk + ntp + 2) * 4, 256);
@@ -893,6 +948,7 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
 
 int pm_find_median(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int64_t la, int64_t lb, int64_t* out2,
                    void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return fail(PM_ERR_ARG, "null context");
   if (key_bytes != 4 && key_bytes != 8) return fail(PM_ERR_ARG, "key_bytes must be 4 or 8");
   if (la < 0 || lb < 0 || !out2 || (la && !a) || (lb && !b)) return fail(PM_ERR_ARG, "bad find_median arguments");
@@ -905,6 +961,7 @@ int pm_find_median(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int
 
 int pm_find_splits(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int64_t la, int64_t lb,
                    const int64_t* diags, int64_t nd, int64_t* out_a, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return fail(PM_ERR_ARG, "null context");
   if (key_bytes != 4 && key_bytes != 8) return fail(PM_ERR_ARG, "key_bytes must be 4 or 8");
   if (la < 0 || lb < 0 || nd < 0 || (nd && (!diags || !out_a)) || (la && !a) || (lb && !b))
@@ -920,6 +977,7 @@ int pm_find_splits(pm_ctx* ctx, const void* a, const void* b, int key_bytes, int
 
 int pm_plan_intervals(pm_ctx* ctx, const void* keys, int key_bytes, int64_t start, int64_t middle, int64_t end,
                       int32_t threads, int64_t* nodes, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   int rc = check_common(ctx, keys, key_bytes, nullptr, 0);
   if (rc) return rc;
   if (threads < 1 || (threads & (threads - 1)))  // soptmov.py:87-90
@@ -935,7 +993,12 @@ int pm_plan_intervals(pm_ctx* ctx, const void* keys, int key_bytes, int64_t star
 }
 
 int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx) return fail(PM_ERR_ARG, "null context");
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_stream(ctx, static_cast<cudaStream_t>(stream));  // the status covers the latest call on any stream
+  }
   PM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   Ctl h;
   PM_CUDA(cudaMemcpy(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
@@ -960,6 +1023,7 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
 // the two PCIe directions overlap.
 int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_host, int64_t width, int64_t start,
                   int64_t middle, int64_t end, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
   if (!ctx || !keys_host || (key_bytes != 4 && key_bytes != 8) || width < 0 || (width && !payload_host))
     return fail(PM_ERR_ARG, "bad pm_merge_host arguments");
   if (!(0 <= start && start <= middle && middle <= end)) return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");

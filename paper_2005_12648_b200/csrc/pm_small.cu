@@ -240,11 +240,16 @@ cudaError_t launch_merge_small(void* keys, void* payload, int64_t w, int64_t s, 
                                cudaStream_t st) {
   const int64_t n = e - s;
   const size_t smem = (size_t)small_merge_smem(sizeof(KT), w, n);
-  static std::atomic<int> attrs_set{0};
-  if (!attrs_set.load(std::memory_order_acquire)) {
-    cudaError_t ce = cudaFuncSetAttribute(k_merge_small<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  // function attributes belong to each device's context: set once per device
+  static std::atomic<uint64_t> attrs_set{0};
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return ce;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (dev >= 64 || !(attrs_set.load(std::memory_order_acquire) & bit)) {
+    ce = cudaFuncSetAttribute(k_merge_small<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (ce != cudaSuccess) return ce;
-    attrs_set.store(1, std::memory_order_release);
+    attrs_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   k_merge_small<KT><<<1, kSmallThreads, smem, st>>>(static_cast<KT*>(keys) + s,
                                                     w ? static_cast<uint8_t*>(payload) + s * w : nullptr, w,
@@ -276,14 +281,18 @@ cudaError_t launch_merge_cluster(void* keys, void* payload, int64_t w, int64_t s
                                  int lchunk, cudaStream_t st) {
   const int64_t chunk = (int64_t)1 << lchunk;
   const size_t smem = (size_t)(3 * (((chunk * (int64_t)sizeof(KT) + 15) & ~15ll) + ((chunk * w + 15) & ~15ll)));
-  // function attributes are set once per process (each call costs host time on the launch path)
-  static std::atomic<int> attrs_set{0};
-  cudaError_t ce = cudaSuccess;
-  if (!attrs_set.load(std::memory_order_acquire)) {
+  // function attributes belong to each device's context: set once per device
+  // (each call costs host time on the launch path)
+  static std::atomic<uint64_t> attrs_set{0};
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return ce;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (dev >= 64 || !(attrs_set.load(std::memory_order_acquire) & bit)) {
     ce = cudaFuncSetAttribute(k_merge_cluster<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kClusterSmem));
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_merge_cluster<KT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (ce != cudaSuccess) return ce;
-    attrs_set.store(1, std::memory_order_release);
+    attrs_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);

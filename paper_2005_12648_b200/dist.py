@@ -25,6 +25,7 @@ the host logic can be tested with the gloo backend on CPU tensors.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from typing import Callable
 
 import torch
@@ -77,8 +78,23 @@ def _split_search(keys_local: torch.Tensor, off: int, diags: torch.Tensor, la: i
 
 
 # CUDA graphs of the probe rounds, per (keys buffer, geometry): ~30 small ops and a
-# collective per round are replayed without host dispatch (NCCL supports capture)
-_graphs: dict = {}
+# collective per round are replayed without host dispatch (NCCL supports capture).
+# Bounded (least recently used first out); PM_DIST_GRAPHS=0 keeps the search eager.
+_graphs: OrderedDict = OrderedDict()
+_GRAPH_CAP = 8
+_PEER_CAP = 64
+
+
+def clear_caches() -> None:
+    """Release the captured split-search graphs and the mapped peer blocks."""
+    _graphs.clear()
+    _PEER_CACHE.clear()
+
+
+def _graph_capture_enabled() -> bool:
+    import os
+
+    return os.environ.get("PM_DIST_GRAPHS", "1") != "0"
 
 
 def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: int, group=None) -> list[int]:
@@ -98,8 +114,11 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
     if rounds == 0:
         return [min(max(d - lb, 0), la) for d in offsets]
     key = (keys_local.data_ptr(), keys_local.numel(), keys_local.dtype, off, tuple(offsets), la, rounds,
-           id(group)) if keys_local.is_cuda and dist.get_backend(group) == "nccl" else None
+           id(group)) if (keys_local.is_cuda and dist.get_backend(group) == "nccl"
+                          and _graph_capture_enabled()) else None
     ent = _graphs.get(key) if key else None
+    if key is not None and ent is not None:
+        _graphs.move_to_end(key)
     if ent is None:
         diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
         lo, hi = _split_search(keys_local, off, diags, la, lb, rounds, group)
@@ -111,8 +130,11 @@ def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: in
                 with torch.cuda.graph(g):
                     slo, shi = _split_search(keys_local, off, sd, la, lb, rounds, group)
                 _graphs[key] = (g, slo, shi)
-            except Exception:  # (capture unsupported here: stay eager)
+            except Exception:  # (capture unsupported here: stay eager; the partial graph is dropped)
+                torch.cuda.synchronize(dev)
                 _graphs[key] = False
+            while len(_graphs) > _GRAPH_CAP:
+                _graphs.popitem(last=False)
     elif ent is False:
         diags = torch.tensor(offsets, dtype=torch.int64, device=dev)
         lo, hi = _split_search(keys_local, off, diags, la, lb, rounds, group)
@@ -208,7 +230,7 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
 # Exchange fused with the merge: every rank maps the others' blocks (CUDA IPC, NVLink peer
 # access) and pm_merge_peers streams its A and B pieces straight out of peer memory into a
 # staging block -- no all-to-all pass, no send/receive copies.
-_PEER_CACHE: dict = {}
+_PEER_CACHE: OrderedDict = OrderedDict()
 
 
 def _peer_view(meta, numel: int, dtype, shape_tail, elem_off: int) -> torch.Tensor:
@@ -218,6 +240,10 @@ def _peer_view(meta, numel: int, dtype, shape_tail, elem_off: int) -> torch.Tens
     if st is None:
         st = torch.UntypedStorage._new_shared_cuda(*meta)
         _PEER_CACHE[key] = st
+        while len(_PEER_CACHE) > _PEER_CAP:  # unmap the least recently used peer block
+            _PEER_CACHE.popitem(last=False)
+    else:
+        _PEER_CACHE.move_to_end(key)
     t = torch.empty(0, dtype=dtype, device=st.device)
     t.set_(st, elem_off, (numel, *shape_tail))
     return t

@@ -1,0 +1,62 @@
+"""C-ABI behaviour around the kernels: calls on several streams sharing one context,
+the caller's current device left alone, span checks of the block exchange."""
+import numpy as np
+import pytest
+import torch
+
+pm = pytest.importorskip("paper_2005_12648_b200")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2005_12648_b200 import _ops  # noqa: E402
+
+
+def _job(n, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    h = n // 2
+    k = torch.cat([torch.randint(0, 2**31 - 1, (h,), generator=g, device="cuda", dtype=torch.int32).sort().values,
+                   torch.randint(0, 2**31 - 1, (n - h,), generator=g, device="cuda", dtype=torch.int32).sort().values])
+    return k, h
+
+
+@pytest.mark.parametrize("mode", ["auto", "bounded"])
+def test_streams_share_one_context(mode):
+    """Merges issued back to back on two streams use the same per-device workspace;
+    the library orders them (an event on the previous stream), so none corrupts another."""
+    _ops.set_engine_only(True)
+    _ops.set_flow_mode(mode)
+    try:
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        jobs = [_job(1 << 21, s) for s in range(6)]
+        arrs = [pm.KeyedArray(k.clone()) for k, _ in jobs]
+        torch.cuda.synchronize()
+        with pm.deferred_checks():
+            for i, (a, (k, h)) in enumerate(zip(arrs, jobs)):
+                with torch.cuda.stream(streams[i % 2]):
+                    _ops.merge(a, 0, h, k.numel())
+            torch.cuda.synchronize()
+        for a, (k, h) in zip(arrs, jobs):
+            assert torch.equal(a.keys, torch.sort(k).values)
+    finally:
+        _ops.set_engine_only(False)
+        _ops.set_flow_mode("auto")
+
+
+def test_current_device_untouched():
+    before = torch.cuda.current_device()
+    k, h = _job(1 << 18, 3)
+    a = pm.KeyedArray(k.clone())
+    _ops.merge(a, 0, h, k.numel())
+    assert torch.cuda.current_device() == before
+
+
+def test_shift_span_checked():
+    a = pm.KeyedArray(torch.arange(10, dtype=torch.int32, device="cuda"))
+    with pytest.raises(IndexError):
+        pm.shift_region(a, 6, 3, 3, "linear")
+    with pytest.raises(IndexError):
+        pm.shift_region(a, -1, 2, 2, "linear")
+    pm.shift_region(a, 4, 3, 3, "linear")
+    assert a.keys.cpu().tolist() == [0, 1, 2, 3, 7, 8, 9, 4, 5, 6]
