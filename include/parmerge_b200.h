@@ -90,6 +90,18 @@ int pm_shift(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t widt
              int64_t lo, int64_t len_a, int64_t len_b, void *stream);
 
 /*
+ * Replaces reorder_multi / reorder_cycles (soptmov.py:146-192, _kernels.py:317-369):
+ * permute [start, end) into the leaf layout A_0 B_0 A_1 B_1 ... where the A run is
+ * [start, start + sum|A_i|) cut into consecutive slices of the given sizes and the B
+ * run follows likewise (leaf_sizes: host int64[2*nleaves] = |A_0|, |B_0|, |A_1|, ...).
+ * One in-place pass of the scheduled engine (plan, salvage copy, streaming
+ * gather): every record is read and written once plus the salvaged ones; no keys
+ * are marked (the reference's marker offsets are not needed).
+ */
+int pm_reorder(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t width, int64_t start, int64_t end,
+               const int64_t *leaf_sizes, int32_t nleaves, void *stream);
+
+/*
  * Alg. 1 pivot pair of the sorted runs a[0, la) and b[0, lb) (DEVICE
  * pointers), exactly as find_median (median.py:23-60).  out2 is a DEVICE
  * int64[2] receiving (p_a, p_b).

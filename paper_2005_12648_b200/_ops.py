@@ -126,6 +126,22 @@ def shift(arr: KeyedArray, lo: int, len_a: int, len_b: int):
     return None
 
 
+def reorder(arr: KeyedArray, start: int, end: int, leaf_sizes: list[int]):
+    """In-place permutation of [start, end) into the leaf layout A_0 B_0 A_1 B_1 ...
+    (pm_reorder; ``leaf_sizes`` = [|A_0|, |B_0|, |A_1|, |B_1|, ...])."""
+    require_cuda(arr)
+    if len(leaf_sizes) % 2 or not leaf_sizes:
+        raise ValueError("leaf_sizes must hold |A_i|, |B_i| pairs")
+    dev = arr.keys.device.index
+    tab = (ctypes.c_int64 * len(leaf_sizes))(*[int(x) for x in leaf_sizes])
+    rc = _capi.lib().pm_reorder(_capi.context(dev), _ptr(arr.keys), arr.key_bytes, _ptr(arr.payload),
+                                arr.payload.shape[1], start, end, tab, len(leaf_sizes) // 2, _stream(dev))
+    _capi.check(rc, "pm_reorder")
+    if _check_each_call:
+        return _capi.status(dev, torch.cuda.current_stream(dev).cuda_stream)
+    return None
+
+
 def _run_tensor(x) -> torch.Tensor:
     if isinstance(x, torch.Tensor) and x.is_cuda:
         t = x

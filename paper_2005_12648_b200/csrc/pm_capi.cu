@@ -246,7 +246,7 @@ static int run_wide(pm_ctx* ctx, char* keys, int ks, uint8_t* pay, int64_t w, in
 // out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
 // keys_b / pay_b (copy mode only): the B run lives there instead of at keys + m.
 static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                    cudaStream_t st);
+                    cudaStream_t st, const int64_t* leaf_sizes = nullptr, int32_t nleaves = 0);
 
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys, void* out_payload,
@@ -456,7 +456,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 // behind it on the device: it runs only if the plan's salvage exceeds the pool
 // (FC_FAIL), so the whole call stays asynchronous.
 static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int64_t* leaf_sizes, int32_t nleaves) {
   int64_t M, T;
   int32_t mu;
   // regions: the largest power of two <= 8192 records whose keys + rows fit a tile
@@ -520,6 +520,7 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.nsb = (e - m) > F.phi ? (e - m - F.phi + S - 1) / S : 0;
   const size_t o_sa = take((size_t)(F.nsa + 1) * ks), o_sb = take((size_t)(F.nsb + 1) * ks);
   const size_t o_pc = take((size_t)K * 64), o_z = take((size_t)K * 24);
+  const size_t o_leaf = take((size_t)(2 * nleaves + 2) * 8);
   int rc = ensure(&ctx->fws, &ctx->fws_bytes, off);
   if (rc) return rc;
   char* b = static_cast<char*>(ctx->fws);
@@ -540,6 +541,23 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.samp_a = b + o_sa;
   F.samp_b = b + o_sb;
   F.pieces = reinterpret_cast<int4*>(b + o_pc);
+  F.nleaves = nleaves;
+  if (nleaves) {  // prescribed layout: leaf output starts and A prefixes, job-local
+    std::vector<int64_t> tab(2 * nleaves + 2);
+    int64_t L = 0, Apre = 0;
+    for (int32_t i = 0; i < nleaves; ++i) {
+      tab[i] = L;
+      tab[nleaves + 1 + i] = Apre;
+      L += leaf_sizes[2 * i] + leaf_sizes[2 * i + 1];
+      Apre += leaf_sizes[2 * i];
+    }
+    tab[nleaves] = L;
+    tab[2 * nleaves + 1] = Apre;
+    PM_CUDA(cudaMemcpyAsync(b + o_leaf, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+    PM_CUDA(cudaStreamSynchronize(st));  // (pageable source: keep it alive until copied)
+    F.leaf_l = reinterpret_cast<const int64_t*>(b + o_leaf);
+    F.leaf_a = F.leaf_l + nleaves + 1;
+  }
   F.z = reinterpret_cast<float2*>(b + o_z);
   F.nsync = PM_FLOW_SYNC;
   F.nsync_div = PM_FLOW_SYNC_DIV;
@@ -548,7 +566,8 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.force = ctx->flow_mode == 2 ? 0 : ctx->flow_mode == 3 ? 1 : ctx->flow_mode == 4 ? 2 : -1;
   // salvage pool, phase matched to the caller's (16-byte aligned) arrays
   const int64_t n = e - s;
-  F.pool_cap = n / PM_FLOW_POOL_DIV + 32 * T;
+  // a prescribed layout has no fallback engine: its pool holds any salvage (<= every slot)
+  F.pool_cap = nleaves ? n + 32 * T + 16 * K : n / PM_FLOW_POOL_DIV + 32 * T;
   const size_t pk = (size_t)align_up(F.pool_cap * ks + 16, 256);
   rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w + 16 : 0));
   if (rc) return rc;
@@ -895,6 +914,26 @@ int pm_merge(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
   use_stream(ctx, static_cast<cudaStream_t>(stream));
   return run_engine(ctx, keys, key_bytes, payload, width, start, middle, end, MODE_MERGE, scratch_records,
                     static_cast<cudaStream_t>(stream));
+}
+
+int pm_reorder(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t start, int64_t end,
+               const int64_t* leaf_sizes, int32_t nleaves, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
+  int rc = check_common(ctx, keys, key_bytes, payload, width);
+  if (rc) return rc;
+  if (start < 0 || end < start || nleaves < 1 || !leaf_sizes) return fail(PM_ERR_ARG, "bad pm_reorder arguments");
+  int64_t tot = 0, ta = 0;
+  for (int32_t i = 0; i < 2 * nleaves; ++i) {
+    if (leaf_sizes[i] < 0) return fail(PM_ERR_ARG, "negative leaf slice");
+    tot += leaf_sizes[i];
+    if (!(i & 1)) ta += leaf_sizes[i];
+  }
+  if (tot != end - start) return fail(PM_ERR_ARG, "leaf slices do not cover [start, end)");
+  if (end - start == 0 || ta == 0 || ta == end - start) return PM_OK;  // one run: already in place
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, static_cast<cudaStream_t>(stream));
+  return run_flow(ctx, keys, key_bytes, payload, width, start, start + ta, end, static_cast<cudaStream_t>(stream),
+                  leaf_sizes, nleaves);
 }
 
 int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t width, int64_t lo, int64_t len_a,

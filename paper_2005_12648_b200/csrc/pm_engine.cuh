@@ -209,6 +209,11 @@ struct FlowParams {
   int32_t nbits;        // itinerary length of the angle key
   int32_t nb;           // angle bins
   int32_t force;        // -1: choose per job, 0: two-front, 1: angle order, 2: force the fallback
+  // prescribed layout (pm_reorder, reorder_multi): nleaves > 0 leaves, leaf i = the
+  // A slice of size leafpre[..] then the B slice; the output is their concatenation
+  const int64_t* leaf_l;  // [nleaves + 1] output start of each leaf (job-local), leaf_l[nleaves] = N
+  const int64_t* leaf_a;  // [nleaves + 1] A records before each leaf
+  int32_t nleaves;
   int32_t lS;           // log2 of the split-search sample stride S (S divides M)
   int32_t phi;          // B samples sit at B[k S + phi], phi = (-s - 1) mod S
   void* samp_a;         // A[k S]            k < ceil(LA / S)

@@ -165,12 +165,13 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
   if (tid < FC_WORDS) F.fc[tid] = 0;
   if (tid == 0) {
     *P.ticket = 0;
-    const bool nothing = P.m == P.s || P.m == P.e || A[P.m - P.s - 1] <= B[0];  // srecpar.py:56-57
+    // (a prescribed layout has no such shortcut: identity regions are skipped instead)
+    const bool nothing = P.m == P.s || P.m == P.e || (!F.nleaves && A[P.m - P.s - 1] <= B[0]);  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
     for (int i = 0; i < 16; ++i) P.stats[i] = 0;
   }
   // (four independent strided loads in flight per thread before their stores)
-  for (int64_t k0 = tid; k0 < F.nsa + F.nsb; k0 += 4 * nthr) {
+  for (int64_t k0 = tid; !F.nleaves && k0 < F.nsa + F.nsb; k0 += 4 * nthr) {
     KT v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -214,11 +215,45 @@ __device__ __forceinline__ int64_t last_true8(int64_t lo, int64_t hi, Pred&& pre
   return lo;
 }
 
+// leaf of job-local output position d: the largest i with leaf_l[i] <= d
+__device__ __forceinline__ int32_t leaf_of(const FlowParams& F, int64_t d) {
+  int32_t lo = 0, hi = F.nleaves - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (F.leaf_l[mid] <= d) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// prescribed layout: A records among the first d outputs of A_0 B_0 A_1 B_1 ...
+__device__ __forceinline__ void ph_split_leaves(const FlowParams& F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = tid; q <= P.Q; q += nthr) {
+    const int64_t d = g.diag(q);
+    int64_t a;
+    if (d >= g.N()) {
+      a = g.LA();
+    } else {
+      const int32_t i = leaf_of(F, d);
+      const int64_t na = F.leaf_a[i + 1] - F.leaf_a[i];
+      a = F.leaf_a[i] + min(d - F.leaf_l[i], na);
+    }
+    P.split_a[q] = a;
+  }
+}
+
 template <typename KT>
 __device__ __forceinline__ void ph_split(const FlowParams& F) {
   const EngineParams& P = F.P;
   FlowGeo g(P);
   if (*(volatile int32_t*)P.noop) return;
+  if (F.nleaves) {
+    ph_split_leaves(F);
+    return;
+  }
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const KT* A = reinterpret_cast<const KT*>(P.keys) + P.s;
   const KT* B = reinterpret_cast<const KT*>(P.keys) + P.m;
@@ -749,6 +784,40 @@ __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
   }
 }
 
+// Prescribed layout (pm_reorder): output o of the region at job-local diagonal d0
+// is A[a] or B[b] of its leaf; thread gt writes outputs [o0, o1) (consecutive,
+// one leaf search per thread, then a linear walk across leaf boundaries).
+template <typename KT, int GT>
+__device__ __forceinline__ void concat_tile(const FlowParams& F, int64_t d0, int64_t a0, int64_t b0, const KT* As,
+                                            const KT* Bs, int32_t nout, KT* ko, uint8_t* po, const uint8_t* PA,
+                                            const uint8_t* PB, int64_t w, int gt) {
+  const int32_t E = (nout + GT - 1) / GT;
+  const int32_t o0 = min(gt * E, nout), o1 = min(o0 + E, nout);
+  if (o0 >= o1) return;
+  int32_t i = leaf_of(F, d0 + o0);
+  int64_t lend = F.leaf_l[i + 1], lstart = F.leaf_l[i], na = F.leaf_a[i + 1] - F.leaf_a[i], apre = F.leaf_a[i];
+  for (int32_t o = o0; o < o1; ++o) {
+    const int64_t d = d0 + o;
+    while (d >= lend) {
+      ++i;
+      lstart = lend;
+      lend = F.leaf_l[i + 1];
+      apre = F.leaf_a[i];
+      na = F.leaf_a[i + 1] - apre;
+    }
+    const int64_t off = d - lstart;
+    if (off < na) {
+      const int64_t x = apre + off - a0;  // staged A position
+      ko[o] = As[x];
+      if (w) for (int64_t c = 0; c < w; ++c) po[(int64_t)o * w + c] = PA[x * w + c];
+    } else {
+      const int64_t x = d - (apre + na) - b0;  // B index d - leaf_a[i+1], staged
+      ko[o] = Bs[x];
+      if (w) for (int64_t c = 0; c < w; ++c) po[(int64_t)o * w + c] = PB[x * w + c];
+    }
+  }
+}
+
 // ---- k_flow: the streaming in-place merge ---------------------------------------
 struct FlowDesc {
   int64_t d0;
@@ -937,16 +1006,24 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
     } else {
       uint8_t* kin = STAGE(cur);
       uint8_t* pin = STAGE(cur) + P.smem_keys;
-      if (!w) {
-        write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, tid, MT);
-        named_barrier_sync(1, MT);
+      if (F.nleaves) {  // prescribed layout: concatenate the leaf slices
+        const int64_t a0 = F.P.split_a[R.r];
+        concat_tile<KT, kFlowThreads - 32>(F, R.d0, a0, R.d0 - a0, reinterpret_cast<const KT*>(kin + R.offA),
+                                           reinterpret_cast<const KT*>(kin + R.offB), R.nout,
+                                           reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                           pin + R.poffB, w, tid);
+      } else {
+        if (!w) {
+          write_sentinels<KT>(kin, R.offA, R.alpha, R.offB, R.beta, tid, MT);
+          named_barrier_sync(1, MT);
+        }
+        const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
+        if (!(PM_FLOW_ABLATE & 2))
+          merge_tile<KT, kFlowThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
+                                            reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                                            reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                            pin + R.poffB, w, wq4, tid);
       }
-      const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-      if (!(PM_FLOW_ABLATE & 2))
-      merge_tile<KT, kFlowThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
-                                        reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
-                                        reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
-                                        pin + R.poffB, w, wq4, tid);
       fence_proxy_async_smem();
     }
     __syncthreads();  // tile complete, slot clear

@@ -171,3 +171,36 @@ def test_config5_single_gpu_full_size():
         a0, b0 = lo, p - lo
         cand = torch.cat([A[a0:a0 + W], B[b0:b0 + W]]).sort(stable=True).values[:W]
         assert torch.equal(keys[p:p + W], cand), f"window at {p}"
+
+
+@pytest.mark.parametrize("width", [0, 4, 7])
+def test_reorder_prescribed_layouts(width):
+    """pm_reorder (reorder_multi's one-pass device realisation): random leaf layouts
+    A_0 B_0 A_1 B_1 ... over sizes up to 2^22 against a host gather of the slices."""
+    rng = np.random.default_rng(404 + width)
+    for n, t in [(1 << 12, 2), (100003, 8), (1 << 20, 64), (3 << 20, 1024), (1 << 22, 16)]:
+        la = int(rng.integers(1, n))
+        cuts_a = np.sort(rng.integers(0, la + 1, t - 1))
+        cuts_b = np.sort(rng.integers(0, n - la + 1, t - 1))
+        ea = np.diff(np.concatenate([[0], cuts_a, [la]]))
+        eb = np.diff(np.concatenate([[0], cuts_b, [n - la]]))
+        sizes = [int(x) for pair in zip(ea, eb) for x in pair]
+        keys = rng.integers(-2**31, 2**31 - 1, n).astype(np.int32)
+        payload = rng.integers(0, 256, (n, width), dtype=np.uint8)
+        lo = int(rng.integers(0, 50))
+        kk = np.concatenate([np.full(lo, 9, np.int32), keys, np.full(3, 8, np.int32)])
+        pp = np.concatenate([np.zeros((lo, width), np.uint8), payload, np.ones((3, width), np.uint8)])
+        srcs, a0, b0 = [], 0, la
+        for i in range(t):
+            srcs.append((a0, int(ea[i])))
+            srcs.append((b0, int(eb[i])))
+            a0 += int(ea[i])
+            b0 += int(eb[i])
+        want_k = kk.copy()
+        want_p = pp.copy()
+        want_k[lo:lo + n] = np.concatenate([keys[s:s + c] for s, c in srcs])
+        want_p[lo:lo + n] = np.concatenate([payload[s:s + c] for s, c in srcs])
+        arr = to_gpu(kk, pp)
+        _ops.reorder(arr, lo, lo + n, sizes)
+        k, p = arr.numpy()
+        assert np.array_equal(k, want_k) and np.array_equal(p, want_p), (n, t, width)
