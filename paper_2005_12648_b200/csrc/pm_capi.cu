@@ -62,6 +62,7 @@ struct pm_ctx {
   int device = 0;
   int num_sms = 148;
   std::mutex mu;
+  std::mutex host_mu;  // pm_merge_host: one call at a time per context (staging buffer, its streams and events)
   void* ws = nullptr;  // split_a | state | loc | reads | next_free | next_scr
   size_t ws_bytes = 0;
   Ctl* ctl = nullptr;
@@ -1080,6 +1081,9 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   }
   const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)align_up(n * width, 256);
   int rc;
+  // host threads calling concurrently (the reference's pool runs leaf merges in
+  // parallel) share the staging buffer and the pipeline streams: one at a time
+  std::lock_guard<std::mutex> host_lk(ctx->host_mu);
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
     rc = ensure(&ctx->stage, &ctx->stage_bytes, 2 * (kb + pb) + 256);

@@ -60,3 +60,27 @@ def test_shift_span_checked():
         pm.shift_region(a, -1, 2, 2, "linear")
     pm.shift_region(a, 4, 3, 3, "linear")
     assert a.keys.cpu().tolist() == [0, 1, 2, 3, 7, 8, 9, 4, 5, 6]
+
+
+def test_merge_host_from_many_threads():
+    """pm_merge_host called concurrently from host threads on one context (the
+    reference's worker pool does this for its leaf merges): each call is exact."""
+    import concurrent.futures as cf
+
+    from oracle import oracle as orc
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(8)
+    jobs = []
+    for i in range(24):
+        n = int(rng.integers(1000, 300000))
+        h = int(rng.integers(1, n))
+        k = np.concatenate([np.sort(rng.integers(0, 1000, h)), np.sort(rng.integers(0, 1000, n - h))]).astype(np.int32)
+        p = rng.integers(0, 256, (n, 4), dtype=np.uint8)
+        wk, wp = k.copy(), p.copy()
+        orc.seq_merge_buffered(wk, wp, 0, h, n)
+        jobs.append((k, p, h, wk, wp))
+    with cf.ThreadPoolExecutor(8) as ex:
+        list(ex.map(lambda j: _ops.merge_host(j[0], j[1], 0, j[2], len(j[0])), jobs))
+    for k, p, h, wk, wp in jobs:
+        assert np.array_equal(k, wk) and np.array_equal(p, wp)
