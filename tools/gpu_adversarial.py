@@ -1,4 +1,5 @@
-"""Engine stress on adversarial layouts at large sizes (in place, default bounded pool).
+"""Engine stress on adversarial layouts at large sizes: the scheduled engine (order chosen per job)
+and the bounded-pool engine, in place, device-timed (median of 3 after a warm-up).
 
 Each case: merge, compare with a stable device sort, print time.  Cases: B entirely
 before A (one big rotation), perfect interleave, tiny B inside A, tiny A, heavy
@@ -34,23 +35,35 @@ cases = {
                                torch.randint(0, 2**31 - 1, (n - n // 16,), generator=g, device="cuda", dtype=torch.int32).sort().values]), n // 16),
 }
 ok_all = True
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for name, (k0, m) in cases.items():
     idx = torch.arange(k0.numel(), device="cuda", dtype=torch.int32)
     pay0 = idx.view(torch.uint8).view(-1, 4)
-    arr = pm.KeyedArray(k0.clone(), pay0.clone())
-    _ops.set_engine_only(True)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    try:
-        _ops.merge(arr, 0, m, k0.numel())
-        err = ""
-    except Exception as ex:  # noqa: BLE001
-        err = str(ex)[:120]
-    dt = time.perf_counter() - t0
-    _ops.set_engine_only(False)
     ref = torch.sort(k0.to(torch.int64), stable=True)
-    ok = not err and torch.equal(arr.keys.to(torch.int64), ref.values) and torch.equal(
-        arr.payload.contiguous().view(torch.int32).view(-1).to(torch.int64), ref.indices)
-    ok_all &= bool(ok)
-    print(f"{name:24s} n=2^{L} {dt * 1e3:8.2f} ms  ok={ok} {err}", flush=True)
+    for mode in ("auto", "bounded"):
+        arr = pm.KeyedArray(k0.clone(), pay0.clone())
+        _ops.set_engine_only(True)
+        _ops.set_flow_mode(mode)
+        ts, err, st = [], "", None
+        try:
+            for r in range(4):
+                arr.keys.copy_(k0)
+                arr.payload.copy_(pay0)
+                ev0.record()
+                with pm.deferred_checks():
+                    _ops.merge(arr, 0, m, k0.numel())
+                    ev1.record()
+                ts.append(ev0.elapsed_time(ev1))
+            st = pm.synchronize()
+        except Exception as ex:  # noqa: BLE001
+            err = str(ex)[:120]
+        _ops.set_engine_only(False)
+        _ops.set_flow_mode("auto")
+        ok = not err and torch.equal(arr.keys.to(torch.int64), ref.values) and torch.equal(
+            arr.payload.contiguous().view(torch.int32).view(-1).to(torch.int64), ref.indices)
+        ok_all &= bool(ok)
+        order = {1: "two-front", 2: "angle"}.get(st[4], "bounded") if st else "?"
+        t = sorted(ts[1:])[len(ts[1:]) // 2] if len(ts) > 1 else float("nan")
+        print(f"{name:24s} n=2^{L} {mode:8s} {t:8.3f} ms  order={order:9s} salvage={st[1] / k0.numel() if st else 0:.3f}N "
+              f"ok={ok} {err}", flush=True)
 print("ALL OK" if ok_all else "FAILURES")
