@@ -128,6 +128,16 @@ int pm_plan_intervals(pm_ctx *ctx, const void *keys, int key_bytes, int64_t star
                       int64_t end, int32_t threads, int64_t *nodes, void *stream);
 
 /*
+ * Global stable splits of a block-distributed A|B (the distributed form of
+ * median.find_median's split search, median.py:23-60, made stable): for each
+ * diagonal diags[i] the number of A records among the first diags[i] outputs,
+ * read through the peer-pointer table (one thread per diagonal, dependent peer
+ * loads over NVLink).  Host diags / out_a; synchronises the stream.
+ */
+int pm_peer_splits(pm_ctx *ctx, const void *const *peer_keys, int world, int64_t block, int64_t len_a,
+                   int key_bytes, const int64_t *diags, int nd, int64_t *out_a, void *stream);
+
+/*
  * Multi-GPU merge with the partition exchange fused into the merge's loads.
  * The global array X = A|B (A = X[0, len_a), B = X[len_a, N), N = world*block)
  * is block-distributed: block k (records [k*block, (k+1)*block)) at

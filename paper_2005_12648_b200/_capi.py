@@ -29,7 +29,7 @@ EXPORTED = (
     "pm_find_median", "pm_find_splits", "pm_plan_intervals", "pm_status", "pm_merge_host",
     "pm_set_timing", "pm_kernel_ms", "pm_debug_order", "pm_debug_splits", "pm_debug_stats", "pm_merge_copy", "pm_launch_count",
     "pm_debug_permute_rows", "pm_debug_engine_only", "pm_merge_peers", "pm_ipc_handle", "pm_ipc_open",
-    "pm_ipc_close", "pm_debug_flow", "pm_kernel_ms_detail", "pm_reorder",
+    "pm_ipc_close", "pm_debug_flow", "pm_kernel_ms_detail", "pm_reorder", "pm_peer_splits",
 )
 
 _lib = None
@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
         L.pm_debug_engine_only.argtypes = [vp, i32]
         L.pm_debug_flow.argtypes = [vp, i32]
         L.pm_kernel_ms_detail.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+        L.pm_peer_splits.argtypes = [vp, vp, i32, i64, i64, i32, ctypes.POINTER(ctypes.c_int64), i32,
+                                     ctypes.POINTER(ctypes.c_int64), vp]
         L.pm_reorder.argtypes = [vp, vp, i32, vp, i64, i64, i64, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, vp]
         L.pm_merge_peers.argtypes = [vp, vp, vp, i32, i32, i64, i64, i32, i64, vp, vp, vp]
         L.pm_ipc_handle.argtypes = [vp, vp]

@@ -253,6 +253,22 @@ def merge_peers(peer_keys: list, peer_payload: list | None, len_a: int, rank: in
     _capi.check(rc, "pm_merge_peers")
 
 
+def peer_splits(peer_keys: list, len_a: int, diags: list[int]) -> list[int]:
+    """pm_peer_splits: the stable split (A records among the first d outputs) of every
+    diagonal d of the block-distributed A|B, read through the peer-pointer table
+    (blocks ``peer_keys[k]`` of equal length; one launch, dependent peer loads)."""
+    world = len(peer_keys)
+    block = peer_keys[0].numel()
+    tk = (ctypes.c_void_p * world)(*[t.data_ptr() for t in peer_keys])
+    dq = (ctypes.c_int64 * len(diags))(*[int(d) for d in diags])
+    out = (ctypes.c_int64 * len(diags))()
+    dev = peer_keys[0].device.index
+    rc = _capi.lib().pm_peer_splits(_capi.context(dev), tk, world, block, len_a, peer_keys[0].element_size(),
+                                    dq, len(diags), out, _stream(dev))
+    _capi.check(rc, "pm_peer_splits")
+    return [int(x) for x in out]
+
+
 def ipc_handle(t: torch.Tensor) -> bytes:
     """64-byte CUDA IPC handle of the allocation holding ``t`` (pm_ipc_handle) and t's offset in it."""
     base = t.untyped_storage().data_ptr()

@@ -653,6 +653,44 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   return PM_OK;
 }
 
+int pm_peer_splits(pm_ctx* ctx, const void* const* peer_keys, int world, int64_t block, int64_t len_a, int key_bytes,
+                   const int64_t* diags, int nd, int64_t* out_a, void* stream) {
+  DeviceGuard dg_(ctx ? ctx->device : -1);
+  if (!ctx || !peer_keys || world < 1 || block < 0 || (key_bytes != 4 && key_bytes != 8) || nd < 0 || (nd && (!diags || !out_a)))
+    return fail(PM_ERR_ARG, "bad pm_peer_splits arguments");
+  const int64_t N = (int64_t)world * block;
+  if (len_a < 0 || len_a > N) return fail(PM_ERR_ARG, "len_a outside [0, world*block]");
+  for (int i = 0; i < nd; ++i)
+    if (diags[i] < 0 || diags[i] > N) return fail(PM_ERR_ARG, "diagonal outside [0, world*block]");
+  for (int k = 0; k < world; ++k)
+    if (block && !peer_keys[k]) return fail(PM_ERR_ARG, "null peer block");
+  if (nd == 0) return PM_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  use_stream(ctx, st);
+  const size_t o_q = (size_t)align_up((int64_t)world * 8, 256), o_out = o_q + (size_t)align_up((int64_t)nd * 16, 256);
+  int rc = ensure(&ctx->peer, &ctx->peer_bytes, o_out + (size_t)nd * 8);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->peer);
+  const void** dtab = reinterpret_cast<const void**>(base);
+  int64_t* dq = reinterpret_cast<int64_t*>(base + o_q);
+  int64_t* dout = reinterpret_cast<int64_t*>(base + o_out);
+  std::vector<int64_t> q(2 * (size_t)nd);
+  for (int i = 0; i < nd; ++i) {
+    q[2 * i] = 0;  // stable split (A wins ties)
+    q[2 * i + 1] = diags[i];
+  }
+  PM_CUDA(cudaMemcpyAsync(dtab, peer_keys, (size_t)world * sizeof(void*), cudaMemcpyHostToDevice, st));
+  PM_CUDA(cudaMemcpyAsync(dq, q.data(), q.size() * 8, cudaMemcpyHostToDevice, st));
+  const int64_t la = len_a, lb = N - len_a;
+  cudaError_t ce = key_bytes == 4 ? launch_peer_queries<int32_t>(dtab, block, la, lb, dq, nd, dout, st)
+                                  : launch_peer_queries<int64_t>(dtab, block, la, lb, dq, nd, dout, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "k_peer_queries launch");
+  PM_CUDA(cudaMemcpyAsync(out_a, dout, (size_t)nd * 8, cudaMemcpyDeviceToHost, st));
+  PM_CUDA(cudaStreamSynchronize(st));
+  return PM_OK;
+}
+
 int pm_merge_peers(pm_ctx* ctx, const void* const* peer_keys, const void* const* peer_payload, int world, int rank,
                    int64_t block, int64_t len_a, int key_bytes, int64_t width, void* out_keys, void* out_payload,
                    void* stream) {

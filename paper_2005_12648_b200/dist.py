@@ -8,9 +8,12 @@ with the GPUs as the partitions:
 
 1. **Global split points** (the median search of the reference, made stable):
    for every rank boundary diagonal d = off_r, the number of A records among
-   the first d outputs.  All G+1 searches run together as a 33-ary search;
-   each round all-reduces the 32 probe keys per diagonal that the owning ranks
-   contribute (about log_33 N rounds of a few-KB all-reduce).
+   the first d outputs.  On CUDA with equal blocks the ranks map each other's
+   blocks (CUDA IPC, cached) and one kernel launch runs every search over the
+   peer-pointer table (pm_peer_splits, dependent NVLink loads).  Otherwise (gloo,
+   CPU tensors, unequal blocks, PM_DIST_SPLITS=torch) all G+1 searches run
+   together as a 33-ary search; each round all-reduces the 32 probe keys per
+   diagonal that the owning ranks contribute (about log_33 N rounds).
 2. **Partition exchange**: rank r needs A[a_r, a_{r+1}) and B[b_r, b_{r+1});
    every rank's A part and B part are already ordered by destination, so two
    ``all_to_all_single`` calls (NCCL send/recv over NVLink) deliver rank r's
@@ -89,6 +92,12 @@ def clear_caches() -> None:
     """Release the captured split-search graphs and the mapped peer blocks."""
     _graphs.clear()
     _PEER_CACHE.clear()
+
+
+def _peer_splits_enabled() -> bool:
+    import os
+
+    return os.environ.get("PM_DIST_SPLITS", "peer") != "torch"
 
 
 def _graph_capture_enabled() -> bool:
@@ -182,7 +191,14 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
     for t in all_sizes:
         offsets.append(offsets[-1] + int(t.item()))
     la = global_len_a
-    a = global_splits(keys_local, offsets, la, group)
+    peers = None
+    if keys_local.is_cuda and world > 1 and _peer_splits_enabled() and len(set(offsets[i + 1] - offsets[i]
+                                                                                for i in range(world))) == 1:
+        try:  # the split search reads the peers' blocks directly (same box: CUDA IPC + NVLink)
+            peers = peer_blocks(keys_local, None, group)
+        except RuntimeError:
+            peers = None
+    a = global_splits_p2p(peers[0], offsets, la) if peers else global_splits(keys_local, offsets, la, group)
     b = [offsets[i] - a[i] for i in range(world + 1)]
     off = offsets[rank]
     # this block's A part [off, min(off+n, la)) and B part [max(off, la), off+n) in X coordinates
@@ -247,6 +263,40 @@ def _peer_view(meta, numel: int, dtype, shape_tail, elem_off: int) -> torch.Tens
     t = torch.empty(0, dtype=dtype, device=st.device)
     t.set_(st, elem_off, (numel, *shape_tail))
     return t
+
+
+def peer_blocks(keys_local: torch.Tensor, payload_local: torch.Tensor | None, group=None):
+    """Every rank's block mapped into this process (CUDA IPC storage sharing, cached):
+    ([keys blocks], [payload blocks]) in rank order; None unless all blocks are CUDA
+    tensors of equal length."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = keys_local.numel()
+    w = payload_local.shape[1] if payload_local is not None else 0
+    sizes = [None] * world
+    mine = (n, keys_local.untyped_storage()._share_cuda_(), keys_local.storage_offset(),
+            payload_local.untyped_storage()._share_cuda_() if w else None, payload_local.storage_offset() if w else 0)
+    dist.all_gather_object(sizes, mine, group=group)
+    if any(s[0] != n for s in sizes):
+        return None
+    pk, pp = [], []
+    for r, (_, mk, ok, mp, op) in enumerate(sizes):
+        if r == rank:
+            pk.append(keys_local)
+            pp.append(payload_local)
+        else:
+            pk.append(_peer_view(mk, n, keys_local.dtype, (), ok))
+            pp.append(_peer_view(mp, n, torch.uint8, (w,), op) if w else payload_local)
+    return pk, pp
+
+
+def global_splits_p2p(peer_keys: list, offsets: list[int], global_len_a: int) -> list[int]:
+    """global_splits through the peer-pointer table: one kernel launch of one-thread
+    stable merge-path searches reading the peers' blocks (pm_peer_splits), instead of
+    the probe rounds with an all-reduce each."""
+    from . import _ops
+
+    return _ops.peer_splits(peer_keys, global_len_a, offsets)
 
 
 def merge_distributed_p2p(keys_local: torch.Tensor, payload_local: torch.Tensor | None, global_len_a: int,
