@@ -204,3 +204,30 @@ def test_reorder_prescribed_layouts(width):
         _ops.reorder(arr, lo, lo + n, sizes)
         k, p = arr.numpy()
         assert np.array_equal(k, want_k) and np.array_equal(p, want_p), (n, t, width)
+
+
+@pytest.mark.parametrize("cfg", [4, 3, 2])
+def test_full_size_matches_reference_checksum(cfg):
+    """BASELINE configs 2/3/4 at FULL size (2^30 int32; 2^28 + 2^16 int64 skew; 2^27
+    key + index records) against sha256 checksums of the REFERENCE's own stable core
+    on the same seeded inputs (tests/golden/make_golden_full.py)."""
+    import hashlib
+
+    import golden_io
+    from gen import config_input
+
+    g = golden_io.load("big_full.npz")
+    keys, payload, middle = config_input(cfg, seed=0, log_len=29 if cfg == 2 else None)
+
+    def sha(*arrays):
+        h = hashlib.sha256()
+        for a in arrays:
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()
+
+    assert sha(keys, payload) == str(g[f"cfg{cfg}_in"]), "host generator drifted from the golden input"
+    arr = to_gpu(keys, payload)
+    del keys, payload
+    pm.merge_srecpar(arr, pm.MergeJob(0, middle, len(arr)), 8)
+    k, p = arr.numpy()
+    assert sha(k, p) == str(g[f"cfg{cfg}_out"])
