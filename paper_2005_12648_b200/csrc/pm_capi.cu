@@ -53,6 +53,7 @@ struct Ctl {
   Line32 err_;
   Line32 noop_;
   Line32 need_space_;
+  Line32 stage_gate_;  // staged path: the runs are out of order (k_order_gate)
 };
 
 
@@ -257,7 +258,8 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   int64_t M, T;
   int32_t mu;
   // the fallback behind the scheduled engine goes straight to the bounded-pool engine
-  const bool direct = gate != nullptr;
+  // (a gated copy-mode call is the staged path's merge, not a fallback)
+  const bool direct = gate != nullptr && !copy;
   // small in-place jobs: one CTA with both runs in shared memory
   if (mode == MODE_MERGE && !copy && !direct && !ctx->engine_only && small_merge_smem(ks, w, e - s) <= PM_SMALL_BYTES)
     return launch_merge_small_(ks, keys, payload, w, s, m, e, st);
@@ -283,10 +285,26 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
     uint8_t* sp = reinterpret_cast<uint8_t*>(static_cast<char*>(ctx->buf) + kb + (w ? (((uintptr_t)payload + s * w) & 15) : 0));
     char* k0 = static_cast<char*>(keys) + s * ks;
     uint8_t* p0 = w ? static_cast<uint8_t*>(payload) + s * w : nullptr;
-    rc = run_engine(ctx, k0, ks, p0, w, 0, m - s, n, MODE_MERGE, 0, st, sk, w ? sp : nullptr, nullptr, nullptr);
+    // runs already in order (srecpar.py:56-57): the device skips the merge and the
+    // copy back (the streaming pipeline's path; the wide-row path always runs)
+    int64_t Mt, Tt;
+    int32_t mut;
+    const bool gated = !(w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &Mt, &Tt, &mut)));
+    int32_t* gate = gated ? &ctx->ctl->stage_gate_.v : nullptr;
+    if (gated) {
+      cudaError_t ge = launch_order_gate(k0, ks, m - s, gate, st);
+      if (ge != cudaSuccess) return cuda_fail(ge, "k_order_gate launch");
+    }
+    rc = run_engine(ctx, k0, ks, p0, w, 0, m - s, n, MODE_MERGE, 0, st, sk, w ? sp : nullptr, nullptr, nullptr, gate);
     if (rc) return rc;
-    PM_CUDA(cudaMemcpyAsync(k0, sk, (size_t)(n * ks), cudaMemcpyDeviceToDevice, st));
-    if (w) PM_CUDA(cudaMemcpyAsync(p0, sp, (size_t)(n * w), cudaMemcpyDeviceToDevice, st));
+    if (gated) {
+      cudaError_t ce2 = launch_copy_gated(k0, sk, n * ks, gate, ctx->num_sms, st);
+      if (ce2 == cudaSuccess && w) ce2 = launch_copy_gated(p0, sp, n * w, gate, ctx->num_sms, st);
+      if (ce2 != cudaSuccess) return cuda_fail(ce2, "k_copy_gated launch");
+    } else {
+      PM_CUDA(cudaMemcpyAsync(k0, sk, (size_t)(n * ks), cudaMemcpyDeviceToDevice, st));
+      if (w) PM_CUDA(cudaMemcpyAsync(p0, sp, (size_t)(n * w), cudaMemcpyDeviceToDevice, st));
+    }
     return PM_OK;
   }
   if (mode == MODE_MERGE && w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &M, &T, &mu)))

@@ -1194,6 +1194,7 @@ __device__ __forceinline__ void buf_issue(const EngineParams& P, const BufRegion
 // only merge, so no round trip sits on the merge's critical path.
 template <typename KT>
 __global__ void __launch_bounds__(kBufferedThreads) k_buffered(EngineParams P, int32_t buf_a) {
+  if (P.gate && !*(volatile const int32_t*)P.gate) return;  // (staged path: the runs are already in order)
   constexpr int NS = kBufStages;
   extern __shared__ __align__(128) uint8_t dyn[];
   __shared__ uint64_t bar[NS];
@@ -1429,6 +1430,40 @@ __global__ void __launch_bounds__(1024) k_compact(EngineParams P) {
     __syncthreads();
   }
   if (tid == 0) *P.ntick = base;
+}
+
+// ---- staged path helpers: skip the whole pass when the runs are already in order ----
+// gate = 1 iff A[m-1] > B[0] (srecpar.py:56-57: otherwise nothing moves)
+template <typename KT>
+__global__ void k_order_gate(const KT* keys, int64_t m, int32_t* gate) {
+  *gate = keys[m - 1] > keys[m] ? 1 : 0;
+}
+// dst <- src (n bytes, identical 16-byte phase), only if *gate
+__global__ void __launch_bounds__(256) k_copy_gated(uint8_t* dst, const uint8_t* src, int64_t n, const int32_t* gate) {
+  if (!*(volatile const int32_t*)gate) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+  if (head > n) head = n;
+  const int64_t nv = (n - head) >> 4;
+  for (int64_t b = tid; b < head; b += nthr) dst[b] = src[b];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (int64_t i = tid; i < nv; i += nthr) d4[i] = __ldcs(s4 + i);
+  for (int64_t b = head + (nv << 4) + tid; b < n; b += nthr) dst[b] = src[b];
+}
+
+cudaError_t launch_order_gate(const void* keys, int ks, int64_t m, int32_t* gate, cudaStream_t st) {
+  if (ks == 4) k_order_gate<int32_t><<<1, 1, 0, st>>>(static_cast<const int32_t*>(keys), m, gate);
+  else k_order_gate<int64_t><<<1, 1, 0, st>>>(static_cast<const int64_t*>(keys), m, gate);
+  count_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32_t* gate, int num_sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((n / 16 + 255) / 256 + 1, (int64_t)num_sms * 8);
+  k_copy_gated<<<grid, 256, 0, st>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n, gate);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 // ---- host launchers (called from pm_capi.cu) --------------------------------

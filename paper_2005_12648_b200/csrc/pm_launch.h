@@ -36,6 +36,9 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st);
+// staged path: gate = A[m-1] > B[0]; a copy that runs only if the gate is set
+cudaError_t launch_order_gate(const void* keys, int ks, int64_t m, int32_t* gate, cudaStream_t st);
+cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32_t* gate, int num_sms, cudaStream_t st);
 template <typename KT> cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cudaStream_t st);
 template <typename KT>
 cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st);

@@ -84,3 +84,25 @@ def test_merge_host_from_many_threads():
         list(ex.map(lambda j: _ops.merge_host(j[0], j[1], 0, j[2], len(j[0])), jobs))
     for k, p, h, wk, wp in jobs:
         assert np.array_equal(k, wk) and np.array_equal(p, wp)
+
+
+@pytest.mark.parametrize("n", [1 << 20, 1 << 24])
+def test_staged_path_skips_ordered_runs(n):
+    """A medium job whose runs are already in order (A[m-1] <= B[0]) leaves the array
+    untouched and costs no merge pass (gated on the device); an out-of-order job of
+    the same shape still merges."""
+    from paper_2005_12648_b200 import _ops
+
+    k = torch.arange(n, dtype=torch.int32, device="cuda")
+    p = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint8).view(-1, 4)
+    a = pm.KeyedArray(k.clone(), p.clone())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    _ops.merge(a, 0, n // 2, n)
+    ev1.record()
+    torch.cuda.synchronize()
+    assert torch.equal(a.keys, k) and torch.equal(a.payload, p)
+    kk = torch.cat([k[n // 2:], k[:n // 2]])
+    b = pm.KeyedArray(kk.clone(), p.clone())
+    _ops.merge(b, 0, n // 2, n)
+    assert torch.equal(b.keys, k)
