@@ -58,8 +58,11 @@ int pm_ctx_destroy(pm_ctx *ctx);
  * _kernels.py:227-313), seq_merge_rotation (_kernels.py:201-223) and
  * merge_srecpar(threads=1) (srecpar.py:33-60).  Replaces the partition + shift
  * + leaf-merge pipeline of merge_srecpar / merge_soptmov (srecpar.py:63-84,
- * soptmov.py:195-240).  `scratch_records` is a lower bound on the bounded
- * salvage pool (0 = default, O(grid * tile)).
+ * soptmov.py:195-240).  `scratch_records` is the caller's scratch budget in
+ * records: 0 = the library default (the scheduled engine may salvage up to N/4
+ * records into its pool); > 0 caps that pool -- a job whose planned salvage does
+ * not fit runs the bounded-pool engine instead (decided on the device), whose
+ * own pool is at least `scratch_records` records.
  */
 int pm_merge(pm_ctx *ctx, void *keys, int key_bytes, void *payload, int64_t width,
              int64_t start, int64_t middle, int64_t end, int64_t scratch_records, void *stream);

@@ -248,7 +248,8 @@ static int run_wide(pm_ctx* ctx, char* keys, int ks, uint8_t* pay, int64_t w, in
 // out[s,e) (the streaming pipeline of the buffered mode, nothing overlaps).
 // keys_b / pay_b (copy mode only): the B run lives there instead of at keys + m.
 static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                    cudaStream_t st, const int64_t* leaf_sizes = nullptr, int32_t nleaves = 0);
+                    cudaStream_t st, const int64_t* leaf_sizes = nullptr, int32_t nleaves = 0,
+                    int64_t scratch_records = 0);
 
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys, void* out_payload,
@@ -318,7 +319,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #endif
   // the scheduled engine (pm_flow.cu) for in-place merges
   if (mode == MODE_MERGE && !copy && !direct && ctx->flow_mode != 0)
-    return run_flow(ctx, keys, ks, payload, w, s, m, e, st);
+    return run_flow(ctx, keys, ks, payload, w, s, m, e, st, nullptr, 0, scratch_records);
   const bool buffered = copy || (!direct && PM_USE_BUFFERED && mode == MODE_MERGE && scratch_records >= std::min(m - s, e - m));
   // (the engine stages one input and one output tile; the buffered pipeline
   //  kBufStages inputs and two outputs)
@@ -475,11 +476,14 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 // behind it on the device: it runs only if the plan's salvage exceeds the pool
 // (FC_FAIL), so the whole call stays asynchronous.
 static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
-                    cudaStream_t st, const int64_t* leaf_sizes, int32_t nleaves) {
+                    cudaStream_t st, const int64_t* leaf_sizes, int32_t nleaves, int64_t scratch_records) {
   int64_t M, T;
   int32_t mu;
   // regions: the largest power of two <= 8192 records whose keys + rows fit a tile
-  M = 8192;
+#ifndef PM_FLOW_MAXM
+#define PM_FLOW_MAXM 8192  // tune: largest scheduled-engine region (records)
+#endif
+  M = PM_FLOW_MAXM;
   while (M > 16 && M * (ks + w) > PM_FLOW_TILE) M >>= 1;
   if (M * (ks + w) > PM_FLOW_TILE) return fail(PM_ERR_UNSUPPORTED, "payload rows too wide for the staging tiles");
   T = M;
@@ -585,8 +589,10 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.force = ctx->flow_mode == 2 ? 0 : ctx->flow_mode == 3 ? 1 : ctx->flow_mode == 4 ? 2 : -1;
   // salvage pool, phase matched to the caller's (16-byte aligned) arrays
   const int64_t n = e - s;
-  // a prescribed layout has no fallback engine: its pool holds any salvage (<= every slot)
-  F.pool_cap = nleaves ? n + 32 * T + 16 * K : n / PM_FLOW_POOL_DIV + 32 * T;
+  // a prescribed layout has no fallback engine: its pool holds any salvage (<= every slot);
+  // otherwise the caller's budget (scratch_records > 0) or the default N / PM_FLOW_POOL_DIV
+  F.pool_cap = nleaves ? n + 32 * T + 16 * K
+                       : scratch_records > 0 ? scratch_records : n / PM_FLOW_POOL_DIV + 32 * T;
   const size_t pk = (size_t)align_up(F.pool_cap * ks + 16, 256);
   rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w + 16 : 0));
   if (rc) return rc;
@@ -611,8 +617,8 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
     ctx->ev_recorded = true;
   }
   // the bounded-pool engine, gated on the plan's overflow word
-    return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, 0, st, nullptr, nullptr, nullptr, nullptr,
-                    reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
+    return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, scratch_records, st, nullptr, nullptr, nullptr,
+                    nullptr, reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
 }
 
 static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* payload, int64_t w) {
