@@ -910,6 +910,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
   __shared__ int64_t s_t[NS];
   __shared__ FlowDesc s_d[NS];
   __shared__ int32_t s_early[NS];
+  __shared__ FlowTicket s_next;  // the leader's prefetched ticket (in shared memory: no registers for all threads)
   const EngineParams& P = F.P;
   FlowGeo g(P);
   constexpr int NT = kFlowThreads;
@@ -925,7 +926,6 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
 #define STAGE(b) (dyn + (size_t)(b) * tile)
 #define OUTB(b) (dyn + (size_t)(NS + (b)) * tile)
   int64_t t_next = ntick;  // leader: the next ticket to issue, its descriptor loaded ahead
-  FlowTicket T_next;
   if (leader) {
     for (int k = 0; k < NS; ++k) {
       mbar_init(&bar[k], 1);
@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
       flow_issue<KT>(F, g, load_ticket(F.tk + t0), s_d[k], STAGE(k), STAGE(k) + P.smem_keys, &bar[k]);
     }
     t_next = atomicAdd(P.ticket, 1);
-    if (t_next < ntick) T_next = load_ticket(F.tk + t_next);
+    if (t_next < ntick) s_next = load_ticket(F.tk + t_next);
     else t_next = ntick;
   }
   __syncthreads();
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
     const int cur = it % NS, ob = kFlowOut == 2 ? (it & 1) : 0;
     const int64_t t = s_t[cur];
     if (t >= ntick) break;
-    const FlowDesc R = s_d[cur];
+    const FlowDesc& R = s_d[cur];  // (read in place: the leader rewrites it only after the next barrier)
     int32_t pv = 0;
     if (leader) {
       pv = ld_relaxed(&F.pend[R.r]);  // first poll of this region's store condition, in flight now
@@ -959,9 +959,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
       s_t[nx] = tn;
       s_early[nx] = 0;
       if (tn < ntick) {
-        flow_issue<KT>(F, g, T_next, s_d[nx], STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
+        flow_issue<KT>(F, g, s_next, s_d[nx], STAGE(nx), STAGE(nx) + P.smem_keys, &bar[nx]);
         t_next = atomicAdd(P.ticket, 1);
-        if (t_next < ntick) T_next = load_ticket(F.tk + t_next);  // used next iteration
+        if (t_next < ntick) s_next = load_ticket(F.tk + t_next);  // used next iteration
         else t_next = ntick;
       }
     }
