@@ -60,6 +60,7 @@
 #include "pm_tile.cuh"
 
 #include <cooperative_groups.h>
+#include <nvtx3/nvToolsExt.h>
 namespace cg = cooperative_groups;
 
 namespace pm {
@@ -1060,6 +1061,11 @@ cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
 
 // plan kernels (after launch_plan's splits); ev (may be null) is recorded between
 // the plan and the merge
+struct NvtxRange {
+  explicit NvtxRange(const char* what) { nvtxRangePushA(what); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename KT>
 cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev,
                         cudaEvent_t ev_merge) {
@@ -1069,6 +1075,8 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   if (bps < 1) return cudaErrorInvalidConfiguration;
   FlowParams Fa = F;
   void* args[] = {&Fa};
+  // NVTX phase ranges (host-side enqueue spans; nsys correlates them with the kernels)
+  NvtxRange r_all("pm_merge: scheduled engine");
   e = cudaLaunchCooperativeKernel((const void*)k_flow_plan<KT>, dim3(num_sms * std::min(bps, 2)), dim3(kFlowChunk), args,
                                   0, st);
   if (e != cudaSuccess) return e;
@@ -1077,14 +1085,20 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
     e = cudaEventRecord(ev, st);
     if (e != cudaSuccess) return e;
   }
-  k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
+  {
+    NvtxRange r("pm_flow: salvage copy");
+    k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
+  }
   e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (ev_merge) {
     e = cudaEventRecord(ev_merge, st);
     if (e != cudaSuccess) return e;
   }
-  k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
+  {
+    NvtxRange r("pm_flow: merge");
+    k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
+  }
   count_launches(2);
 
   return cudaGetLastError();

@@ -178,6 +178,9 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
     if timed:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         evs[0].record()
+    nvtx = keys_local.is_cuda
+    if nvtx:  # NVTX phase ranges: split search / exchange / local merge
+        torch.cuda.nvtx.range_push("dist: global splits")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = keys_local.device
@@ -219,6 +222,9 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
     split_at = max(0, min(n, la - off))
     out_k = torch.empty_like(keys_local)
     out_p = torch.empty_like(payload_local)
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_push("dist: exchange (NCCL all-to-all)")
     if timed:
         evs[1].record()
         rec = keys_local.element_size() + payload_local.shape[1]
@@ -230,6 +236,9 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
         dist.all_to_all_single(out_p[na:], payload_local[split_at:].contiguous(), recv_b, send_b, group=group)
     if timed:
         evs[2].record()
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_push("dist: local merge")
     if local_merge is None:
         _default_local_merge(out_k, out_p, na, keys_local, payload_local)
         if timed:
@@ -239,6 +248,8 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
         local_merge(out_k, out_p, na)
         keys_local.copy_(out_k)
         payload_local.copy_(out_p)
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
     return keys_local, payload_local
 
 
