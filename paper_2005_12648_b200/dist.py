@@ -199,6 +199,8 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
                                                                                 for i in range(world))) == 1:
         try:  # the split search reads the peers' blocks directly (same box: CUDA IPC + NVLink)
             peers = peer_blocks(keys_local, None, group)
+            if peers and not _all_peers_reachable(peers[0], keys_local.device):
+                peers = None
         except RuntimeError:
             peers = None
     a = global_splits_p2p(peers[0], offsets, la) if peers else global_splits(keys_local, offsets, la, group)
@@ -299,6 +301,12 @@ def peer_blocks(keys_local: torch.Tensor, payload_local: torch.Tensor | None, gr
             pk.append(_peer_view(mk, n, keys_local.dtype, (), ok))
             pp.append(_peer_view(mp, n, torch.uint8, (w,), op) if w else payload_local)
     return pk, pp
+
+
+def _all_peers_reachable(peer_keys: list, device) -> bool:
+    """Every mapped block lives on this device or on one it can read directly (P2P)."""
+    here = device.index
+    return all(t.device.index == here or torch.cuda.can_device_access_peer(here, t.device.index) for t in peer_keys)
 
 
 def global_splits_p2p(peer_keys: list, offsets: list[int], global_len_a: int) -> list[int]:
