@@ -91,6 +91,7 @@ _PEER_CAP = 64
 def clear_caches() -> None:
     """Release the captured split-search graphs and the mapped peer blocks."""
     _graphs.clear()
+    _PEER_TABLES.clear()
     _PEER_CACHE.clear()
 
 
@@ -260,6 +261,7 @@ def merge_distributed(keys_local: torch.Tensor, payload_local: torch.Tensor | No
 # access) and pm_merge_peers streams its A and B pieces straight out of peer memory into a
 # staging block -- no all-to-all pass, no send/receive copies.
 _PEER_CACHE: OrderedDict = OrderedDict()
+_PEER_TABLES: dict = {}  # group -> (this rank's buffer key, the mapped table)
 
 
 def _peer_view(meta, numel: int, dtype, shape_tail, elem_off: int) -> torch.Tensor:
@@ -286,11 +288,20 @@ def peer_blocks(keys_local: torch.Tensor, payload_local: torch.Tensor | None, gr
     rank = dist.get_rank(group)
     n = keys_local.numel()
     w = payload_local.shape[1] if payload_local is not None else 0
+    # the table is exchanged once per set of buffers: later calls only agree (one tiny
+    # all-reduce) that no rank's buffers changed
+    my_key = (keys_local.data_ptr(), n, payload_local.data_ptr() if w else 0, w)
+    cached = _PEER_TABLES.get(id(group))
+    changed = torch.tensor([0 if cached is not None and cached[0] == my_key else 1], device=keys_local.device)
+    dist.all_reduce(changed, op=dist.ReduceOp.MAX, group=group)
+    if not int(changed.item()):
+        return cached[1]
     sizes = [None] * world
     mine = (n, keys_local.untyped_storage()._share_cuda_(), keys_local.storage_offset(),
             payload_local.untyped_storage()._share_cuda_() if w else None, payload_local.storage_offset() if w else 0)
     dist.all_gather_object(sizes, mine, group=group)
     if any(s[0] != n for s in sizes):
+        _PEER_TABLES.pop(id(group), None)
         return None
     pk, pp = [], []
     for r, (_, mk, ok, mp, op) in enumerate(sizes):
@@ -300,6 +311,7 @@ def peer_blocks(keys_local: torch.Tensor, payload_local: torch.Tensor | None, gr
         else:
             pk.append(_peer_view(mk, n, keys_local.dtype, (), ok))
             pp.append(_peer_view(mp, n, torch.uint8, (w,), op) if w else payload_local)
+    _PEER_TABLES[id(group)] = (my_key, (pk, pp))
     return pk, pp
 
 
