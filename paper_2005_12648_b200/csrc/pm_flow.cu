@@ -1077,7 +1077,14 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   void* args[] = {&Fa};
   // NVTX phase ranges (host-side enqueue spans; nsys correlates them with the kernels)
   NvtxRange r_all("pm_merge: scheduled engine");
-  e = cudaLaunchCooperativeKernel((const void*)k_flow_plan<KT>, dim3(num_sms * std::min(bps, 2)), dim3(kFlowChunk), args,
+  // plan grid sized to the job (grid barriers over fewer CTAs are cheaper; every phase
+  // strides over its items): ~PM_FLOW_PLAN_PER regions per CTA, at most every SM
+#ifndef PM_FLOW_PLAN_PER
+#define PM_FLOW_PLAN_PER 256
+#endif
+  const int pgrid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)num_sms * std::min(bps, 2), (F.P.Q + PM_FLOW_PLAN_PER - 1) / PM_FLOW_PLAN_PER));
+  e = cudaLaunchCooperativeKernel((const void*)k_flow_plan<KT>, dim3(pgrid), dim3(kFlowChunk), args,
                                   0, st);
   if (e != cudaSuccess) return e;
   count_launches(1);
