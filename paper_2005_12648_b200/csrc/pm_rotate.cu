@@ -11,6 +11,7 @@
 
 #include "pm_common.cuh"
 #include "pm_launch.h"
+#include "pm_tile.cuh"
 
 namespace pm {
 
@@ -228,89 +229,122 @@ static void reverse_wide_pair(KT* k, uint8_t* p, int64_t w, int64_t lo, int64_t 
 
 // ---- one-pass block exchange when one block is small (the reference's staged
 // exchange, _kernels.py:46-90, for blocks of up to PM_SLIDE_STASH bytes) ----
+constexpr int kSlideTile = 32768;
+constexpr int kSlideThreads = 256;
+constexpr int kSlideStages = 2;
+
+// Aligned 16-byte destination chunks [c0, c0 + 16 nc) from the staged source image:
+// destination byte x reads stage byte x + dlt, and dlt's 16-byte phase is the same
+// for every chunk (Q words + S bits).  Two conflict-free 16-byte shared loads per
+// chunk and a funnel shift realign it.
+template <int Q>
+__device__ __forceinline__ void slide_chunks(uint8_t* dst, const uint8_t* src, int64_t nc, int sh) {
+  for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    const uint4* q = reinterpret_cast<const uint4*>(src + c * 16);
+    uint4 v;
+    if (Q == 0 && sh == 0) {
+      v = q[0];
+    } else {
+      const uint4 a = q[0], b = q[1];
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      v = make_uint4(__funnelshift_r(w[Q], w[Q + 1], sh), __funnelshift_r(w[Q + 1], w[Q + 2], sh),
+                     __funnelshift_r(w[Q + 2], w[Q + 3], sh), __funnelshift_r(w[Q + 3], w[Q + 4], sh));
+    }
+    __stcs(reinterpret_cast<uint4*>(dst + c * 16), v);
+  }
+}
+
+// One tile's destination bytes [d0, d1) from its staged source: stage byte of
+// destination x is x + dlt.  Aligned 16-byte chunks, bytewise at the range edges.
+__device__ __forceinline__ void slide_store(uint8_t* plane, const uint8_t* tile, int64_t d0, int64_t d1, int64_t dlt) {
+  const uintptr_t c0 = ((uintptr_t)(plane + d0) + 15) & ~(uintptr_t)15;
+  const uintptr_t c1 = (uintptr_t)(plane + d1) & ~(uintptr_t)15;
+  if (c1 > c0) {
+    const int64_t x0 = (int64_t)(c0 - (uintptr_t)plane), nc = (int64_t)((c1 - c0) >> 4);
+    const int64_t so = x0 + dlt;  // stage offset of the first chunk's source
+    const int r = (int)(so & 15), sh = (r & 3) * 8;
+    const uint8_t* src = tile + (so - r);
+    switch (r >> 2) {
+      case 0: slide_chunks<0>(plane + x0, src, nc, sh); break;
+      case 1: slide_chunks<1>(plane + x0, src, nc, sh); break;
+      case 2: slide_chunks<2>(plane + x0, src, nc, sh); break;
+      default: slide_chunks<3>(plane + x0, src, nc, sh); break;
+    }
+    const int64_t h = (int64_t)(c0 - (uintptr_t)(plane + d0)), tl = (int64_t)((uintptr_t)(plane + d1) - c1);
+    for (int64_t bt = threadIdx.x; bt < h + tl; bt += blockDim.x) {
+      const int64_t x = bt < h ? d0 + bt : (int64_t)(c1 - (uintptr_t)plane) + (bt - h);
+      plane[x] = tile[x + dlt];
+    }
+  } else {
+    for (int64_t x = d0 + threadIdx.x; x < d1; x += blockDim.x) plane[x] = tile[x + dlt];
+  }
+}
+
 // The small block is stashed (stream-ordered copies on the host side), the big
 // block slides over it in one pass, the stash lands at the far end.  The slide
 // is an overlapping move: plane bytes [S0, S0+L) move by -D (left) or +D
 // (right).  A persistent grid claims kSlideTile-byte source tiles in the
-// direction of the move (ascending for left), stages a tile in shared memory,
-// publishes "read" for it, waits until every earlier-claimed tile whose source
-// the tile's destination overlaps has been read, then writes the destination
-// (16-byte stores; bytewise at the range edges).  Waits only ever target tiles
-// claimed earlier by resident CTAs, so they always resolve.
-constexpr int kSlideTile = 32768;
-constexpr int kSlideThreads = 256;
-
+// direction of the move (ascending for left); each CTA keeps kSlideStages tiles in
+// flight: the TMA bulk load of its next tile lands while it stores the current one.
+// A landed tile publishes "read"; before storing, a tile waits until every
+// earlier-claimed tile whose source its destination overlaps has been read.  Waits
+// only ever target tiles claimed earlier (whose loads were issued at claim time),
+// so they always resolve.
 __global__ void __launch_bounds__(kSlideThreads) k_slide(uint8_t* plane, int64_t S0, int64_t L, int64_t D, int right,
                                                          int32_t* flags, int32_t* ticket, int32_t* err) {
-  __shared__ __align__(16) uint8_t tile[kSlideTile + 32];
-  __shared__ int64_t s_i;
+  extern __shared__ __align__(128) uint8_t sdyn[];
+  __shared__ uint64_t bar[kSlideStages];
+  __shared__ int64_t s_i[kSlideStages];
   const int64_t ntiles = (L + kSlideTile - 1) / kSlideTile;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const int64_t t = atomicAdd(ticket, 1);
-      s_i = t < ntiles ? (right ? ntiles - 1 - t : t) : -1;
+  constexpr size_t kStage = kSlideTile + 64;
+  auto issue = [&](int stg) {  // thread 0: claim the next tile, TMA-load its 16-byte-aligned superset
+    const int64_t t = atomicAdd(ticket, 1);
+    const int64_t i = t < ntiles ? (right ? ntiles - 1 - t : t) : -1;
+    s_i[stg] = i;
+    if (i >= 0) {
+      const int64_t s0 = S0 + i * kSlideTile, s1 = min(S0 + L, s0 + kSlideTile);
+      copy_g2s_superset(sdyn + stg * kStage + (((uintptr_t)(plane + s0)) & 15), plane + s0, s1 - s0, &bar[stg]);
     }
-    __syncthreads();
-    const int64_t i = s_i;
-    __syncthreads();
+    mbar_arrive(&bar[stg]);
+  };
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kSlideStages; ++k) mbar_init(&bar[k], 1);
+    for (int k = 0; k < kSlideStages; ++k) issue(k);
+  }
+  __syncthreads();
+  uint32_t ph = 0;
+  for (int it = 0;; ++it) {
+    const int cur = it % kSlideStages;
+    while (!mbar_try_wait(&bar[cur], (ph >> cur) & 1)) {
+    }
+    ph ^= 1u << cur;
+    const int64_t i = s_i[cur];
     if (i < 0) break;
+    if (threadIdx.x == 0) st_release(&flags[i], 1);  // this tile's source is read (it landed)
     const int64_t s0 = S0 + i * kSlideTile, s1 = min(S0 + L, s0 + kSlideTile);
-    // stage the 16-byte-aligned superset of [s0, s1)
-    const uintptr_t sb = (uintptr_t)(plane + s0) & ~(uintptr_t)15;
-    const uintptr_t se = ((uintptr_t)(plane + s1) + 15) & ~(uintptr_t)15;
-    const int nv = (int)((se - sb) >> 4);
-    for (int v = threadIdx.x; v < nv; v += blockDim.x)
-      reinterpret_cast<uint4*>(tile)[v] = __ldcs(reinterpret_cast<const uint4*>(sb) + v);
-    __syncthreads();
-    if (threadIdx.x == 0) st_release(&flags[i], 1);  // this tile's source is read
-    // source tiles the destination overlaps (other than i): wait until read
     const int64_t d0 = right ? s0 + D : s0 - D, d1 = right ? s1 + D : s1 - D;
     const int64_t lo = max(d0, S0), hi = min(d1, S0 + L);  // the part over the big block's source
     if (hi > lo) {
       const int64_t j0 = (lo - S0) / kSlideTile, j1 = (hi - 1 - S0) / kSlideTile;
       for (int64_t j = j0 + threadIdx.x; j <= j1; j += blockDim.x) {
         if (j == i) continue;
-        for (uint32_t it = 0; ld_acquire(&flags[j]) == 0; ++it) {
-          if (it > kSpinLimit) {
+        for (uint32_t w = 0; ld_acquire(&flags[j]) == 0; ++w) {
+          if (w > kSpinLimit) {
             raise_error(err, PM_ERR_TIMEOUT);
             break;
           }
-          backoff(it);
+          backoff(w);
         }
       }
     }
     __syncthreads();
-    // destination [d0, d1): aligned 16-byte chunks from the staged bytes at +/-D
-    const int64_t shift = right ? -D : D;  // smem byte for destination x: x + shift - (sb - plane)
-    const int64_t base = (int64_t)(sb - (uintptr_t)plane);
-    const uintptr_t c0 = ((uintptr_t)(plane + d0) + 15) & ~(uintptr_t)15;
-    const uintptr_t c1 = (uintptr_t)(plane + d1) & ~(uintptr_t)15;
-    const bool w4 = (D & 3) == 0;
-    if (c1 > c0) {
-      const int64_t nc = (int64_t)((c1 - c0) >> 4);
-      for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) {
-        const int64_t x = (int64_t)(c0 - (uintptr_t)plane) + c * 16;  // plane offset of the chunk
-        const int64_t off = x + shift - base;
-        uint4 v;
-        if (w4) {
-          const uint32_t* q = reinterpret_cast<const uint32_t*>(tile + off);
-          v = make_uint4(q[0], q[1], q[2], q[3]);
-        } else {
-          uint8_t* b = reinterpret_cast<uint8_t*>(&v);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) b[k] = tile[off + k];
-        }
-        *reinterpret_cast<uint4*>(plane + x) = v;
-      }
-      // unaligned head [d0, c0) and tail [c1, d1)
-      const int64_t h = (int64_t)(c0 - (uintptr_t)(plane + d0)), tl = (int64_t)((uintptr_t)(plane + d1) - c1);
-      for (int64_t b = threadIdx.x; b < h + tl; b += blockDim.x) {
-        const int64_t x = b < h ? d0 + b : (int64_t)(c1 - (uintptr_t)plane) + (b - h);
-        plane[x] = tile[x + shift - base];
-      }
-    } else {
-      for (int64_t x = d0 + threadIdx.x; x < d1; x += blockDim.x) plane[x] = tile[x + shift - base];
-    }
+    const uint8_t* tile = sdyn + cur * kStage;
+    // the stage holds the source's 16-byte-aligned superset from stage byte 0: plane byte x
+    // sits at stage byte x - sbase
+    const int64_t sbase = (int64_t)(((uintptr_t)(plane + s0)) & ~(uintptr_t)15) - (int64_t)(uintptr_t)plane;
+    slide_store(plane, tile, d0, d1, (right ? -D : D) - sbase);
+    __syncthreads();  // the stage is free
+    if (threadIdx.x == 0) issue(cur);
   }
 }
 
@@ -322,8 +356,11 @@ cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool rig
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(ticket, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms * 6);
-  k_slide<<<grid, kSlideThreads, 0, st>>>(static_cast<uint8_t*>(plane), S0, L, D, right ? 1 : 0, flags, ticket, err);
+  const size_t smem = kSlideStages * (kSlideTile + 64);
+  e = cudaFuncSetAttribute(k_slide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms * 3);
+  k_slide<<<grid, kSlideThreads, smem, st>>>(static_cast<uint8_t*>(plane), S0, L, D, right ? 1 : 0, flags, ticket, err);
   count_launches(1);
   return cudaGetLastError();
 }
