@@ -190,26 +190,38 @@ static int launch_merge_small_(int ks, void* keys, void* payload, int64_t w, int
 #ifndef PM_WIDE_MIN
 #define PM_WIDE_MIN 256  // tune: bytes per payload row from which the wide path runs
 #endif
+#ifndef PM_FLOW_WIDE_MAX
+#define PM_FLOW_WIDE_MAX 2048  // tune: bytes per record up to which in-place wide rows take the scheduled engine
+#endif
 #ifndef PM_WIDE_SAVE_BYTES
 #define PM_WIDE_SAVE_BYTES (256ll << 20)  // bound on the saved cut rows (G grows past 16 to respect it)
 #endif
 // In-place row permutation new_row[p] = old_row[idx[p]] (idx: DEVICE int32[n], a
 // permutation of [0, n)), cycles cut every G rows (pm_wide.cu).
+#ifndef PM_CYC_LMAX
+#define PM_CYC_LMAX 32  // tune: longest chain of the cycle walk (longer segments get extra cuts)
+#endif
 static int permute_rows(pm_ctx* ctx, uint8_t* pay, int64_t w, const int32_t* idx, int64_t n, int32_t G,
                         cudaStream_t st) {
   const int64_t ncut = (n + G - 1) / G;
+  // extra cuts: at most one per Lmax positions, and within the save budget
+  const int32_t Lmax = PM_CYC_LMAX;
+  const int64_t xcap = std::max<int64_t>(1, std::min<int64_t>(n / Lmax + 1, PM_WIDE_SAVE_BYTES / w));
   const size_t o_d1 = (size_t)align_up(n * 8, 256);
   const size_t o_heads = o_d1 + (size_t)align_up(n * 8, 256);
-  const size_t o_unres = o_heads + (size_t)align_up(n * 4, 256);
-  const size_t o_ctl = o_unres + (size_t)align_up(n, 256);
+  const size_t o_unres = o_heads + (size_t)align_up(n * 8, 256);
+  const size_t o_segs = o_unres + (size_t)align_up(n, 256);
+  const size_t o_xpos = o_segs + (size_t)align_up((ncut + xcap) * 16, 256);
+  const size_t o_ctl = o_xpos + (size_t)align_up(xcap * 4, 256);
   const size_t o_save = o_ctl + 256;
-  int rc = ensure(&ctx->wperm, &ctx->wperm_bytes, o_save + (size_t)(ncut * w));
+  int rc = ensure(&ctx->wperm, &ctx->wperm_bytes, o_save + (size_t)((ncut + xcap) * w));
   if (rc) return rc;
   char* base = static_cast<char*>(ctx->wperm);
   cudaError_t ce = launch_cycle_permute(pay, w, idx, n, G, reinterpret_cast<int2*>(base), reinterpret_cast<int2*>(base + o_d1),
-                                        reinterpret_cast<int32_t*>(base + o_heads), reinterpret_cast<int32_t*>(base + o_ctl),
-                                        reinterpret_cast<uint8_t*>(base + o_unres), reinterpret_cast<uint8_t*>(base + o_save),
-                                        ctx->num_sms, st);
+                                        reinterpret_cast<int2*>(base + o_heads), reinterpret_cast<int32_t*>(base + o_ctl),
+                                        reinterpret_cast<uint8_t*>(base + o_unres), reinterpret_cast<int4*>(base + o_segs),
+                                        reinterpret_cast<int32_t*>(base + o_xpos), (int32_t)xcap, Lmax,
+                                        reinterpret_cast<uint8_t*>(base + o_save), ctx->num_sms, st);
   return ce == cudaSuccess ? PM_OK : cuda_fail(ce, "cycle permutation launch");
 }
 
@@ -308,7 +320,14 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
     }
     return PM_OK;
   }
-  if (mode == MODE_MERGE && w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &M, &T, &mu)))
+  // in-place wide rows of up to PM_FLOW_WIDE_MAX bytes per record take the scheduled
+  // engine (tiles of >= 16 records read and written sequentially beat the cycle
+  // walk's random rows: 1.17 vs 1.55 ms at 508-byte rows, 2 GB); its device-side
+  // fallback is the bounded-pool engine, never the (ungated) wide path
+  const bool wide = mode == MODE_MERGE && w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &M, &T, &mu));
+  const bool flow_wide = wide && !copy && !ctx->engine_only && ctx->flow_mode != 0 && ks + w <= PM_FLOW_WIDE_MAX &&
+                         pick_tiles(ks, w, kTileBudget, &M, &T, &mu);
+  if (wide && !flow_wide)
     return run_wide(ctx, static_cast<char*>(keys), ks, static_cast<uint8_t*>(payload), w, s, m, e, st,
                     static_cast<char*>(out_keys), static_cast<uint8_t*>(out_payload),
                     static_cast<const char*>(keys_b), static_cast<const uint8_t*>(pay_b));

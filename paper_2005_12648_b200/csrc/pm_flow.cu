@@ -1019,7 +1019,12 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
           named_barrier_sync(1, MT);
         }
         const bool wq4 = w && (w & 3) == 0 && ((php | R.poffA | R.poffB) & 3) == 0;
-        if (!(PM_FLOW_ABLATE & 2))
+        if (wq4 && w >= kWideRow)
+          merge_tile_wide<KT, kFlowThreads - 32>(reinterpret_cast<const KT*>(kin + R.offA),
+                                                 reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
+                                                 reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,
+                                                 pin + R.poffB, w, tid, 1);
+        else if (!(PM_FLOW_ABLATE & 2))
           merge_tile<KT, kFlowThreads - 32>(MODE_MERGE, reinterpret_cast<const KT*>(kin + R.offA),
                                             reinterpret_cast<const KT*>(kin + R.offB), R.alpha, R.beta, R.nout,
                                             reinterpret_cast<KT*>(kout_s + phk), pout_s + php, pin + R.poffA,

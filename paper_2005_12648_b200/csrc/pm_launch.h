@@ -55,8 +55,8 @@ cudaError_t launch_iota(int32_t* idx, int64_t n, int num_sms, cudaStream_t st);
 cudaError_t launch_gather_rows(uint8_t* out, const uint8_t* a, const uint8_t* b, const int32_t* idx, int64_t n,
                                int64_t la, int64_t w, int num_sms, cudaStream_t st);
 cudaError_t launch_cycle_permute(uint8_t* pay, int64_t w, const int32_t* idx, int64_t n, int32_t G, int2* dbl0,
-                                 int2* dbl1, int32_t* heads, int32_t* ctl, uint8_t* unres, uint8_t* save, int num_sms,
-                                 cudaStream_t st);
+                                 int2* dbl1, int2* heads, int32_t* ctl, uint8_t* unres, int4* segs, int32_t* xpos,
+                                 int32_t xcap, int32_t Lmax, uint8_t* save, int num_sms, cudaStream_t st);
 // one-pass overlapping move of a byte plane by D bytes (pm_rotate.cu); flags: one int32 per 32 KB tile
 cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool right, int32_t* flags, int32_t* ticket,
                          int32_t* err, int num_sms, cudaStream_t st);

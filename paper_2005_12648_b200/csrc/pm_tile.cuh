@@ -263,6 +263,62 @@ __device__ __forceinline__ void merge_tile(int32_t mode, const KT* As, const KT*
   }
 }
 
+// merge_tile for wide payload rows (w >= kWideRow, rows 4-byte aligned): the
+// per-thread spans of merge_tile would leave most threads idle (a 32 KB tile holds
+// only 32 KB / w records) and copy each row with one thread.  Phase 1: one thread
+// per output finds its source by the merge-path search (A first on ties: stable),
+// writes the key and parks the source row's offset in the first word of its output
+// row.  Phase 2, after a barrier over the GT merging threads: one warp per output
+// row reads the offset and copies the row with 16-byte (or 4-byte) words.
+#ifndef PM_WIDE_ROW
+#define PM_WIDE_ROW 384  // tune: payload bytes from which the tile merge copies rows warp-cooperatively (124 B: 1.18 vs 1.37 ms per-thread)
+#endif
+constexpr int64_t kWideRow = PM_WIDE_ROW;
+template <typename KT, int GT>
+__device__ __forceinline__ void merge_tile_wide(const KT* As, const KT* Bs, int64_t alpha, int64_t beta, int64_t nout,
+                                                KT* ko, uint8_t* po, const uint8_t* PA, const uint8_t* PB, int64_t w,
+                                                int gt, int bar_id) {
+  const int32_t al = (int32_t)alpha, bl = (int32_t)beta, no = (int32_t)nout, w32 = (int32_t)w;
+  for (int32_t o = gt; o < no; o += GT) {
+    int32_t lo = o > bl ? o - bl : 0, hi = o < al ? o : al;
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (As[mid] <= Bs[o - 1 - mid]) lo = mid + 1;
+      else hi = mid;
+    }
+    const int32_t i = lo, j = o - lo;
+    const bool takeA = j >= bl || (i < al && As[i] <= Bs[j]);
+    ko[o] = takeA ? As[i] : Bs[j];
+    const uint8_t* src = takeA ? PA + (int64_t)i * w32 : PB + (int64_t)j * w32;
+    *reinterpret_cast<int32_t*>(po + (int64_t)o * w32) = (int32_t)(src - PA);
+  }
+  named_barrier_sync(bar_id, GT);
+  // lane groups of L = 2^lg lanes per row (>= ~4 vector words per lane), 32 / L rows
+  // per warp step; a group reads its row's parked offset before anyone overwrites it
+  const int lane = gt & 31;
+  const bool v16 = (w32 & 15) == 0 && ((((uintptr_t)po) | ((uintptr_t)PA) | ((uintptr_t)PB)) & 15) == 0;
+  const int vb = v16 ? 16 : 4;
+  int lg = 5;
+  while (lg > 0 && (w32 / vb) < (4 << lg)) --lg;
+  const int L = 1 << lg, grp = lane >> lg, sub = lane & (L - 1), rpw = 32 >> lg;
+  for (int32_t o0 = (gt >> 5) * rpw; o0 < no; o0 += (GT / 32) * rpw) {
+    const int32_t o = o0 + grp;
+    uint8_t* dst = po + (int64_t)o * w32;
+    const int32_t off = o < no ? *reinterpret_cast<const int32_t*>(dst) : 0;
+    __syncwarp();
+    if (o < no) {
+      const uint8_t* src = PA + off;
+      if (v16) {
+        for (int32_t c = sub * 16; c < w32; c += L * 16)
+          *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(src + c);
+      } else {
+        for (int32_t c = sub * 4; c < w32; c += L * 4)
+          *reinterpret_cast<uint32_t*>(dst + c) = *reinterpret_cast<const uint32_t*>(src + c);
+      }
+    }
+  }
+}
+
 // Stream n bytes from a shared-memory tile to global memory with the same 16-byte
 // phase: thread `gt` == 0 issues one TMA bulk store for the aligned body; the
 // first threads write the unaligned head / tail bytes.
