@@ -190,6 +190,9 @@ static int launch_merge_small_(int ks, void* keys, void* payload, int64_t w, int
 #ifndef PM_WIDE_MIN
 #define PM_WIDE_MIN 256  // tune: bytes per payload row from which the wide path runs
 #endif
+#ifndef PM_FLOW_TF_Q
+#define PM_FLOW_TF_Q 32768  // tune: regions below which the scheduled engine plans the two-front order only (2^26/side: 336 vs 352 us; 2^27: even)
+#endif
 #ifndef PM_FLOW_WIDE_MAX
 #define PM_FLOW_WIDE_MAX 2048  // tune: bytes per record up to which in-place wide rows take the scheduled engine
 #endif
@@ -606,12 +609,17 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   F.nbits = PM_FLOW_BITS;
   F.nb = PM_FLOW_BINS;
   F.force = ctx->flow_mode == 2 ? 0 : ctx->flow_mode == 3 ? 1 : ctx->flow_mode == 4 ? 2 : -1;
-  // salvage pool, phase matched to the caller's (16-byte aligned) arrays
+  // small jobs: the two-front order with the lean plan (the itinerary phases cost
+  // more than the extra salvage copy below ~PM_FLOW_TF_Q regions); its salvage is
+  // ~N/3, so its default pool is N/2
   const int64_t n = e - s;
+  const bool lean = F.force < 0 && !nleaves && P.Q < PM_FLOW_TF_Q && (scratch_records == 0 || scratch_records >= n / 2);
+  if (lean) F.force = 0;
+  // salvage pool, phase matched to the caller's (16-byte aligned) arrays
   // a prescribed layout has no fallback engine: its pool holds any salvage (<= every slot);
   // otherwise the caller's budget (scratch_records > 0) or the default N / PM_FLOW_POOL_DIV
   F.pool_cap = nleaves ? n + 32 * T + 16 * K
-                       : scratch_records > 0 ? scratch_records : n / PM_FLOW_POOL_DIV + 32 * T;
+                       : scratch_records > 0 ? scratch_records : n / (lean ? 2 : PM_FLOW_POOL_DIV) + 32 * T;
   const size_t pk = (size_t)align_up(F.pool_cap * ks + 16, 256);
   rc = ensure(&ctx->fpool, &ctx->fpool_bytes, pk + (size_t)(w ? F.pool_cap * w + 16 : 0));
   if (rc) return rc;

@@ -164,6 +164,8 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
   KT* sa = reinterpret_cast<KT*>(F.samp_a);
   KT* sb = reinterpret_cast<KT*>(F.samp_b);
   if (tid < FC_WORDS) F.fc[tid] = 0;
+  for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;  // (before ph_readers counts identity regions)
+  for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
   if (tid == 0) {
     *P.ticket = 0;
     // (a prescribed layout has no such shortcut: identity regions are skipped instead)
@@ -312,12 +314,15 @@ __device__ __forceinline__ void ph_readers(const FlowParams& F) {
   FlowGeo g(P);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if (*(volatile int32_t*)P.noop) return;
-  for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;
-  for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
+  TwoFront tf{P.Q, P.qc};
   for (int64_t j = tid; j < P.K; j += nthr) {  // (Q == K: region j writes slot j)
     const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
     const bool idn = g.identity(j, a0, a1);
     F.idn[j] = idn ? 1 : 0;
+    if (idn) {  // identity regions per two-front chunk (ph_rank's compaction), and in total
+      atomicAdd(&F.chunk[tf.order(j) / kFlowChunk], 1);
+      atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], 1ull);
+    }
     int4 pc[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
@@ -348,7 +353,6 @@ __device__ __forceinline__ void ph_angle(const FlowParams& F) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   const int n = F.nbits;
   const float step = 6.283185307179586f / (float)n;
-  TwoFront tf{P.Q, P.qc};
   for (int64_t j = tid; j < P.K; j += nthr) {
     float zr = 0.f, zi = 0.f;
     if (!F.idn[j]) {
@@ -363,9 +367,6 @@ __device__ __forceinline__ void ph_angle(const FlowParams& F) {
         }
         x = v & 0x7fffffff;
       }
-    } else {
-      atomicAdd(&F.chunk[tf.order(j) / kFlowChunk], 1);
-      atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], 1ull);
     }
     F.z[j] = make_float2(zr, zi);
     F.z[P.K + j] = make_float2(0.f, 0.f);
@@ -730,21 +731,23 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
   ph_readers(F);
   PM_FLOW_DBG(3);
   grid.sync();
-  ph_angle(F);
-  PM_FLOW_DBG(4);
-  grid.sync();
-  const bool angle = F.force < 0 || F.force == 1;
-  for (int it = 0; angle && it < F.nsync; ++it) {
-    ph_sync(F, it);
-  PM_FLOW_DBG(5);
+  if (F.force != 0) {  // (the two-front order needs no itinerary: lean plan)
+    ph_angle(F);
+    PM_FLOW_DBG(4);
+    grid.sync();
+    const bool angle = F.force < 0 || F.force == 1;
+    for (int it = 0; angle && it < F.nsync; ++it) {
+      ph_sync(F, it);
+      PM_FLOW_DBG(5);
+      grid.sync();
+    }
+    ph_key(F, angle ? F.nsync % 3 : 0);
+    PM_FLOW_DBG(6);
+    grid.sync();
+    ph_choose(F);
+    PM_FLOW_DBG(7);
     grid.sync();
   }
-  ph_key(F, angle ? F.nsync % 3 : 0);
-  PM_FLOW_DBG(6);
-  grid.sync();
-  ph_choose(F);
-  PM_FLOW_DBG(7);
-  grid.sync();
   if (blockIdx.x == 0) ph_decide(F);
   PM_FLOW_DBG(8);
   grid.sync();

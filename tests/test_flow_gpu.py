@@ -81,9 +81,10 @@ def test_misaligned_bases(flow_mode, mode, koff, poff, width):
 
 
 def test_pool_overflow_falls_back(flow_mode):
-    """One big rotation needs half the job salvaged (> the pool's N/4): the plan
-    raises the overflow word and the gated bounded-pool engine merges instead."""
-    flow_mode("auto")
+    """One big rotation needs half the job salvaged (> the pool's N/4 under the
+    itinerary order): the plan raises the overflow word and the gated bounded-pool
+    engine merges instead."""
+    flow_mode("angle")
     h = 1 << 22
     ar = torch.arange(h, device="cuda", dtype=torch.int32)
     k0 = torch.cat([ar + h, ar])
@@ -91,6 +92,34 @@ def test_pool_overflow_falls_back(flow_mode):
     st = _ops.merge(arr, 0, h, 2 * h)
     assert torch.equal(arr.keys, torch.sort(k0).values)
     assert st[4] == 0  # no scheduled order reported: the bounded-pool engine ran
+
+
+def test_lean_plan_small_jobs(flow_mode):
+    """Below PM_FLOW_TF_Q regions the plan is the lean two-front one with an N/2 pool:
+    the same rotation fits it (no fallback), and a uniform job reports the two-front
+    order; both bit-exact."""
+    flow_mode("auto")
+    h = 1 << 22
+    ar = torch.arange(h, device="cuda", dtype=torch.int32)
+    k0 = torch.cat([ar + h, ar])
+    arr = pm.KeyedArray(k0.clone())
+    _ops.set_engine_only(True)
+    try:
+        st = _ops.merge(arr, 0, h, 2 * h)
+        assert torch.equal(arr.keys, torch.sort(k0).values)
+        assert st[4] == 1  # two-front order (FC_MODE 0, reported + 1)
+        g = torch.Generator(device="cuda").manual_seed(9)
+        k1 = torch.randint(0, 1 << 20, (2 * h,), device="cuda", dtype=torch.int32, generator=g)
+        k1[:h] = k1[:h].sort().values
+        k1[h:] = k1[h:].sort().values
+        p1 = torch.arange(2 * h, device="cuda", dtype=torch.int32).view(torch.uint8).view(2 * h, 4)
+        arr = pm.KeyedArray(k1.clone(), p1.clone())
+        st = _ops.merge(arr, 0, h, 2 * h)
+        order = torch.sort(k1, stable=True).indices
+        assert torch.equal(arr.keys, k1[order]) and torch.equal(arr.payload, p1[order])
+        assert st[4] == 1
+    finally:
+        _ops.set_engine_only(False)
 
 
 def test_geometries_back_to_back(flow_mode):
