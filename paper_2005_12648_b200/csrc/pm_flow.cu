@@ -248,6 +248,9 @@ __device__ __forceinline__ void ph_split_leaves(const FlowParams& F) {
   }
 }
 
+#ifndef PM_FLOW_SAMPLE_BIN
+#define PM_FLOW_SAMPLE_BIN 0  // tune: binary instead of 8-ary search over the samples
+#endif
 template <typename KT>
 __device__ __forceinline__ void ph_split(const FlowParams& F) {
   const EngineParams& P = F.P;
@@ -275,7 +278,17 @@ __device__ __forceinline__ void ph_split(const FlowParams& F) {
       const int64_t c = (d - 1 - F.phi) >> F.lS;  // exact: d - 1 - phi is a multiple of S
       int64_t wlo = lo, whi = min(hi, klo << F.lS);  // window if no sample point passes
       if (klo <= khi && sa[klo] <= sb[c - klo]) {
+#if PM_FLOW_SAMPLE_BIN
+        int64_t blo = klo, bhi = khi;  // (tuning: binary search over the samples)
+        while (blo < bhi) {
+          const int64_t mid = (blo + bhi + 1) >> 1;
+          if (sa[mid] <= sb[c - mid]) blo = mid;
+          else bhi = mid - 1;
+        }
+        const int64_t k = blo;
+#else
         const int64_t k = last_true8(klo, khi, [&](int64_t x) { return sa[x] <= sb[c - x]; });
+#endif
         wlo = (k << F.lS) + 1;
         whi = min(hi, wlo - 1 + S);
       }
@@ -722,44 +735,44 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
   cg::grid_group grid = cg::this_grid();
   PM_FLOW_DBG(0);
   ph_sample<KT>(F);
-  PM_FLOW_DBG(1);
   grid.sync();
+  PM_FLOW_DBG(1);
   if (*(volatile int32_t*)F.P.noop) return;
   ph_split<KT>(F);
+  grid.sync();
   PM_FLOW_DBG(2);
-  grid.sync();
   ph_readers(F);
-  PM_FLOW_DBG(3);
   grid.sync();
+  PM_FLOW_DBG(3);
   if (F.force != 0) {  // (the two-front order needs no itinerary: lean plan)
     ph_angle(F);
-    PM_FLOW_DBG(4);
     grid.sync();
+    PM_FLOW_DBG(4);
     const bool angle = F.force < 0 || F.force == 1;
     for (int it = 0; angle && it < F.nsync; ++it) {
       ph_sync(F, it);
-      PM_FLOW_DBG(5);
       grid.sync();
+      PM_FLOW_DBG(5);
     }
     ph_key(F, angle ? F.nsync % 3 : 0);
+    grid.sync();
     PM_FLOW_DBG(6);
-    grid.sync();
     ph_choose(F);
-    PM_FLOW_DBG(7);
     grid.sync();
+    PM_FLOW_DBG(7);
   }
   if (blockIdx.x == 0) ph_decide(F);
+  grid.sync();
   PM_FLOW_DBG(8);
-  grid.sync();
   ph_rank(F);
+  grid.sync();
   PM_FLOW_DBG(9);
-  grid.sync();
   ph_hull(F);
+  grid.sync();
   PM_FLOW_DBG(10);
-  grid.sync();
   ph_alloc(F);
-  PM_FLOW_DBG(11);
   grid.sync();
+  PM_FLOW_DBG(11);
   ph_tickets(F);
   PM_FLOW_DBG(12);
 }
