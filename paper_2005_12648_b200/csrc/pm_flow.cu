@@ -79,9 +79,6 @@ constexpr int kFlowChunk = 1024;
       __trap();                                                                    \
     }                                                                              \
   } while (0)
-#ifndef PM_FLOW_WIN4
-#define PM_FLOW_WIN4 0  // tune: 4-ary window search in the split phase
-#endif
 #ifndef PM_FLOW_ABLATE
 #define PM_FLOW_ABLATE 0  // k_flow timing ablations (tuning builds; results are wrong): 1 no pend wait, 2 no merge, 4 no store
 #endif  // two-front tickets per compaction block
@@ -248,8 +245,11 @@ __device__ __forceinline__ void ph_split_leaves(const FlowParams& F) {
   }
 }
 
-#ifndef PM_FLOW_SAMPLE_BIN
-#define PM_FLOW_SAMPLE_BIN 0  // tune: binary instead of 8-ary search over the samples
+#ifndef PM_FLOW_SPLIT_ABLATE
+#define PM_FLOW_SPLIT_ABLATE 0  // timing ablations of the split search (tuning builds; wrong splits): 1 no window search, 2 no sample search
+#endif
+#ifndef PM_FLOW_INTERP
+#define PM_FLOW_INTERP 8  // tune: interpolation probes of the split search before binary search (2^30: split 66 -> 30 us)
 #endif
 template <typename KT>
 __device__ __forceinline__ void ph_split(const FlowParams& F) {
@@ -277,36 +277,50 @@ __device__ __forceinline__ void ph_split(const FlowParams& F) {
       const int64_t klo = (lo + S - 1) >> F.lS, khi = (hi - 1) >> F.lS;
       const int64_t c = (d - 1 - F.phi) >> F.lS;  // exact: d - 1 - phi is a multiple of S
       int64_t wlo = lo, whi = min(hi, klo << F.lS);  // window if no sample point passes
-      if (klo <= khi && sa[klo] <= sb[c - klo]) {
-#if PM_FLOW_SAMPLE_BIN
-        int64_t blo = klo, bhi = khi;  // (tuning: binary search over the samples)
-        while (blo < bhi) {
-          const int64_t mid = (blo + bhi + 1) >> 1;
-          if (sa[mid] <= sb[c - mid]) blo = mid;
-          else bhi = mid - 1;
-        }
-        const int64_t k = blo;
-#else
+      // f(x) = A[x] - B[d-1-x] rises with x; the split is the first x with f(x) > 0.
+      // Known: f <= 0 at xl = wlo - 1 (fl), f > 0 at xh = whi (fh) when `ends`.
+      double fl = 0.0, fh = 0.0;
+      bool ends = false;
+      if (!(PM_FLOW_SPLIT_ABLATE & 2) && klo <= khi && sa[klo] <= sb[c - klo]) {
         const int64_t k = last_true8(klo, khi, [&](int64_t x) { return sa[x] <= sb[c - x]; });
-#endif
         wlo = (k << F.lS) + 1;
         whi = min(hi, wlo - 1 + S);
+        if (k < khi) {  // (k + 1) S <= hi - 1: both bracket values are samples
+          fl = (double)sa[k] - (double)sb[c - k];
+          fh = (double)sa[k + 1] - (double)sb[c - k - 1];
+          ends = true;
+        }
       }
-      // the split is in [wlo, whi]
-#if PM_FLOW_WIN4
-      // 4-ary: three probes per step, half the dependent DRAM round trips
-      while (whi - wlo > 3) {
-        const int64_t span = whi - wlo;
-        const int64_t p1 = wlo + span / 4, p2 = wlo + span / 2, p3 = wlo + (3 * span) / 4;
-        const bool f1 = __ldg(A + p1) <= __ldg(B + d - 1 - p1);
-        const bool f2 = __ldg(A + p2) <= __ldg(B + d - 1 - p2);
-        const bool f3 = __ldg(A + p3) <= __ldg(B + d - 1 - p3);
-        if (f3) wlo = p3 + 1;
-        else if (f2) { wlo = p2 + 1; whi = p3; }
-        else if (f1) { wlo = p1 + 1; whi = p2; }
-        else whi = p1;
+      // the split is in [wlo, whi].  Interpolation on f first: a probe lands where
+      // the line through the bracket values crosses zero (for keys spread like the
+      // samples, within a few records of the split), and each probe replaces a
+      // bracket end (Illinois rule against one end creeping).  At most
+      // PM_FLOW_INTERP probes, then binary search, so the worst case stays
+      // logarithmic plus PM_FLOW_INTERP.  The probes are the random DRAM reads the
+      // split phase is bound by: ~2-3 instead of ~6 distinct lines per side.
+      int side = 0;  // the bracket end the last probe replaced (-1 low, +1 high)
+      for (int it = 0; ends && it < PM_FLOW_INTERP && whi - wlo > 8; ++it) {
+        const int64_t xl = wlo - 1, xh = whi;
+        int64_t x = xl + (int64_t)((-fl) / (fh - fl) * (double)(xh - xl));
+        x = min(max(x, xl + 1), xh - 1);
+        const KT av = __ldg(A + x), bv = __ldg(B + d - 1 - x);
+        const int s_now = av <= bv ? -1 : 1;
+        if (s_now < 0) {
+          wlo = x + 1;
+          fl = (double)av - (double)bv;
+        } else {
+          whi = x;
+          fh = (double)av - (double)bv;
+        }
+        // Illinois step: the same end replaced twice -> halve the other end's value,
+        // so the next probe moves towards it instead of creeping
+        if (s_now == side) {
+          if (s_now < 0) fh *= 0.5;
+          else fl *= 0.5;
+        }
+        side = s_now;
       }
-#endif
+      if (PM_FLOW_SPLIT_ABLATE & 1) whi = wlo;  // (timing ablation: wrong splits)
       while (wlo < whi) {  // binary (its late probes share DRAM lines)
         const int64_t mid = (wlo + whi) >> 1;
         if (__ldg(A + mid) <= __ldg(B + d - 1 - mid)) wlo = mid + 1;

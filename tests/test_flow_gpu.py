@@ -122,6 +122,34 @@ def test_lean_plan_small_jobs(flow_mode):
         _ops.set_engine_only(False)
 
 
+@pytest.mark.parametrize("dist", ["exp", "steps", "clustered"])
+def test_split_search_skewed_keys(flow_mode, dist):
+    """The split phase interpolates between sample values before its binary search;
+    key distributions far from linear (exponential, step-like, clustered) must give
+    the same bit-exact merge (the bracket invariant never depends on the guess)."""
+    flow_mode("auto")
+    rng = np.random.default_rng({"exp": 1, "steps": 2, "clustered": 3}[dist])
+    n = 1 << 22
+    if dist == "exp":
+        raw = np.exp(rng.uniform(0, 21, n)).astype(np.int64)
+    elif dist == "steps":
+        raw = (rng.integers(0, 6, n) * (1 << 28) + rng.integers(0, 3, n)).astype(np.int64)
+    else:
+        c = rng.integers(0, 2**31 - 2**20, 7)
+        raw = c[rng.integers(0, 7, n)] + rng.integers(0, 2**10, n)
+    keys = raw.astype(np.int32)
+    m = int(n * 0.45)
+    keys[:m].sort()
+    keys[m:].sort()
+    payload = np.arange(n, dtype=np.int32).view(np.uint8).reshape(n, 4)
+    want_k, want_p = keys.copy(), payload.copy()
+    orc.seq_merge_buffered(want_k, want_p, 0, m, n)
+    arr = to_gpu(keys, payload)
+    _ops.merge(arr, 0, m, n)
+    k, p = arr.numpy()
+    assert np.array_equal(k, want_k) and np.array_equal(p, want_p), dist
+
+
 def test_geometries_back_to_back(flow_mode):
     """Workspace and pool reuse across shrinking / growing jobs and key widths."""
     flow_mode("auto")
