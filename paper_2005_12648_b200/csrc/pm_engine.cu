@@ -80,6 +80,9 @@ __device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* n
 // ============================================================================
 // k_plan: merge-path splits + workspace reset
 // ============================================================================
+#ifndef PM_PLAN_INTERP
+#define PM_PLAN_INTERP 8  // tune: interpolation probes of k_plan's split search (0: binary only)
+#endif
 constexpr int kCoarse = 64;  // k_plan_coarse searches every kCoarse-th region boundary
 // Full-range merge-path searches at every kCoarse-th boundary (and the last);
 // k_plan then searches the boundaries in between inside these brackets.
@@ -133,6 +136,14 @@ __global__ void k_plan(EngineParams P) {
         // a is monotone in d and so is b = d - a: both stay between the coarse splits
         int64_t lo = max(max(a0, d - b1), max(d - lb, (int64_t)0));
         int64_t hi = min(min(a1, d - b0), min(d, la));
+        // both bracket ends inside the runs: their values (one round trip), then
+        // interpolation (pm_search.cuh) before the binary search
+        if (hi - lo > 64 && lo - 1 >= max(d - lb, (int64_t)0) && hi < la && d - 1 - hi >= 0) {
+          const KT* A = keys + P.s;
+          const double fl = (double)__ldg(A + lo - 1) - (double)__ldg(B + d - lo);
+          const double fh = (double)__ldg(A + hi) - (double)__ldg(B + d - 1 - hi);
+          if (fl <= 0.0 && fh > 0.0) interp_bracket<KT>(A, B, d, &lo, &hi, fl, fh, PM_PLAN_INTERP);
+        }
         while (lo < hi) {
           const int64_t mid = (lo + hi) >> 1;
           if (__ldg(keys + P.s + mid) <= __ldg(B + d - 1 - mid)) lo = mid + 1;

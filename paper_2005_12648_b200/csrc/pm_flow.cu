@@ -58,6 +58,7 @@
 #include "pm_engine.cuh"
 #include "pm_launch.h"
 #include "pm_tile.cuh"
+#include "pm_search.cuh"
 
 #include <cooperative_groups.h>
 #include <nvtx3/nvToolsExt.h>
@@ -291,35 +292,10 @@ __device__ __forceinline__ void ph_split(const FlowParams& F) {
           ends = true;
         }
       }
-      // the split is in [wlo, whi].  Interpolation on f first: a probe lands where
-      // the line through the bracket values crosses zero (for keys spread like the
-      // samples, within a few records of the split), and each probe replaces a
-      // bracket end (Illinois rule against one end creeping).  At most
-      // PM_FLOW_INTERP probes, then binary search, so the worst case stays
-      // logarithmic plus PM_FLOW_INTERP.  The probes are the random DRAM reads the
-      // split phase is bound by: ~2-3 instead of ~6 distinct lines per side.
-      int side = 0;  // the bracket end the last probe replaced (-1 low, +1 high)
-      for (int it = 0; ends && it < PM_FLOW_INTERP && whi - wlo > 8; ++it) {
-        const int64_t xl = wlo - 1, xh = whi;
-        int64_t x = xl + (int64_t)((-fl) / (fh - fl) * (double)(xh - xl));
-        x = min(max(x, xl + 1), xh - 1);
-        const KT av = __ldg(A + x), bv = __ldg(B + d - 1 - x);
-        const int s_now = av <= bv ? -1 : 1;
-        if (s_now < 0) {
-          wlo = x + 1;
-          fl = (double)av - (double)bv;
-        } else {
-          whi = x;
-          fh = (double)av - (double)bv;
-        }
-        // Illinois step: the same end replaced twice -> halve the other end's value,
-        // so the next probe moves towards it instead of creeping
-        if (s_now == side) {
-          if (s_now < 0) fh *= 0.5;
-          else fl *= 0.5;
-        }
-        side = s_now;
-      }
+      // the split is in [wlo, whi]: interpolation between the bracketing samples
+      // (pm_search.cuh), then binary search.  The probes are the random DRAM reads
+      // the split phase is bound by: ~2-3 instead of ~6 distinct lines per run.
+      if (ends) interp_bracket<KT>(A, B, d, &wlo, &whi, fl, fh, PM_FLOW_INTERP);
       if (PM_FLOW_SPLIT_ABLATE & 1) whi = wlo;  // (timing ablation: wrong splits)
       while (wlo < whi) {  // binary (its late probes share DRAM lines)
         const int64_t mid = (wlo + whi) >> 1;

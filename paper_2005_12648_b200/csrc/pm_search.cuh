@@ -44,6 +44,43 @@ __device__ __forceinline__ int64_t merge_path_warp(const KT* A, int64_t la, cons
 }
 
 // one thread: stable merge-path split of diagonal d (A wins ties)
+// Narrow a stable merge-path bracket by interpolation.  f(x) = A[x] - B[d-1-x]
+// rises with x; the split is the first x with f(x) > 0.  On entry the split is in
+// [*lo, *hi], f(*lo - 1) = fl <= 0 and f(*hi) = fh > 0.  Each probe lands where the
+// line through the bracket values crosses zero (a few records from the split when
+// the keys are spread like the bracket ends) and replaces one end; the Illinois
+// rule halves a retained end's value so the bracket cannot creep.  At most
+// `probes` probes (the caller finishes with a binary search, so the worst case is
+// logarithmic plus `probes`); each probe is one random DRAM line per run instead of
+// the ~log2(window / 32) distinct lines a binary search touches.
+template <typename KT>
+__device__ __forceinline__ void interp_bracket(const KT* A, const KT* B, int64_t d, int64_t* lo, int64_t* hi, double fl,
+                                               double fh, int probes) {
+  int64_t wlo = *lo, whi = *hi;
+  int side = 0;
+  for (int it = 0; it < probes && whi - wlo > 8; ++it) {
+    const int64_t xl = wlo - 1, xh = whi;
+    int64_t x = xl + (int64_t)((-fl) / (fh - fl) * (double)(xh - xl));
+    x = x < xl + 1 ? xl + 1 : (x > xh - 1 ? xh - 1 : x);
+    const KT av = __ldg(A + x), bv = __ldg(B + d - 1 - x);
+    const int s_now = av <= bv ? -1 : 1;
+    if (s_now < 0) {
+      wlo = x + 1;
+      fl = (double)av - (double)bv;
+    } else {
+      whi = x;
+      fh = (double)av - (double)bv;
+    }
+    if (s_now == side) {
+      if (s_now < 0) fh *= 0.5;
+      else fl *= 0.5;
+    }
+    side = s_now;
+  }
+  *lo = wlo;
+  *hi = whi;
+}
+
 template <typename KT>
 __device__ __forceinline__ int64_t merge_path_thread(const KT* A, int64_t la, const KT* B, int64_t lb, int64_t d) {
   int64_t lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
