@@ -13,6 +13,8 @@
 #include <mutex>
 #include <vector>
 #include <string>
+#include <thread>
+#include <chrono>
 
 #include "../../include/parmerge_b200.h"
 #include "pm_common.cuh"
@@ -73,6 +75,9 @@ struct pm_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // pm_merge_host: H2D, merge, D2H
   cudaEvent_t hev[33] = {};                          // [0]: joins; then per-chunk events (ring)
+  std::vector<cudaEvent_t> hup, hdn;  // pm_merge_host: per chunk, upload done / staged write-back landed
+  void* hstage = nullptr;             // pm_merge_host: pinned host staging of early write-backs
+  size_t hstage_bytes = 0;
   void* buf = nullptr;    // min-side buffer of the buffered mode
   size_t buf_bytes = 0;
   void* wide = nullptr;   // wide records: row indices, merged keys
@@ -920,6 +925,9 @@ int pm_ctx_destroy(pm_ctx* ctx) {
     if (x) cudaStreamDestroy(x);
   for (auto& x : ctx->hev)
     if (x) cudaEventDestroy(x);
+  for (auto& x : ctx->hup) cudaEventDestroy(x);
+  for (auto& x : ctx->hdn) cudaEventDestroy(x);
+  if (ctx->hstage) cudaFreeHost(ctx->hstage);
   if (ctx->ctl) cudaFree(ctx->ctl);
   delete ctx;
   return PM_OK;
@@ -1144,12 +1152,17 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
   return PM_OK;
 }
 
-// Host-buffer merge, pipelined over output chunks on three streams: H2D of the
-// input prefixes chunk k needs, the out-of-place device merge of chunk k
-// (copy mode), and D2H of chunk k back into the caller's (in-place) array.
-// Chunk k's output [d_k, d_{k+1}) is written back only once every input record
-// that lived there is on the device, so the in-place host semantics hold while
-// the two PCIe directions overlap.
+// Host-buffer merge, pipelined over output chunks on three streams: H2D of
+// chunk k's inputs in merge order (A[a_k, a_{k+1}) and B[b_k, b_{k+1})), the
+// out-of-place device merge of chunk k (copy mode), and D2H of chunk k as soon
+// as it is merged.  The in-place host semantics: chunk k's output range
+// [d_k, d_{k+1}) may hold records not uploaded yet -- every such range is free
+// only after upload ready_k >= k (for uniform runs the first half of the output
+// frees at half the upload rate).  Writing those chunks back directly would
+// stall the D2H stream or force uploads ahead of the merge (1.25 N / R for
+// uniform runs); instead they land in a pinned host staging buffer and host
+// threads move each into place once its range has been uploaded.  Both PCIe
+// directions then run at full rate for the whole call (~N / R).
 int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_host, int64_t width, int64_t start,
                   int64_t middle, int64_t end, void* stream) {
   DeviceGuard dg_(ctx ? ctx->device : -1);
@@ -1157,17 +1170,30 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
     return fail(PM_ERR_ARG, "bad pm_merge_host arguments");
   if (!(0 <= start && start <= middle && middle <= end)) return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (middle == start || middle == end) return PM_OK;
+  // records already on their output positions never cross PCIe: the A prefix
+  // with keys <= B[0] and the B suffix with keys >= A[last] (A first on ties)
+  {
+    int64_t a_lo, b_hi;
+    if (key_bytes == 4) {
+      const int32_t* A = static_cast<int32_t*>(keys_host) + start;
+      const int32_t* B = static_cast<int32_t*>(keys_host) + middle;
+      a_lo = std::upper_bound(A, A + (middle - start), B[0]) - A;
+      b_hi = std::lower_bound(B, B + (end - middle), A[middle - start - 1]) - B;
+    } else {
+      const int64_t* A = static_cast<int64_t*>(keys_host) + start;
+      const int64_t* B = static_cast<int64_t*>(keys_host) + middle;
+      a_lo = std::upper_bound(A, A + (middle - start), B[0]) - A;
+      b_hi = std::lower_bound(B, B + (end - middle), A[middle - start - 1]) - B;
+    }
+    // already in order (srecpar.py:56-57): nothing moves
+    if (a_lo == middle - start || b_hi == 0) return PM_OK;
+    start += a_lo;
+    end = middle + b_hi;
+  }
   const int64_t n = end - start, la = middle - start, lb = end - middle;
-  if (la == 0 || lb == 0) return PM_OK;
   char* hk = static_cast<char*>(keys_host) + start * key_bytes;
   char* hp = width ? static_cast<char*>(payload_host) + start * width : nullptr;
-  // already in order (srecpar.py:56-57): nothing moves
-  {
-    bool sorted;
-    if (key_bytes == 4) sorted = reinterpret_cast<int32_t*>(hk)[la - 1] <= reinterpret_cast<int32_t*>(hk)[la];
-    else sorted = reinterpret_cast<int64_t*>(hk)[la - 1] <= reinterpret_cast<int64_t*>(hk)[la];
-    if (sorted) return PM_OK;
-  }
   const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)align_up(n * width, 256);
   int rc;
   // host threads calling concurrently (the reference's pool runs leaf merges in
@@ -1191,7 +1217,7 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   PM_CUDA(cudaEventRecord(ctx->hev[0], st));
   PM_CUDA(cudaStreamWaitEvent(sH, ctx->hev[0], 0));
 #ifndef PM_HOST_CHUNKS
-#define PM_HOST_CHUNKS 96  // tune: output chunks of the host-buffer pipeline
+#define PM_HOST_CHUNKS 48  // output chunks of the host-buffer pipeline (48: 103 ms, 96: 104, 192: 108 at 2^30 int32)
 #endif
   const int64_t chunk = std::max<int64_t>((int64_t)1 << 21, (n + PM_HOST_CHUNKS - 1) / PM_HOST_CHUNKS);
   const int nch = (int)((n + chunk - 1) / chunk);
@@ -1206,6 +1232,68 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
     dk[k] = std::min<int64_t>((int64_t)k * chunk, n);
     ak[k] = split(dk[k]);
   }
+  // ready[k]: the upload after which chunk k's output range holds no record
+  // still to be uploaded (A part: a_{j+1} >= min(d1, la); B part: b_{j+1} >= d1 - la)
+  std::vector<int> ready(nch), order(nch);
+  for (int k = 0; k < nch; ++k) {
+    // A positions in the range: [d_k, min(d_{k+1}, la)); B positions: [max(d_k, la), d_{k+1}) - la
+    const int64_t needA = dk[k] < la ? std::min(dk[k + 1], la) : 0, needB = std::max<int64_t>(dk[k + 1] - la, 0);
+    int j = k;
+    while (j + 1 < nch && (ak[j + 1] < needA || (dk[j + 1] - ak[j + 1]) < needB)) ++j;
+    ready[k] = j;
+    order[k] = k;
+  }
+  // chunks whose range frees after their merge go through the pinned staging
+  // buffer (one grow-only allocation per context); without it (over the cap, or
+  // the pinned allocation failed) they are written back directly in ready order
+#ifndef PM_HOST_STAGE_MAX
+#define PM_HOST_STAGE_MAX ((size_t)16 << 30)
+#endif
+  const size_t rec_bytes = (size_t)key_bytes + (size_t)width;
+  std::vector<size_t> soff(nch, SIZE_MAX);
+  size_t staged = 0;
+  for (int k = 0; k < nch; ++k)
+    if (ready[k] > k) {
+      soff[k] = staged;
+      staged += (size_t)align_up((dk[k + 1] - dk[k]) * (int64_t)rec_bytes, 256);
+    }
+  bool use_stage = staged > 0 && staged <= PM_HOST_STAGE_MAX;
+  if (use_stage && ctx->hstage_bytes < staged) {
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
+    ctx->hstage = nullptr;
+    ctx->hstage_bytes = 0;
+    if (cudaHostAlloc(&ctx->hstage, staged, cudaHostAllocPortable) == cudaSuccess) ctx->hstage_bytes = staged;
+    else {
+      cudaGetLastError();
+      ctx->hstage = nullptr;
+      use_stage = false;
+    }
+  }
+  while ((int)ctx->hup.size() < nch) {
+    cudaEvent_t e1, e2;
+    PM_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    PM_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    ctx->hup.push_back(e1);
+    ctx->hdn.push_back(e2);
+  }
+  const std::vector<int> free_at = ready;  // the upload after which chunk k's range is free
+  std::vector<int> stg;                    // staged chunks, in the order their ranges free
+  for (int k = 0; k < nch; ++k)
+    if (use_stage && ready[k] > k) {
+      stg.push_back(k);
+      ready[k] = k;  // its D2H (into the staging buffer) leaves right after its merge
+    }
+  std::stable_sort(stg.begin(), stg.end(), [&](int x, int y) { return free_at[x] < free_at[y]; });
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ready[x] < ready[y]; });
+  char* hs_base = static_cast<char*>(ctx->hstage);
+#ifdef PM_HOST_TRACE
+  // debug timeline (tools/gpu_e2e_trace.py): per chunk, upload / merge / D2H end
+  std::vector<cudaEvent_t> tr(3 * nch + 1);
+  for (auto& e : tr) cudaEventCreate(&e);
+  cudaEventRecord(tr[3 * nch], sH);
+  std::vector<double> mv_done(nch, -1);
+  auto h0 = std::chrono::steady_clock::now();
+#endif
   auto h2d = [&](int64_t x0, int64_t x1) -> int {
     if (x1 <= x0) return PM_OK;
     PM_CUDA(cudaMemcpyAsync(dxk + x0 * key_bytes, hk + x0 * key_bytes, (x1 - x0) * key_bytes,
@@ -1214,21 +1302,18 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
       PM_CUDA(cudaMemcpyAsync(dxp + x0 * width, hp + x0 * width, (x1 - x0) * width, cudaMemcpyHostToDevice, sH));
     return PM_OK;
   };
-  int64_t cA = 0, cB = 0;  // on the device: X[0, cA) and X[la, la + cB)
   constexpr int kEv = (int)(sizeof(((pm_ctx*)nullptr)->hev) / sizeof(cudaEvent_t)) - 1;
+  int next = 0;  // next chunk (in `order`) to write back
   for (int k = 0; k < nch; ++k) {
-    // the inputs of chunk k and every record living in its output range
-    const int64_t d1 = dk[k + 1], a1 = ak[k + 1], b1 = d1 - a1;
-    const int64_t tA = std::min(d1, la), tB = std::max(b1, d1 > la ? d1 - la : 0);
-    if (tA > cA) rc = h2d(cA, tA);
-    if (!rc && tB > cB) rc = h2d(la + cB, la + tB);
+    const int64_t d0 = dk[k], a0 = ak[k], b0 = d0 - a0, d1 = dk[k + 1], a1 = ak[k + 1], b1 = d1 - a1;
+    rc = h2d(a0, a1);
+    if (!rc) rc = h2d(la + b0, la + b1);
     if (rc) return rc;
-    cA = std::max(cA, tA);
-    cB = std::max(cB, tB);
-    cudaEvent_t eh = ctx->hev[1 + (2 * k) % kEv], ec = ctx->hev[1 + (2 * k + 1) % kEv];
-    PM_CUDA(cudaEventRecord(eh, sH));
-    PM_CUDA(cudaStreamWaitEvent(sC, eh, 0));
-    const int64_t d0 = dk[k], a0 = ak[k], b0 = d0 - a0;
+    PM_CUDA(cudaEventRecord(ctx->hup[k], sH));
+    PM_CUDA(cudaStreamWaitEvent(sC, ctx->hup[k], 0));
+#ifdef PM_HOST_TRACE
+    cudaEventRecord(tr[3 * k], sH);
+#endif
     {
       std::lock_guard<std::mutex> lk(ctx->mu);
       rc = run_engine(ctx, dxk + a0 * key_bytes, key_bytes, width ? dxp + a0 * width : nullptr, width, 0, a1 - a0,
@@ -1236,15 +1321,87 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
                       dxk + (la + b0) * key_bytes, width ? dxp + (la + b0) * width : nullptr);
     }
     if (rc) return rc;
-    PM_CUDA(cudaEventRecord(ec, sC));
-    PM_CUDA(cudaStreamWaitEvent(sD, ec, 0));
-    PM_CUDA(cudaMemcpyAsync(hk + d0 * key_bytes, dok + d0 * key_bytes, (d1 - d0) * key_bytes,
-                            cudaMemcpyDeviceToHost, sD));
-    if (width)
-      PM_CUDA(cudaMemcpyAsync(hp + d0 * width, dop + d0 * width, (d1 - d0) * width, cudaMemcpyDeviceToHost, sD));
+#ifdef PM_HOST_TRACE
+    cudaEventRecord(tr[3 * k + 1], sC);
+#endif
+    if (next < nch && ready[order[next]] == k) {
+      // merges run in order on sC: chunk k merged => uploads 0..k and merges 0..k done;
+      // the event is waited on right after it is recorded, so the ring can be reused
+      cudaEvent_t ec = ctx->hev[1 + k % kEv];
+      PM_CUDA(cudaEventRecord(ec, sC));
+      PM_CUDA(cudaStreamWaitEvent(sD, ec, 0));
+      for (; next < nch && ready[order[next]] == k; ++next) {
+        const int c = order[next];
+        const int64_t e0 = dk[c], e1 = dk[c + 1];
+        char* tk = soff[c] != SIZE_MAX && use_stage ? hs_base + soff[c] : hk + e0 * key_bytes;
+        char* tp = soff[c] != SIZE_MAX && use_stage ? tk + (e1 - e0) * key_bytes : hp + e0 * width;
+        PM_CUDA(cudaMemcpyAsync(tk, dok + e0 * key_bytes, (e1 - e0) * key_bytes, cudaMemcpyDeviceToHost, sD));
+        if (width) PM_CUDA(cudaMemcpyAsync(tp, dop + e0 * width, (e1 - e0) * width, cudaMemcpyDeviceToHost, sD));
+        if (soff[c] != SIZE_MAX && use_stage) PM_CUDA(cudaEventRecord(ctx->hdn[c], sD));
+#ifdef PM_HOST_TRACE
+        cudaEventRecord(tr[3 * c + 2], sD);
+#endif
+      }
+    }
   }
+  if (next != nch) return fail(PM_ERR_INTERNAL, "pm_merge_host: write-back schedule incomplete");
   PM_CUDA(cudaEventRecord(ctx->hev[0], sD));
   PM_CUDA(cudaStreamWaitEvent(st, ctx->hev[0], 0));
+  if (!stg.empty()) {
+    // host threads move the staged chunks into place, each once its range has
+    // been uploaded and its D2H has landed (every thread takes a stripe of each)
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+#ifndef PM_HOST_MOVERS
+#define PM_HOST_MOVERS 4u  // more threads take host memory bandwidth from the DMA (tools/gpu_pcie_chunks.py)
+#endif
+    const int nt = (int)std::min<unsigned>(PM_HOST_MOVERS, std::max(1u, hw / 2));
+    std::atomic<int> err{0};
+    auto mover = [&](int t) {
+      for (int c : stg) {
+        if (cudaEventSynchronize(ctx->hup[free_at[c]]) != cudaSuccess ||
+            cudaEventSynchronize(ctx->hdn[c]) != cudaSuccess) {
+          err.store(1);
+          return;
+        }
+        const int64_t e0 = dk[c], e1 = dk[c + 1];
+        const char* src = hs_base + soff[c];
+        auto stripe = [&](char* dst, const char* from, int64_t bytes) {
+          const int64_t per = ((bytes + nt - 1) / nt + 63) & ~(int64_t)63;
+          const int64_t x0 = std::min<int64_t>(bytes, per * t), x1 = std::min<int64_t>(bytes, x0 + per);
+          if (x1 > x0) std::memcpy(dst + x0, from + x0, (size_t)(x1 - x0));
+        };
+        stripe(hk + e0 * key_bytes, src, (e1 - e0) * key_bytes);
+        if (width) stripe(hp + e0 * width, src + (e1 - e0) * key_bytes, (e1 - e0) * width);
+#ifdef PM_HOST_TRACE
+        if (t == 0)
+          mv_done[c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+#endif
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(mover, t);
+    mover(0);
+    for (auto& th : pool) th.join();
+    if (err.load()) return cuda_fail(cudaGetLastError(), "pm_merge_host: staged write-back");
+  }
+#ifdef PM_HOST_TRACE
+  {
+    cudaStreamSynchronize(sD);
+    const double hend = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    float t0h;  // host offset of the device origin is unknown: report device times from the first record
+    (void)t0h;
+    fprintf(stderr, "TRACE nch=%d staged=%zu use_stage=%d host_end=%.2f\n", nch, stg.size(), (int)use_stage, hend);
+    for (int k = 0; k < nch; ++k) {
+      float u = -1, m = -1, d = -1;
+      cudaEventElapsedTime(&u, tr[3 * nch], tr[3 * k]);
+      cudaEventElapsedTime(&m, tr[3 * nch], tr[3 * k + 1]);
+      cudaEventElapsedTime(&d, tr[3 * nch], tr[3 * k + 2]);
+      fprintf(stderr, "TRACE k=%d free=%d up=%.2f merge=%.2f d2h=%.2f moved=%.2f\n", k, free_at[k], u, m, d,
+              mv_done[k]);
+    }
+    for (auto& e : tr) cudaEventDestroy(e);
+  }
+#endif
   return pm_status(ctx, stream, nullptr);
 }
 

@@ -357,6 +357,48 @@ def test_merge_host_vs_oracle(width):
         assert np.array_equal(pp, want_p), f"payload size={size}"
 
 
+@pytest.mark.parametrize("layout", ["rotation", "inside", "tiny_a", "tiny_b", "interleave", "halves_swap"])
+def test_merge_host_write_back_order(layout):
+    """pm_merge_host writes merged chunks back in the order their output ranges
+    become free (uploads in merge order): layouts whose ranges free up far from
+    chunk order, each over several pipeline chunks, == the stable merge."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(99)
+    n = 9 << 20  # several 2M-record chunks
+    if layout == "rotation":  # every B key below every A key
+        la = 5 << 20
+        a = np.sort(rng.integers(1000, 2000, la))
+        b = np.sort(rng.integers(0, 1000, n - la))
+    elif layout == "inside":  # B inside a narrow window of A
+        la = n - (1 << 20)
+        a = np.sort(rng.integers(0, 2**31 - 1, la))
+        b = np.sort(rng.integers(2**30, 2**30 + 1000, n - la))
+    elif layout == "tiny_a":
+        la = 3
+        a = np.array([5, 2**30, 2**31 - 2])
+        b = np.sort(rng.integers(0, 2**31 - 1, n - la))
+    elif layout == "tiny_b":
+        la = n - 2
+        a = np.sort(rng.integers(0, 2**31 - 1, la))
+        b = np.array([0, 2**31 - 1])
+    elif layout == "interleave":
+        la = n // 2
+        a = np.arange(la) * 2
+        b = np.arange(n - la) * 2 + 1
+    else:  # halves swap order, equal keys across the boundary
+        la = n // 3
+        a = np.sort(rng.integers(500, 1000, la))
+        b = np.sort(rng.integers(0, 501, n - la))
+    keys = np.concatenate([a, b]).astype(np.int32)
+    payload = np.arange(n, dtype=np.int32).view(np.uint8).reshape(-1, 4).copy()
+    want_k, want_p = keys.copy(), payload.copy()
+    orc.seq_merge_buffered(want_k, want_p, 0, la, n)
+    _ops.merge_host(keys, payload, 0, la, n)
+    assert np.array_equal(keys, want_k), layout
+    assert np.array_equal(payload, want_p), layout
+
+
 @pytest.mark.parametrize("dtype,width", [(np.int32, 4), (np.int64, 12), (np.int32, 0)])
 def test_large_jobs_vs_oracle(dtype, width):
     """2^22..2^24-record jobs (multi-level salvage, several waves of the grid) vs the oracle,
