@@ -815,7 +815,7 @@ def run_ours(args):
         "engine": {"name": "scheduled (pm_flow.cu)", "order": order,
                    "salvaged_records_frac": salvaged / n, "pool_bytes_used": salvaged * rec,
                    "pool_bytes_reserved": (n // 4) * rec,
-                   "salvage_estimates": {"angle": stats[5] / n, "two_front": stats[6] / n}},
+                   "salvage_estimates": {"angle": stats[5] / n if stats[5] < 2**63 else "not evaluated (two fronts already below n/32)", "two_front": stats[6] / n}},
         "bounded_pool_engine": bounded,
         "buffered_mode": buffered,
         "copy_mode": copy_mode,

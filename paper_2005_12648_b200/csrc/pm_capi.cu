@@ -14,6 +14,7 @@
 #include <vector>
 #include <string>
 #include <thread>
+#include <map>
 #include <chrono>
 
 #include "../../include/parmerge_b200.h"
@@ -75,6 +76,10 @@ struct pm_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // pm_merge_host: H2D, merge, D2H
   cudaEvent_t hev[33] = {};                          // [0]: joins; then per-chunk events (ring)
+  std::map<std::pair<int, size_t>, std::pair<int, int>> flow_occ;  // (key bytes, smem) -> k_flow, plan CTAs/SM
+  size_t flow_attr[2] = {0, 0};  // k_flow<int32/int64>: dynamic shared memory limit set so far
+  cudaStream_t fside = nullptr;  // the scheduled engine's gated fallback runs here (forked after the plan)
+  cudaEvent_t ffork = nullptr, fjoin = nullptr;  // (key bytes, smem) -> k_flow, plan CTAs/SM
   std::vector<cudaEvent_t> hup, hdn;  // pm_merge_host: per chunk, upload done / staged write-back landed
   void* hstage = nullptr;             // pm_merge_host: pinned host staging of early write-backs
   size_t hstage_bytes = 0;
@@ -541,9 +546,21 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
     return fail(PM_ERR_INTERNAL, "tile merge span exceeds the sentinel gap");
   P.smem_pay = w ? (size_t)align_up(M * w + 48, 128) : 0;
   const size_t smem = (kFlowStages + kFlowOut) * (P.smem_keys + P.smem_pay);
-  int bps = 0;
-  cudaError_t ce = ks == 4 ? flow_occupancy<int32_t>(smem, &bps) : flow_occupancy<int64_t>(smem, &bps);
-  if (ce != cudaSuccess) return cuda_fail(ce, "flow occupancy");
+  int bps = 0, plan_bps = 0;
+  cudaError_t ce;
+  {
+    auto it = ctx->flow_occ.find({ks, smem});
+    if (it == ctx->flow_occ.end()) {
+      size_t& attr = ctx->flow_attr[ks == 8];
+      attr = std::max(attr, smem);
+      ce = ks == 4 ? flow_occupancy<int32_t>(smem, attr, &bps, &plan_bps)
+                   : flow_occupancy<int64_t>(smem, attr, &bps, &plan_bps);
+      if (ce != cudaSuccess) return cuda_fail(ce, "flow occupancy");
+      it = ctx->flow_occ.emplace(std::make_pair(ks, smem), std::make_pair(bps, plan_bps)).first;
+    }
+    bps = it->second.first;
+    plan_bps = it->second.second;
+  }
   if (bps < 1) return fail(PM_ERR_UNSUPPORTED, "scheduled engine does not fit on an SM");
   const int grid = (int)std::min<int64_t>((int64_t)bps * ctx->num_sms, P.Q);
   P.grid = grid;
@@ -636,21 +653,35 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   P.err = &ctx->ctl->err_.v;
   P.noop = &ctx->ctl->noop_.v;
   P.need_space = &ctx->ctl->need_space_.v;
+  // the bounded-pool engine, gated on the plan's overflow word, runs on a side
+  // stream forked right after the plan: its five gated launches (~16 us of launch
+  // and exit when the flow engine runs) overlap the salvage copy and the merge
+  // instead of trailing them; the caller's stream joins it at the end.  The
+  // flow kernels exit at once when the word is set, so the two never both move data.
+  if (!ctx->fside) {
+    PM_CUDA(cudaStreamCreateWithFlags(&ctx->fside, cudaStreamNonBlocking));
+    PM_CUDA(cudaEventCreateWithFlags(&ctx->ffork, cudaEventDisableTiming));
+    PM_CUDA(cudaEventCreateWithFlags(&ctx->fjoin, cudaEventDisableTiming));
+  }
   // plan (splits, order, salvage, tickets) and merge
   if (ctx->timing) PM_CUDA(cudaEventRecord(ctx->ev[0], st));
-  ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr,
-                                      ctx->timing ? ctx->ev[3] : nullptr)
-               : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, st, ctx->timing ? ctx->ev[1] : nullptr,
-                                      ctx->timing ? ctx->ev[3] : nullptr);
+  ce = ks == 4 ? launch_flow<int32_t>(F, grid, smem, ctx->num_sms, plan_bps, st, ctx->timing ? ctx->ev[1] : nullptr,
+                                      ctx->timing ? ctx->ev[3] : nullptr, ctx->ffork)
+               : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, plan_bps, st, ctx->timing ? ctx->ev[1] : nullptr,
+                                      ctx->timing ? ctx->ev[3] : nullptr, ctx->ffork);
   ctx->ev_mid = ctx->timing;
   if (ce != cudaSuccess) return cuda_fail(ce, "k_flow launch");
   if (ctx->timing) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
     ctx->ev_recorded = true;
   }
-  // the bounded-pool engine, gated on the plan's overflow word
-    return run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, scratch_records, st, nullptr, nullptr, nullptr,
-                    nullptr, reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
+  PM_CUDA(cudaStreamWaitEvent(ctx->fside, ctx->ffork, 0));
+  rc = run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, scratch_records, ctx->fside, nullptr, nullptr,
+                  nullptr, nullptr, reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
+  if (rc) return rc;
+  PM_CUDA(cudaEventRecord(ctx->fjoin, ctx->fside));
+  PM_CUDA(cudaStreamWaitEvent(st, ctx->fjoin, 0));
+  return PM_OK;
 }
 
 static int check_common(pm_ctx* ctx, const void* keys, int ks, const void* payload, int64_t w) {
@@ -925,6 +956,9 @@ int pm_ctx_destroy(pm_ctx* ctx) {
     if (x) cudaStreamDestroy(x);
   for (auto& x : ctx->hev)
     if (x) cudaEventDestroy(x);
+  if (ctx->fside) cudaStreamDestroy(ctx->fside);
+  if (ctx->ffork) cudaEventDestroy(ctx->ffork);
+  if (ctx->fjoin) cudaEventDestroy(ctx->fjoin);
   for (auto& x : ctx->hup) cudaEventDestroy(x);
   for (auto& x : ctx->hdn) cudaEventDestroy(x);
   if (ctx->hstage) cudaFreeHost(ctx->hstage);

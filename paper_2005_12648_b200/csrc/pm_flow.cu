@@ -318,6 +318,7 @@ __device__ __forceinline__ void ph_readers(const FlowParams& F) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if (*(volatile int32_t*)P.noop) return;
   TwoFront tf{P.Q, P.qc};
+  unsigned long long sal_tf = 0;
   for (int64_t j = tid; j < P.K; j += nthr) {  // (Q == K: region j writes slot j)
     const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
     const bool idn = g.identity(j, a0, a1);
@@ -331,13 +332,16 @@ __device__ __forceinline__ void ph_readers(const FlowParams& F) {
     for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
     int i = 0;
     // every slot's middle record lies in exactly one region's A or B range: that
-    // region is the slot's reader D[] (the itinerary's next step)
+    // region is the slot's reader D[] (the itinerary's next step); the two-front
+    // order's salvage is counted here (it decides whether the itinerary phases run)
+    const int64_t oj = tf.order(j);
     for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
       const int64_t ymid = (g.slot_lo(jj) + g.slot_hi(jj) - 1) >> 1;
       if (lo <= ymid && ymid < hi) F.D[jj] = (int32_t)j | (sd ? (int32_t)0x80000000 : 0);
       if (!idn) {
         const int64_t base = g.slot_base(jj);
         pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
+        if (jj != j && oj > tf.order(jj)) sal_tf += (unsigned long long)(hi - lo);
       }
     });
 #pragma unroll
@@ -347,6 +351,9 @@ __device__ __forceinline__ void ph_readers(const FlowParams& F) {
     F.shi[j] = 0;
     F.pend[j] = 0;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sal_tf += __shfl_xor_sync(0xffffffffu, sal_tf, o);
+  if ((threadIdx.x & 31) == 0 && sal_tf) atomicAdd((unsigned long long*)&F.fc[FC_SAL_TF], sal_tf);
 }
 
 // ---- k_flow_angle: itinerary vector per slot --------------------------------------
@@ -441,7 +448,7 @@ __device__ __forceinline__ void ph_key(const FlowParams& F, int zbuf) {
   }
 }
 
-// ---- k_flow_choose: salvage volume of both orders ------------------------------
+// ---- k_flow_choose: salvage volume of the angle order (two fronts: ph_readers) ---
 // Region q reads piece (slot j, n records); it reads the salvage entry iff it
 // comes after j.  Angle order ties (same bin) are broken by region index here
 // (the counting sort breaks them arbitrarily -- an estimate suffices).
@@ -449,30 +456,21 @@ __device__ __forceinline__ void ph_choose(const FlowParams& F) {
   const EngineParams& P = F.P;
   if (block_flow_off(F) || F.force >= 0) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
-  TwoFront tf{P.Q, P.qc};
-  unsigned long long sa = 0, st = 0;
+  unsigned long long sa = 0;
   for (int64_t q = tid; q < P.Q; q += nthr) {
     if (F.idn[q]) continue;
     const uint32_t kq = F.key[q];
-    const int64_t oq = tf.order(q);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int4 pc = F.pieces[4 * q + i];
       if (pc.x < 0 || pc.x == q) continue;
       const uint32_t kj = F.key[pc.x];
       if (kq > kj || (kq == kj && q > pc.x)) sa += (unsigned long long)(pc.z - pc.y);
-      if (oq > tf.order(pc.x)) st += (unsigned long long)(pc.z - pc.y);
     }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    sa += __shfl_xor_sync(0xffffffffu, sa, o);
-    st += __shfl_xor_sync(0xffffffffu, st, o);
-  }
-  if ((threadIdx.x & 31) == 0 && (sa | st)) {
-    atomicAdd((unsigned long long*)&F.fc[FC_SAL_ANGLE], sa);
-    atomicAdd((unsigned long long*)&F.fc[FC_SAL_TF], st);
-  }
+  for (int o = 16; o; o >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, o);
+  if ((threadIdx.x & 31) == 0 && sa) atomicAdd((unsigned long long*)&F.fc[FC_SAL_ANGLE], sa);
 }
 
 // block-wide exclusive scan of one int32 per thread (blockDim.x <= 1024); returns
@@ -520,13 +518,14 @@ __device__ __forceinline__ void cta_scan_inplace(int32_t* v, int64_t n) {
 }
 
 // ---- k_flow_decide (one CTA): the order, then its scan ------------------------
-__device__ __forceinline__ void ph_decide(const FlowParams& F) {
+__device__ __forceinline__ void ph_decide(const FlowParams& F, bool skipped) {
   const EngineParams& P = F.P;
   if (block_flow_off(F)) return;
   __shared__ int32_t s_mode;
   if (threadIdx.x == 0) {
     int32_t mode = F.force;
-    if (mode < 0) mode = F.fc[FC_SAL_ANGLE] < F.fc[FC_SAL_TF] ? 1 : 0;
+    if (mode < 0) mode = !skipped && F.fc[FC_SAL_ANGLE] < F.fc[FC_SAL_TF] ? 1 : 0;
+    if (skipped) F.fc[FC_SAL_ANGLE] = -1;  // (not evaluated)
     if (mode == 2) {  // debug: exercise the device-side fallback
       F.fc[FC_FAIL] = 1;
       mode = 0;
@@ -712,6 +711,9 @@ __device__ __forceinline__ void ph_tickets(const FlowParams& F) {
 #ifndef PM_FLOW_DEBUG
 #define PM_FLOW_DEBUG 0
 #endif
+#ifndef PM_FLOW_TF_EARLY
+#define PM_FLOW_TF_EARLY 32
+#endif
 // tuning builds (-DPM_FLOW_DEBUG=1): %globaltimer after each phase -> stats[32 + k]
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -734,7 +736,13 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
   ph_readers(F);
   grid.sync();
   PM_FLOW_DBG(3);
-  if (F.force != 0) {  // (the two-front order needs no itinerary: lean plan)
+  // the two-front order needs no itinerary (lean plan): forced, or in auto mode
+  // when its salvage is already below 1/PM_FLOW_TF_EARLY of the job (skewed or
+  // translated inputs: the angle order could save at most that copy, its phases
+  // cost more); the word is final after the barrier, so every CTA agrees
+  const bool skip = F.force == 0 || (F.force < 0 && *(volatile long long*)&F.fc[FC_SAL_TF] * PM_FLOW_TF_EARLY <=
+                                                        (long long)(F.P.e - F.P.s));
+  if (!skip) {
     ph_angle(F);
     grid.sync();
     PM_FLOW_DBG(4);
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
     grid.sync();
     PM_FLOW_DBG(7);
   }
-  if (blockIdx.x == 0) ph_decide(F);
+  if (blockIdx.x == 0) ph_decide(F, skip && F.force < 0);
   grid.sync();
   PM_FLOW_DBG(8);
   ph_rank(F);
@@ -768,7 +776,10 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
 }
 
 // ---- k_flow_save: copy the salvage entries into the pool ------------------------
-// One warp per slot (grid-stride); 16-byte vectors, identical phase on both sides.
+// Each warp scans 32 slots at a time (one per lane), then copies the
+// slots that have an entry one after another with the whole warp (16-byte
+// vectors, identical phase on both sides): the scan is one round trip for all
+// but the largest jobs, and slots without salvage (most of them) cost nothing.
 __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
   const EngineParams& P = F.P;
   FlowGeo g(P);
@@ -776,18 +787,30 @@ __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
   const int lane = threadIdx.x & 31;
   const int64_t ks = P.ks, w = P.w;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j = w0; j < P.K; j += nw) {
-    const int32_t lo = F.slo[j], hi = F.shi[j];
-    if (hi <= lo) continue;
-    const int64_t base = g.slot_base(j);
-    // copy the records of the hull that belong to the job
-    const int64_t x0 = max(base + lo, g.slot_lo(j)), x1 = min(base + hi, g.slot_hi(j));
-    if (x1 <= x0) continue;
-    const int64_t dl = F.pdelta[j];
-    FLOW_CHECK(x0 + dl >= 0 && x1 + dl <= F.pool_cap && x0 >= P.s && x1 <= P.e);
-    copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (x0 + dl) * ks),
-                  reinterpret_cast<const uint8_t*>(P.keys + x0 * ks), (x1 - x0) * ks, lane);
-    if (w) copy_g2g_warp(F.pool_pay + (x0 + dl) * w, P.pay + x0 * w, (x1 - x0) * w, lane);
+  for (int64_t j0 = w0; j0 < P.K; j0 += nw * 32) {
+    const int64_t j = j0 + lane * nw;  // (lane-strided: every warp gets slots while K >= warps)
+    int64_t x0 = 0, x1 = 0, dl = 0;
+    if (j < P.K) {
+      const int32_t lo = F.slo[j], hi = F.shi[j];
+      if (hi > lo) {
+        const int64_t base = g.slot_base(j);
+        // the records of the hull that belong to the job
+        x0 = max(base + lo, g.slot_lo(j));
+        x1 = min(base + hi, g.slot_hi(j));
+        dl = F.pdelta[j];
+      }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, x1 > x0);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
+      const int64_t d = __shfl_sync(0xffffffffu, dl, src);
+      FLOW_CHECK(y0 + d >= 0 && y1 + d <= F.pool_cap && y0 >= P.s && y1 <= P.e);
+      copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (y0 + d) * ks),
+                    reinterpret_cast<const uint8_t*>(P.keys + y0 * ks), (y1 - y0) * ks, lane);
+      if (w) copy_g2g_warp(F.pool_pay + (y0 + d) * w, P.pay + y0 * w, (y1 - y0) * w, lane);
+    }
   }
 }
 
@@ -1063,11 +1086,17 @@ __global__ void __launch_bounds__(kFlowThreads) k_flow(FlowParams F) {
 }
 
 // ---- host launcher ---------------------------------------------------------------
+// (the caller caches both answers per device and geometry: these queries and the
+// attribute call cost more host time than the launches they configure)
+// attr_smem: the k_flow dynamic shared memory limit to set (>= smem; the largest any
+// call on this device has needed, so a cached geometry never sees a lowered limit)
 template <typename KT>
-cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t flow_occupancy(size_t smem, size_t attr_smem, int* blocks_per_sm, int* plan_blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr_smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_flow<KT>, kFlowThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_flow<KT>, kFlowThreads, smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(plan_blocks_per_sm, k_flow_plan<KT>, kFlowChunk, 0);
 }
 
 // plan kernels (after launch_plan's splits); ev (may be null) is recorded between
@@ -1078,11 +1107,9 @@ struct NvtxRange {
 };
 
 template <typename KT>
-cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev,
-                        cudaEvent_t ev_merge) {
-  int bps = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_flow_plan<KT>, kFlowChunk, 0);
-  if (e != cudaSuccess) return e;
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, int bps, cudaStream_t st,
+                        cudaEvent_t ev, cudaEvent_t ev_merge, cudaEvent_t ev_fork) {
+  cudaError_t e;
   if (bps < 1) return cudaErrorInvalidConfiguration;
   FlowParams Fa = F;
   void* args[] = {&Fa};
@@ -1103,12 +1130,14 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
     e = cudaEventRecord(ev, st);
     if (e != cudaSuccess) return e;
   }
+  if (ev_fork) {  // the gated fallback engine may start on a side stream from here
+    e = cudaEventRecord(ev_fork, st);
+    if (e != cudaSuccess) return e;
+  }
   {
     NvtxRange r("pm_flow: salvage copy");
     k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
   }
-  e = cudaFuncSetAttribute(k_flow<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   if (ev_merge) {
     e = cudaEventRecord(ev_merge, st);
     if (e != cudaSuccess) return e;
@@ -1122,9 +1151,11 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
   return cudaGetLastError();
 }
 
-template cudaError_t flow_occupancy<int32_t>(size_t, int*);
-template cudaError_t flow_occupancy<int64_t>(size_t, int*);
-template cudaError_t launch_flow<int32_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t, cudaEvent_t);
-template cudaError_t launch_flow<int64_t>(const FlowParams&, int, size_t, int, cudaStream_t, cudaEvent_t, cudaEvent_t);
+template cudaError_t flow_occupancy<int32_t>(size_t, size_t, int*, int*);
+template cudaError_t flow_occupancy<int64_t>(size_t, size_t, int*, int*);
+template cudaError_t launch_flow<int32_t>(const FlowParams&, int, size_t, int, int, cudaStream_t, cudaEvent_t,
+                                          cudaEvent_t, cudaEvent_t);
+template cudaError_t launch_flow<int64_t>(const FlowParams&, int, size_t, int, int, cudaStream_t, cudaEvent_t,
+                                          cudaEvent_t, cudaEvent_t);
 
 }  // namespace pm

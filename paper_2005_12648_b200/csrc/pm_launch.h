@@ -29,10 +29,11 @@ template <typename KT> cudaError_t buffered_occupancy(size_t smem, int* blocks_p
 constexpr int kFlowStages = PM_FLOW_STAGES;
 constexpr int kFlowOut = PM_FLOW_OUT;
 constexpr int kFlowThreads = PM_FLOW_THREADS;
-template <typename KT> cudaError_t flow_occupancy(size_t smem, int* blocks_per_sm);
 template <typename KT>
-cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, cudaStream_t st, cudaEvent_t ev,
-                        cudaEvent_t ev_merge);
+cudaError_t flow_occupancy(size_t smem, size_t attr_smem, int* blocks_per_sm, int* plan_blocks_per_sm);
+template <typename KT>
+cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms, int plan_bps, cudaStream_t st,
+                        cudaEvent_t ev, cudaEvent_t ev_merge, cudaEvent_t ev_fork);
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st);

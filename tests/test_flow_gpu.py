@@ -122,6 +122,40 @@ def test_lean_plan_small_jobs(flow_mode):
         _ops.set_engine_only(False)
 
 
+@pytest.mark.parametrize("kind", ["window", "translated", "uniform"])
+def test_early_two_front_decision(flow_mode, kind):
+    """Above PM_FLOW_TF_Q regions the plan counts the two-front salvage first and
+    skips the itinerary phases when it is already below n/32 (config-3-like skew,
+    a translated run); a uniform job still evaluates and takes the angle order.
+    Key + index payload, checked against a stable sort."""
+    flow_mode("auto")
+    g = torch.Generator(device="cuda").manual_seed(77)
+    la = 1 << 27
+    if kind == "window":  # B (2^16) inside a narrow window of A, as config 3
+        a = torch.randint(-(1 << 62), 1 << 62, (la,), device="cuda", dtype=torch.int64, generator=g).sort().values
+        lo, hi = a[la // 2 - (1 << 12)].item(), a[la // 2 + (1 << 12)].item()
+        b = torch.randint(lo, hi, (1 << 16,), device="cuda", dtype=torch.int64, generator=g).sort().values
+    elif kind == "translated":  # B = A's keys shifted up by a little: a near-translation
+        a = torch.randint(0, 1 << 40, (la,), device="cuda", dtype=torch.int64, generator=g).sort().values
+        b = a[: la // 2] + (1 << 20)
+    else:
+        a = torch.randint(0, 1 << 40, (la,), device="cuda", dtype=torch.int64, generator=g).sort().values
+        b = torch.randint(0, 1 << 40, (la,), device="cuda", dtype=torch.int64, generator=g).sort().values
+    k0 = torch.cat([a, b])
+    n = k0.numel()
+    p0 = torch.arange(n, device="cuda", dtype=torch.int32).view(torch.uint8).view(n, 4)
+    arr = pm.KeyedArray(k0.clone(), p0.clone())
+    st = _ops.merge(arr, 0, la, n)
+    order = torch.sort(k0, stable=True).indices
+    assert torch.equal(arr.keys, k0[order]) and torch.equal(arr.payload, p0[order])
+    if kind == "uniform":
+        assert st[4] == 2 and st[5] < n  # angle order, both orders evaluated
+    elif kind == "window":
+        assert st[4] == 1 and st[5] == 2**64 - 1  # two fronts, angle phases skipped
+    if st[5] == 2**64 - 1:
+        assert st[4] == 1 and st[6] * 32 <= n
+
+
 @pytest.mark.parametrize("dist", ["exp", "steps", "clustered"])
 def test_split_search_skewed_keys(flow_mode, dist):
     """The split phase interpolates between sample values before its binary search;

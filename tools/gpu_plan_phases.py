@@ -1,6 +1,6 @@
 """Per-phase times of the cooperative plan kernel (build with -DPM_FLOW_DEBUG=1).
 
-usage: PM_LIB=libparmerge_b200_<v>.so python tools/gpu_plan_phases.py [L]
+usage: PM_LIB=libparmerge_b200_<v>.so python tools/gpu_plan_phases.py [L] [cfg]
 """
 import ctypes
 import sys
@@ -13,7 +13,8 @@ from paper_2005_12648_b200 import _capi, _ops
 from paper_2005_12648_b200.workloads import config_input_device
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 29
-k0, p0, m = config_input_device(2, seed=3, log_len=L)
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+k0, p0, m = config_input_device(cfg, seed=3, log_len=L)
 n = k0.numel()
 arr = pm.KeyedArray(k0.clone(), p0.clone())
 names = ["sample", "split", "readers", "angle", "sync*", "key", "choose", "decide", "rank", "hull", "alloc", "tickets"]
