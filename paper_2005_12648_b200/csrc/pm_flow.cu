@@ -318,42 +318,57 @@ __device__ __forceinline__ void ph_readers(const FlowParams& F) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if (*(volatile int32_t*)P.noop) return;
   TwoFront tf{P.Q, P.qc};
-  unsigned long long sal_tf = 0;
-  for (int64_t j = tid; j < P.K; j += nthr) {  // (Q == K: region j writes slot j)
-    const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
-    const bool idn = g.identity(j, a0, a1);
-    F.idn[j] = idn ? 1 : 0;
-    if (idn) {  // identity regions per two-front chunk (ph_rank's compaction), and in total
-      atomicAdd(&F.chunk[tf.order(j) / kFlowChunk], 1);
-      atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], 1ull);
+  unsigned long long sal_tf = 0, nid = 0;
+  const int lane = threadIdx.x & 31;
+  // (warp-uniform trip count: the identity counts below are warp-aggregated --
+  //  one atomic per warp and chunk instead of one per region; skewed jobs such as
+  //  config 3 have tens of thousands of identity regions)
+  for (int64_t jb = tid - lane; jb < P.K; jb += nthr) {  // (Q == K: region j writes slot j)
+    const int64_t j = jb + lane;
+    bool idn = false;
+    if (j < P.K) {
+      const int64_t a0 = g.split(j), a1 = g.split(j + 1), d0 = g.diag(j), d1 = g.diag(j + 1);
+      idn = g.identity(j, a0, a1);
+      F.idn[j] = idn ? 1 : 0;
+      int4 pc[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
+      int i = 0;
+      // every slot's middle record lies in exactly one region's A or B range: that
+      // region is the slot's reader D[] (the itinerary's next step); the two-front
+      // order's salvage is counted here (it decides whether the itinerary phases run)
+      const int64_t oj = tf.order(j);
+      for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
+        const int64_t ymid = (g.slot_lo(jj) + g.slot_hi(jj) - 1) >> 1;
+        if (lo <= ymid && ymid < hi) F.D[jj] = (int32_t)j | (sd ? (int32_t)0x80000000 : 0);
+        if (!idn) {
+          const int64_t base = g.slot_base(jj);
+          pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
+          if (jj != j && oj > tf.order(jj)) sal_tf += (unsigned long long)(hi - lo);
+        }
+      });
+#pragma unroll
+      for (int k = 0; k < 4; ++k) F.pieces[4 * j + k] = pc[k];
+      F.rank[j] = INT32_MAX;
+      F.slo[j] = (int32_t)P.T;
+      F.shi[j] = 0;
+      F.pend[j] = 0;
     }
-    int4 pc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) pc[i] = make_int4(-1, 0, 0, 0);
-    int i = 0;
-    // every slot's middle record lies in exactly one region's A or B range: that
-    // region is the slot's reader D[] (the itinerary's next step); the two-front
-    // order's salvage is counted here (it decides whether the itinerary phases run)
-    const int64_t oj = tf.order(j);
-    for_pieces(P, P.s + a0, P.s + a1, P.m + d0 - a0, P.m + d1 - a1, [&](int64_t jj, int64_t lo, int64_t hi, int k, int sd) {
-      const int64_t ymid = (g.slot_lo(jj) + g.slot_hi(jj) - 1) >> 1;
-      if (lo <= ymid && ymid < hi) F.D[jj] = (int32_t)j | (sd ? (int32_t)0x80000000 : 0);
-      if (!idn) {
-        const int64_t base = g.slot_base(jj);
-        pc[i++] = make_int4((int32_t)jj, (int32_t)(lo - base), (int32_t)(hi - base), 2 * sd + k);
-        if (jj != j && oj > tf.order(jj)) sal_tf += (unsigned long long)(hi - lo);
-      }
-    });
-#pragma unroll
-    for (int k = 0; k < 4; ++k) F.pieces[4 * j + k] = pc[k];
-    F.rank[j] = INT32_MAX;
-    F.slo[j] = (int32_t)P.T;
-    F.shi[j] = 0;
-    F.pend[j] = 0;
+    // identity regions per two-front chunk (ph_rank's compaction), and in total
+    if (__ballot_sync(0xffffffffu, idn)) {
+      const int64_t c = idn ? tf.order(j) / kFlowChunk : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, c);
+      if (idn && lane == __ffs(peers) - 1) atomicAdd(&F.chunk[c], __popc(peers));
+      nid += idn ? 1 : 0;
+    }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sal_tf += __shfl_xor_sync(0xffffffffu, sal_tf, o);
-  if ((threadIdx.x & 31) == 0 && sal_tf) atomicAdd((unsigned long long*)&F.fc[FC_SAL_TF], sal_tf);
+  for (int o = 16; o; o >>= 1) {
+    sal_tf += __shfl_xor_sync(0xffffffffu, sal_tf, o);
+    nid += __shfl_xor_sync(0xffffffffu, nid, o);
+  }
+  if (lane == 0 && sal_tf) atomicAdd((unsigned long long*)&F.fc[FC_SAL_TF], sal_tf);
+  if (lane == 0 && nid) atomicAdd((unsigned long long*)&F.fc[FC_NIDENT], nid);
 }
 
 // ---- k_flow_angle: itinerary vector per slot --------------------------------------
@@ -776,10 +791,14 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
 }
 
 // ---- k_flow_save: copy the salvage entries into the pool ------------------------
-// Each warp scans 32 slots at a time (one per lane), then copies the
-// slots that have an entry one after another with the whole warp (16-byte
-// vectors, identical phase on both sides): the scan is one round trip for all
-// but the largest jobs, and slots without salvage (most of them) cost nothing.
+// Work items are (slot, chunk of the slot): a skewed job's salvage sits in a few
+// slots, and one warp copying a whole 32 KB entry is a chain of dependent round
+// trips; chunks spread an entry over several warps.  As many chunks per slot as
+// keep the scan to one pass (lanes of all warps >= items), at least 8 KB of keys
+// each (2 KB items: 0.24 -> 0.35 ms at 2^30 int32, 0.07 -> 0.11 ms at config 4).
+// Each warp scans 32 items at a time (one per lane, lane-strided so every warp
+// gets items), then copies the items that hold salvage one after another with
+// the whole warp (16-byte vectors, identical phase on both sides).
 __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
   const EngineParams& P = F.P;
   FlowGeo g(P);
@@ -787,11 +806,14 @@ __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
   const int lane = threadIdx.x & 31;
   const int64_t ks = P.ks, w = P.w;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j0 = w0; j0 < P.K; j0 += nw * 32) {
-    const int64_t j = j0 + lane * nw;  // (lane-strided: every warp gets slots while K >= warps)
+  const int64_t nc = max((int64_t)1, min(32 * nw / P.K, P.T * ks / 8192)), items = P.K * nc;
+  const int32_t csz = (int32_t)((P.T + nc - 1) / nc);
+  for (int64_t i0 = w0; i0 < items; i0 += nw * 32) {
+    const int64_t it = i0 + lane * nw;  // (lane-strided: every warp gets items while items >= warps)
     int64_t x0 = 0, x1 = 0, dl = 0;
-    if (j < P.K) {
-      const int32_t lo = F.slo[j], hi = F.shi[j];
+    if (it < items) {
+      const int64_t j = it / nc, c = it - j * nc;
+      const int32_t lo = max(F.slo[j], (int32_t)c * csz), hi = min(F.shi[j], (int32_t)(c + 1) * csz);
       if (hi > lo) {
         const int64_t base = g.slot_base(j);
         // the records of the hull that belong to the job
