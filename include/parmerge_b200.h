@@ -172,7 +172,8 @@ int pm_ipc_close(void *ptr);
  * the last job's counters: [0] salvaged units, [1] salvaged records, [2] merged
  * regions, [3] identity (skipped) regions, [4..9] summed per-CTA cycles in the
  * engine phases (ticket, gather issue, gather land, salvage, merge, store),
- * [10..11] spin iterations in reader / occupant waits.
+ * [10..11] spin iterations in reader / occupant waits; [13] 1 when a pure
+ * rotation took the block-exchange route (three reversals) instead of the engine.
  */
 int pm_status(pm_ctx *ctx, void *stream, uint64_t *stats);
 

@@ -679,6 +679,19 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
   rc = run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, scratch_records, ctx->fside, nullptr, nullptr,
                   nullptr, nullptr, reinterpret_cast<const int32_t*>(&F.fc[FC_FAIL]));
   if (rc) return rc;
+  // a pure rotation (every B key below every A key) whose salvage overflows the pool
+  // (N/2 for equal runs) takes a gated block exchange instead of the bounded-pool
+  // engine: equal runs one block swap (2 N w of traffic), otherwise three streaming
+  // reversals (4 N w); neither needs workspace
+  if (!nleaves) {
+    const int32_t* rg = reinterpret_cast<const int32_t*>(&F.fc[FC_ROTFAIL]);
+    if (m - s == e - m)
+      ce = launch_swap_blocks(keys, ks, payload, w, s, m - s, ctx->num_sms, ctx->fside, rg);
+    else
+      ce = ks == 4 ? launch_rotate<int32_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg)
+                   : launch_rotate<int64_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg);
+    if (ce != cudaSuccess) return cuda_fail(ce, "block exchange launch (gated)");
+  }
   PM_CUDA(cudaEventRecord(ctx->fjoin, ctx->fside));
   PM_CUDA(cudaStreamWaitEvent(st, ctx->fjoin, 0));
   return PM_OK;
@@ -1076,6 +1089,14 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
   if (lo < 0 || len_a < 0 || len_b < 0) return fail(PM_ERR_ARG, "lengths must be non-negative");  // shift.py:157
   if (len_a == 0 || len_b == 0) return PM_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // equal blocks: one swap pass, every record read and written once
+  if (len_a == len_b && !ctx->engine_only) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_stream(ctx, st);
+    const cudaError_t e = launch_swap_blocks(keys, key_bytes, payload, width, lo, len_a, ctx->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_swap_blocks launch");
+    return PM_OK;
+  }
   // one small block: stash it, slide the big block over it in one pass, land the
   // stash at the far end (the reference's staged exchange, _kernels.py:46-90)
   const int64_t small = std::min(len_a, len_b), big = std::max(len_a, len_b);

@@ -181,8 +181,11 @@ struct FlowTicket {
 static_assert(sizeof(FlowTicket) == 80, "FlowTicket is loaded as five 16-byte vectors");
 
 // flow control words (int64, one 256-byte line)
+// FC_ROT: the job is a pure rotation (every B key below every A key; set by the
+// sample phase); FC_ROTFAIL: its salvage overflowed the pool, so the gated block
+// exchange (three reversals, pm_rotate.cu) runs instead of the bounded-pool engine
 enum : int { FC_SAL_ANGLE = 0, FC_SAL_TF = 1, FC_POOL = 2, FC_NIDENT = 3, FC_MODE = 4, FC_FAIL = 5, FC_NTICK = 6,
-             FC_NSALV = 7, FC_WORDS = 32 };
+             FC_NSALV = 7, FC_ROT = 8, FC_ROTFAIL = 9, FC_WORDS = 32 };
 
 struct FlowParams {
   EngineParams P;       // geometry (T == M, one slot per region, Q == K), splits, ticket/err/noop/stats

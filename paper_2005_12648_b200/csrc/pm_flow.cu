@@ -133,7 +133,8 @@ __device__ __forceinline__ void for_pieces(const EngineParams& P, int64_t xa0, i
 }
 
 __device__ __forceinline__ bool flow_off(const FlowParams& F) {
-  return *(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_FAIL];
+  return *(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_FAIL] ||
+         *(volatile long long*)&F.fc[FC_ROTFAIL];
 }
 // The same test inside the cooperative plan, where FC_FAIL may be raised during a
 // phase (k_flow_alloc / the forced fallback): one thread reads it for the whole
@@ -161,7 +162,7 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
   const KT* B = reinterpret_cast<const KT*>(P.keys) + P.m;
   KT* sa = reinterpret_cast<KT*>(F.samp_a);
   KT* sb = reinterpret_cast<KT*>(F.samp_b);
-  if (tid < FC_WORDS) F.fc[tid] = 0;
+  if (tid < FC_WORDS && tid != FC_ROT) F.fc[tid] = 0;  // (FC_ROT: thread 0 below)
   for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;  // (before ph_readers counts identity regions)
   for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
   if (tid == 0) {
@@ -169,6 +170,7 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
     // (a prescribed layout has no such shortcut: identity regions are skipped instead)
     const bool nothing = P.m == P.s || P.m == P.e || (!F.nleaves && A[P.m - P.s - 1] <= B[0]);  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
+    F.fc[FC_ROT] = !nothing && !F.nleaves && A[0] > B[P.e - P.m - 1] ? 1 : 0;
     for (int i = 0; i < 16; ++i) P.stats[i] = 0;
   }
   // (four independent strided loads in flight per thread before their stores)
@@ -658,8 +660,9 @@ __device__ __forceinline__ void ph_alloc(const FlowParams& F) {
     __syncthreads();
     if (sz) {
       const long long off = base + ex;  // multiple of 16 records
-      if (off + sz > F.pool_cap) {
-        atomicExch((unsigned long long*)&F.fc[FC_FAIL], 1ull);
+      if (off + sz > F.pool_cap) {  // (a pure rotation takes the block exchange instead)
+        atomicExch((unsigned long long*)&F.fc[F.fc[FC_ROT] ? FC_ROTFAIL : FC_FAIL], 1ull);
+        if (F.fc[FC_ROT]) P.stats[13] = 1;  // pm_status: the block-exchange route ran
       } else {
         F.pdelta[j] = off - (g.slot_base(j) + L);
         atomicAdd((unsigned long long*)&F.fc[FC_NSALV], 1ull);

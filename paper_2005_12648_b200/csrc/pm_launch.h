@@ -36,7 +36,10 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
                         cudaEvent_t ev, cudaEvent_t ev_merge, cudaEvent_t ev_fork);
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
-                          cudaStream_t st);
+                          cudaStream_t st, const int32_t* gate = nullptr);  // gate: run only if *gate != 0
+// equal blocks: [lo, lo + len) <-> [lo + len, lo + 2 len), keys and payload planes (gated likewise)
+cudaError_t launch_swap_blocks(void* keys, int ks, void* payload, int64_t w, int64_t lo, int64_t len, int num_sms,
+                               cudaStream_t st, const int32_t* gate = nullptr);
 // staged path: gate = A[m-1] > B[0]; a copy that runs only if the gate is set
 cudaError_t launch_order_gate(const void* keys, int ks, int64_t m, int32_t* gate, cudaStream_t st);
 cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32_t* gate, int num_sms, cudaStream_t st);

@@ -5,6 +5,7 @@
 // (_kernels.py:92-197) behind pm_shift; the result is the same array (the
 // reference's instrumented move counts are computed on the host, shift.py).
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include <algorithm>
 #include <cstdint>
@@ -41,8 +42,9 @@ __device__ __forceinline__ void swap_rows(uint8_t* pay, int64_t w, bool w4, int6
 // mirrored ones descend, both coalesced.  Four pairs per thread per round keep
 // eight loads in flight.
 template <typename KT>
-__global__ void __launch_bounds__(256) k_reverse(KT* keys, uint8_t* pay, int64_t w, int64_t lo0, int64_t len0,
-                                                 int64_t lo1, int64_t len1) {
+__global__ void __launch_bounds__(256) k_reverse(const int32_t* gate, KT* keys, uint8_t* pay, int64_t w, int64_t lo0,
+                                                 int64_t len0, int64_t lo1, int64_t len1) {
+  if (gate && !*(volatile const int32_t*)gate) return;
   const int64_t p0 = len0 >> 1, np = p0 + (len1 >> 1);
   const bool w4 = w && (w & 3) == 0 && (((uintptr_t)pay) & 3) == 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -84,7 +86,9 @@ __global__ void __launch_bounds__(256) k_reverse(KT* keys, uint8_t* pay, int64_t
 // before the first aligned chunk and after the last full one are swapped by one
 // extra job per segment, element by element.  Jobs never share a record.
 template <typename KT, int C>
-__global__ void __launch_bounds__(256) k_reverse_vec(KT* keys, int64_t lo0, int64_t len0, int64_t lo1, int64_t len1) {
+__global__ void __launch_bounds__(256) k_reverse_vec(const int32_t* gate, KT* keys, int64_t lo0, int64_t len0, int64_t lo1,
+                                                     int64_t len1) {
+  if (gate && !*(volatile const int32_t*)gate) return;
   constexpr int V = 16 / sizeof(KT);
   __shared__ __align__(16) KT Lb[C];
   __shared__ __align__(16) KT Rb[C + 2 * V];
@@ -170,8 +174,9 @@ template <> struct RowWord<2> { using T = uint16_t; };
 template <> struct RowWord<1> { using T = uint8_t; };
 
 template <typename KT, int V>
-__global__ void __launch_bounds__(256) k_reverse_wide(KT* keys, uint8_t* pay, int64_t w, int64_t lo0, int64_t len0,
-                                                      int64_t lo1, int64_t len1) {
+__global__ void __launch_bounds__(256) k_reverse_wide(const int32_t* gate, KT* keys, uint8_t* pay, int64_t w, int64_t lo0,
+                                                      int64_t len0, int64_t lo1, int64_t len1) {
+  if (gate && !*(volatile const int32_t*)gate) return;
   using T = typename RowWord<V>::T;
   constexpr int CW = 4;
   const int lane = threadIdx.x & 31;
@@ -212,14 +217,14 @@ __global__ void __launch_bounds__(256) k_reverse_wide(KT* keys, uint8_t* pay, in
 
 template <typename KT, int V>
 static void reverse_wide_pair(KT* k, uint8_t* p, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
-                              cudaStream_t st) {
+                              cudaStream_t st, const int32_t* gate) {
   const int64_t nch = (w / V + 127) / 128;
   const int64_t pairs = (la >> 1) + (lb >> 1), all = (la + lb) >> 1;
   auto grid_for = [&](int64_t items) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)num_sms * 8));
   };
-  if (pairs > 0) k_reverse_wide<KT, V><<<grid_for(pairs * nch), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);
-  if (all > 0) k_reverse_wide<KT, V><<<grid_for(all * nch), 256, 0, st>>>(k, p, w, lo, la + lb, 0, 0);
+  if (pairs > 0) k_reverse_wide<KT, V><<<grid_for(pairs * nch), 256, 0, st>>>(gate, k, p, w, lo, la, lo + la, lb);
+  if (all > 0) k_reverse_wide<KT, V><<<grid_for(all * nch), 256, 0, st>>>(gate, k, p, w, lo, la + lb, 0, 0);
   count_launches((pairs > 0) + (all > 0));
 }
 
@@ -365,9 +370,81 @@ cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool rig
   return cudaGetLastError();
 }
 
+#ifndef PM_SWAP_HINTS
+#define PM_SWAP_HINTS 1  // streaming (evict-first) loads / stores in the block swap
+#endif
+#if PM_SWAP_HINTS
+#define SWAP_LD(p) __ldcs(p)
+#define SWAP_ST(p, v) __stcs(p, v)
+#else
+#define SWAP_LD(p) (*(p))
+#define SWAP_ST(p, v) (*(p) = (v))
+#endif
+// ---- block swap of two equal adjacent blocks: [X | Y] -> [Y | X] ----------------
+// A rotation with |A| == |B| needs no reversal: every word of X trades places with
+// the word len bytes ahead (one read and one write per record: 2 N w of traffic
+// instead of the reversals' 4 N w).  Grid-stride, four words per thread in flight;
+// 16-byte words when both blocks share the 16-byte grid, else 4- or 1-byte words.
+template <typename WT>
+__global__ void __launch_bounds__(256) k_swap_blocks(const int32_t* gate, uint8_t* x, int64_t nbytes) {
+  if (gate && !*(volatile const int32_t*)gate) return;
+  WT* a = reinterpret_cast<WT*>(x);
+  WT* b = reinterpret_cast<WT*>(x + nbytes);
+  const int64_t n = nbytes / (int64_t)sizeof(WT), stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
+    WT va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        va[u] = SWAP_LD(a + i);
+        vb[u] = SWAP_LD(b + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        SWAP_ST(a + i, vb[u]);
+        SWAP_ST(b + i, va[u]);
+      }
+    }
+  }
+}
+
+// grid: every resident CTA once (a grid-stride kernel with a second partial wave
+// leaves the late CTAs running alone: 0.66 of the copy peak at 2^30 with 1184 CTAs)
+template <typename WT>
+static cudaError_t swap_launch(uint8_t* x, int64_t nbytes, int num_sms, cudaStream_t st, const int32_t* gate) {
+  int bps = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_swap_blocks<WT>, 256, 0);
+  if (e != cudaSuccess) return e;
+  const int64_t words = nbytes / (int64_t)sizeof(WT);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((words + 1023) / 1024, (int64_t)num_sms * std::max(bps, 1)));
+  k_swap_blocks<WT><<<grid, 256, 0, st>>>(gate, x, nbytes);
+  return cudaGetLastError();
+}
+static cudaError_t swap_plane(uint8_t* x, int64_t nbytes, int num_sms, cudaStream_t st, const int32_t* gate) {
+  if (nbytes <= 0) return cudaSuccess;
+  const uintptr_t al = (uintptr_t)x | (uintptr_t)nbytes;
+  count_launches(1);
+  if ((al & 15) == 0) return swap_launch<uint4>(x, nbytes, num_sms, st, gate);
+  if ((al & 3) == 0) return swap_launch<uint32_t>(x, nbytes, num_sms, st, gate);
+  return swap_launch<uint8_t>(x, nbytes, num_sms, st, gate);
+}
+
+// [lo, lo + len) <-> [lo + len, lo + 2 len) in the keys and the payload planes
+cudaError_t launch_swap_blocks(void* keys, int ks, void* payload, int64_t w, int64_t lo, int64_t len, int num_sms,
+                               cudaStream_t st, const int32_t* gate) {
+  cudaError_t e = swap_plane(static_cast<uint8_t*>(keys) + lo * ks, len * ks, num_sms, st, gate);
+  if (e == cudaSuccess && w) e = swap_plane(static_cast<uint8_t*>(payload) + lo * w, len * w, num_sms, st, gate);
+  return e;
+}
+
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int32_t* gate) {
   KT* k = static_cast<KT*>(keys);
   uint8_t* p = static_cast<uint8_t*>(payload);
   const int64_t pairs = (la >> 1) + (lb >> 1);
@@ -375,32 +452,43 @@ cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int6
   auto grid_for = [&](int64_t np) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((np + 1023) / 1024, (int64_t)num_sms * 8));
   };
-  if (!w && (((uintptr_t)keys) & 15) == 0) {
-    // keys only: vectorised block jobs (the array base must be 16-byte aligned)
-    constexpr int C = 8192 / sizeof(KT);
+  // vectorised block jobs on one plane of 4- or 8-byte elements (its base 16-byte aligned)
+  auto vec_plane = [&](auto* base) {
+    using ET = std::remove_pointer_t<decltype(base)>;
+    constexpr int C = 8192 / sizeof(ET);
     auto jobs = [&](int64_t a, int64_t b) { return (a / 2) / C + (b / 2) / C + 2; };
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>(jobs(la, lb), (int64_t)num_sms * 8));
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(jobs(la + lb, 0), (int64_t)num_sms * 8));
-    if (pairs > 0) k_reverse_vec<KT, C><<<g1, 256, 0, st>>>(k, lo, la, lo + la, lb);
-    if (all > 0) k_reverse_vec<KT, C><<<g2, 256, 0, st>>>(k, lo, la + lb, 0, 0);
+    if (pairs > 0) k_reverse_vec<ET, C><<<g1, 256, 0, st>>>(gate, base, lo, la, lo + la, lb);
+    if (all > 0) k_reverse_vec<ET, C><<<g2, 256, 0, st>>>(gate, base, lo, la + lb, 0, 0);
     count_launches((pairs > 0) + (all > 0));
+  };
+  const bool kal = (((uintptr_t)keys) & 15) == 0, pal = (((uintptr_t)payload) & 15) == 0;
+  if (kal && (!w || ((w == 4 || w == 8) && pal))) {
+    // keys, and 4- / 8-byte payload rows as a plane of int32 / int64 elements (SoA):
+    // each plane reversed with 16-byte vectors (a row-wise swap is 3-4x slower)
+    vec_plane(k);
+    if (w == 4) vec_plane(reinterpret_cast<int32_t*>(p));
+    if (w == 8) vec_plane(reinterpret_cast<int64_t*>(p));
     return cudaGetLastError();
   }
   if (w >= PM_ROTATE_WIDE_MIN) {
     const uintptr_t al = (uintptr_t)p | (uintptr_t)w;
-    if ((al & 15) == 0) reverse_wide_pair<KT, 16>(k, p, w, lo, la, lb, num_sms, st);
-    else if ((al & 7) == 0) reverse_wide_pair<KT, 8>(k, p, w, lo, la, lb, num_sms, st);
-    else if ((al & 3) == 0) reverse_wide_pair<KT, 4>(k, p, w, lo, la, lb, num_sms, st);
-    else if ((al & 1) == 0) reverse_wide_pair<KT, 2>(k, p, w, lo, la, lb, num_sms, st);
-    else reverse_wide_pair<KT, 1>(k, p, w, lo, la, lb, num_sms, st);
+    if ((al & 15) == 0) reverse_wide_pair<KT, 16>(k, p, w, lo, la, lb, num_sms, st, gate);
+    else if ((al & 7) == 0) reverse_wide_pair<KT, 8>(k, p, w, lo, la, lb, num_sms, st, gate);
+    else if ((al & 3) == 0) reverse_wide_pair<KT, 4>(k, p, w, lo, la, lb, num_sms, st, gate);
+    else if ((al & 1) == 0) reverse_wide_pair<KT, 2>(k, p, w, lo, la, lb, num_sms, st, gate);
+    else reverse_wide_pair<KT, 1>(k, p, w, lo, la, lb, num_sms, st, gate);
     return cudaGetLastError();
   }
-  if (pairs > 0) k_reverse<KT><<<grid_for(pairs), 256, 0, st>>>(k, p, w, lo, la, lo + la, lb);
-  if (all > 0) k_reverse<KT><<<grid_for(all), 256, 0, st>>>(k, p, w, lo, la + lb, 0, 0);
+  if (pairs > 0) k_reverse<KT><<<grid_for(pairs), 256, 0, st>>>(gate, k, p, w, lo, la, lo + la, lb);
+  if (all > 0) k_reverse<KT><<<grid_for(all), 256, 0, st>>>(gate, k, p, w, lo, la + lb, 0, 0);
   count_launches((pairs > 0) + (all > 0));
   return cudaGetLastError();
 }
-template cudaError_t launch_rotate<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
-template cudaError_t launch_rotate<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
+template cudaError_t launch_rotate<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t,
+                                            const int32_t*);
+template cudaError_t launch_rotate<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t,
+                                            const int32_t*);
 
 }  // namespace pm

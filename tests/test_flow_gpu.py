@@ -81,17 +81,44 @@ def test_misaligned_bases(flow_mode, mode, koff, poff, width):
 
 
 def test_pool_overflow_falls_back(flow_mode):
-    """One big rotation needs half the job salvaged (> the pool's N/4 under the
+    """A near-rotation needs half the job salvaged (> the pool's N/4 under the
     itinerary order): the plan raises the overflow word and the gated bounded-pool
     engine merges instead."""
     flow_mode("angle")
     h = 1 << 22
     ar = torch.arange(h, device="cuda", dtype=torch.int32)
     k0 = torch.cat([ar + h, ar])
+    k0[-1] = 3 * h  # B's last key above A's first: not a pure rotation
     arr = pm.KeyedArray(k0.clone())
     st = _ops.merge(arr, 0, h, 2 * h)
     assert torch.equal(arr.keys, torch.sort(k0).values)
-    assert st[4] == 0  # no scheduled order reported: the bounded-pool engine ran
+    assert st[4] == 0 and st[13] == 0  # no scheduled order reported: the bounded-pool engine ran
+
+
+@pytest.mark.parametrize("mode", ["auto", "angle"])
+@pytest.mark.parametrize("la,lb,width,dtype", [(1 << 22, 1 << 22, 0, torch.int32), (3 << 21, 5 << 20, 4, torch.int32),
+                                                (1 << 21, 1 << 21, 12, torch.int64), (1 << 20, 1 << 22, 0, torch.int64)])
+def test_pure_rotation_block_exchange(flow_mode, mode, la, lb, width, dtype):
+    """Every B key below every A key (ties are not a rotation) with salvage over the
+    pool: the gated three-reversal block exchange runs instead of the bounded-pool
+    engine (stats[13]); keys and payload rows exactly B then A."""
+    flow_mode(mode)
+    g = torch.Generator(device="cuda").manual_seed(la + lb + width)
+    a = torch.randint(1000, 2000, (la,), device="cuda", dtype=torch.int64, generator=g).sort().values.to(dtype)
+    b = torch.randint(0, 1000, (lb,), device="cuda", dtype=torch.int64, generator=g).sort().values.to(dtype)
+    k0 = torch.cat([a, b])
+    n = la + lb
+    p0 = torch.randint(0, 256, (n, width), device="cuda", dtype=torch.uint8, generator=g)
+    arr = pm.KeyedArray(k0.clone(), p0.clone())
+    st = _ops.merge(arr, 0, la, n)
+    assert torch.equal(arr.keys, torch.cat([b, a]))
+    assert torch.equal(arr.payload, torch.cat([p0[la:], p0[:la]]))
+    if mode == "angle" and la == lb:  # salvage N/2 > the N/4 pool
+        assert st[13] == 1
+    if st[13] == 0:  # the plan's salvage fitted the pool: the scheduled engine merged it
+        assert st[4] in (1, 2)
+    else:
+        assert st[4] == 0
 
 
 def test_lean_plan_small_jobs(flow_mode):

@@ -473,6 +473,29 @@ def test_shift_offsets_and_alignment(dtype):
             assert np.array_equal(got, want), f"lo={lo} la={la} lb={lb} {dtype.__name__}"
 
 
+@pytest.mark.parametrize("width", [0, 1, 4, 8, 12])
+def test_shift_equal_blocks(width):
+    """Equal blocks take the one-pass block swap (pm_shift and the gated rotation
+    route): every byte phase of keys and payload rows (16-byte, 4-byte and byte words)."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(808 + width)
+    n = 200_011
+    for dtype in (np.int32, np.int64):
+        base = rng.integers(-10**6, 10**6, n).astype(dtype)
+        pbase = rng.integers(0, 256, (n, width), dtype=np.uint8)
+        for lo in (0, 1, 3, 4):
+            for L in (1, 2, 3, 4, 5, 31, 64, 99_999):
+                keys, pay = base.copy(), pbase.copy()
+                want_k, want_p = keys.copy(), pay.copy()
+                want_k[lo:lo + 2 * L] = np.concatenate([keys[lo + L:lo + 2 * L], keys[lo:lo + L]])
+                want_p[lo:lo + 2 * L] = np.concatenate([pay[lo + L:lo + 2 * L], pay[lo:lo + L]])
+                arr = to_gpu(keys, pay)
+                _ops.shift(arr, lo, L, L)
+                pm.synchronize()
+                assert_same(arr, want_k, want_p, f"lo={lo} L={L} w={width} {dtype.__name__}")
+
+
 def _wide_cases(rng, width):
     """Wide-row instances: random, heavy duplicates, exact interleave (many short
     cycles), B entirely before A (one rotation), all-equal keys (identity).
