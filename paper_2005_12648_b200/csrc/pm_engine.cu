@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(256) k_copy_run(EngineParams P, int64_t x0, in
     for (int64_t b = tid; b < head; b += nthr) dst[b] = src[b];
     const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
     uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (int64_t i = tid; i < nv; i += nthr) d4[i] = __ldcs(s4 + i);
+    for (int64_t i = tid; i < nv; i += nthr) d4[i] = PM_COPY_LD(s4 + i);
     for (int64_t b = head + (nv << 4) + tid; b < n; b += nthr) dst[b] = src[b];
   }
 }
@@ -1459,7 +1459,7 @@ __global__ void __launch_bounds__(256) k_copy_gated(uint8_t* dst, const uint8_t*
   for (int64_t b = tid; b < head; b += nthr) dst[b] = src[b];
   const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
   uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-  for (int64_t i = tid; i < nv; i += nthr) d4[i] = __ldcs(s4 + i);
+  for (int64_t i = tid; i < nv; i += nthr) d4[i] = PM_COPY_LD(s4 + i);
   for (int64_t b = head + (nv << 4) + tid; b < n; b += nthr) dst[b] = src[b];
 }
 

@@ -162,7 +162,7 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
   const KT* B = reinterpret_cast<const KT*>(P.keys) + P.m;
   KT* sa = reinterpret_cast<KT*>(F.samp_a);
   KT* sb = reinterpret_cast<KT*>(F.samp_b);
-  if (tid < FC_WORDS && tid != FC_ROT) F.fc[tid] = 0;  // (FC_ROT: thread 0 below)
+  if (tid < FC_WORDS && tid != FC_ROT && tid != FC_ROTFAIL) F.fc[tid] = 0;  // (FC_ROT, FC_ROTFAIL: thread 0 below)
   for (int64_t b = tid; b <= F.nb; b += nthr) F.hist[b] = 0;  // (before ph_readers counts identity regions)
   for (int64_t c = tid; c < P.Q / kFlowChunk + 2; c += nthr) F.chunk[c] = 0;
   if (tid == 0) {
@@ -170,8 +170,14 @@ __device__ __forceinline__ void ph_sample(const FlowParams& F) {
     // (a prescribed layout has no such shortcut: identity regions are skipped instead)
     const bool nothing = P.m == P.s || P.m == P.e || (!F.nleaves && A[P.m - P.s - 1] <= B[0]);  // srecpar.py:56-57
     *P.noop = nothing ? 1 : 0;
-    F.fc[FC_ROT] = !nothing && !F.nleaves && A[0] > B[P.e - P.m - 1] ? 1 : 0;
+    const bool rot = !nothing && !F.nleaves && A[0] > B[P.e - P.m - 1];
+    F.fc[FC_ROT] = rot ? 1 : 0;
+    // equal runs: the block swap (2 N w) always beats the engine (N/2 salvaged); the
+    // plan stops here.  Unequal rotations only take the reversals (4 N w) when the
+    // engine's salvage overflows the pool (ph_alloc).
+    F.fc[FC_ROTFAIL] = rot && P.m - P.s == P.e - P.m ? 1 : 0;
     for (int i = 0; i < 16; ++i) P.stats[i] = 0;
+    if (F.fc[FC_ROTFAIL]) P.stats[13] = 1;
   }
   // (four independent strided loads in flight per thread before their stores)
   for (int64_t k0 = tid; !F.nleaves && k0 < F.nsa + F.nsb; k0 += 4 * nthr) {
@@ -747,7 +753,7 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
   ph_sample<KT>(F);
   grid.sync();
   PM_FLOW_DBG(1);
-  if (*(volatile int32_t*)F.P.noop) return;
+  if (*(volatile int32_t*)F.P.noop || *(volatile long long*)&F.fc[FC_ROTFAIL]) return;
   ph_split<KT>(F);
   grid.sync();
   PM_FLOW_DBG(2);

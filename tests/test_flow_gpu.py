@@ -113,7 +113,7 @@ def test_pure_rotation_block_exchange(flow_mode, mode, la, lb, width, dtype):
     st = _ops.merge(arr, 0, la, n)
     assert torch.equal(arr.keys, torch.cat([b, a]))
     assert torch.equal(arr.payload, torch.cat([p0[la:], p0[:la]]))
-    if mode == "angle" and la == lb:  # salvage N/2 > the N/4 pool
+    if la == lb:  # equal runs: the block swap, decided in the sample phase
         assert st[13] == 1
     if st[13] == 0:  # the plan's salvage fitted the pool: the scheduled engine merged it
         assert st[4] in (1, 2)
@@ -123,12 +123,13 @@ def test_pure_rotation_block_exchange(flow_mode, mode, la, lb, width, dtype):
 
 def test_lean_plan_small_jobs(flow_mode):
     """Below PM_FLOW_TF_Q regions the plan is the lean two-front one with an N/2 pool:
-    the same rotation fits it (no fallback), and a uniform job reports the two-front
-    order; both bit-exact."""
+    the same near-rotation fits it (no fallback), and a uniform job reports the
+    two-front order; both bit-exact."""
     flow_mode("auto")
     h = 1 << 22
     ar = torch.arange(h, device="cuda", dtype=torch.int32)
     k0 = torch.cat([ar + h, ar])
+    k0[-1] = 3 * h  # (not a pure rotation: those take the block swap)
     arr = pm.KeyedArray(k0.clone())
     _ops.set_engine_only(True)
     try:
