@@ -5,7 +5,7 @@ ARCH ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG := paper_2005_12648_b200
 SRC := $(PKG)/csrc/pm_engine.cu $(PKG)/csrc/pm_flow.cu $(PKG)/csrc/pm_plan.cu $(PKG)/csrc/pm_rotate.cu $(PKG)/csrc/pm_wide.cu $(PKG)/csrc/pm_small.cu $(PKG)/csrc/pm_peers.cu $(PKG)/csrc/pm_capi.cu
-HDR := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/pm_launch.h include/parmerge_b200.h
+HDR := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/pm_launch.h $(PKG)/csrc/pm_hostcache.h include/parmerge_b200.h
 OBJ := $(SRC:.cu=.o)
 LIB := $(PKG)/libparmerge_b200.so
 

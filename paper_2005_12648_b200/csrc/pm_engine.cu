@@ -22,6 +22,7 @@
 #include "pm_engine.cuh"
 #include "pm_search.cuh"
 #include "pm_tile.cuh"
+#include "pm_hostcache.h"
 
 namespace pm {
 
@@ -84,6 +85,13 @@ __device__ __forceinline__ int32_t stack_pop(unsigned long long* top, int32_t* n
 #define PM_PLAN_INTERP 8  // tune: interpolation probes of k_plan's split search (0: binary only)
 #endif
 constexpr int kCoarse = 64;  // k_plan_coarse searches every kCoarse-th region boundary
+// Up to kWarpPlan boundaries (jobs of up to ~2^24 records) k_plan alone runs one
+// warp per boundary over the full range (33-ary ballot search: ~5 dependent
+// probes), without k_plan_coarse: the two-level plan's thread-per-boundary
+// binary searches were a chain of ~18 dependent DRAM probes on 3 CTAs (2^21
+// records: 6 + 15 us of plan for an 11 us merge).  Larger jobs keep the two
+// levels (a warp per boundary would multiply the probe traffic by 32).
+constexpr int64_t kWarpPlan = 8192;
 // Full-range merge-path searches at every kCoarse-th boundary (and the last);
 // k_plan then searches the boundaries in between inside these brackets.
 template <typename KT>
@@ -118,10 +126,26 @@ __global__ void k_plan(EngineParams P) {
   Geo g(P);
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
+  if (P.Q + 1 <= kWarpPlan) {  // one warp per boundary, full range
+    const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = w0; q <= P.Q; q += nw) {
+      const int64_t d = g.diag(q);
+      int64_t a;
+      if (P.mode == MODE_MERGE) {
+        a = merge_path_warp<KT>(keys + P.s, la, B, lb, d, lane);
+      } else {
+        a = d - lb;
+        a = a < 0 ? 0 : (a > la ? la : a);
+      }
+      if (lane == 0) P.split_a[q] = a;
+    }
+  } else {
   // one thread per region boundary: binary search of the stable merge path
   // (2 independent loads per step, every search in flight at once), bounded by
   // the coarse splits k_plan_coarse found every kCoarse boundaries
-  {
     const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthr0 = (int64_t)gridDim.x * blockDim.x;
     const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
@@ -1480,9 +1504,15 @@ cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32
 // ---- host launchers (called from pm_capi.cu) --------------------------------
 template <typename KT>
 cudaError_t launch_plan(const EngineParams& P, int grid, cudaStream_t st) {
-  k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 8) / 8, 2048), 256, 0, st>>>(P);
-  k_plan<KT><<<grid, 256, 0, st>>>(P);
-  count_launches(2);
+  if (P.Q + 1 <= kWarpPlan) {  // one level: a warp per boundary (k_plan)
+    grid = (int)std::max<int64_t>(grid, std::min<int64_t>((P.Q + 1 + 7) / 8, 2048));
+    k_plan<KT><<<grid, 256, 0, st>>>(P);
+    count_launches(1);
+  } else {
+    k_plan_coarse<KT><<<(int)std::min<int64_t>((P.Q / kCoarse + 8) / 8, 2048), 256, 0, st>>>(P);
+    k_plan<KT><<<grid, 256, 0, st>>>(P);
+    count_launches(2);
+  }
   if (P.tlist && PM_TLIST) {
     k_flags<<<(int)std::min<int64_t>((P.Q + 255) / 256, 1184), 256, 0, st>>>(P);
     k_compact<<<1, 1024, 0, st>>>(P);
@@ -1499,15 +1529,15 @@ cudaError_t launch_engine(const EngineParams& P, int grid, int block, size_t sme
 }
 template <typename KT>
 cudaError_t engine_occupancy(int block, size_t smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_engine<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void*)k_engine<KT>, smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_engine<KT>, block, smem);
+  return cached_occupancy(blocks_per_sm, (const void*)k_engine<KT>, block, smem);
 }
 template <typename KT>
 cudaError_t buffered_occupancy(size_t smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void*)k_buffered<KT>, smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_buffered<KT>, kBufferedThreads, smem);
+  return cached_occupancy(blocks_per_sm, (const void*)k_buffered<KT>, kBufferedThreads, smem);
 }
 template <typename KT>
 cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size_t smem, cudaStream_t st) {
@@ -1519,7 +1549,7 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
   count_launches(2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = ensure_smem_attr((const void*)k_buffered<KT>, smem);
   if (e != cudaSuccess) return e;
   k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, buf_a);
   count_launches(1);
@@ -1527,7 +1557,7 @@ cudaError_t launch_buffered(const EngineParams& P, int32_t buf_a, int grid, size
 }
 template <typename KT>
 cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_buffered<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void*)k_buffered<KT>, smem);
   if (e != cudaSuccess) return e;
   k_buffered<KT><<<grid, kBufferedThreads, smem, st>>>(P, 1);
   count_launches(1);

@@ -13,6 +13,7 @@
 #include "pm_common.cuh"
 #include "pm_launch.h"
 #include "pm_tile.cuh"
+#include "pm_hostcache.h"
 
 namespace pm {
 
@@ -362,7 +363,7 @@ cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool rig
   e = cudaMemsetAsync(ticket, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
   const size_t smem = kSlideStages * (kSlideTile + 64);
-  e = cudaFuncSetAttribute(k_slide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = ensure_smem_attr((const void*)k_slide, smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms * 3);
   k_slide<<<grid, kSlideThreads, smem, st>>>(static_cast<uint8_t*>(plane), S0, L, D, right ? 1 : 0, flags, ticket, err);
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(256) k_swap_blocks(const int32_t* gate, uint8_
 template <typename WT>
 static cudaError_t swap_launch(uint8_t* x, int64_t nbytes, int num_sms, cudaStream_t st, const int32_t* gate) {
   int bps = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_swap_blocks<WT>, 256, 0);
+  cudaError_t e = cached_occupancy(&bps, (const void*)k_swap_blocks<WT>, 256, 0);
   if (e != cudaSuccess) return e;
   const int64_t words = nbytes / (int64_t)sizeof(WT);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((words + 1023) / 1024, (int64_t)num_sms * std::max(bps, 1)));

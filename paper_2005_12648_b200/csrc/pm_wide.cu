@@ -31,6 +31,7 @@
 
 #include "pm_common.cuh"
 #include "pm_launch.h"
+#include "pm_hostcache.h"
 
 namespace pm {
 
@@ -459,7 +460,7 @@ cudaError_t launch_cycle_permute(uint8_t* pay, int64_t w, const int32_t* idx, in
   while (((int64_t)1 << rounds) < n) ++rounds;
   {
     int bps = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_cyc_fallback, kWideThreads, 0);
+    e = cached_occupancy(&bps, (const void*)k_cyc_fallback, kWideThreads, 0);
     if (e != cudaSuccess) return e;
     const int fg = std::max(1, std::min(bps * num_sms, g));
     int32_t* cnt = ctl;
@@ -477,9 +478,9 @@ cudaError_t launch_cycle_permute(uint8_t* pay, int64_t w, const int32_t* idx, in
   int mgrid = 0;
   PM_WIDE_DISPATCH(v, ({
     auto kern = k_cyc_move<kV>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCycSmem);
+    e = ensure_smem_attr((const void*)kern, kCycSmem);
     int bm = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bm, kern, kCycWarps * 32, kCycSmem);
+    if (e == cudaSuccess) e = cached_occupancy(&bm, (const void*)kern, kCycWarps * 32, kCycSmem);
     mgrid = std::max(1, bm) * num_sms;
     if (e == cudaSuccess)
       kern<<<mgrid, kCycWarps * 32, kCycSmem, st>>>(pay, save, idx, segs, ctl + 5, heads, ctl, n, w, G, Lmax);
