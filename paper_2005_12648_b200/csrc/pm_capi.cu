@@ -56,7 +56,7 @@ struct Ctl {
   Line32 err_;
   Line32 noop_;
   Line32 need_space_;
-  Line32 stage_gate_;  // staged path: the runs are out of order (k_order_gate)
+  Line32 stage_gate_;  // staged path: the runs are out of order (computed by k_plan)
 };
 
 
@@ -169,7 +169,7 @@ static bool pick_tiles(int ks, int64_t w, int64_t budget, int64_t* M, int64_t* T
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys = nullptr,
                       void* out_payload = nullptr, const void* keys_b = nullptr, const void* pay_b = nullptr,
-                      const int32_t* gate = nullptr);
+                      const int32_t* gate = nullptr, int32_t* gate_out = nullptr);
 
 #ifndef PM_SLIDE_STASH
 #define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
@@ -278,7 +278,7 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
 
 static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, int64_t s, int64_t m, int64_t e,
                       int mode, int64_t scratch_records, cudaStream_t st, void* out_keys, void* out_payload,
-                      const void* keys_b, const void* pay_b, const int32_t* gate) {
+                      const void* keys_b, const void* pay_b, const int32_t* gate, int32_t* gate_out) {
   const bool copy = out_keys != nullptr;
   if (e - s <= 0 || (!copy && (m == s || m == e))) return PM_OK;
   int64_t M, T;
@@ -317,11 +317,9 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
     int32_t mut;
     const bool gated = !(w > 0 && (w >= PM_WIDE_MIN || !pick_tiles(ks, w, kTileBudget, &Mt, &Tt, &mut)));
     int32_t* gate = gated ? &ctx->ctl->stage_gate_.v : nullptr;
-    if (gated) {
-      cudaError_t ge = launch_order_gate(k0, ks, m - s, gate, st);
-      if (ge != cudaSuccess) return cuda_fail(ge, "k_order_gate launch");
-    }
-    rc = run_engine(ctx, k0, ks, p0, w, 0, m - s, n, MODE_MERGE, 0, st, sk, w ? sp : nullptr, nullptr, nullptr, gate);
+    // (k_plan computes the gate before the gated merge and copy read it)
+    rc = run_engine(ctx, k0, ks, p0, w, 0, m - s, n, MODE_MERGE, 0, st, sk, w ? sp : nullptr, nullptr, nullptr, gate,
+                    gate);
     if (rc) return rc;
     if (gated) {
       cudaError_t ce2 = launch_copy_gated(k0, sk, n * ks, gate, ctx->num_sms, st);
@@ -365,6 +363,7 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
   P.keys_b = static_cast<const char*>(keys_b);
   P.pay_b = static_cast<const uint8_t*>(pay_b);
   P.gate = gate;
+  P.gate_out = gate_out;
   P.w = w;
   P.ks = ks;
   P.mode = mode;

@@ -96,7 +96,7 @@ constexpr int64_t kWarpPlan = 8192;
 // k_plan then searches the boundaries in between inside these brackets.
 template <typename KT>
 __global__ void __launch_bounds__(256) k_plan_coarse(EngineParams P) {
-  if (P.gate && !*(volatile const int32_t*)P.gate) return;
+  if (!P.gate_out && P.gate && !*(volatile const int32_t*)P.gate) return;  // (gate_out: k_plan computes it next)
   Geo g(P);
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
@@ -122,10 +122,14 @@ __global__ void __launch_bounds__(256) k_plan_coarse(EngineParams P) {
 
 template <typename KT>
 __global__ void k_plan(EngineParams P) {
-  if (P.gate && !*(volatile const int32_t*)P.gate) return;
   Geo g(P);
   const KT* keys = reinterpret_cast<const KT*>(P.keys);
   const int64_t la = g.LA(), lb = g.LB();
+  if (P.gate_out) {  // staged path: the gate the later kernels read (srecpar.py:56-57)
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.gate_out = keys[P.m - 1] > keys[P.m] ? 1 : 0;
+  } else if (P.gate && !*(volatile const int32_t*)P.gate) {
+    return;
+  }
   if (P.Q + 1 <= kWarpPlan) {  // one warp per boundary, full range
     const KT* B = P.keys_b ? reinterpret_cast<const KT*>(P.keys_b) : keys + P.m;
     const int lane = threadIdx.x & 31;
@@ -1468,11 +1472,6 @@ __global__ void __launch_bounds__(1024) k_compact(EngineParams P) {
 }
 
 // ---- staged path helpers: skip the whole pass when the runs are already in order ----
-// gate = 1 iff A[m-1] > B[0] (srecpar.py:56-57: otherwise nothing moves)
-template <typename KT>
-__global__ void k_order_gate(const KT* keys, int64_t m, int32_t* gate) {
-  *gate = keys[m - 1] > keys[m] ? 1 : 0;
-}
 // dst <- src (n bytes, identical 16-byte phase), only if *gate
 __global__ void __launch_bounds__(256) k_copy_gated(uint8_t* dst, const uint8_t* src, int64_t n, const int32_t* gate) {
   if (!*(volatile const int32_t*)gate) return;
@@ -1487,12 +1486,6 @@ __global__ void __launch_bounds__(256) k_copy_gated(uint8_t* dst, const uint8_t*
   for (int64_t b = head + (nv << 4) + tid; b < n; b += nthr) dst[b] = src[b];
 }
 
-cudaError_t launch_order_gate(const void* keys, int ks, int64_t m, int32_t* gate, cudaStream_t st) {
-  if (ks == 4) k_order_gate<int32_t><<<1, 1, 0, st>>>(static_cast<const int32_t*>(keys), m, gate);
-  else k_order_gate<int64_t><<<1, 1, 0, st>>>(static_cast<const int64_t*>(keys), m, gate);
-  count_launches(1);
-  return cudaGetLastError();
-}
 cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32_t* gate, int num_sms, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>((n / 16 + 255) / 256 + 1, (int64_t)num_sms * 8);

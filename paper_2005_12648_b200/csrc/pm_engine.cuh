@@ -162,6 +162,7 @@ struct EngineParams {
   // bounded-pool engine behind the scheduled engine, taken when the latter's plan
   // does not fit its pool -- pm_flow.cu)
   const int32_t* gate;
+  int32_t* gate_out;   // staged path: k_plan computes the order gate (A[m-1] > B[0]) into it first
 };
 
 // Scheduled in-place merge (pm_flow.cu).  Per region ("ticket") of the plan's

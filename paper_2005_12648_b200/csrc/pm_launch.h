@@ -40,8 +40,7 @@ cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int6
 // equal blocks: [lo, lo + len) <-> [lo + len, lo + 2 len), keys and payload planes (gated likewise)
 cudaError_t launch_swap_blocks(void* keys, int ks, void* payload, int64_t w, int64_t lo, int64_t len, int num_sms,
                                cudaStream_t st, const int32_t* gate = nullptr);
-// staged path: gate = A[m-1] > B[0]; a copy that runs only if the gate is set
-cudaError_t launch_order_gate(const void* keys, int ks, int64_t m, int32_t* gate, cudaStream_t st);
+// staged path: a copy that runs only if the gate (A[m-1] > B[0], set by k_plan) is set
 cudaError_t launch_copy_gated(void* dst, const void* src, int64_t n, const int32_t* gate, int num_sms, cudaStream_t st);
 template <typename KT> cudaError_t launch_merge_copy(const EngineParams& P, int grid, size_t smem, cudaStream_t st);
 template <typename KT>
