@@ -1403,34 +1403,56 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   PM_CUDA(cudaStreamWaitEvent(st, ctx->hev[0], 0));
   if (!stg.empty()) {
     // host threads move the staged chunks into place, each once its range has
-    // been uploaded and its D2H has landed (every thread takes a stripe of each)
+    // been uploaded and its D2H has landed.  The work is cut into pieces of at most
+    // PM_HOST_PIECE bytes, taken in order from one counter: a thread that the OS
+    // deschedules delays only its current piece (fixed per-thread stripes made
+    // the slowest thread the critical path: 102 ms median, 129 ms outliers)
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
 #ifndef PM_HOST_MOVERS
 #define PM_HOST_MOVERS 4u  // more threads take host memory bandwidth from the DMA (tools/gpu_pcie_chunks.py)
 #endif
+#ifndef PM_HOST_PIECE
+#define PM_HOST_PIECE ((int64_t)16 << 20)  // 4 MB: 103.8 ms mean, 16 MB: 102.6 (2^30 int32)
+#endif
     const int nt = (int)std::min<unsigned>(PM_HOST_MOVERS, std::max(1u, hw / 2));
+    struct Piece {
+      int c;          // staged chunk
+      char* dst;
+      const char* src;
+      int64_t bytes;
+    };
+    std::vector<Piece> pieces;
+    for (int c : stg) {
+      const int64_t e0 = dk[c], e1 = dk[c + 1];
+      const char* src = hs_base + soff[c];
+      auto cut = [&](char* dst, const char* from, int64_t bytes) {
+        for (int64_t x = 0; x < bytes; x += PM_HOST_PIECE)
+          pieces.push_back({c, dst + x, from + x, std::min<int64_t>(PM_HOST_PIECE, bytes - x)});
+      };
+      cut(hk + e0 * key_bytes, src, (e1 - e0) * key_bytes);
+      if (width) cut(hp + e0 * width, src + (e1 - e0) * key_bytes, (e1 - e0) * width);
+    }
+    std::atomic<size_t> next_piece{0};
     std::atomic<int> err{0};
     auto mover = [&](int t) {
-      for (int c : stg) {
-        if (cudaEventSynchronize(ctx->hup[free_at[c]]) != cudaSuccess ||
-            cudaEventSynchronize(ctx->hdn[c]) != cudaSuccess) {
-          err.store(1);
-          return;
+      int ready_c = -1;  // the chunk whose events this thread has seen complete
+      for (size_t i; (i = next_piece.fetch_add(1)) < pieces.size();) {
+        const Piece& pc = pieces[i];
+        if (pc.c != ready_c) {
+          if (cudaEventSynchronize(ctx->hup[free_at[pc.c]]) != cudaSuccess ||
+              cudaEventSynchronize(ctx->hdn[pc.c]) != cudaSuccess) {
+            err.store(1);
+            return;
+          }
+          ready_c = pc.c;
         }
-        const int64_t e0 = dk[c], e1 = dk[c + 1];
-        const char* src = hs_base + soff[c];
-        auto stripe = [&](char* dst, const char* from, int64_t bytes) {
-          const int64_t per = ((bytes + nt - 1) / nt + 63) & ~(int64_t)63;
-          const int64_t x0 = std::min<int64_t>(bytes, per * t), x1 = std::min<int64_t>(bytes, x0 + per);
-          if (x1 > x0) std::memcpy(dst + x0, from + x0, (size_t)(x1 - x0));
-        };
-        stripe(hk + e0 * key_bytes, src, (e1 - e0) * key_bytes);
-        if (width) stripe(hp + e0 * width, src + (e1 - e0) * key_bytes, (e1 - e0) * width);
+        std::memcpy(pc.dst, pc.src, (size_t)pc.bytes);
 #ifdef PM_HOST_TRACE
-        if (t == 0)
-          mv_done[c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+        if (i + 1 == pieces.size() || pieces[i + 1].c != pc.c)
+          mv_done[pc.c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
 #endif
       }
+      (void)t;
     };
     std::vector<std::thread> pool;
     for (int t = 1; t < nt; ++t) pool.emplace_back(mover, t);
