@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--cfg", type=int, default=2,
                     help="BASELINE config (2: int32 uniform, 3: int64 skew, 4: KV dup, 5: 2^33 int32)")
     ap.add_argument("--log-len", type=int, default=None, help="log2 of the run length per side")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/cpu/clock/extra legs (profiling runs)")
     ap.add_argument("--no-buffered", action="store_true", help="skip the buffered / copy-mode legs")
