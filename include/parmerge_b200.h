@@ -181,10 +181,21 @@ int pm_status(pm_ctx *ctx, void *stream, uint64_t *stats);
  * End-to-end entry point with HOST buffers (the reference's calling
  * convention: numpy arrays in host memory).  Copies keys/payload to the
  * device, merges, copies back, synchronises and returns the status.
- * Pinned host memory gives full PCIe bandwidth.
+ * Pinned host memory gives full PCIe bandwidth.  Records already on their
+ * output positions (the A prefix <= B[0], the B suffix >= A[last]) never cross
+ * PCIe; chunks are uploaded in merge order and written back as soon as merged
+ * (through a grow-only pinned staging buffer per context, moved into place by
+ * host threads once their range has been uploaded).
  */
 int pm_merge_host(pm_ctx *ctx, void *keys_host, int key_bytes, void *payload_host, int64_t width,
                   int64_t start, int64_t middle, int64_t end, void *stream);
+/* The host side of pm_merge_host, no device calls (CPU tests): out_span = the
+ * trimmed job [start, end) or {-1, -1} when nothing moves; *out_nch chunks with
+ * output boundaries out_d[0..nch] and A splits out_a[0..nch] (trimmed-job local)
+ * and out_free[k] = the upload after which chunk k's output range is free. */
+int pm_debug_host_plan(const void *keys_host, int key_bytes, int64_t start, int64_t middle, int64_t end,
+                       int64_t min_chunk, int32_t chunks, int64_t *out_span, int64_t *out_d, int64_t *out_a,
+                       int32_t *out_free, int32_t cap, int32_t *out_nch);
 
 /*
  * Instrumentation (no reference counterpart): when enabled, the context

@@ -29,7 +29,7 @@ EXPORTED = (
     "pm_find_median", "pm_find_splits", "pm_plan_intervals", "pm_status", "pm_merge_host",
     "pm_set_timing", "pm_kernel_ms", "pm_debug_order", "pm_debug_splits", "pm_debug_stats", "pm_merge_copy", "pm_launch_count",
     "pm_debug_permute_rows", "pm_debug_engine_only", "pm_merge_peers", "pm_ipc_handle", "pm_ipc_open",
-    "pm_ipc_close", "pm_debug_flow", "pm_kernel_ms_detail", "pm_reorder", "pm_peer_splits",
+    "pm_ipc_close", "pm_debug_flow", "pm_kernel_ms_detail", "pm_reorder", "pm_peer_splits", "pm_debug_host_plan",
 )
 
 _lib = None
@@ -66,6 +66,8 @@ def lib() -> ctypes.CDLL:
         L.pm_plan_intervals.argtypes = [vp, vp, i32, i64, i64, i64, ctypes.c_int32, vp, vp]
         L.pm_status.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
         L.pm_merge_host.argtypes = [vp, vp, i32, vp, i64, i64, i64, i64, vp]
+        L.pm_debug_host_plan.argtypes = [vp, i32, i64, i64, i64, i64, ctypes.c_int32, vp, vp, vp, vp,
+                                         ctypes.c_int32, vp]
         L.pm_set_timing.argtypes = [vp, i32]
         L.pm_debug_order.argtypes = [i64, i64, i64, vp]
         L.pm_debug_splits.argtypes = [vp, vp, i64]

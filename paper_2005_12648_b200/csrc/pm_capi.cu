@@ -719,6 +719,64 @@ static int64_t host_split(const KT* A, int64_t la, const KT* B, int64_t lb, int6
   return lo;
 }
 
+// The host side of pm_merge_host (no device calls; pm_debug_host_plan exposes it
+// to the CPU tests).  The identity trim: the A prefix with keys <= B[0] and the B
+// suffix with keys >= A[last] (A first on ties) are already on their output
+// positions and never cross PCIe.  Then output chunks [d_k, d_{k+1}) of the
+// trimmed job with their stable merge-path splits a_k (read from the host arrays
+// before anything is written back), and free_at[k]: the first upload j >= k
+// (uploads in merge order: upload j brings A[a_j, a_{j+1}) and B[b_j, b_{j+1}))
+// after which no record of chunk k's output range is still to be uploaded.
+struct HostPlan {
+  bool nothing = false;
+  int64_t start = 0, end = 0;
+  std::vector<int64_t> dk, ak;
+  std::vector<int> free_at;
+};
+template <typename KT>
+static HostPlan host_plan_t(const KT* keys, int64_t start, int64_t middle, int64_t end, int64_t min_chunk, int chunks) {
+  HostPlan p;
+  if (middle == start || middle == end) {
+    p.nothing = true;
+    return p;
+  }
+  const KT* A = keys + start;
+  const KT* B = keys + middle;
+  const int64_t a_lo = std::upper_bound(A, A + (middle - start), B[0]) - A;
+  const int64_t b_hi = std::lower_bound(B, B + (end - middle), A[middle - start - 1]) - B;
+  if (a_lo == middle - start || b_hi == 0) {  // already in order (srecpar.py:56-57): nothing moves
+    p.nothing = true;
+    return p;
+  }
+  p.start = start + a_lo;
+  p.end = middle + b_hi;
+  const int64_t n = p.end - p.start, la = middle - p.start, lb = p.end - middle;
+  const KT* X = keys + p.start;
+  const int64_t chunk = std::max<int64_t>(min_chunk, (n + chunks - 1) / chunks);
+  const int nch = (int)((n + chunk - 1) / chunk);
+  p.dk.resize(nch + 1);
+  p.ak.resize(nch + 1);
+  for (int k = 0; k <= nch; ++k) {
+    p.dk[k] = std::min<int64_t>((int64_t)k * chunk, n);
+    p.ak[k] = host_split(X, la, X + la, lb, p.dk[k]);
+  }
+  p.free_at.resize(nch);
+  for (int k = 0; k < nch; ++k) {
+    // A positions in the range: [d_k, min(d_{k+1}, la)); B positions: [max(d_k, la), d_{k+1}) - la
+    const int64_t needA = p.dk[k] < la ? std::min(p.dk[k + 1], la) : 0;
+    const int64_t needB = std::max<int64_t>(p.dk[k + 1] - la, 0);
+    int j = k;
+    while (j + 1 < nch && (p.ak[j + 1] < needA || (p.dk[j + 1] - p.ak[j + 1]) < needB)) ++j;
+    p.free_at[k] = j;
+  }
+  return p;
+}
+static HostPlan host_plan(const void* keys, int key_bytes, int64_t start, int64_t middle, int64_t end,
+                          int64_t min_chunk, int chunks) {
+  return key_bytes == 4 ? host_plan_t(static_cast<const int32_t*>(keys), start, middle, end, min_chunk, chunks)
+                        : host_plan_t(static_cast<const int64_t*>(keys), start, middle, end, min_chunk, chunks);
+}
+
 namespace pm {
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -1206,6 +1264,26 @@ int pm_status(pm_ctx* ctx, void* stream, uint64_t* stats) {
   return PM_OK;
 }
 
+int pm_debug_host_plan(const void* keys_host, int key_bytes, int64_t start, int64_t middle, int64_t end,
+                       int64_t min_chunk, int32_t chunks, int64_t* out_span, int64_t* out_d, int64_t* out_a,
+                       int32_t* out_free, int32_t cap, int32_t* out_nch) {
+  if (!keys_host || (key_bytes != 4 && key_bytes != 8) || !(0 <= start && start <= middle && middle <= end) ||
+      min_chunk < 1 || chunks < 1 || !out_span || !out_nch)
+    return fail(PM_ERR_ARG, "bad pm_debug_host_plan arguments");
+  const HostPlan p = host_plan(keys_host, key_bytes, start, middle, end, min_chunk, chunks);
+  out_span[0] = p.nothing ? -1 : p.start;
+  out_span[1] = p.nothing ? -1 : p.end;
+  const int nch = p.nothing ? 0 : (int)p.dk.size() - 1;
+  *out_nch = nch;
+  if (nch > cap) return fail(PM_ERR_ARG, "pm_debug_host_plan: more chunks than the output arrays hold");
+  for (int k = 0; k <= nch && nch; ++k) {
+    if (out_d) out_d[k] = p.dk[k];
+    if (out_a) out_a[k] = p.ak[k];
+    if (out_free && k < nch) out_free[k] = p.free_at[k];
+  }
+  return PM_OK;
+}
+
 // Host-buffer merge, pipelined over output chunks on three streams: H2D of
 // chunk k's inputs in merge order (A[a_k, a_{k+1}) and B[b_k, b_{k+1})), the
 // out-of-place device merge of chunk k (copy mode), and D2H of chunk k as soon
@@ -1224,28 +1302,14 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
     return fail(PM_ERR_ARG, "bad pm_merge_host arguments");
   if (!(0 <= start && start <= middle && middle <= end)) return fail(PM_ERR_ARG, "need 0 <= start <= middle <= end");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (middle == start || middle == end) return PM_OK;
-  // records already on their output positions never cross PCIe: the A prefix
-  // with keys <= B[0] and the B suffix with keys >= A[last] (A first on ties)
-  {
-    int64_t a_lo, b_hi;
-    if (key_bytes == 4) {
-      const int32_t* A = static_cast<int32_t*>(keys_host) + start;
-      const int32_t* B = static_cast<int32_t*>(keys_host) + middle;
-      a_lo = std::upper_bound(A, A + (middle - start), B[0]) - A;
-      b_hi = std::lower_bound(B, B + (end - middle), A[middle - start - 1]) - B;
-    } else {
-      const int64_t* A = static_cast<int64_t*>(keys_host) + start;
-      const int64_t* B = static_cast<int64_t*>(keys_host) + middle;
-      a_lo = std::upper_bound(A, A + (middle - start), B[0]) - A;
-      b_hi = std::lower_bound(B, B + (end - middle), A[middle - start - 1]) - B;
-    }
-    // already in order (srecpar.py:56-57): nothing moves
-    if (a_lo == middle - start || b_hi == 0) return PM_OK;
-    start += a_lo;
-    end = middle + b_hi;
-  }
-  const int64_t n = end - start, la = middle - start, lb = end - middle;
+#ifndef PM_HOST_CHUNKS
+#define PM_HOST_CHUNKS 48  // output chunks of the host-buffer pipeline (48: 103 ms, 96: 104, 192: 108 at 2^30 int32)
+#endif
+  HostPlan plan = host_plan(keys_host, key_bytes, start, middle, end, (int64_t)1 << 21, PM_HOST_CHUNKS);
+  if (plan.nothing) return PM_OK;
+  start = plan.start;
+  end = plan.end;
+  const int64_t n = end - start, la = middle - start;
   char* hk = static_cast<char*>(keys_host) + start * key_bytes;
   char* hp = width ? static_cast<char*>(payload_host) + start * width : nullptr;
   const size_t kb = (size_t)align_up(n * key_bytes, 256), pb = (size_t)align_up(n * width, 256);
@@ -1270,33 +1334,13 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   // order after the caller's stream
   PM_CUDA(cudaEventRecord(ctx->hev[0], st));
   PM_CUDA(cudaStreamWaitEvent(sH, ctx->hev[0], 0));
-#ifndef PM_HOST_CHUNKS
-#define PM_HOST_CHUNKS 48  // output chunks of the host-buffer pipeline (48: 103 ms, 96: 104, 192: 108 at 2^30 int32)
-#endif
-  const int64_t chunk = std::max<int64_t>((int64_t)1 << 21, (n + PM_HOST_CHUNKS - 1) / PM_HOST_CHUNKS);
-  const int nch = (int)((n + chunk - 1) / chunk);
-  auto split = [&](int64_t d) -> int64_t {
-    if (key_bytes == 4)
-      return host_split(reinterpret_cast<const int32_t*>(hk), la, reinterpret_cast<const int32_t*>(hk) + la, lb, d);
-    return host_split(reinterpret_cast<const int64_t*>(hk), la, reinterpret_cast<const int64_t*>(hk) + la, lb, d);
-  };
-  // the splits are read from the host arrays before any chunk is written back
-  std::vector<int64_t> dk(nch + 1), ak(nch + 1);
-  for (int k = 0; k <= nch; ++k) {
-    dk[k] = std::min<int64_t>((int64_t)k * chunk, n);
-    ak[k] = split(dk[k]);
-  }
-  // ready[k]: the upload after which chunk k's output range holds no record
-  // still to be uploaded (A part: a_{j+1} >= min(d1, la); B part: b_{j+1} >= d1 - la)
-  std::vector<int> ready(nch), order(nch);
-  for (int k = 0; k < nch; ++k) {
-    // A positions in the range: [d_k, min(d_{k+1}, la)); B positions: [max(d_k, la), d_{k+1}) - la
-    const int64_t needA = dk[k] < la ? std::min(dk[k + 1], la) : 0, needB = std::max<int64_t>(dk[k + 1] - la, 0);
-    int j = k;
-    while (j + 1 < nch && (ak[j + 1] < needA || (dk[j + 1] - ak[j + 1]) < needB)) ++j;
-    ready[k] = j;
-    order[k] = k;
-  }
+  const std::vector<int64_t>& dk = plan.dk;
+  const std::vector<int64_t>& ak = plan.ak;
+  const int nch = (int)dk.size() - 1;
+  // ready[k]: the upload after which chunk k's D2H is issued (plan.free_at, or k
+  // for a chunk that goes through the staging buffer); order: the D2H issue order
+  std::vector<int> ready = plan.free_at, order(nch);
+  for (int k = 0; k < nch; ++k) order[k] = k;
   // chunks whose range frees after their merge go through the pinned staging
   // buffer (one grow-only allocation per context); without it (over the cap, or
   // the pinned allocation failed) they are written back directly in ready order
@@ -1330,7 +1374,7 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
     ctx->hup.push_back(e1);
     ctx->hdn.push_back(e2);
   }
-  const std::vector<int> free_at = ready;  // the upload after which chunk k's range is free
+  const std::vector<int>& free_at = plan.free_at;  // the upload after which chunk k's range is free
   std::vector<int> stg;                    // staged chunks, in the order their ranges free
   for (int k = 0; k < nch; ++k)
     if (use_stage && ready[k] > k) {
@@ -1370,6 +1414,7 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
 #endif
     {
       std::lock_guard<std::mutex> lk(ctx->mu);
+      use_stream(ctx, sC);  // (the copy merges share the context's workspace with calls on other streams)
       rc = run_engine(ctx, dxk + a0 * key_bytes, key_bytes, width ? dxp + a0 * width : nullptr, width, 0, a1 - a0,
                       d1 - d0, MODE_MERGE, 0, sC, dok + d0 * key_bytes, width ? dop + d0 * width : nullptr,
                       dxk + (la + b0) * key_bytes, width ? dxp + (la + b0) * width : nullptr);

@@ -66,3 +66,70 @@ def test_two_front_order_is_a_bijection_with_contiguous_windows(Q, qc):
         assert lo <= region <= hi and hi - lo == t  # window = the t+1 regions with order <= t
         assert lo >= 0 and hi < Q
     assert seen == set(range(Q))
+
+
+def _host_plan(keys, start, middle, end, min_chunk, chunks):
+    lib = _capi.lib()
+    span = np.zeros(2, np.int64)
+    cap = chunks + 2
+    d = np.zeros(cap + 1, np.int64)
+    a = np.zeros(cap + 1, np.int64)
+    fr = np.zeros(cap, np.int32)
+    nch = ctypes.c_int32()
+    rc = lib.pm_debug_host_plan(keys.ctypes.data, keys.itemsize, start, middle, end, min_chunk, chunks,
+                                span.ctypes.data, d.ctypes.data, a.ctypes.data, fr.ctypes.data, cap, ctypes.byref(nch))
+    assert rc == 0, lib.pm_last_error()
+    n = nch.value
+    return span, d[:n + 1], a[:n + 1], fr[:n]
+
+
+@pytest.mark.parametrize("layout", ["uniform", "rotation", "inside", "dups", "sorted", "tiny_b", "skew"])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_host_plan_of_merge_host(layout, dtype):
+    """pm_merge_host's host side (no GPU): the identity trim, the chunks' stable
+    merge-path splits, and free_at[k] -- the first upload (merge order) after which
+    chunk k's output range holds no record still to be uploaded -- checked from
+    first principles against numpy on the same keys."""
+    rng = np.random.default_rng(hash((layout, dtype().itemsize)) % 2**32)
+    n = 50_000
+    la = {"tiny_b": n - 3, "skew": n // 9}.get(layout, n // 2)
+    lb = n - la
+    if layout == "uniform":
+        a, b = np.sort(rng.integers(0, 10**6, la)), np.sort(rng.integers(0, 10**6, lb))
+    elif layout == "rotation":
+        a, b = np.sort(rng.integers(500, 1000, la)), np.sort(rng.integers(0, 500, lb))
+    elif layout == "inside":
+        a, b = np.sort(rng.integers(0, 10**6, la)), np.sort(rng.integers(400_000, 400_500, lb))
+    elif layout == "dups":
+        a, b = np.sort(rng.integers(0, 7, la)), np.sort(rng.integers(0, 7, lb))
+    elif layout == "sorted":
+        a, b = np.arange(la), np.arange(la, n)
+    else:
+        a, b = np.sort(rng.integers(0, 10**6, la)), np.sort(rng.integers(0, 10**6, lb))
+    lo, hi = 11, 5
+    keys = np.concatenate([np.full(lo, -1), a, b, np.full(hi, 2 * 10**6)]).astype(dtype)
+    start, middle, end = lo, lo + la, lo + n
+    span, d, asp, free = _host_plan(keys, start, middle, end, 1000, 16)
+    A, B = keys[start:middle], keys[middle:end]
+    if A[-1] <= B[0]:
+        assert span[0] == -1 and len(free) == 0
+        return
+    # identity trim: A prefix <= B[0] and B suffix >= A[last] (stable ties) stay put
+    assert span[0] == start + np.searchsorted(A, B[0], side="right")
+    assert span[1] == middle + np.searchsorted(B, A[-1], side="left")
+    s0, e0 = int(span[0]), int(span[1])
+    X = keys[s0:e0]
+    tla, tlb, tn = middle - s0, e0 - middle, e0 - s0
+    assert d[0] == 0 and d[-1] == tn and np.all(np.diff(d) > 0)
+    # splits: the stable merge path (A wins ties) of the trimmed job at every boundary
+    order = np.argsort(np.concatenate([X[:tla], X[tla:]]), kind="stable")
+    from_a = order < tla
+    for k, dk in enumerate(d):
+        assert asp[k] == from_a[:dk].sum(), (layout, k)
+    # free_at: minimal upload j >= k covering chunk k's output range
+    bsp = d - asp
+    for k in range(len(free)):
+        need_a = min(d[k + 1], tla) if d[k] < tla else 0
+        need_b = max(d[k + 1] - tla, 0)
+        covered = [j for j in range(k, len(free)) if asp[j + 1] >= need_a and bsp[j + 1] >= need_b]
+        assert covered and free[k] == covered[0], (layout, k, free[k], covered[:1])
