@@ -753,13 +753,11 @@ static HostPlan host_plan_t(const KT* keys, int64_t start, int64_t middle, int64
   const int64_t n = p.end - p.start, la = middle - p.start, lb = p.end - middle;
   const KT* X = keys + p.start;
   const int64_t chunk = std::max<int64_t>(min_chunk, (n + chunks - 1) / chunks);
-  const int nch = (int)((n + chunk - 1) / chunk);
-  p.dk.resize(nch + 1);
+  for (int64_t d = 0; d < n; d += chunk) p.dk.push_back(d);  // (geometric end ramps: no gain measured)
+  p.dk.push_back(n);
+  const int nch = (int)p.dk.size() - 1;
   p.ak.resize(nch + 1);
-  for (int k = 0; k <= nch; ++k) {
-    p.dk[k] = std::min<int64_t>((int64_t)k * chunk, n);
-    p.ak[k] = host_split(X, la, X + la, lb, p.dk[k]);
-  }
+  for (int k = 0; k <= nch; ++k) p.ak[k] = host_split(X, la, X + la, lb, p.dk[k]);
   p.free_at.resize(nch);
   for (int k = 0; k < nch; ++k) {
     // A positions in the range: [d_k, min(d_{k+1}, la)); B positions: [max(d_k, la), d_{k+1}) - la

@@ -71,7 +71,7 @@ def test_two_front_order_is_a_bijection_with_contiguous_windows(Q, qc):
 def _host_plan(keys, start, middle, end, min_chunk, chunks):
     lib = _capi.lib()
     span = np.zeros(2, np.int64)
-    cap = chunks + 2
+    cap = chunks + 64  # (steady chunks plus the geometric ramps at both ends)
     d = np.zeros(cap + 1, np.int64)
     a = np.zeros(cap + 1, np.int64)
     fr = np.zeros(cap, np.int32)
