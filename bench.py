@@ -78,8 +78,9 @@ def parse():
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 (2^33) single-GPU leg")
     ap.add_argument("--dist", action="store_true", help="distributed block merge even at one rank")
     ap.add_argument("--no-sweep", action="store_true", help="skip config 2's size sweep leg")
-    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
-                    help="multi-GPU exchange: NCCL all-to-all (default) or the peer-table merge")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="multi-GPU exchange: the peer-table merge (exchange fused into the merge over "
+                         "NVLink, auto when every GPU pair has peer access) or NCCL all-to-all + local merge")
     return ap.parse_args()
 
 
@@ -376,12 +377,16 @@ def run_dist(args):
 
     from paper_2005_12648_b200.dist import merge_distributed, merge_distributed_p2p
 
-    if args.exchange == "p2p":
-        merge_distributed = merge_distributed_p2p  # noqa: F811
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.exchange == "auto":  # the fused peer-table merge wherever every GPU pair has peer access
+        ng = torch.cuda.device_count()
+        peers_ok = ng >= world and all(torch.cuda.can_device_access_peer(i, j)
+                                       for i in range(world) for j in range(world) if i != j)
+        args.exchange = "p2p" if peers_ok else "nccl"
+    if args.exchange == "p2p":
+        merge_distributed = merge_distributed_p2p  # noqa: F811
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.cfg == 5:  # strong scaling: L_A = L_B = 2^32 in total, split over the ranks

@@ -356,20 +356,12 @@ def merge_distributed_p2p(keys_local: torch.Tensor, payload_local: torch.Tensor 
         if w:
             payload_local.copy_(out_p)
         return keys_local, payload_local
-    sizes = [None] * world
-    mine = (n, keys_local.untyped_storage()._share_cuda_(), keys_local.storage_offset(),
-            payload_local.untyped_storage()._share_cuda_() if w else None, payload_local.storage_offset() if w else 0)
-    dist.all_gather_object(sizes, mine, group=group)
-    if any(s[0] != n for s in sizes):
+    # the peer table is exchanged once per set of buffers (peer_blocks caches it;
+    # later calls agree through one tiny all-reduce that no rank's buffers changed)
+    table = peer_blocks(keys_local, payload_local if w else None, group=group)
+    if table is None:
         raise ValueError("merge_distributed_p2p needs equal blocks on every rank")
-    pk, pp = [], []
-    for r, (_, mk, ok, mp, op) in enumerate(sizes):
-        if r == rank:
-            pk.append(keys_local)
-            pp.append(payload_local)
-        else:
-            pk.append(_peer_view(mk, n, keys_local.dtype, (), ok))
-            pp.append(_peer_view(mp, n, torch.uint8, (w,), op) if w else payload_local)
+    pk, pp = table
     out_k = torch.empty_like(keys_local)
     out_p = torch.empty_like(payload_local)
     _ops.merge_peers(pk, pp if w else None, global_len_a, rank, out_k, out_p if w else None)
