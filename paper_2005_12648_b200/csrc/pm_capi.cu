@@ -577,7 +577,7 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
                o_chunk = take((P.Q / 1024 + 2) * 4), o_idn = take(K), o_fc = take(FC_WORDS * 8);
   // split-search samples (stride S = min(256, M); S divides M)
 #ifndef PM_FLOW_SAMPLE
-#define PM_FLOW_SAMPLE 2048  // split-search sample stride (records)
+#define PM_FLOW_SAMPLE 8192  // split-search sample stride (records; capped at the region size): 2^30 int32 plan 0.136 -> 0.127 ms vs 2048 (fewer row activations in the sample phase, the interpolation probes absorb the wider window)
 #endif
   const int64_t S = std::min<int64_t>(PM_FLOW_SAMPLE, M);
   F.lS = 63 - __builtin_clzll((unsigned long long)S);
