@@ -357,8 +357,9 @@ def test_merge_host_vs_oracle(width):
         assert np.array_equal(pp, want_p), f"payload size={size}"
 
 
+@pytest.mark.parametrize("dtype,width", [(np.int32, 4), (np.int64, 12), (np.int32, 0)])
 @pytest.mark.parametrize("layout", ["rotation", "inside", "tiny_a", "tiny_b", "interleave", "halves_swap"])
-def test_merge_host_write_back_order(layout):
+def test_merge_host_write_back_order(layout, dtype, width):
     """pm_merge_host writes merged chunks back in the order their output ranges
     become free (uploads in merge order): layouts whose ranges free up far from
     chunk order, each over several pipeline chunks, == the stable merge."""
@@ -390,8 +391,8 @@ def test_merge_host_write_back_order(layout):
         la = n // 3
         a = np.sort(rng.integers(500, 1000, la))
         b = np.sort(rng.integers(0, 501, n - la))
-    keys = np.concatenate([a, b]).astype(np.int32)
-    payload = np.arange(n, dtype=np.int32).view(np.uint8).reshape(-1, 4).copy()
+    keys = np.concatenate([a, b]).astype(dtype)
+    payload = np.random.default_rng(5).integers(0, 256, (n, width), dtype=np.uint8)
     want_k, want_p = keys.copy(), payload.copy()
     orc.seq_merge_buffered(want_k, want_p, 0, la, n)
     _ops.merge_host(keys, payload, 0, la, n)
