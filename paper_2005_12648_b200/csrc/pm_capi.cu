@@ -175,13 +175,16 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
 #endif
 #ifndef PM_CLUSTER_MERGE
-#define PM_CLUSTER_MERGE 1  // tune: in-place jobs of up to ~3 MB in one thread-block cluster
+#define PM_CLUSTER_MERGE 0  // 1: jobs of up to ~1 MB in one thread-block cluster (distributed shared memory) --
+                            // the one-launch grid merge is faster at every such size (2^15 records per side:
+                            // 26.8 vs 14.7 us, 2^17: 30.0 vs 18.4 us), so it is off by default
 #endif
 #ifndef PM_STAGE_WIDE
 #define PM_STAGE_WIDE 1  // tune: wide rows also take the staged path (row gather + copy back; 0.20 vs 0.31-0.45 ms at 200 MB)
 #endif
 #ifndef PM_SMALL_BYTES
-#define PM_SMALL_BYTES (200 * 1024)  // records staged by the one-CTA small merge (shared memory)
+#define PM_SMALL_BYTES (64 * 1024)  // one-CTA small merge up to 32 KB of records (in + out tile in shared
+                                    // memory); beyond, the grid merge is faster (2^13 per side: 19.2 vs 16.3 us)
 #endif
 #ifndef PM_STAGE_BYTES
 #define PM_STAGE_BYTES (256ll << 20)  // in-place jobs up to this size merge via a staging buffer (a constant, below the engine pool)
@@ -297,6 +300,23 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
       cudaError_t ce = ks == 4 ? launch_merge_cluster<int32_t>(keys, payload, w, s, m, e, C, lchunk, st)
                                : launch_merge_cluster<int64_t>(keys, payload, w, s, m, e, C, lchunk, st);
       if (ce != cudaSuccess) return cuda_fail(ce, "k_merge_cluster launch");
+      return PM_OK;
+    }
+  }
+  // up to ~14 MB (one CTA per SM holding a 100 KB output tile): one cooperative
+  // launch that merges every CTA's range into shared memory and stores it in place
+  // after a grid barrier (pm_small.cu, k_merge_grid)
+#ifndef PM_GRID_MERGE
+#define PM_GRID_MERGE 1
+#endif
+  if (mode == MODE_MERGE && !copy && !direct && !ctx->engine_only && w <= 64 && PM_GRID_MERGE) {
+    int ctas = 0;
+    size_t gsm = 0;
+    const int64_t R = grid_merge_plan(ks, w, e - s, ctx->num_sms, &ctas, &gsm);
+    if (R > 0) {
+      cudaError_t ce = ks == 4 ? launch_merge_grid<int32_t>(keys, payload, w, s, m, e, ctas, R, gsm, st)
+                               : launch_merge_grid<int64_t>(keys, payload, w, s, m, e, ctas, R, gsm, st);
+      if (ce != cudaSuccess) return cuda_fail(ce, "k_merge_grid launch");
       return PM_OK;
     }
   }

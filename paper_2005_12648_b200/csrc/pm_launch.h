@@ -74,6 +74,12 @@ cudaError_t launch_merge_small(void* keys, void* payload, int64_t w, int64_t s, 
                                cudaStream_t st);
 // cluster size (0: does not fit) and log2 chunk of the cluster merge; its launcher
 int cluster_merge_plan(int ks, int64_t w, int64_t n, int* lchunk);
+// grid merge (one cooperative launch, one CTA per SM, tiles in shared memory): R
+// records per CTA, 0 when the job does not fit
+int64_t grid_merge_plan(int ks, int64_t w, int64_t n, int num_sms, int* ctas, size_t* smem);
+template <typename KT>
+cudaError_t launch_merge_grid(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int ctas,
+                              int64_t R, size_t smem, cudaStream_t st);
 template <typename KT>
 cudaError_t launch_merge_cluster(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int C,
                                  int lchunk, cudaStream_t st);

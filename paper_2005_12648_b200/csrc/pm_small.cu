@@ -11,10 +11,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cstdint>
 
 #include "pm_launch.h"
+#include "pm_hostcache.h"
+#include "pm_search.cuh"
 
 namespace pm {
 
@@ -231,6 +234,79 @@ __global__ void __launch_bounds__(kSmallThreads) k_merge_cluster(KT* keys, uint8
   tile_out<KT>(keys + x0, w ? pay + (int64_t)x0 * w : pay, ok, op, x1 - x0, w);
 }
 
+// ---- grid merge: up to ~14 MB in one cooperative launch, no staging buffer ----
+// CTA c (one per SM) owns the output range [c R, (c + 1) R): two warps find its
+// stable merge-path splits over the whole job (33-ary ballot searches), the CTA
+// loads its A and B pieces into shared memory (each at its source's 16-byte
+// phase, so the bulk of the copy is 16-byte words), merges them into a shared
+// output tile, and after one grid-wide barrier -- every CTA has read its inputs --
+// stores the tile in place.  One read and one write per record and a single
+// launch, where the staged path takes a plan kernel, a copy-mode merge into a
+// staging buffer and a copy back (2^21 records: 34 us).
+template <int W>
+__device__ __forceinline__ void g2s_words(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+  using T = typename std::conditional<W == 16, uint4, typename std::conditional<W == 4, uint32_t, uint8_t>::type>::type;
+  T* d = reinterpret_cast<T*>(dst);
+  const T* s = reinterpret_cast<const T*>(src);
+  for (int64_t i = threadIdx.x; i < bytes / W; i += blockDim.x) d[i] = s[i];
+}
+// dst and src share the 16-byte phase: head bytes, 16-byte body, tail bytes
+__device__ __forceinline__ void g2s_phased(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+  const int64_t head = min(bytes, (int64_t)((16 - ((uintptr_t)src & 15)) & 15));
+  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+  const int64_t body = (bytes - head) & ~(int64_t)15;
+  g2s_words<16>(dst + head, src + head, body);
+  const int64_t t0 = head + body;
+  if (t0 + threadIdx.x < bytes) dst[t0 + threadIdx.x] = src[t0 + threadIdx.x];
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_merge_grid(KT* keys, uint8_t* pay, int64_t w, int64_t la,
+                                                                 int64_t lb, int64_t R) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int64_t s_split[2];
+  cg::grid_group grid = cg::this_grid();
+  const int64_t n = la + lb;
+  const int64_t x0 = min(n, (int64_t)blockIdx.x * R), x1 = min(n, x0 + R);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 2) {
+    const int64_t a = merge_path_warp<KT>(keys, la, keys + la, lb, warp ? x1 : x0, lane);
+    if (lane == 0) s_split[warp] = a;
+  }
+  __syncthreads();
+  const int64_t a0 = s_split[0], a1 = s_split[1], b0 = x0 - a0, b1 = x1 - a1;
+  const int alpha = (int)(a1 - a0), beta = (int)(b1 - b0), no = (int)(x1 - x0);
+  // shared layout: A keys, B keys (each at its source's 16-byte phase), A rows, B
+  // rows (same), output keys, output rows
+  const uint8_t* gka = reinterpret_cast<const uint8_t*>(keys + a0);
+  const uint8_t* gkb = reinterpret_cast<const uint8_t*>(keys + la + b0);
+  uint8_t* ska = sm + ((uintptr_t)gka & 15);
+  uint8_t* skb = sm + ((((uintptr_t)(ska + (int64_t)alpha * sizeof(KT)) + 15) & ~(uintptr_t)15) - (uintptr_t)sm) +
+                 ((uintptr_t)gkb & 15);
+  uint8_t* end = skb + (int64_t)beta * sizeof(KT);
+  g2s_phased(ska, gka, (int64_t)alpha * sizeof(KT));
+  g2s_phased(skb, gkb, (int64_t)beta * sizeof(KT));
+  uint8_t *spa = end, *spb = end;
+  if (w) {
+    const uint8_t* gpa = pay + a0 * w;
+    const uint8_t* gpb = pay + (la + b0) * w;
+    spa = reinterpret_cast<uint8_t*>((((uintptr_t)end + 15) & ~(uintptr_t)15) + ((uintptr_t)gpa & 15));
+    spb = reinterpret_cast<uint8_t*>((((uintptr_t)(spa + (int64_t)alpha * w) + 15) & ~(uintptr_t)15) +
+                                     ((uintptr_t)gpb & 15));
+    g2s_phased(spa, gpa, (int64_t)alpha * w);
+    g2s_phased(spb, gpb, (int64_t)beta * w);
+    end = spb + (int64_t)beta * w;
+  }
+  KT* ok = reinterpret_cast<KT*>(((uintptr_t)end + 15) & ~(uintptr_t)15);
+  uint8_t* op = reinterpret_cast<uint8_t*>((((uintptr_t)(ok + no)) + 15) & ~(uintptr_t)15);
+  __syncthreads();
+  merge_spans_to_tile<KT>(reinterpret_cast<const KT*>(ska), alpha, reinterpret_cast<const KT*>(skb), beta, spa, spb,
+                          w, ok, op);
+  __syncthreads();
+  grid.sync();  // every CTA has read its pieces: the output ranges may be overwritten
+  tile_out<KT>(keys + x0, w ? pay + x0 * w : pay, ok, op, no, w);
+}
+
 }  // namespace
 
 int64_t small_merge_smem(int ks, int64_t w, int64_t n) { return 2 * (((n * ks + 15) & ~15ll) + ((n * w + 15) & ~15ll)); }
@@ -316,5 +392,39 @@ template cudaError_t launch_merge_cluster<int32_t>(void*, void*, int64_t, int64_
                                                    cudaStream_t);
 template cudaError_t launch_merge_cluster<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, int,
                                                    cudaStream_t);
+
+// Grid merge plan: the output range per CTA (R records, every SM busy once the job
+// has >= 1024 records per SM) and its shared memory; 0 when the job does not fit
+// one resident CTA per SM (tile bytes kGridTile per CTA, inputs + output = 2x).
+constexpr int64_t kGridTile = 100 * 1024;
+int64_t grid_merge_plan(int ks, int64_t w, int64_t n, int num_sms, int* ctas, size_t* smem) {
+  const int64_t rec = ks + w;
+  const int64_t rmax = kGridTile / rec;
+  if (n <= 0 || rmax < 64 || n > rmax * num_sms) return 0;
+  const int64_t g = std::min<int64_t>(num_sms, std::max<int64_t>(1, (n + 1023) / 1024));
+  const int64_t R = (n + g - 1) / g;
+  if (R > rmax) return 0;
+  *ctas = (int)((n + R - 1) / R);
+  *smem = (size_t)(2 * R * rec + 6 * 16 + 64);
+  return R;
+}
+
+template <typename KT>
+cudaError_t launch_merge_grid(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int ctas,
+                              int64_t R, size_t smem, cudaStream_t st) {
+  cudaError_t ce = ensure_smem_attr((const void*)k_merge_grid<KT>, smem);
+  if (ce != cudaSuccess) return ce;
+  KT* k = static_cast<KT*>(keys) + s;
+  uint8_t* p = w ? static_cast<uint8_t*>(payload) + s * w : nullptr;
+  int64_t la = m - s, lb = e - m;
+  void* args[] = {(void*)&k, (void*)&p, (void*)&w, (void*)&la, (void*)&lb, (void*)&R};
+  ce = cudaLaunchCooperativeKernel((const void*)k_merge_grid<KT>, dim3(ctas), dim3(kSmallThreads), args, smem, st);
+  count_launches(1);
+  return ce != cudaSuccess ? ce : cudaGetLastError();
+}
+template cudaError_t launch_merge_grid<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, int64_t,
+                                                size_t, cudaStream_t);
+template cudaError_t launch_merge_grid<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int, int64_t,
+                                                size_t, cudaStream_t);
 
 }  // namespace pm

@@ -400,6 +400,30 @@ def test_merge_host_write_back_order(layout, dtype, width):
     assert np.array_equal(payload, want_p), layout
 
 
+@pytest.mark.parametrize("dtype,width", [(np.int32, 0), (np.int32, 4), (np.int64, 12), (np.int32, 5), (np.int64, 64)])
+def test_grid_merge_sizes_vs_oracle(dtype, width):
+    """The one-launch grid merge's range (~1 MB .. ~14 MB of records, k_merge_grid):
+    sizes around its CTA-count and tile boundaries, odd offsets (every 16-byte
+    phase of the pieces), heavy duplicates and skewed splits."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(4242 + width)
+    rec = np.dtype(dtype).itemsize + width
+    top = (148 * 100 * 1024) // rec
+    for size in (300_001, 151_552, 1 << 20, top - 1, top):
+        for domain, split in ((3, 0.5), (2**31 - 1, 0.3), (1000, 0.97)):
+            keys, payload, middle = random_instance(rng, size, split, domain, width)
+            keys = keys.astype(dtype)
+            lo, hi = int(rng.integers(0, 16)), int(rng.integers(0, 9))
+            kk = np.concatenate([np.full(lo, -5, dtype), keys, np.full(hi, 2**31 - 1, dtype)])
+            pp = np.concatenate([np.full((lo, width), 1, np.uint8), payload, np.full((hi, width), 2, np.uint8)])
+            want_k, want_p = kk.copy(), pp.copy()
+            orc.seq_merge_buffered(want_k, want_p, lo, lo + middle, lo + size)
+            arr = to_gpu(kk, pp)
+            _ops.merge(arr, lo, lo + middle, lo + size)
+            assert_same(arr, want_k, want_p, f"size={size} dom={domain} split={split} w={width} lo={lo}")
+
+
 @pytest.mark.parametrize("dtype,width", [(np.int32, 4), (np.int64, 12), (np.int32, 0)])
 def test_large_jobs_vs_oracle(dtype, width):
     """2^22..2^24-record jobs (multi-level salvage, several waves of the grid) vs the oracle,
