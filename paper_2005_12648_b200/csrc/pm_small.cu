@@ -18,6 +18,7 @@
 #include "pm_launch.h"
 #include "pm_hostcache.h"
 #include "pm_search.cuh"
+#include "pm_common.cuh"
 
 namespace pm {
 
@@ -240,24 +241,35 @@ __global__ void __launch_bounds__(kSmallThreads) k_merge_cluster(KT* keys, uint8
 // loads its A and B pieces into shared memory (each at its source's 16-byte
 // phase, so the bulk of the copy is 16-byte words), merges them into a shared
 // output tile, and after one grid-wide barrier -- every CTA has read its inputs --
-// stores the tile in place.  One read and one write per record and a single
+// stores the tile in place (TMA bulk copies both ways, tiles at the source /
+// destination 16-byte phase).  One read and one write per record and a single
 // launch, where the staged path takes a plan kernel, a copy-mode merge into a
-// staging buffer and a copy back (2^21 records: 34 us).
-template <int W>
-__device__ __forceinline__ void g2s_words(uint8_t* dst, const uint8_t* src, int64_t bytes) {
-  using T = typename std::conditional<W == 16, uint4, typename std::conditional<W == 4, uint32_t, uint8_t>::type>::type;
-  T* d = reinterpret_cast<T*>(dst);
-  const T* s = reinterpret_cast<const T*>(src);
-  for (int64_t i = threadIdx.x; i < bytes / W; i += blockDim.x) d[i] = s[i];
-}
-// dst and src share the 16-byte phase: head bytes, 16-byte body, tail bytes
-__device__ __forceinline__ void g2s_phased(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+// staging buffer and a copy back (2^21 records: 34 us; here 19 us).
+// TMA staging of a byte range into shared memory at the source's 16-byte phase:
+// the 16-byte-aligned body by one bulk copy (thread 0, completing on `bar`), the
+// <= 15-byte head and tail by threads; returns the body bytes (for expect_tx).
+__device__ __forceinline__ uint32_t g2s_tma(uint8_t* dst, const uint8_t* src, int64_t bytes, uint64_t* bar) {
   const int64_t head = min(bytes, (int64_t)((16 - ((uintptr_t)src & 15)) & 15));
-  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
   const int64_t body = (bytes - head) & ~(int64_t)15;
-  g2s_words<16>(dst + head, src + head, body);
+  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
   const int64_t t0 = head + body;
   if (t0 + threadIdx.x < bytes) dst[t0 + threadIdx.x] = src[t0 + threadIdx.x];
+  if (threadIdx.x == 0 && body) bulk_g2s(dst + head, src + head, (uint32_t)body, bar);
+  return (uint32_t)body;
+}
+__device__ __forceinline__ uint32_t body_bytes(const uint8_t* src, int64_t bytes) {
+  const int64_t head = min(bytes, (int64_t)((16 - ((uintptr_t)src & 15)) & 15));
+  return (uint32_t)((bytes - head) & ~(int64_t)15);
+}
+// shared -> global at the same 16-byte phase: the body by one bulk store (thread 0;
+// committed, waited for by the caller), head and tail by threads
+__device__ __forceinline__ void s2g_tma(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+  const int64_t head = min(bytes, (int64_t)((16 - ((uintptr_t)dst & 15)) & 15));
+  const int64_t body = (bytes - head) & ~(int64_t)15;
+  if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+  const int64_t t0 = head + body;
+  if (t0 + threadIdx.x < bytes) dst[t0 + threadIdx.x] = src[t0 + threadIdx.x];
+  if (threadIdx.x == 0 && body) bulk_s2g(dst + head, src + head, (uint32_t)body);
 }
 
 template <typename KT>
@@ -265,6 +277,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_merge_grid(KT* keys, uint8
                                                                  int64_t lb, int64_t R) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int64_t s_split[2];
+  __shared__ __align__(8) uint64_t bar;
   cg::grid_group grid = cg::this_grid();
   const int64_t n = la + lb;
   const int64_t x0 = min(n, (int64_t)blockIdx.x * R), x1 = min(n, x0 + R);
@@ -273,38 +286,57 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_merge_grid(KT* keys, uint8
     const int64_t a = merge_path_warp<KT>(keys, la, keys + la, lb, warp ? x1 : x0, lane);
     if (lane == 0) s_split[warp] = a;
   }
+  if (threadIdx.x == 64) mbar_init(&bar, 1);
   __syncthreads();
   const int64_t a0 = s_split[0], a1 = s_split[1], b0 = x0 - a0, b1 = x1 - a1;
   const int alpha = (int)(a1 - a0), beta = (int)(b1 - b0), no = (int)(x1 - x0);
   // shared layout: A keys, B keys (each at its source's 16-byte phase), A rows, B
-  // rows (same), output keys, output rows
+  // rows (same), output keys and rows (at the destination's phase): TMA bulk copies
   const uint8_t* gka = reinterpret_cast<const uint8_t*>(keys + a0);
   const uint8_t* gkb = reinterpret_cast<const uint8_t*>(keys + la + b0);
+  auto up16 = [](const uint8_t* p) { return reinterpret_cast<uint8_t*>(((uintptr_t)p + 15) & ~(uintptr_t)15); };
   uint8_t* ska = sm + ((uintptr_t)gka & 15);
-  uint8_t* skb = sm + ((((uintptr_t)(ska + (int64_t)alpha * sizeof(KT)) + 15) & ~(uintptr_t)15) - (uintptr_t)sm) +
-                 ((uintptr_t)gkb & 15);
+  uint8_t* skb = up16(ska + (int64_t)alpha * sizeof(KT)) + ((uintptr_t)gkb & 15);
   uint8_t* end = skb + (int64_t)beta * sizeof(KT);
-  g2s_phased(ska, gka, (int64_t)alpha * sizeof(KT));
-  g2s_phased(skb, gkb, (int64_t)beta * sizeof(KT));
+  const uint8_t* gpa = w ? pay + a0 * w : nullptr;
+  const uint8_t* gpb = w ? pay + (la + b0) * w : nullptr;
   uint8_t *spa = end, *spb = end;
   if (w) {
-    const uint8_t* gpa = pay + a0 * w;
-    const uint8_t* gpb = pay + (la + b0) * w;
-    spa = reinterpret_cast<uint8_t*>((((uintptr_t)end + 15) & ~(uintptr_t)15) + ((uintptr_t)gpa & 15));
-    spb = reinterpret_cast<uint8_t*>((((uintptr_t)(spa + (int64_t)alpha * w) + 15) & ~(uintptr_t)15) +
-                                     ((uintptr_t)gpb & 15));
-    g2s_phased(spa, gpa, (int64_t)alpha * w);
-    g2s_phased(spb, gpb, (int64_t)beta * w);
+    spa = up16(end) + ((uintptr_t)gpa & 15);
+    spb = up16(spa + (int64_t)alpha * w) + ((uintptr_t)gpb & 15);
     end = spb + (int64_t)beta * w;
   }
-  KT* ok = reinterpret_cast<KT*>(((uintptr_t)end + 15) & ~(uintptr_t)15);
-  uint8_t* op = reinterpret_cast<uint8_t*>((((uintptr_t)(ok + no)) + 15) & ~(uintptr_t)15);
-  __syncthreads();
+  uint8_t* dk = reinterpret_cast<uint8_t*>(keys + x0);
+  uint8_t* dp = w ? pay + x0 * w : nullptr;
+  KT* ok = reinterpret_cast<KT*>(up16(end) + ((uintptr_t)dk & 15));
+  uint8_t* op = w ? up16(reinterpret_cast<uint8_t*>(ok + no)) + ((uintptr_t)dp & 15) : nullptr;
+  if (threadIdx.x == 0) {
+    uint32_t tx = body_bytes(gka, (int64_t)alpha * sizeof(KT)) + body_bytes(gkb, (int64_t)beta * sizeof(KT));
+    if (w) tx += body_bytes(gpa, (int64_t)alpha * w) + body_bytes(gpb, (int64_t)beta * w);
+    mbar_expect_tx(&bar, tx);
+  }
+  g2s_tma(ska, gka, (int64_t)alpha * sizeof(KT), &bar);
+  g2s_tma(skb, gkb, (int64_t)beta * sizeof(KT), &bar);
+  if (w) {
+    g2s_tma(spa, gpa, (int64_t)alpha * w, &bar);
+    g2s_tma(spb, gpb, (int64_t)beta * w, &bar);
+  }
+  if (threadIdx.x == 0) mbar_arrive(&bar);
+  while (!mbar_try_wait(&bar, 0)) {
+  }
+  __syncthreads();  // (head / tail bytes by threads)
   merge_spans_to_tile<KT>(reinterpret_cast<const KT*>(ska), alpha, reinterpret_cast<const KT*>(skb), beta, spa, spb,
                           w, ok, op);
   __syncthreads();
   grid.sync();  // every CTA has read its pieces: the output ranges may be overwritten
-  tile_out<KT>(keys + x0, w ? pay + x0 * w : pay, ok, op, no, w);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (generic writes of the tile -> the bulk store)
+  __syncthreads();
+  s2g_tma(dk, reinterpret_cast<const uint8_t*>(ok), (int64_t)no * sizeof(KT));
+  if (w) s2g_tma(dp, op, (int64_t)no * w);
+  if (threadIdx.x == 0) {
+    bulk_commit();
+    bulk_wait_all();
+  }
 }
 
 }  // namespace
@@ -395,17 +427,16 @@ template cudaError_t launch_merge_cluster<int64_t>(void*, void*, int64_t, int64_
 
 // Grid merge plan: the output range per CTA (R records, every SM busy once the job
 // has >= 1024 records per SM) and its shared memory; 0 when the job does not fit
-// one resident CTA per SM (tile bytes kGridTile per CTA, inputs + output = 2x).
-constexpr int64_t kGridTile = 100 * 1024;
+// one resident CTA per SM (tile bytes kGridTileBytes per CTA, inputs + output = 2x).
 int64_t grid_merge_plan(int ks, int64_t w, int64_t n, int num_sms, int* ctas, size_t* smem) {
   const int64_t rec = ks + w;
-  const int64_t rmax = kGridTile / rec;
+  const int64_t rmax = kGridTileBytes / rec;
   if (n <= 0 || rmax < 64 || n > rmax * num_sms) return 0;
   const int64_t g = std::min<int64_t>(num_sms, std::max<int64_t>(1, (n + 1023) / 1024));
   const int64_t R = (n + g - 1) / g;
   if (R > rmax) return 0;
   *ctas = (int)((n + R - 1) / R);
-  *smem = (size_t)(2 * R * rec + 6 * 16 + 64);
+  *smem = (size_t)(2 * R * rec + 256);  // (six regions, each up to 30 bytes of alignment and phase)
   return R;
 }
 

@@ -402,15 +402,16 @@ def test_merge_host_write_back_order(layout, dtype, width):
 
 @pytest.mark.parametrize("dtype,width", [(np.int32, 0), (np.int32, 4), (np.int64, 12), (np.int32, 5), (np.int64, 64)])
 def test_grid_merge_sizes_vs_oracle(dtype, width):
-    """The one-launch grid merge's range (~1 MB .. ~14 MB of records, k_merge_grid):
-    sizes around its CTA-count and tile boundaries, odd offsets (every 16-byte
-    phase of the pieces), heavy duplicates and skewed splits."""
+    """The one-launch grid merge's range (32 KB .. ~14 MB of records in shared-memory
+    tiles, k_merge_grid) and just beyond it (the staged path): sizes around the
+    CTA-count and tile boundaries, odd offsets (every 16-byte phase of the pieces),
+    heavy duplicates, skewed splits."""
     from paper_2005_12648_b200 import _ops
 
     rng = np.random.default_rng(4242 + width)
     rec = np.dtype(dtype).itemsize + width
     top = (148 * 100 * 1024) // rec
-    for size in (300_001, 151_552, 1 << 20, top - 1, top):
+    for size in (300_001, 151_552, 1 << 20, top - 1, top, top + 1, 3 * top + 12_345):  # (beyond top: the staged path)
         for domain, split in ((3, 0.5), (2**31 - 1, 0.3), (1000, 0.97)):
             keys, payload, middle = random_instance(rng, size, split, domain, width)
             keys = keys.astype(dtype)
