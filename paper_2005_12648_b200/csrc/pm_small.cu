@@ -1,4 +1,7 @@
-// pm_small.cu -- small in-place merges in one CTA.
+// pm_small.cu -- small and medium in-place merges in one launch: one CTA (up to
+// 32 KB of records), one cooperative grid with a shared-memory tile per SM (up to
+// ~14 MB, k_merge_grid below), and the thread-block-cluster merge (kept behind
+// PM_CLUSTER_MERGE; the grid merge is faster).
 //
 // When both runs fit in shared memory (keys + payload rows <= kSmallBytes), a
 // single CTA stages A|B on chip (16-byte bulk loads), each thread finds its
