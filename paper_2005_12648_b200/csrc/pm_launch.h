@@ -80,7 +80,7 @@ int64_t grid_merge_plan(int ks, int64_t w, int64_t n, int num_sms, int* ctas, si
 template <typename KT>
 cudaError_t launch_merge_grid(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int ctas,
                               int64_t R, size_t smem, cudaStream_t st);
-constexpr int64_t kGridTileBytes = 100 * 1024;  // records per CTA tile (in + out: 2x in shared memory)
+constexpr int64_t kGridTileBytes = 113 * 1024;  // records per CTA tile (in + out: 2x in shared memory, + 256 B of alignment <= 227 KB); 148 tiles hold 2^21 int32 records per side
 template <typename KT>
 cudaError_t launch_merge_cluster(void* keys, void* payload, int64_t w, int64_t s, int64_t m, int64_t e, int C,
                                  int lchunk, cudaStream_t st);
