@@ -316,8 +316,11 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
     if (R > 0) {
       cudaError_t ce = ks == 4 ? launch_merge_grid<int32_t>(keys, payload, w, s, m, e, ctas, R, gsm, st)
                                : launch_merge_grid<int64_t>(keys, payload, w, s, m, e, ctas, R, gsm, st);
-      if (ce != cudaSuccess) return cuda_fail(ce, "k_merge_grid launch");
-      return PM_OK;
+      if (ce == cudaSuccess) return PM_OK;
+      // not every SM free for a co-resident grid (other work / partitioned GPU):
+      // the staged path below needs no co-residency
+      if (ce != cudaErrorCooperativeLaunchTooLarge) return cuda_fail(ce, "k_merge_grid launch");
+      cudaGetLastError();
     }
   }
   // medium in-place jobs (at most PM_STAGE_BYTES of records): the streaming merge
