@@ -91,7 +91,10 @@ constexpr int kCoarse = 64;  // k_plan_coarse searches every kCoarse-th region b
 // binary searches were a chain of ~18 dependent DRAM probes on 3 CTAs (2^21
 // records: 6 + 15 us of plan for an 11 us merge).  Larger jobs keep the two
 // levels (a warp per boundary would multiply the probe traffic by 32).
-constexpr int64_t kWarpPlan = 8192;
+#ifndef PM_WARP_PLAN
+#define PM_WARP_PLAN 8192
+#endif
+constexpr int64_t kWarpPlan = PM_WARP_PLAN;
 // Full-range merge-path searches at every kCoarse-th boundary (and the last);
 // k_plan then searches the boundaries in between inside these brackets.
 template <typename KT>
