@@ -1413,137 +1413,147 @@ int pm_merge_host(pm_ctx* ctx, void* keys_host, int key_bytes, void* payload_hos
   std::vector<double> mv_done(nch, -1);
   auto h0 = std::chrono::steady_clock::now();
 #endif
-  auto h2d = [&](int64_t x0, int64_t x1) -> int {
-    if (x1 <= x0) return PM_OK;
-    PM_CUDA(cudaMemcpyAsync(dxk + x0 * key_bytes, hk + x0 * key_bytes, (x1 - x0) * key_bytes,
-                            cudaMemcpyHostToDevice, sH));
-    if (width)
-      PM_CUDA(cudaMemcpyAsync(dxp + x0 * width, hp + x0 * width, (x1 - x0) * width, cudaMemcpyHostToDevice, sH));
-    return PM_OK;
-  };
-  constexpr int kEv = (int)(sizeof(((pm_ctx*)nullptr)->hev) / sizeof(cudaEvent_t)) - 1;
-  int next = 0;  // next chunk (in `order`) to write back
-  for (int k = 0; k < nch; ++k) {
-    const int64_t d0 = dk[k], a0 = ak[k], b0 = d0 - a0, d1 = dk[k + 1], a1 = ak[k + 1], b1 = d1 - a1;
-    rc = h2d(a0, a1);
-    if (!rc) rc = h2d(la + b0, la + b1);
-    if (rc) return rc;
-    PM_CUDA(cudaEventRecord(ctx->hup[k], sH));
-    PM_CUDA(cudaStreamWaitEvent(sC, ctx->hup[k], 0));
+  // the pipeline proper: on any failure the three streams are drained before the
+  // error returns, so no transfer still writes the caller's buffers afterwards
+  auto pipeline = [&]() -> int {
+    auto h2d = [&](int64_t x0, int64_t x1) -> int {
+      if (x1 <= x0) return PM_OK;
+      PM_CUDA(cudaMemcpyAsync(dxk + x0 * key_bytes, hk + x0 * key_bytes, (x1 - x0) * key_bytes,
+                              cudaMemcpyHostToDevice, sH));
+      if (width)
+        PM_CUDA(cudaMemcpyAsync(dxp + x0 * width, hp + x0 * width, (x1 - x0) * width, cudaMemcpyHostToDevice, sH));
+      return PM_OK;
+    };
+    constexpr int kEv = (int)(sizeof(((pm_ctx*)nullptr)->hev) / sizeof(cudaEvent_t)) - 1;
+    int next = 0;  // next chunk (in `order`) to write back
+    for (int k = 0; k < nch; ++k) {
+      const int64_t d0 = dk[k], a0 = ak[k], b0 = d0 - a0, d1 = dk[k + 1], a1 = ak[k + 1], b1 = d1 - a1;
+      rc = h2d(a0, a1);
+      if (!rc) rc = h2d(la + b0, la + b1);
+      if (rc) return rc;
+      PM_CUDA(cudaEventRecord(ctx->hup[k], sH));
+      PM_CUDA(cudaStreamWaitEvent(sC, ctx->hup[k], 0));
 #ifdef PM_HOST_TRACE
-    cudaEventRecord(tr[3 * k], sH);
+      cudaEventRecord(tr[3 * k], sH);
 #endif
-    {
-      std::lock_guard<std::mutex> lk(ctx->mu);
-      use_stream(ctx, sC);  // (the copy merges share the context's workspace with calls on other streams)
-      rc = run_engine(ctx, dxk + a0 * key_bytes, key_bytes, width ? dxp + a0 * width : nullptr, width, 0, a1 - a0,
-                      d1 - d0, MODE_MERGE, 0, sC, dok + d0 * key_bytes, width ? dop + d0 * width : nullptr,
-                      dxk + (la + b0) * key_bytes, width ? dxp + (la + b0) * width : nullptr);
-    }
-    if (rc) return rc;
+      {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        use_stream(ctx, sC);  // (the copy merges share the context's workspace with calls on other streams)
+        rc = run_engine(ctx, dxk + a0 * key_bytes, key_bytes, width ? dxp + a0 * width : nullptr, width, 0, a1 - a0,
+                        d1 - d0, MODE_MERGE, 0, sC, dok + d0 * key_bytes, width ? dop + d0 * width : nullptr,
+                        dxk + (la + b0) * key_bytes, width ? dxp + (la + b0) * width : nullptr);
+      }
+      if (rc) return rc;
 #ifdef PM_HOST_TRACE
-    cudaEventRecord(tr[3 * k + 1], sC);
+      cudaEventRecord(tr[3 * k + 1], sC);
 #endif
-    if (next < nch && ready[order[next]] == k) {
-      // merges run in order on sC: chunk k merged => uploads 0..k and merges 0..k done;
-      // the event is waited on right after it is recorded, so the ring can be reused
-      cudaEvent_t ec = ctx->hev[1 + k % kEv];
-      PM_CUDA(cudaEventRecord(ec, sC));
-      PM_CUDA(cudaStreamWaitEvent(sD, ec, 0));
-      for (; next < nch && ready[order[next]] == k; ++next) {
-        const int c = order[next];
-        const int64_t e0 = dk[c], e1 = dk[c + 1];
-        char* tk = soff[c] != SIZE_MAX && use_stage ? hs_base + soff[c] : hk + e0 * key_bytes;
-        char* tp = soff[c] != SIZE_MAX && use_stage ? tk + (e1 - e0) * key_bytes : hp + e0 * width;
-        PM_CUDA(cudaMemcpyAsync(tk, dok + e0 * key_bytes, (e1 - e0) * key_bytes, cudaMemcpyDeviceToHost, sD));
-        if (width) PM_CUDA(cudaMemcpyAsync(tp, dop + e0 * width, (e1 - e0) * width, cudaMemcpyDeviceToHost, sD));
-        if (soff[c] != SIZE_MAX && use_stage) PM_CUDA(cudaEventRecord(ctx->hdn[c], sD));
+      if (next < nch && ready[order[next]] == k) {
+        // merges run in order on sC: chunk k merged => uploads 0..k and merges 0..k done;
+        // the event is waited on right after it is recorded, so the ring can be reused
+        cudaEvent_t ec = ctx->hev[1 + k % kEv];
+        PM_CUDA(cudaEventRecord(ec, sC));
+        PM_CUDA(cudaStreamWaitEvent(sD, ec, 0));
+        for (; next < nch && ready[order[next]] == k; ++next) {
+          const int c = order[next];
+          const int64_t e0 = dk[c], e1 = dk[c + 1];
+          char* tk = soff[c] != SIZE_MAX && use_stage ? hs_base + soff[c] : hk + e0 * key_bytes;
+          char* tp = soff[c] != SIZE_MAX && use_stage ? tk + (e1 - e0) * key_bytes : hp + e0 * width;
+          PM_CUDA(cudaMemcpyAsync(tk, dok + e0 * key_bytes, (e1 - e0) * key_bytes, cudaMemcpyDeviceToHost, sD));
+          if (width) PM_CUDA(cudaMemcpyAsync(tp, dop + e0 * width, (e1 - e0) * width, cudaMemcpyDeviceToHost, sD));
+          if (soff[c] != SIZE_MAX && use_stage) PM_CUDA(cudaEventRecord(ctx->hdn[c], sD));
 #ifdef PM_HOST_TRACE
-        cudaEventRecord(tr[3 * c + 2], sD);
+          cudaEventRecord(tr[3 * c + 2], sD);
 #endif
+        }
       }
     }
-  }
-  if (next != nch) return fail(PM_ERR_INTERNAL, "pm_merge_host: write-back schedule incomplete");
-  PM_CUDA(cudaEventRecord(ctx->hev[0], sD));
-  PM_CUDA(cudaStreamWaitEvent(st, ctx->hev[0], 0));
-  if (!stg.empty()) {
-    // host threads move the staged chunks into place, each once its range has
-    // been uploaded and its D2H has landed.  The work is cut into pieces of at most
-    // PM_HOST_PIECE bytes, taken in order from one counter: a thread that the OS
-    // deschedules delays only its current piece (fixed per-thread stripes made
-    // the slowest thread the critical path: 102 ms median, 129 ms outliers)
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (next != nch) return fail(PM_ERR_INTERNAL, "pm_merge_host: write-back schedule incomplete");
+    PM_CUDA(cudaEventRecord(ctx->hev[0], sD));
+    PM_CUDA(cudaStreamWaitEvent(st, ctx->hev[0], 0));
+    if (!stg.empty()) {
+      // host threads move the staged chunks into place, each once its range has
+      // been uploaded and its D2H has landed.  The work is cut into pieces of at most
+      // PM_HOST_PIECE bytes, taken in order from one counter: a thread that the OS
+      // deschedules delays only its current piece (fixed per-thread stripes made
+      // the slowest thread the critical path: 102 ms median, 129 ms outliers)
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
 #ifndef PM_HOST_MOVERS
 #define PM_HOST_MOVERS 4u  // more threads take host memory bandwidth from the DMA (tools/gpu_pcie_chunks.py)
 #endif
 #ifndef PM_HOST_PIECE
 #define PM_HOST_PIECE ((int64_t)16 << 20)  // 4 MB: 103.8 ms mean, 16 MB: 102.6 (2^30 int32)
 #endif
-    const int nt = (int)std::min<unsigned>(PM_HOST_MOVERS, std::max(1u, hw / 2));
-    struct Piece {
-      int c;          // staged chunk
-      char* dst;
-      const char* src;
-      int64_t bytes;
-    };
-    std::vector<Piece> pieces;
-    for (int c : stg) {
-      const int64_t e0 = dk[c], e1 = dk[c + 1];
-      const char* src = hs_base + soff[c];
-      auto cut = [&](char* dst, const char* from, int64_t bytes) {
-        for (int64_t x = 0; x < bytes; x += PM_HOST_PIECE)
-          pieces.push_back({c, dst + x, from + x, std::min<int64_t>(PM_HOST_PIECE, bytes - x)});
+      const int nt = (int)std::min<unsigned>(PM_HOST_MOVERS, std::max(1u, hw / 2));
+      struct Piece {
+        int c;          // staged chunk
+        char* dst;
+        const char* src;
+        int64_t bytes;
       };
-      cut(hk + e0 * key_bytes, src, (e1 - e0) * key_bytes);
-      if (width) cut(hp + e0 * width, src + (e1 - e0) * key_bytes, (e1 - e0) * width);
-    }
-    std::atomic<size_t> next_piece{0};
-    std::atomic<int> err{0};
-    auto mover = [&](int t) {
-      int ready_c = -1;  // the chunk whose events this thread has seen complete
-      for (size_t i; (i = next_piece.fetch_add(1)) < pieces.size();) {
-        const Piece& pc = pieces[i];
-        if (pc.c != ready_c) {
-          if (cudaEventSynchronize(ctx->hup[free_at[pc.c]]) != cudaSuccess ||
-              cudaEventSynchronize(ctx->hdn[pc.c]) != cudaSuccess) {
-            err.store(1);
-            return;
-          }
-          ready_c = pc.c;
-        }
-        std::memcpy(pc.dst, pc.src, (size_t)pc.bytes);
-#ifdef PM_HOST_TRACE
-        if (i + 1 == pieces.size() || pieces[i + 1].c != pc.c)
-          mv_done[pc.c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-#endif
+      std::vector<Piece> pieces;
+      for (int c : stg) {
+        const int64_t e0 = dk[c], e1 = dk[c + 1];
+        const char* src = hs_base + soff[c];
+        auto cut = [&](char* dst, const char* from, int64_t bytes) {
+          for (int64_t x = 0; x < bytes; x += PM_HOST_PIECE)
+            pieces.push_back({c, dst + x, from + x, std::min<int64_t>(PM_HOST_PIECE, bytes - x)});
+        };
+        cut(hk + e0 * key_bytes, src, (e1 - e0) * key_bytes);
+        if (width) cut(hp + e0 * width, src + (e1 - e0) * key_bytes, (e1 - e0) * width);
       }
-      (void)t;
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(mover, t);
-    mover(0);
-    for (auto& th : pool) th.join();
-    if (err.load()) return cuda_fail(cudaGetLastError(), "pm_merge_host: staged write-back");
-  }
+      std::atomic<size_t> next_piece{0};
+      std::atomic<int> err{0};
+      auto mover = [&](int t) {
+        int ready_c = -1;  // the chunk whose events this thread has seen complete
+        for (size_t i; (i = next_piece.fetch_add(1)) < pieces.size();) {
+          const Piece& pc = pieces[i];
+          if (pc.c != ready_c) {
+            if (cudaEventSynchronize(ctx->hup[free_at[pc.c]]) != cudaSuccess ||
+                cudaEventSynchronize(ctx->hdn[pc.c]) != cudaSuccess) {
+              err.store(1);
+              return;
+            }
+            ready_c = pc.c;
+          }
+          std::memcpy(pc.dst, pc.src, (size_t)pc.bytes);
 #ifdef PM_HOST_TRACE
-  {
-    cudaStreamSynchronize(sD);
-    const double hend = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-    float t0h;  // host offset of the device origin is unknown: report device times from the first record
-    (void)t0h;
-    fprintf(stderr, "TRACE nch=%d staged=%zu use_stage=%d host_end=%.2f\n", nch, stg.size(), (int)use_stage, hend);
-    for (int k = 0; k < nch; ++k) {
-      float u = -1, m = -1, d = -1;
-      cudaEventElapsedTime(&u, tr[3 * nch], tr[3 * k]);
-      cudaEventElapsedTime(&m, tr[3 * nch], tr[3 * k + 1]);
-      cudaEventElapsedTime(&d, tr[3 * nch], tr[3 * k + 2]);
-      fprintf(stderr, "TRACE k=%d free=%d up=%.2f merge=%.2f d2h=%.2f moved=%.2f\n", k, free_at[k], u, m, d,
-              mv_done[k]);
-    }
-    for (auto& e : tr) cudaEventDestroy(e);
-  }
+          if (i + 1 == pieces.size() || pieces[i + 1].c != pc.c)
+            mv_done[pc.c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
 #endif
+        }
+        (void)t;
+      };
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(mover, t);
+      mover(0);
+      for (auto& th : pool) th.join();
+      if (err.load()) return cuda_fail(cudaGetLastError(), "pm_merge_host: staged write-back");
+    }
+#ifdef PM_HOST_TRACE
+    {
+      cudaStreamSynchronize(sD);
+      const double hend = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+      float t0h;  // host offset of the device origin is unknown: report device times from the first record
+      (void)t0h;
+      fprintf(stderr, "TRACE nch=%d staged=%zu use_stage=%d host_end=%.2f\n", nch, stg.size(), (int)use_stage, hend);
+      for (int k = 0; k < nch; ++k) {
+        float u = -1, m = -1, d = -1;
+        cudaEventElapsedTime(&u, tr[3 * nch], tr[3 * k]);
+        cudaEventElapsedTime(&m, tr[3 * nch], tr[3 * k + 1]);
+        cudaEventElapsedTime(&d, tr[3 * nch], tr[3 * k + 2]);
+        fprintf(stderr, "TRACE k=%d free=%d up=%.2f merge=%.2f d2h=%.2f moved=%.2f\n", k, free_at[k], u, m, d,
+                mv_done[k]);
+      }
+      for (auto& e : tr) cudaEventDestroy(e);
+    }
+#endif
+    return PM_OK;
+  };
+  rc = pipeline();
+  if (rc) {
+    for (cudaStream_t x : {sH, sC, sD}) cudaStreamSynchronize(x);
+    return rc;
+  }
   return pm_status(ctx, stream, nullptr);
 }
 
