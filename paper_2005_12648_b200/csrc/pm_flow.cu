@@ -727,6 +727,51 @@ __device__ __forceinline__ void ph_tickets(const FlowParams& F) {
   }
 }
 
+// ---- k_flow_save: copy the salvage entries into the pool ------------------------
+// Work items are (slot, chunk of the slot): a skewed job's salvage sits in a few
+// slots, and one warp copying a whole 32 KB entry is a chain of dependent round
+// trips; chunks spread an entry over several warps.  As many chunks per slot as
+// keep the scan to one pass (lanes of all warps >= items), at least 8 KB of keys
+// each (2 KB items: 0.24 -> 0.35 ms at 2^30 int32, 0.07 -> 0.11 ms at config 4).
+// Each warp scans 32 items at a time (one per lane, lane-strided so every warp
+// gets items), then copies the items that hold salvage one after another with
+// the whole warp (16-byte vectors, identical phase on both sides).
+__device__ __forceinline__ void ph_save(const FlowParams& F) {
+  const EngineParams& P = F.P;
+  FlowGeo g(P);
+  const int lane = threadIdx.x & 31;
+  const int64_t ks = P.ks, w = P.w;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nc = max((int64_t)1, min(32 * nw / P.K, P.T * ks / 8192)), items = P.K * nc;
+  const int32_t csz = (int32_t)((P.T + nc - 1) / nc);
+  for (int64_t i0 = w0; i0 < items; i0 += nw * 32) {
+    const int64_t it = i0 + lane * nw;  // (lane-strided: every warp gets items while items >= warps)
+    int64_t x0 = 0, x1 = 0, dl = 0;
+    if (it < items) {
+      const int64_t j = it / nc, c = it - j * nc;
+      const int32_t lo = max(F.slo[j], (int32_t)c * csz), hi = min(F.shi[j], (int32_t)(c + 1) * csz);
+      if (hi > lo) {
+        const int64_t base = g.slot_base(j);
+        // the records of the hull that belong to the job
+        x0 = max(base + lo, g.slot_lo(j));
+        x1 = min(base + hi, g.slot_hi(j));
+        dl = F.pdelta[j];
+      }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, x1 > x0);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
+      const int64_t d = __shfl_sync(0xffffffffu, dl, src);
+      FLOW_CHECK(y0 + d >= 0 && y1 + d <= F.pool_cap && y0 >= P.s && y1 <= P.e);
+      copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (y0 + d) * ks),
+                    reinterpret_cast<const uint8_t*>(P.keys + y0 * ks), (y1 - y0) * ks, lane);
+      if (w) copy_g2g_warp(F.pool_pay + (y0 + d) * w, P.pay + y0 * w, (y1 - y0) * w, lane);
+    }
+  }
+}
+
 // ---- k_flow_plan: every plan phase in one cooperative launch --------------------
 // One CTA of 1024 threads per SM; a grid-wide barrier between phases replaces a
 // kernel boundary (the phases are short and latency-bound: launch gaps and tails
@@ -734,6 +779,9 @@ __device__ __forceinline__ void ph_tickets(const FlowParams& F) {
 // is taken by the whole grid, after a barrier, so no CTA is left waiting.
 #ifndef PM_FLOW_DEBUG
 #define PM_FLOW_DEBUG 0
+#endif
+#ifndef PM_FLOW_SAVE_IN_PLAN
+#define PM_FLOW_SAVE_IN_PLAN 0  // 1: salvage copy inside the plan kernel, beside the tickets (2^30: plan + copy 0.401 vs 0.129 + 0.225 ms separate -- the plan grid copies slower)
 #endif
 #ifndef PM_FLOW_TF_EARLY
 #define PM_FLOW_TF_EARLY 32
@@ -797,52 +845,16 @@ __global__ void __launch_bounds__(kFlowChunk, 1) k_flow_plan(FlowParams F) {
   PM_FLOW_DBG(11);
   ph_tickets(F);
   PM_FLOW_DBG(12);
+#if PM_FLOW_SAVE_IN_PLAN
+  // the salvage copy in the same phase as the tickets (both need only the pool
+  // offsets): no kernel boundary, and the tickets overlap the copy
+  if (!block_flow_off(F)) ph_save(F);
+#endif
 }
 
-// ---- k_flow_save: copy the salvage entries into the pool ------------------------
-// Work items are (slot, chunk of the slot): a skewed job's salvage sits in a few
-// slots, and one warp copying a whole 32 KB entry is a chain of dependent round
-// trips; chunks spread an entry over several warps.  As many chunks per slot as
-// keep the scan to one pass (lanes of all warps >= items), at least 8 KB of keys
-// each (2 KB items: 0.24 -> 0.35 ms at 2^30 int32, 0.07 -> 0.11 ms at config 4).
-// Each warp scans 32 items at a time (one per lane, lane-strided so every warp
-// gets items), then copies the items that hold salvage one after another with
-// the whole warp (16-byte vectors, identical phase on both sides).
 __global__ void __launch_bounds__(256) k_flow_save(FlowParams F) {
-  const EngineParams& P = F.P;
-  FlowGeo g(P);
   if (flow_off(F)) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t ks = P.ks, w = P.w;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nc = max((int64_t)1, min(32 * nw / P.K, P.T * ks / 8192)), items = P.K * nc;
-  const int32_t csz = (int32_t)((P.T + nc - 1) / nc);
-  for (int64_t i0 = w0; i0 < items; i0 += nw * 32) {
-    const int64_t it = i0 + lane * nw;  // (lane-strided: every warp gets items while items >= warps)
-    int64_t x0 = 0, x1 = 0, dl = 0;
-    if (it < items) {
-      const int64_t j = it / nc, c = it - j * nc;
-      const int32_t lo = max(F.slo[j], (int32_t)c * csz), hi = min(F.shi[j], (int32_t)(c + 1) * csz);
-      if (hi > lo) {
-        const int64_t base = g.slot_base(j);
-        // the records of the hull that belong to the job
-        x0 = max(base + lo, g.slot_lo(j));
-        x1 = min(base + hi, g.slot_hi(j));
-        dl = F.pdelta[j];
-      }
-    }
-    unsigned todo = __ballot_sync(0xffffffffu, x1 > x0);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
-      const int64_t d = __shfl_sync(0xffffffffu, dl, src);
-      FLOW_CHECK(y0 + d >= 0 && y1 + d <= F.pool_cap && y0 >= P.s && y1 <= P.e);
-      copy_g2g_warp(reinterpret_cast<uint8_t*>(F.pool_keys + (y0 + d) * ks),
-                    reinterpret_cast<const uint8_t*>(P.keys + y0 * ks), (y1 - y0) * ks, lane);
-      if (w) copy_g2g_warp(F.pool_pay + (y0 + d) * w, P.pay + y0 * w, (y1 - y0) * w, lane);
-    }
-  }
+  ph_save(F);
 }
 
 // Prescribed layout (pm_reorder): output o of the region at job-local diagonal d0
@@ -1165,9 +1177,10 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
     e = cudaEventRecord(ev_fork, st);
     if (e != cudaSuccess) return e;
   }
-  {
+  if (!PM_FLOW_SAVE_IN_PLAN) {
     NvtxRange r("pm_flow: salvage copy");
     k_flow_save<<<num_sms * 8, 256, 0, st>>>(F);
+    count_launches(1);
   }
   if (ev_merge) {
     e = cudaEventRecord(ev_merge, st);
@@ -1177,7 +1190,7 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
     NvtxRange r("pm_flow: merge");
     k_flow<KT><<<grid, kFlowThreads, smem, st>>>(F);
   }
-  count_launches(2);
+  count_launches(1);
 
   return cudaGetLastError();
 }
