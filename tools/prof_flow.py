@@ -15,7 +15,8 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 29
 mode = sys.argv[2] if len(sys.argv) > 2 else "auto"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 _ops.set_flow_mode(mode)
-k0, p0, m = config_input_device(2, seed=3, log_len=L)
+import os
+k0, p0, m = config_input_device(int(os.environ.get("CFG", "2")), seed=3, log_len=L)
 n = k0.numel()
 arr = pm.KeyedArray(k0.clone(), p0.clone())
 for r in range(reps):
