@@ -692,6 +692,17 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
                : launch_flow<int64_t>(F, grid, smem, ctx->num_sms, plan_bps, st, ctx->timing ? ctx->ev[1] : nullptr,
                                       ctx->timing ? ctx->ev[3] : nullptr, ctx->ffork);
   ctx->ev_mid = ctx->timing;
+  if (ce == cudaErrorCooperativeLaunchTooLarge && !nleaves) {
+    // the cooperative plan grid cannot be co-resident (SMs taken by other work, a
+    // partitioned GPU): nothing was launched -- the bounded-pool engine needs no
+    // co-residency (its persistent grid only needs forward progress)
+    cudaGetLastError();
+    const int fm = ctx->flow_mode;
+    ctx->flow_mode = 0;
+    const int rc2 = run_engine(ctx, keys, ks, payload, w, s, m, e, MODE_MERGE, scratch_records, st);
+    ctx->flow_mode = fm;
+    return rc2;
+  }
   if (ce != cudaSuccess) return cuda_fail(ce, "k_flow launch");
   if (ctx->timing) {
     PM_CUDA(cudaEventRecord(ctx->ev[2], st));
