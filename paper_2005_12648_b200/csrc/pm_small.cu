@@ -98,6 +98,7 @@ __device__ __forceinline__ void tile_out(KT* keys, uint8_t* pay, const KT* ok, c
 template <typename KT>
 __global__ void __launch_bounds__(kSmallThreads) k_merge_small(KT* keys, uint8_t* pay, int64_t w, int la, int lb) {
   extern __shared__ __align__(16) uint8_t sm[];
+  if (keys[la - 1] <= keys[la]) return;  // already in order (srecpar.py:56-57): nothing moves
   const int n = la + lb;
   const int64_t kreg = ((int64_t)n * sizeof(KT) + 15) & ~(int64_t)15, preg = ((int64_t)n * w + 15) & ~(int64_t)15;
   KT* sk = reinterpret_cast<KT*>(sm);
@@ -282,6 +283,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_merge_grid(KT* keys, uint8
   __shared__ int64_t s_split[2];
   __shared__ __align__(8) uint64_t bar;
   cg::grid_group grid = cg::this_grid();
+  // already in order (srecpar.py:56-57): nothing moves (every CTA reads the same two
+  // keys and leaves before the grid barrier, so no CTA waits there alone)
+  if (keys[la - 1] <= keys[la]) return;
   const int64_t n = la + lb;
   const int64_t x0 = min(n, (int64_t)blockIdx.x * R), x1 = min(n, x0 + R);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

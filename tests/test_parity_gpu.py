@@ -425,6 +425,24 @@ def test_grid_merge_sizes_vs_oracle(dtype, width):
             assert_same(arr, want_k, want_p, f"size={size} dom={domain} split={split} w={width} lo={lo}")
 
 
+@pytest.mark.parametrize("size", [100, 5000, 300_000, 1 << 21])
+def test_already_ordered_jobs_unchanged(size):
+    """A[last] <= B[0] (ties included): nothing moves (srecpar.py:56-57) on every
+    route -- keys and payload bytes unchanged."""
+    from paper_2005_12648_b200 import _ops
+
+    rng = np.random.default_rng(size)
+    middle = size // 3
+    a = np.sort(rng.integers(0, 1000, middle))
+    b = np.sort(rng.integers(999, 2000, size - middle))
+    b[0] = a[-1]  # a tie across the boundary still needs no move
+    keys = np.concatenate([a, b]).astype(np.int32)
+    payload = rng.integers(0, 256, (size, 4), dtype=np.uint8)
+    arr = to_gpu(keys, payload)
+    _ops.merge(arr, 0, middle, size)
+    assert_same(arr, keys, payload, f"size={size}")
+
+
 @pytest.mark.parametrize("dtype,width", [(np.int32, 4), (np.int64, 12), (np.int32, 0)])
 def test_large_jobs_vs_oracle(dtype, width):
     """2^22..2^24-record jobs (multi-level salvage, several waves of the grid) vs the oracle,
