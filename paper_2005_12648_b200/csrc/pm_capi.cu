@@ -174,6 +174,10 @@ static int run_engine(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w,
 #ifndef PM_SLIDE_STASH
 #define PM_SLIDE_STASH (64ll << 20)  // pm_shift: one-pass slide when the smaller block fits this stash
 #endif
+#ifndef PM_GRIES_MILLS
+#define PM_GRIES_MILLS 0  // 1: block exchanges by Gries-Mills swaps + reversals for the remainder -- slower than the
+                          // reversals alone (2^30, 1:2 blocks: 3.94 vs 2.97 ms; unaligned swaps, several launches)
+#endif
 #ifndef PM_CLUSTER_MERGE
 #define PM_CLUSTER_MERGE 0  // 1: jobs of up to ~1 MB in one thread-block cluster (distributed shared memory) --
                             // the one-launch grid merge is faster at every such size (2^15 records per side:
@@ -720,6 +724,9 @@ static int run_flow(pm_ctx* ctx, void* keys, int ks, void* payload, int64_t w, i
     const int32_t* rg = reinterpret_cast<const int32_t*>(&F.fc[FC_ROTFAIL]);
     if (m - s == e - m)
       ce = launch_swap_blocks(keys, ks, payload, w, s, m - s, ctx->num_sms, ctx->fside, rg);
+    else if (PM_GRIES_MILLS)
+      ce = ks == 4 ? launch_block_exchange<int32_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg)
+                   : launch_block_exchange<int64_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg);
     else
       ce = ks == 4 ? launch_rotate<int32_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg)
                    : launch_rotate<int64_t>(keys, payload, w, s, m - s, e - m, ctx->num_sms, ctx->fside, rg);
@@ -1219,10 +1226,15 @@ int pm_shift(pm_ctx* ctx, void* keys, int key_bytes, void* payload, int64_t widt
     if (width) PM_CUDA(cudaMemcpyAsync(Pp + xdst * width, stash_p, (size_t)(small * width), cudaMemcpyDeviceToDevice, st));
     return PM_OK;
   }
-  // three reversals (pm_rotate.cu): two streaming passes, no workspace
-  const cudaError_t e = key_bytes == 4
-                            ? launch_rotate<int32_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st)
-                            : launch_rotate<int64_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st);
+  // Gries-Mills block swaps (the reference's linear shift) while the smaller block
+  // is >= 1/16 of the exchange, three streaming reversals for the rest (pm_rotate.cu);
+  // no workspace
+  const cudaError_t e =
+      PM_GRIES_MILLS
+          ? (key_bytes == 4 ? launch_block_exchange<int32_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st)
+                            : launch_block_exchange<int64_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st))
+          : (key_bytes == 4 ? launch_rotate<int32_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st)
+                            : launch_rotate<int64_t>(keys, payload, width, lo, len_a, len_b, ctx->num_sms, st));
   if (e != cudaSuccess) return cuda_fail(e, "k_reverse launch");
   return PM_OK;
 }

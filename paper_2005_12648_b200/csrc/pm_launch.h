@@ -37,6 +37,10 @@ cudaError_t launch_flow(const FlowParams& F, int grid, size_t smem, int num_sms,
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,
                           cudaStream_t st, const int32_t* gate = nullptr);  // gate: run only if *gate != 0
+// A|B -> B|A on [lo, lo + la + lb) by Gries-Mills block swaps, three reversals for the remainder (gated likewise)
+template <typename KT>
+cudaError_t launch_block_exchange(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb,
+                                  int num_sms, cudaStream_t st, const int32_t* gate = nullptr);
 // equal blocks: [lo, lo + len) <-> [lo + len, lo + 2 len), keys and payload planes (gated likewise)
 cudaError_t launch_swap_blocks(void* keys, int ks, void* payload, int64_t w, int64_t lo, int64_t len, int num_sms,
                                cudaStream_t st, const int32_t* gate = nullptr);

@@ -387,10 +387,10 @@ cudaError_t launch_slide(void* plane, int64_t S0, int64_t L, int64_t D, bool rig
 // instead of the reversals' 4 N w).  Grid-stride, four words per thread in flight;
 // 16-byte words when both blocks share the 16-byte grid, else 4- or 1-byte words.
 template <typename WT>
-__global__ void __launch_bounds__(256) k_swap_blocks(const int32_t* gate, uint8_t* x, int64_t nbytes) {
+__global__ void __launch_bounds__(256) k_swap_blocks(const int32_t* gate, uint8_t* x, uint8_t* y, int64_t nbytes) {
   if (gate && !*(volatile const int32_t*)gate) return;
   WT* a = reinterpret_cast<WT*>(x);
-  WT* b = reinterpret_cast<WT*>(x + nbytes);
+  WT* b = reinterpret_cast<WT*>(y);
   const int64_t n = nbytes / (int64_t)sizeof(WT), stride = (int64_t)gridDim.x * blockDim.x;
   constexpr int U = 4;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
@@ -417,31 +417,76 @@ __global__ void __launch_bounds__(256) k_swap_blocks(const int32_t* gate, uint8_
 // grid: every resident CTA once (a grid-stride kernel with a second partial wave
 // leaves the late CTAs running alone: 0.66 of the copy peak at 2^30 with 1184 CTAs)
 template <typename WT>
-static cudaError_t swap_launch(uint8_t* x, int64_t nbytes, int num_sms, cudaStream_t st, const int32_t* gate) {
+static cudaError_t swap_launch(uint8_t* x, uint8_t* y, int64_t nbytes, int num_sms, cudaStream_t st,
+                               const int32_t* gate) {
   int bps = 0;
   cudaError_t e = cached_occupancy(&bps, (const void*)k_swap_blocks<WT>, 256, 0);
   if (e != cudaSuccess) return e;
   const int64_t words = nbytes / (int64_t)sizeof(WT);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((words + 1023) / 1024, (int64_t)num_sms * std::max(bps, 1)));
-  k_swap_blocks<WT><<<grid, 256, 0, st>>>(gate, x, nbytes);
+  k_swap_blocks<WT><<<grid, 256, 0, st>>>(gate, x, y, nbytes);
   return cudaGetLastError();
 }
-static cudaError_t swap_plane(uint8_t* x, int64_t nbytes, int num_sms, cudaStream_t st, const int32_t* gate) {
+// swap the disjoint byte blocks [x, x + nbytes) and [y, y + nbytes)
+static cudaError_t swap_plane(uint8_t* x, uint8_t* y, int64_t nbytes, int num_sms, cudaStream_t st,
+                              const int32_t* gate) {
   if (nbytes <= 0) return cudaSuccess;
-  const uintptr_t al = (uintptr_t)x | (uintptr_t)nbytes;
+  const uintptr_t al = (uintptr_t)x | (uintptr_t)y | (uintptr_t)nbytes;
   count_launches(1);
-  if ((al & 15) == 0) return swap_launch<uint4>(x, nbytes, num_sms, st, gate);
-  if ((al & 3) == 0) return swap_launch<uint32_t>(x, nbytes, num_sms, st, gate);
-  return swap_launch<uint8_t>(x, nbytes, num_sms, st, gate);
+  if ((al & 15) == 0) return swap_launch<uint4>(x, y, nbytes, num_sms, st, gate);
+  if ((al & 3) == 0) return swap_launch<uint32_t>(x, y, nbytes, num_sms, st, gate);
+  return swap_launch<uint8_t>(x, y, nbytes, num_sms, st, gate);
+}
+// records [x0, x0 + len) <-> [y0, y0 + len) (disjoint) in the keys and payload planes
+static cudaError_t swap_records(void* keys, int ks, void* payload, int64_t w, int64_t x0, int64_t y0, int64_t len,
+                                int num_sms, cudaStream_t st, const int32_t* gate) {
+  uint8_t* K = static_cast<uint8_t*>(keys);
+  cudaError_t e = swap_plane(K + x0 * ks, K + y0 * ks, len * ks, num_sms, st, gate);
+  if (e == cudaSuccess && w) {
+    uint8_t* P = static_cast<uint8_t*>(payload);
+    e = swap_plane(P + x0 * w, P + y0 * w, len * w, num_sms, st, gate);
+  }
+  return e;
 }
 
 // [lo, lo + len) <-> [lo + len, lo + 2 len) in the keys and the payload planes
 cudaError_t launch_swap_blocks(void* keys, int ks, void* payload, int64_t w, int64_t lo, int64_t len, int num_sms,
                                cudaStream_t st, const int32_t* gate) {
-  cudaError_t e = swap_plane(static_cast<uint8_t*>(keys) + lo * ks, len * ks, num_sms, st, gate);
-  if (e == cudaSuccess && w) e = swap_plane(static_cast<uint8_t*>(payload) + lo * w, len * w, num_sms, st, gate);
-  return e;
+  return swap_records(keys, ks, payload, w, lo, lo + len, len, num_sms, st, gate);
 }
+
+// Linear shifting by block swaps (the reference's Gries-Mills exchange,
+// _kernels.py:92-150): swap the smaller block with the far end of the larger one
+// -- it lands in its final place -- and continue on the rest.  Each step is one
+// streaming swap (4 s w bytes for a block of s records); the steps stop once the
+// smaller block is under 1/16 of the exchange (or after 16 steps), and three
+// reversals finish the remainder.  Equal blocks: one swap.  The sequence depends
+// only on the lengths, so it is enqueued whole (gated like the reversals).
+template <typename KT>
+cudaError_t launch_block_exchange(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb,
+                                  int num_sms, cudaStream_t st, const int32_t* gate) {
+  const int64_t n = la + lb;
+  cudaError_t e = cudaSuccess;
+  int64_t a = la, b = lb;
+  for (int step = 0; e == cudaSuccess && a > 0 && b > 0 && step < 16; ++step) {
+    if (a == b) return swap_records(keys, sizeof(KT), payload, w, lo, lo + a, a, num_sms, st, gate);
+    if (std::min(a, b) * 16 < n) break;
+    if (a < b) {  // [X | Y1 Y2], |Y2| = a: X <-> Y2 puts X last; rotate [Y2 | Y1] next
+      e = swap_records(keys, sizeof(KT), payload, w, lo, lo + b, a, num_sms, st, gate);
+      b -= a;
+    } else {  // [X1 X2 | Y], |X1| = b: X1 <-> Y puts Y first; rotate [X2 | X1] next
+      e = swap_records(keys, sizeof(KT), payload, w, lo, lo + a, b, num_sms, st, gate);
+      lo += b;
+      a -= b;
+    }
+  }
+  if (e != cudaSuccess || a == 0 || b == 0) return e;
+  return launch_rotate<KT>(keys, payload, w, lo, a, b, num_sms, st, gate);
+}
+template cudaError_t launch_block_exchange<int32_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int,
+                                                    cudaStream_t, const int32_t*);
+template cudaError_t launch_block_exchange<int64_t>(void*, void*, int64_t, int64_t, int64_t, int64_t, int,
+                                                    cudaStream_t, const int32_t*);
 
 template <typename KT>
 cudaError_t launch_rotate(void* keys, void* payload, int64_t w, int64_t lo, int64_t la, int64_t lb, int num_sms,

@@ -14,7 +14,7 @@ from paper_2005_12648_b200 import _ops  # noqa: E402
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 n = 1 << L
 peak = 6451.8
-for la in (n // 2, n // 3):
+for la in (n // 2, n // 3, 2 * n // 5, 3 * n // 10, 7 * n // 10):
     lb = n - la
     for w in (0, 4):
         k0 = torch.cat([torch.arange(lb, device="cuda", dtype=torch.int32) + lb, torch.arange(la, device="cuda", dtype=torch.int32)])
