@@ -300,10 +300,16 @@ __device__ __forceinline__ void ph_split(const FlowParams& F) {
           ends = true;
         }
       }
+      // a window at an end of the feasible range: one probe of the predicate there --
+      // all of A's part (pred(hi - 1)) or none of it (!pred(lo)) settles the boundary
+      // without the window search (the identity stretches of skewed jobs: half of
+      // config 3's boundaries); interior windows (uniform runs) never pay for it
+      if (wlo < whi && whi == hi && __ldg(A + hi - 1) <= __ldg(B + d - hi)) wlo = whi = hi;
+      else if (wlo < whi && wlo == lo && !(__ldg(A + lo) <= __ldg(B + d - 1 - lo))) wlo = whi = lo;
       // the split is in [wlo, whi]: interpolation between the bracketing samples
       // (pm_search.cuh), then binary search.  The probes are the random DRAM reads
       // the split phase is bound by: ~2-3 instead of ~6 distinct lines per run.
-      if (ends) interp_bracket<KT>(A, B, d, &wlo, &whi, fl, fh, PM_FLOW_INTERP);
+      if (ends && wlo < whi) interp_bracket<KT>(A, B, d, &wlo, &whi, fl, fh, PM_FLOW_INTERP);
       if (PM_FLOW_SPLIT_ABLATE & 1) whi = wlo;  // (timing ablation: wrong splits)
       while (wlo < whi) {  // binary (its late probes share DRAM lines)
         const int64_t mid = (wlo + whi) >> 1;
