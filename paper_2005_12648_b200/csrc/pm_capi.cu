@@ -77,6 +77,7 @@ struct pm_ctx {
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // pm_merge_host: H2D, merge, D2H
   cudaEvent_t hev[33] = {};                          // [0]: joins; then per-chunk events (ring)
   std::map<std::pair<int, size_t>, std::pair<int, int>> flow_occ;  // (key bytes, smem) -> k_flow, plan CTAs/SM
+  uint64_t peer_on = 0;  // peer devices whose memory this context's device may access (P2P enabled)
   size_t flow_attr[2] = {0, 0};  // k_flow<int32/int64>: dynamic shared memory limit set so far
   cudaStream_t fside = nullptr;  // the scheduled engine's gated fallback runs here (forked after the plan)
   cudaEvent_t ffork = nullptr, fjoin = nullptr;  // (key bytes, smem) -> k_flow, plan CTAs/SM
@@ -849,6 +850,28 @@ int pm_debug_splits(pm_ctx* ctx, int64_t* host_out, int64_t n) {
   return PM_OK;
 }
 
+// A peer block (mapped through CUDA IPC) on another device: enable P2P access to that
+// device from this context's device once (the IPC mapping itself is made in the
+// owning device's context, so kernels here need the peer access explicitly).
+static int ensure_peer_access(pm_ctx* ctx, const void* p) {
+  cudaPointerAttributes at{};
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return PM_OK;  // (not a CUDA allocation the runtime knows: the kernel's loads decide)
+  }
+  const int dev = at.device;
+  if (at.type != cudaMemoryTypeDevice || dev == ctx->device || dev < 0 || dev >= 64) return PM_OK;
+  if (ctx->peer_on & (1ull << dev)) return PM_OK;
+  int can = 0;
+  PM_CUDA(cudaDeviceCanAccessPeer(&can, ctx->device, dev));
+  if (!can) return fail(PM_ERR_UNSUPPORTED, "a peer block lives on a device without P2P access from this one");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  cudaGetLastError();
+  ctx->peer_on |= 1ull << dev;
+  return PM_OK;
+}
+
 int pm_peer_splits(pm_ctx* ctx, const void* const* peer_keys, int world, int64_t block, int64_t len_a, int key_bytes,
                    const int64_t* diags, int nd, int64_t* out_a, void* stream) {
   DeviceGuard dg_(ctx ? ctx->device : -1);
@@ -863,6 +886,10 @@ int pm_peer_splits(pm_ctx* ctx, const void* const* peer_keys, int world, int64_t
   if (nd == 0) return PM_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::lock_guard<std::mutex> lk(ctx->mu);
+  for (int k = 0; k < world && block; ++k) {
+    const int prc = ensure_peer_access(ctx, peer_keys[k]);
+    if (prc) return prc;
+  }
   use_stream(ctx, st);
   const size_t o_q = (size_t)align_up((int64_t)world * 8, 256), o_out = o_q + (size_t)align_up((int64_t)nd * 16, 256);
   int rc = ensure(&ctx->peer, &ctx->peer_bytes, o_out + (size_t)nd * 8);
@@ -902,6 +929,11 @@ int pm_merge_peers(pm_ctx* ctx, const void* const* peer_keys, const void* const*
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t la = len_a, lb = N - len_a, d0 = (int64_t)rank * block, d1 = d0 + block;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  for (int k = 0; k < world; ++k) {
+    int prc = ensure_peer_access(ctx, peer_keys[k]);
+    if (!prc && width) prc = ensure_peer_access(ctx, peer_payload[k]);
+    if (prc) return prc;
+  }
   use_stream(ctx, st);
   const int maxq = 2 + 2 * (world + 1);
   const size_t o_q = (size_t)align_up((int64_t)world * 8, 256), o_out = o_q + (size_t)maxq * 16;
