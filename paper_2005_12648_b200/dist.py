@@ -82,7 +82,7 @@ def _split_search(keys_local: torch.Tensor, off: int, diags: torch.Tensor, la: i
 
 # CUDA graphs of the probe rounds, per (keys buffer, geometry): ~30 small ops and a
 # collective per round are replayed without host dispatch (NCCL supports capture).
-# Bounded (least recently used first out); PM_DIST_GRAPHS=0 keeps the search eager.
+# Bounded (least recently used first out); only with PM_DIST_GRAPHS=1 (opt-in).
 _graphs: OrderedDict = OrderedDict()
 _GRAPH_CAP = 8
 _PEER_CAP = 64
@@ -102,9 +102,13 @@ def _peer_splits_enabled() -> bool:
 
 
 def _graph_capture_enabled() -> bool:
+    """CUDA-graph capture of the NCCL split-search rounds: opt-in (PM_DIST_GRAPHS=1).
+    Capturing NCCL collectives has only run at one rank here; a capture that fails on
+    one rank and not another would pair eager and graph collectives, so multi-rank
+    jobs stay eager unless asked (the peer-table search needs no collectives at all)."""
     import os
 
-    return os.environ.get("PM_DIST_GRAPHS", "1") != "0"
+    return os.environ.get("PM_DIST_GRAPHS", "0") == "1"
 
 
 def global_splits(keys_local: torch.Tensor, offsets: list[int], global_len_a: int, group=None) -> list[int]:
